@@ -1,0 +1,322 @@
+"""The acquisition hot path behind the reference's own Python API.
+
+Signatures, argument meaning, return values and exceptions follow the reference functions they
+replace; each docstring names its counterpart.  Every number is produced on the GPU by
+libbx_sm100; the host only samples the pool (so the caller's RNG stream is consumed exactly as the
+reference consumes it), encodes/decodes configurations and runs the O(n_starts x steps) control
+logic of the hill climb.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from .device import Candidate, Scorer, scorer
+
+N_CANDIDATES = 5000   # acquisition.py:23
+N_STARTS = 10         # acquisition.py:24
+MAX_CLIMB_STEPS = 50  # acquisition.py:25
+
+
+class SpaceExhausted(Exception):
+    """Every feasible configuration has already been evaluated (acquisition.py:30-31)."""
+
+
+def _exhausted_type(space):
+    # raise the reference's own exception class when the caller uses the reference package
+    mod = type(space).__module__.rsplit(".", 1)[0]
+    try:
+        import importlib
+
+        return importlib.import_module(mod + ".acquisition").SpaceExhausted
+    except Exception:
+        return SpaceExhausted
+
+
+class _State:
+    """Tracks which model objects are resident on the device (identity-keyed)."""
+
+    def __init__(self):
+        self.gen = -1
+        self.gp = None
+        self.feas = None
+        self.feas_set = False
+        self.evaluated_len = -1
+        self.evaluated_id = None
+
+
+_STATE: dict = {}
+
+
+def _state(sc: Scorer) -> _State:
+    st = _STATE.setdefault(id(sc), _State())
+    if st.gen != sc.space_gen:  # a space change dropped every model upload
+        st.__init__()
+        st.gen = sc.space_gen
+    return st
+
+
+def _prepare(ctx, sc: Scorer, evaluated: bool):
+    st = _state(sc)
+    gp = ctx.gp
+    if st.gp is not gp:
+        sc.set_gp(gp)
+        st = _state(sc)
+        st.gp = gp
+        st.evaluated_len = -1
+    if not st.feas_set or st.feas is not ctx.feas:
+        sc.set_forest(ctx.feas)
+        st.feas, st.feas_set = ctx.feas, True
+    if evaluated:
+        ev = ctx.evaluated if ctx.evaluated is not None else ()
+        if st.evaluated_id != id(ev) or st.evaluated_len != len(ev):
+            sc.set_evaluated(list(ev))
+            st.evaluated_id, st.evaluated_len = id(ev), len(ev)
+    return sc.layout
+
+
+def scores(ctx, configs):
+    """`_scores(ctx, configs) -> (values, probs)` (acquisition.py:70-79) on the GPU."""
+    configs = list(configs)
+    sc = scorer()
+    lay = _prepare(ctx, sc, evaluated=False)
+    f_model = ctx.gp.objective_to_model(ctx.best_feasible_value)
+    rows = sc.to_device(lay.encode(configs))
+    _, values, probs = sc.score(rows, f_model, ctx.eps_f, k=0, want_values=True, summary=False)
+    return values.cpu().numpy(), probs.cpu().numpy()
+
+
+def acquisition_value(ctx, cfg) -> float:
+    """acquisition.py:82-84."""
+    return float(scores(ctx, [cfg])[0][0])
+
+
+def predict_batch(gp, configs, include_noise: bool = False):
+    """`GPModel.predict_batch` (surrogate.py:315-328) on the GPU."""
+    sc = scorer()
+    st = _state(sc)
+    if st.gp is not gp:
+        sc.set_gp(gp)
+        st = _state(sc)
+        st.gp = gp
+    rows = sc.to_device(sc.layout.encode(list(configs)))
+    mean, var = sc.predict(rows)
+    mean, var = mean.cpu().numpy(), var.cpu().numpy()
+    if include_noise:
+        var = var + gp.noise * gp.y_std ** 2
+    return mean, var
+
+
+def predict_proba_batch(feas, configs):
+    """`FeasibilityModel.predict_proba_batch` (feasibility.py:72-89) on the GPU, bit-exact."""
+    configs = list(configs)
+    if feas.constant is not None:
+        return np.full(len(configs), feas.constant)
+    if feas.roots is None or len(feas.roots) == 0:
+        from .device import N
+        raise N.NativeError(N.BX_ERR_NO_TREES, "feasibility model has no trees")
+    sc = scorer()
+    if sc.layout is None or sc.layout.space is not feas.space or \
+            sc.layout.use_transforms != bool(feas.use_transforms):
+        sc.set_space(feas.space, feas.use_transforms)
+    st = _state(sc)
+    if st.feas is not feas or not st.feas_set:
+        sc.set_forest(feas)
+        st.feas, st.feas_set = feas, True
+    rows = sc.to_device(sc.layout.encode(configs))
+    return sc.rf_predict(rows).cpu().numpy()
+
+
+def neighbors(space, cfg, cot=None) -> list:
+    """`neighbors(space, cfg, cot)` (space.py:289-309) on the GPU: same set, same order."""
+    sc = scorer()
+    lay = sc.layout_for(space)
+    if cot is not None:
+        sc.set_cot(cot)
+    out, valid = sc.neighbors(sc.to_device(lay.encode([cfg])), use_cot=cot is not None)
+    keep = out[valid.bool()]
+    return lay.decode(keep.cpu().numpy().view(np.uint32))
+
+
+def contains_batch(cot, configs) -> np.ndarray:
+    """`ChainOfTrees.contains` (constraints.py:413-430) over a batch, bit-exact."""
+    sc = scorer()
+    lay = sc.layout_for(cot.space)
+    sc.set_cot(cot)
+    return sc.cot_contains(sc.to_device(lay.encode(list(configs)))).cpu().numpy().astype(bool)
+
+
+def constraints_batch(space, configs) -> np.ndarray:
+    """all(eval_constraint(c, cfg) is True for c in space.constraints) over a batch."""
+    sc = scorer()
+    lay = sc.layout_for(space)
+    sc.set_constraints(space)
+    return sc.constraints_eval(sc.to_device(lay.encode(list(configs)))).cpu().numpy().astype(bool)
+
+
+# ---------------------------------------------------------------------------------------------
+# whole-path replacement
+# ---------------------------------------------------------------------------------------------
+def _default_sampler(space, cot):
+    """acquisition.py:114-134, consuming the RNG identically."""
+    if cot is not None:
+        return lambda n, rng: cot.sample_leaf_uniform(n, rng)
+    sample_uniform = _sample_uniform_for(space)
+    if not space.constraints:
+        return lambda n, rng: sample_uniform(space, n, rng)
+
+    def rejection(n, rng):
+        out, attempts = [], 0
+        while len(out) < n and attempts < 50 * n:
+            batch = sample_uniform(space, n, rng)
+            attempts += n
+            ok = constraints_batch(space, batch)
+            for cfg, good in zip(batch, ok):
+                if good:
+                    out.append(cfg)
+                    if len(out) == n:
+                        break
+        return out
+
+    return rejection
+
+
+def _sample_uniform_for(space):
+    mod = type(space).__module__
+    try:
+        import importlib
+
+        return importlib.import_module(mod).sample_uniform
+    except Exception:
+        from .space import sample_uniform
+        return sample_uniform
+
+
+def _better(a_val, a_cfg, b_val, b_cfg) -> bool:
+    """(value desc, configuration asc) - the order of _argbest / _Tracker (acquisition.py:87-111)."""
+    return a_val > b_val or (a_val == b_val and a_cfg < b_cfg)
+
+
+def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: bool = True,
+                         n_candidates: int = N_CANDIDATES, n_starts: int = N_STARTS):
+    """`optimize_acquisition` (acquisition.py:152-206) with every score, top-k, tracker reduction and
+    neighbour set computed on the GPU."""
+    Exhausted = _exhausted_type(space)
+    if sample_fn is None:
+        sample_fn = _default_sampler(space, cot)
+    raw = sample_fn(n_candidates, ctx.rng)
+    candidates = list(dict.fromkeys(raw))
+    if not candidates:
+        raise Exhausted("candidate sampler produced nothing")
+    sc = scorer()
+    lay = _prepare(ctx, sc, evaluated=True)
+    if cot is not None:
+        sc.set_cot(cot)
+    f_model = ctx.gp.objective_to_model(ctx.best_feasible_value)
+    rows = sc.to_device(lay.encode(candidates))
+    summ, _, _ = sc.score(rows, f_model, ctx.eps_f, k=min(n_starts, 32),
+                          rf_pairwise=len(candidates) == 1)
+    if summ.n_finite == 0:  # acquisition.py:179-184
+        if summ.best_prob is None:
+            return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
+        return candidates[summ.best_prob.index]
+
+    best = summ.best
+    best_val = best.value if best else -math.inf
+    best_cfg = candidates[best.index] if best else None
+    if local_search:
+        for start in summ.top[:n_starts]:
+            cur_cfg, cur_v = candidates[start.index], start.value
+            cur_row = rows[start.index:start.index + 1]
+            for _ in range(MAX_CLIMB_STEPS):
+                nb, valid = sc.neighbors(cur_row, use_cot=cot is not None)
+                nb = nb[valid.bool()]
+                if nb.shape[0] == 0:
+                    break
+                s2, vals, _ = sc.score(nb, f_model, ctx.eps_f, k=1, want_values=True)
+                if s2.best is not None:
+                    cfg2 = lay.decode(s2.best.row)[0]
+                    if best_cfg is None or _better(s2.best.value, cfg2, best_val, best_cfg):
+                        best_val, best_cfg = s2.best.value, cfg2
+                v = vals.cpu().numpy()
+                i = int(np.argmax(v))
+                ties = np.flatnonzero(v == v[i])
+                nb_host = nb.cpu().numpy().view(np.uint32)
+                if len(ties) > 1:
+                    cfgs = lay.decode(nb_host[ties])
+                    j = min(range(len(ties)), key=lambda t: cfgs[t])
+                    i, nxt = int(ties[j]), cfgs[j]
+                else:
+                    nxt = lay.decode(nb_host[i])[0]
+                if v[i] <= cur_v:  # acquisition.py:200
+                    break
+                cur_cfg, cur_v, cur_row = nxt, float(v[i]), nb[i:i + 1]
+    if best_cfg is None:
+        return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
+    return best_cfg
+
+
+def _enumerate_feasible(space, cot, Exhausted):
+    """acquisition.py:137-149."""
+    import itertools
+
+    if cot is not None:
+        yield from cot.enumerate()
+        return
+    if any(p.kind == "real" for p in space.parameters):
+        raise Exhausted("cannot enumerate a space with real parameters")
+    doms = [list(range(int(p.lo), int(p.hi) + 1)) if p.kind == "integer"
+            else list(p.values) if p.kind != "permutation"
+            else [tuple(q) for q in itertools.permutations(range(1, p.size + 1))]
+            for p in space.parameters]
+    for batch in _chunks(itertools.product(*doms), 65536):
+        ok = constraints_batch(space, batch) if space.constraints else [True] * len(batch)
+        for cfg, good in zip(batch, ok):
+            if good:
+                yield cfg
+
+
+def _chunks(it, n):
+    buf = []
+    for x in it:
+        buf.append(x)
+        if len(buf) == n:
+            yield buf
+            buf = []
+    if buf:
+        yield buf
+
+
+def _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted):
+    """acquisition.py:209-222."""
+    remaining = []
+    for cfg in _enumerate_feasible(space, cot, Exhausted):
+        if cfg not in ctx.evaluated:
+            remaining.append(cfg)
+            if len(remaining) >= 20_000:
+                break
+    if not remaining:
+        raise Exhausted("every feasible configuration has been evaluated")
+    rows = sc.to_device(sc.layout.encode(remaining))
+    _, vals, probs = sc.score(rows, f_model, ctx.eps_f, k=0, want_values=True, summary=False,
+                              rf_pairwise=len(remaining) == 1)
+    v = vals.cpu().numpy()
+    key = probs.cpu().numpy() if np.all(v == -np.inf) else v
+    best = None
+    for i, x in enumerate(key):
+        if best is None or _better(x, remaining[i], key[best], remaining[best]):
+            best = i
+    return remaining[best]
+
+
+def batched_coarse_lml(sq_dists, z, thetas):
+    """`_batched_coarse_lml` (surrogate.py:420-456) on the GPU: one CTA per hyperparameter
+    candidate, -inf where the Cholesky factorisation fails."""
+    sc = scorer()
+    dev = f"cuda:{sc.device}"
+    sq = torch.as_tensor(np.ascontiguousarray(sq_dists, dtype=np.float64), device=dev)
+    zz = torch.as_tensor(np.ascontiguousarray(z, dtype=np.float64), device=dev)
+    th = torch.as_tensor(np.ascontiguousarray(thetas, dtype=np.float64), device=dev)
+    return sc.lml_batched(sq, zz, th).cpu().numpy()

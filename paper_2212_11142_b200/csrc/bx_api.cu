@@ -1,0 +1,729 @@
+// bx_api.cu — the C ABI (include/bx_sm100.h): handle, model-state uploads, launches.
+// No exception crosses the boundary; every failure becomes a status code + bx_last_error().
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bx_common.cuh"
+
+namespace bx {
+int score_smem_bytes(int cpw, int ncols, int n_params, int row_words);
+size_t lml_scratch_doubles(int n, int c);
+}  // namespace bx
+
+using namespace bx;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need < 256 ? 256 : need);
+    if (e == cudaSuccess) bytes = need < 256 ? 256 : need;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct bx_handle {
+  int device = 0;
+  int sm_count = 148;
+  std::string err;
+  // space
+  bool has_space = false;
+  int n_params = 0, row_words = 0, n_features = 0, n_slots = 0;
+  std::vector<bx_param_desc> params;
+  std::vector<int32_t> rank_host;
+  DevBuf d_params, d_coord, d_rank, d_feat_param, d_feat_sub, d_slot_param, d_slot_move;
+  // gp
+  bool has_gp = false;
+  int gp_n = 0, gp_ncols = 0, gp_rows = 0, gp_lda = 0;
+  double outputscale = 1, y_mean = 0, y_std = 1;
+  DevBuf d_A, d_L, d_planes, d_kmask, d_inv_l, d_inv_l2, d_disc_tab, d_disc_off, d_train;
+  // forest
+  bool has_forest = false;
+  ForestDev forest{};
+  DevBuf d_nodes, d_roots;
+  // evaluated
+  int ev_count = 0, ev_mask = 0;
+  DevBuf d_ev_rows, d_ev_table;
+  // cot
+  bool has_cot = false;
+  CotDev cot{};
+  DevBuf d_g_kind, d_g_pbeg, d_g_params, d_g_root, d_child_begin, d_child_count, d_child_value;
+  // constraints
+  bool has_constraints = false;
+  ConstraintDev cons{};
+  DevBuf d_prog_begin, d_code, d_consts, d_vtag, d_vint, d_vflt, d_voff, d_str_id, d_fault;
+  // scratch
+  DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+int fail(bx_handle* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  return code;
+}
+
+#define BX_CUDA(h, call)                                                                       \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(h, BX_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));             \
+  } while (0)
+
+template <typename T>
+cudaError_t upload(DevBuf& b, const T* host, size_t count) {
+  cudaError_t e = b.ensure(count * sizeof(T) + 16);
+  if (e != cudaSuccess) return e;
+  if (count == 0) return cudaSuccess;
+  return cudaMemcpy(b.p, host, count * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+SpaceDev space_dev(const bx_handle* h) {
+  SpaceDev s;
+  s.params = h->d_params.as<bx_param_desc>();
+  s.coord_lut = h->d_coord.as<double>();
+  s.rank_lut = h->d_rank.as<int32_t>();
+  s.feat_param = h->d_feat_param.as<int32_t>();
+  s.feat_sub = h->d_feat_sub.as<int32_t>();
+  s.slot_param = h->d_slot_param.as<int32_t>();
+  s.slot_move = h->d_slot_move.as<int32_t>();
+  s.n_params = h->n_params;
+  s.row_words = h->row_words;
+  s.n_features = h->n_features;
+  s.n_slots = h->n_slots;
+  return s;
+}
+
+GpDev gp_dev(const bx_handle* h) {
+  GpDev g;
+  g.n = h->gp_n;
+  g.ncols_pad = h->gp_ncols;
+  g.rows_pad = h->gp_rows;
+  g.lda = h->gp_lda;
+  g.A = h->d_A.as<double>();
+  g.planes = h->d_planes.as<uint64_t>();
+  g.kmask = h->d_kmask.as<uint64_t>();
+  g.inv_l = h->d_inv_l.as<double>();
+  g.inv_l2 = h->d_inv_l2.as<double>();
+  g.disc_tab = h->d_disc_tab.as<double>();
+  g.disc_off = h->d_disc_off.as<int32_t>();
+  g.outputscale = h->outputscale;
+  g.y_mean = h->y_mean;
+  g.y_std = h->y_std;
+  return g;
+}
+
+EvalSetDev eval_dev(const bx_handle* h) {
+  EvalSetDev e;
+  e.rows = h->d_ev_rows.as<uint32_t>();
+  e.table = h->d_ev_table.as<int32_t>();
+  e.count = h->ev_count;
+  e.table_mask = h->ev_mask;
+  return e;
+}
+
+uint64_t host_row_hash(const uint32_t* row, int words) {
+  uint64_t hsh = 1469598103934665603ull;
+  for (int w = 0; w < words; ++w) {
+    hsh ^= row[w];
+    hsh *= 1099511628211ull;
+    hsh ^= hsh >> 29;
+  }
+  return hsh;
+}
+
+int check_space(bx_handle* h) {
+  if (!h) return BX_ERR_ARG;
+  if (!h->has_space) return fail(h, BX_ERR_STATE, "bx_set_space has not been called");
+  return BX_OK;
+}
+
+int check_gp(bx_handle* h) {
+  int r = check_space(h);
+  if (r) return r;
+  if (!h->has_gp) return fail(h, BX_ERR_STATE, "bx_set_gp has not been called");
+  return BX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bx_abi_version(void) { return BX_ABI_VERSION; }
+
+bx_handle* bx_create(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  bx_handle* h = new (std::nothrow) bx_handle();
+  if (!h) return nullptr;
+  h->device = device;
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
+  }
+  return h;
+}
+
+void bx_destroy(bx_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  DevBuf* bufs[] = {&h->d_params, &h->d_coord, &h->d_rank, &h->d_feat_param, &h->d_feat_sub,
+                    &h->d_slot_param, &h->d_slot_move, &h->d_A, &h->d_L, &h->d_planes,
+                    &h->d_kmask, &h->d_inv_l, &h->d_inv_l2, &h->d_disc_tab, &h->d_disc_off,
+                    &h->d_train, &h->d_nodes, &h->d_roots, &h->d_ev_rows, &h->d_ev_table,
+                    &h->d_g_kind, &h->d_g_pbeg, &h->d_g_params, &h->d_g_root,
+                    &h->d_child_begin, &h->d_child_count, &h->d_child_value, &h->d_prog_begin, &h->d_code,
+                    &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
+                    &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
+                    &h->d_host_rows[0], &h->d_host_rows[1]};
+  for (DevBuf* b : bufs) b->release();
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
+    if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+  }
+  delete h;
+}
+
+const char* bx_last_error(bx_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int bx_device_sm_count(bx_handle* h) { return h ? h->sm_count : 0; }
+
+int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, int32_t row_words,
+                 const double* coord_lut, int32_t coord_len, const int32_t* rank_lut,
+                 int32_t rank_len, int32_t n_features) {
+  if (!h) return BX_ERR_ARG;
+  if (n_params < 1 || n_params > BX_MAX_PARAMS)
+    return fail(h, BX_ERR_UNSUPPORTED, "n_params=%d outside [1, %d]", n_params, BX_MAX_PARAMS);
+  if (row_words < 1 || row_words > BX_MAX_ROW_WORDS)
+    return fail(h, BX_ERR_UNSUPPORTED, "row_words=%d outside [1, %d]", row_words, BX_MAX_ROW_WORDS);
+  cudaSetDevice(h->device);
+  std::vector<int32_t> fparam, fsub, sparam, smove;
+  for (int k = 0; k < n_params; ++k) {
+    const bx_param_desc& p = params[k];
+    int nw = p.kind == BX_REAL ? 4 : (p.kind == BX_PERMUTATION ? 2 : 1);
+    if (p.word < 0 || p.word + nw > row_words)
+      return fail(h, BX_ERR_ARG, "parameter %d overflows the row (%d words)", k, row_words);
+    if (p.kind == BX_PERMUTATION) {
+      if (p.size < 2 || p.size > BX_MAX_PERM)
+        return fail(h, BX_ERR_UNSUPPORTED, "permutation size %d outside [2, 16]", p.size);
+      if ((p.word & 1) != 0) return fail(h, BX_ERR_ARG, "permutation %d not 8-byte aligned", k);
+      for (int e = 0; e < p.size; ++e) { fparam.push_back(k); fsub.push_back(e); }
+      for (int m = 0; m < p.size * (p.size - 1) / 2; ++m) { sparam.push_back(k); smove.push_back(m); }
+    } else if (p.kind == BX_CATEGORICAL) {
+      for (int e = 0; e < p.size; ++e) { fparam.push_back(k); fsub.push_back(e); }
+      for (int m = 0; m < p.size - 1; ++m) { sparam.push_back(k); smove.push_back(m); }
+    } else {
+      if (p.kind == BX_REAL && (p.word & 1) != 0)
+        return fail(h, BX_ERR_ARG, "real parameter %d not 8-byte aligned", k);
+      fparam.push_back(k);
+      fsub.push_back(0);
+      sparam.push_back(k); smove.push_back(0);
+      sparam.push_back(k); smove.push_back(1);
+    }
+  }
+  if ((int)fparam.size() != n_features)
+    return fail(h, BX_ERR_ARG, "n_features=%d but the parameters imply %d", n_features,
+                (int)fparam.size());
+  BX_CUDA(h, upload(h->d_params, params, n_params));
+  BX_CUDA(h, upload(h->d_coord, coord_lut, (size_t)coord_len));
+  BX_CUDA(h, upload(h->d_rank, rank_lut, (size_t)rank_len));
+  BX_CUDA(h, upload(h->d_feat_param, fparam.data(), fparam.size()));
+  BX_CUDA(h, upload(h->d_feat_sub, fsub.data(), fsub.size()));
+  BX_CUDA(h, upload(h->d_slot_param, sparam.data(), sparam.size()));
+  BX_CUDA(h, upload(h->d_slot_move, smove.data(), smove.size()));
+  h->params.assign(params, params + n_params);
+  h->rank_host.assign(rank_lut, rank_lut + rank_len);
+  h->n_params = n_params;
+  h->row_words = row_words;
+  h->n_features = n_features;
+  h->n_slots = (int)sparam.size();
+  h->has_space = true;
+  h->has_gp = false;  // planes depend on the space
+  return BX_OK;
+}
+
+int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double* L,
+              const double* alpha, double outputscale, const double* lengthscales, double y_mean,
+              double y_std, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (n < 1) return fail(h, BX_ERR_ARG, "need at least one training point");
+  if (!(outputscale > 0)) return fail(h, BX_ERR_ARG, "outputscale must be positive");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int D = h->n_params;
+  std::vector<double> inv_l(D), inv_l2(D);
+  std::vector<int32_t> disc_off(D, 0);
+  std::vector<double> disc;
+  for (int k = 0; k < D; ++k) {
+    const double l = lengthscales[k];
+    if (!(l > 0)) return fail(h, BX_ERR_ARG, "lengthscale %d must be positive", k);
+    inv_l[k] = 1.0 / l;
+    inv_l2[k] = 1.0 / (l * l);  // surrogate.py:222 1.0 / l ** 2
+    const bx_param_desc& p = h->params[k];
+    disc_off[k] = (int)disc.size();
+    if (p.kind == BX_PERMUTATION) {
+      const int m = p.size;
+      int raw_max = m * m * m;  // >= every semimetric maximum
+      for (int raw = 0; raw <= raw_max; ++raw) disc.push_back(((double)raw / p.raw_mx) * inv_l2[k]);
+    } else if (p.kind == BX_CATEGORICAL) {
+      disc.push_back(0.0);
+      disc.push_back(inv_l2[k]);
+    }
+  }
+  disc.push_back(0.0);
+  h->gp_n = n;
+  h->gp_ncols = ((n + 15) / 16) * 16;
+  h->gp_rows = ((n + 1 + 15) / 16) * 16;
+  h->gp_lda = h->gp_ncols;
+  const size_t a_elems = (size_t)h->gp_rows * h->gp_lda;
+  BX_CUDA(h, h->d_A.ensure(a_elems * 8));
+  BX_CUDA(h, cudaMemsetAsync(h->d_A.p, 0, a_elems * 8, s));
+  BX_CUDA(h, h->d_L.ensure((size_t)n * n * 8));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_L.p, L, (size_t)n * n * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_A.as<double>() + (size_t)n * h->gp_lda, alpha, (size_t)n * 8,
+                             cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_train.ensure((size_t)n * h->row_words * 4));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_train.p, train_rows, (size_t)n * h->row_words * 4,
+                             cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_inv_l.ensure(D * 8));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_inv_l.p, inv_l.data(), D * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_inv_l2.ensure(D * 8));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_inv_l2.p, inv_l2.data(), D * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_disc_tab.ensure(disc.size() * 8));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_disc_tab.p, disc.data(), disc.size() * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_disc_off.ensure(D * 4));
+  BX_CUDA(h, cudaMemcpyAsync(h->d_disc_off.p, disc_off.data(), D * 4, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, h->d_planes.ensure((size_t)D * n * 8));
+  BX_CUDA(h, h->d_kmask.ensure((size_t)D * n * 16));
+  BX_CUDA(h, launch_tri_inverse(h->d_L.as<double>(), n, h->d_A.as<double>(), h->gp_lda, s));
+  BX_CUDA(h, launch_gp_planes(space_dev(h), h->d_train.as<uint32_t>(), n, h->d_inv_l.as<double>(),
+                              h->d_planes.as<uint64_t>(), h->d_kmask.as<uint64_t>(), s));
+  BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
+  h->outputscale = outputscale;
+  h->y_mean = y_mean;
+  h->y_std = y_std;
+  h->has_gp = true;
+  return BX_OK;
+}
+
+int bx_set_forest(bx_handle* h, const int32_t* feature, const double* threshold, const int32_t* left,
+                  const int32_t* right, const double* value, int32_t n_nodes, const int32_t* roots,
+                  int32_t n_trees, int32_t max_depth, double constant) {
+  int r = check_space(h);
+  if (r) return r;
+  cudaSetDevice(h->device);
+  h->forest = ForestDev{};
+  if (!std::isnan(constant)) {
+    h->forest.has_trees = 0;
+    h->forest.constant = constant;
+    h->forest.n_trees = 0;
+    h->has_forest = true;
+    return BX_OK;
+  }
+  if (n_trees < 1 || !roots)
+    return fail(h, BX_ERR_NO_TREES, "feasibility model has no trees");
+  // Re-pack breadth-first per tree so that children are adjacent; keep values of every node.
+  std::vector<RfNode> nodes;
+  nodes.reserve(n_nodes);
+  std::vector<int32_t> new_roots(n_trees);
+  std::vector<int32_t> queue;
+  for (int t = 0; t < n_trees; ++t) {
+    const int root = roots[t];
+    if (root < 0 || root >= n_nodes) return fail(h, BX_ERR_ARG, "root %d out of range", root);
+    new_roots[t] = (int)nodes.size();
+    nodes.push_back(RfNode{threshold[root], value[root], feature[root], -1});
+    queue.assign(1, root);
+    std::vector<int32_t> slot(1, new_roots[t]);
+    for (size_t qi = 0; qi < queue.size(); ++qi) {
+      const int old = queue[qi];
+      const int me = slot[qi];
+      if (feature[old] < 0) continue;
+      if (feature[old] >= h->n_features)
+        return fail(h, BX_ERR_ARG, "node %d splits on feature %d >= %d", old, feature[old], h->n_features);
+      const int l = left[old], rr = right[old];
+      if (l < 0 || l >= n_nodes || rr < 0 || rr >= n_nodes)
+        return fail(h, BX_ERR_ARG, "node %d has a child out of range", old);
+      nodes[me].child = (int)nodes.size();
+      nodes.push_back(RfNode{threshold[l], value[l], feature[l], -1});
+      nodes.push_back(RfNode{threshold[rr], value[rr], feature[rr], -1});
+      queue.push_back(l);
+      slot.push_back(nodes[me].child);
+      queue.push_back(rr);
+      slot.push_back(nodes[me].child + 1);
+    }
+  }
+  BX_CUDA(h, upload(h->d_nodes, nodes.data(), nodes.size()));
+  BX_CUDA(h, upload(h->d_roots, new_roots.data(), new_roots.size()));
+  h->forest.nodes = h->d_nodes.as<RfNode>();
+  h->forest.roots = h->d_roots.as<int32_t>();
+  h->forest.n_trees = n_trees;
+  h->forest.max_depth = max_depth;
+  h->forest.has_trees = 1;
+  h->forest.constant = 0.0;
+  h->has_forest = true;
+  return BX_OK;
+}
+
+int bx_clear_forest(bx_handle* h) {
+  if (!h) return BX_ERR_ARG;
+  h->has_forest = false;
+  return BX_OK;
+}
+
+int bx_set_evaluated(bx_handle* h, const uint32_t* rows, int32_t count) {
+  int r = check_space(h);
+  if (r) return r;
+  cudaSetDevice(h->device);
+  const int W = h->row_words;
+  h->ev_count = count > 0 ? count : 0;
+  if (h->ev_count == 0) return BX_OK;
+  int size = 16;
+  while (size < 2 * count) size <<= 1;
+  std::vector<int32_t> table(size, -1);
+  for (int i = 0; i < count; ++i) {
+    const uint32_t* row = rows + (size_t)i * W;
+    int slot = (int)(host_row_hash(row, W) & (uint64_t)(size - 1));
+    while (table[slot] >= 0) {
+      if (std::memcmp(rows + (size_t)table[slot] * W, row, W * 4) == 0) break;  // duplicate
+      slot = (slot + 1) & (size - 1);
+    }
+    if (table[slot] < 0) table[slot] = i;
+  }
+  BX_CUDA(h, upload(h->d_ev_rows, rows, (size_t)count * W));
+  BX_CUDA(h, upload(h->d_ev_table, table.data(), table.size()));
+  h->ev_mask = size - 1;
+  return BX_OK;
+}
+
+int bx_set_cot(bx_handle* h, int32_t n_groups, const int32_t* group_kind,
+               const int32_t* group_param_begin, const int32_t* group_params,
+               const int32_t* group_root, int32_t n_nodes, const int32_t* child_begin,
+               const int32_t* child_count, const int32_t* node_value) {
+  int r = check_space(h);
+  if (r) return r;
+  if (n_groups < 0 || n_nodes < 0) return fail(h, BX_ERR_ARG, "bad chain-of-trees sizes");
+  cudaSetDevice(h->device);
+  const int np = group_param_begin[n_groups];
+  for (int g = 0; g < n_groups; ++g) {
+    if (group_kind[g] == 0 && (group_root[g] < 0 || group_root[g] >= n_nodes))
+      return fail(h, BX_ERR_ARG, "group %d root out of range", g);
+  }
+  for (int u = 0; u < n_nodes; ++u)
+    if (child_count[u] < 0 || child_begin[u] < 0 || child_begin[u] + child_count[u] > n_nodes)
+      return fail(h, BX_ERR_ARG, "node %d children out of range", u);
+  BX_CUDA(h, upload(h->d_g_kind, group_kind, n_groups));
+  BX_CUDA(h, upload(h->d_g_pbeg, group_param_begin, n_groups + 1));
+  BX_CUDA(h, upload(h->d_g_params, group_params, np));
+  BX_CUDA(h, upload(h->d_g_root, group_root, n_groups));
+  BX_CUDA(h, upload(h->d_child_begin, child_begin, n_nodes));
+  BX_CUDA(h, upload(h->d_child_count, child_count, n_nodes));
+  BX_CUDA(h, upload(h->d_child_value, node_value, n_nodes));
+  h->cot.n_groups = n_groups;
+  h->cot.group_kind = h->d_g_kind.as<int32_t>();
+  h->cot.group_param_begin = h->d_g_pbeg.as<int32_t>();
+  h->cot.group_params = h->d_g_params.as<int32_t>();
+  h->cot.group_root = h->d_g_root.as<int32_t>();
+  h->cot.child_begin = h->d_child_begin.as<int32_t>();
+  h->cot.child_count = h->d_child_count.as<int32_t>();
+  h->cot.node_value = h->d_child_value.as<int32_t>();
+  h->has_cot = true;
+  return BX_OK;
+}
+
+int bx_clear_cot(bx_handle* h) {
+  if (!h) return BX_ERR_ARG;
+  h->has_cot = false;
+  return BX_OK;
+}
+
+int bx_set_constraints(bx_handle* h, int32_t n_constraints, const int32_t* prog_begin,
+                       const int32_t* code, int32_t code_len, const double* consts,
+                       int32_t n_consts, const int32_t* value_tag, const int64_t* value_int,
+                       const double* value_float, const int32_t* value_str, int32_t n_values) {
+  int r = check_space(h);
+  if (r) return r;
+  if (n_constraints < 0 || code_len < 0 || n_consts < 0)
+    return fail(h, BX_ERR_ARG, "bad constraint program sizes");
+  cudaSetDevice(h->device);
+  const int D = h->n_params;
+  std::vector<int32_t> voff(D);
+  int total = 0;
+  for (int k = 0; k < D; ++k) {
+    voff[k] = total;
+    const bx_param_desc& p = h->params[k];
+    total += (p.kind == BX_REAL || p.kind == BX_PERMUTATION) ? 0 : p.size;
+  }
+  if (total != n_values)
+    return fail(h, BX_ERR_ARG, "constraint value tables: expected %d entries, got %d", total, n_values);
+  if (n_constraints > 0 && prog_begin[n_constraints] != code_len)
+    return fail(h, BX_ERR_ARG, "prog_begin[n] != code_len");
+  const int lit = n_consts;
+  std::vector<int32_t> vtag(value_tag, value_tag + total), sid(value_str, value_str + total);
+  std::vector<int64_t> vint(value_int, value_int + total);
+  std::vector<double> vflt(value_float, value_float + total);
+  vtag.push_back(0); sid.push_back(0); vint.push_back(0); vflt.push_back(0.0);
+  BX_CUDA(h, upload(h->d_prog_begin, prog_begin, n_constraints + 1));
+  BX_CUDA(h, upload(h->d_code, code, code_len));
+  BX_CUDA(h, upload(h->d_consts, consts, lit));
+  BX_CUDA(h, upload(h->d_vtag, vtag.data(), vtag.size()));
+  BX_CUDA(h, upload(h->d_vint, vint.data(), vint.size()));
+  BX_CUDA(h, upload(h->d_vflt, vflt.data(), vflt.size()));
+  BX_CUDA(h, upload(h->d_voff, voff.data(), voff.size()));
+  BX_CUDA(h, upload(h->d_str_id, sid.data(), sid.size()));
+  BX_CUDA(h, h->d_fault.ensure(16));
+  BX_CUDA(h, cudaMemset(h->d_fault.p, 0, 16));
+  h->cons.n_constraints = n_constraints;
+  h->cons.prog_begin = h->d_prog_begin.as<int32_t>();
+  h->cons.code = h->d_code.as<int32_t>();
+  h->cons.consts = h->d_consts.as<double>();
+  h->cons.vtag = h->d_vtag.as<int32_t>();
+  h->cons.vint = h->d_vint.as<int64_t>();
+  h->cons.vflt = h->d_vflt.as<double>();
+  h->cons.voff = h->d_voff.as<int32_t>();
+  h->cons.str_id = h->d_str_id.as<int32_t>();
+  h->cons.fault = h->d_fault.as<int32_t>();
+  h->has_constraints = true;
+  return BX_OK;
+}
+
+// ---- scoring --------------------------------------------------------------------------------
+
+static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
+                      double f_model, double eps_f, int32_t k, int32_t flags, double* values,
+                      double* probs_out, bx_score_summary* partials, int* grid_used,
+                      cudaStream_t s) {
+  ScoreArgs a{};
+  a.space = space_dev(h);
+  a.gp = gp_dev(h);
+  a.evald = eval_dev(h);
+  a.rows = rows;
+  a.q = q;
+  a.index_base = index_base;
+  a.f_model = f_model;
+  a.eps_f = eps_f;
+  a.k = k;
+  a.flags = flags;
+  a.use_forest = h->has_forest ? 1 : 0;
+  a.forest = h->forest;
+  a.values_out = values;
+  a.probs_out = probs_out;
+  a.partials = partials;
+  if (h->has_forest && h->forest.has_trees) {
+    BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
+    BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
+                         h->d_probs.as<double>(), s));
+    a.probs_in = h->d_probs.as<double>();
+  }
+  BX_CUDA(h, launch_score(a, h->sm_count, s, grid_used));
+  return BX_OK;
+}
+
+int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, double f_model,
+             double eps_f, int32_t k, int32_t flags, double* values, double* probs,
+             bx_score_summary* summary, void* stream) {
+  int r = check_gp(h);
+  if (r) return r;
+  if (q < 1) return fail(h, BX_ERR_ARG, "empty candidate pool");
+  if (k < 0 || k > BX_MAX_K) return fail(h, BX_ERR_ARG, "k=%d outside [0, %d]", k, BX_MAX_K);
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool want = !(flags & BX_SCORE_NO_SUMMARY) && summary != nullptr;
+  bx_score_summary* partials = nullptr;
+  if (want) {
+    BX_CUDA(h, h->d_partials.ensure(sizeof(bx_score_summary) * (size_t)h->sm_count * 8));
+    BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
+    partials = h->d_partials.as<bx_score_summary>();
+  }
+  int grid = 0;
+  r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags, values, probs, partials, &grid, s);
+  if (r) return r;
+  if (want) {
+    BX_CUDA(h, launch_summary_merge(partials, grid, space_dev(h), k, q,
+                                    h->d_summary.as<bx_score_summary>(), s));
+    BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
+                               cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));
+  }
+  return BX_OK;
+}
+
+int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t index_base,
+                  double f_model, double eps_f, int32_t k, int32_t flags,
+                  bx_score_summary* summary, void* stream) {
+  int r = check_gp(h);
+  if (r) return r;
+  if (q < 1) return fail(h, BX_ERR_ARG, "empty candidate pool");
+  if (!summary) return fail(h, BX_ERR_ARG, "bx_score_host needs a summary");
+  if (k < 0 || k > BX_MAX_K) return fail(h, BX_ERR_ARG, "k=%d outside [0, %d]", k, BX_MAX_K);
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = h->row_words;
+  const int64_t chunk = 1 << 18;
+  const int64_t n_chunks = (q + chunk - 1) / chunk;
+  const size_t per_chunk_partials = (size_t)h->sm_count * 8;
+  BX_CUDA(h, h->d_partials.ensure(sizeof(bx_score_summary) * per_chunk_partials * (size_t)n_chunks));
+  BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
+  for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
+  // merge the per-chunk partials as a compact list: record how many partials each chunk wrote
+  int total_partials = 0;
+  bx_score_summary* base = h->d_partials.as<bx_score_summary>();
+  BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
+  BX_CUDA(h, cudaEventRecord(h->ev_done[1], s));
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t off = c * chunk;
+    const int64_t len = (q - off) < chunk ? (q - off) : chunk;
+    // the copy into buffer b waits until the kernel that last read buffer b is done
+    BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
+    BX_CUDA(h, cudaMemcpyAsync(h->d_host_rows[b].p, host_rows + (size_t)off * W, (size_t)len * W * 4,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    BX_CUDA(h, cudaEventRecord(h->ev_copy[b], h->copy_stream));
+    BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
+    int grid = 0;
+    r = score_impl(h, h->d_host_rows[b].as<uint32_t>(), len, index_base + off, f_model, eps_f, k,
+                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total_partials, &grid, s);
+    if (r) return r;
+    total_partials += grid;
+    BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
+  }
+  BX_CUDA(h, launch_summary_merge(base, total_partials, space_dev(h), k, q,
+                                  h->d_summary.as<bx_score_summary>(), s));
+  BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
+                             cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  return BX_OK;
+}
+
+int bx_gp_predict(bx_handle* h, const uint32_t* rows, int64_t q, double* mean, double* var,
+                  void* stream) {
+  int r = check_gp(h);
+  if (r) return r;
+  if (q < 1) return BX_OK;
+  cudaSetDevice(h->device);
+  ScoreArgs a{};
+  a.space = space_dev(h);
+  a.gp = gp_dev(h);
+  a.evald = EvalSetDev{};
+  a.rows = rows;
+  a.q = q;
+  a.f_model = 0.0;
+  a.mean_out = mean;
+  a.var_out = var;
+  int grid = 0;
+  BX_CUDA(h, launch_score(a, h->sm_count, (cudaStream_t)stream, &grid));
+  return BX_OK;
+}
+
+int bx_rf_predict(bx_handle* h, const uint32_t* rows, int64_t q, int32_t flags, double* probs,
+                  void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (!h->has_forest) return fail(h, BX_ERR_STATE, "bx_set_forest has not been called");
+  if (q < 1) return BX_OK;
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->forest.has_trees) {
+    std::vector<double> c((size_t)q, h->forest.constant);
+    BX_CUDA(h, cudaMemcpyAsync(probs, c.data(), (size_t)q * 8, cudaMemcpyHostToDevice, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));
+    return BX_OK;
+  }
+  BX_CUDA(h, launch_rf(space_dev(h), h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
+                       probs, s));
+  return BX_OK;
+}
+
+int bx_neighbor_slots(bx_handle* h) { return (h && h->has_space) ? h->n_slots : -1; }
+
+int bx_neighbors(bx_handle* h, const uint32_t* rows, int32_t count, int32_t use_cot,
+                 uint32_t* out_rows, uint8_t* out_valid, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (use_cot && !h->has_cot) return fail(h, BX_ERR_STATE, "bx_set_cot has not been called");
+  cudaSetDevice(h->device);
+  BX_CUDA(h, launch_neighbors(space_dev(h), use_cot ? &h->cot : nullptr, rows, count, out_rows,
+                              out_valid, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_cot_contains(bx_handle* h, const uint32_t* rows, int64_t q, uint8_t* mask, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (!h->has_cot) return fail(h, BX_ERR_STATE, "bx_set_cot has not been called");
+  cudaSetDevice(h->device);
+  BX_CUDA(h, launch_cot_contains(space_dev(h), h->cot, rows, q, mask, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_constraints_eval(bx_handle* h, const uint32_t* rows, int64_t q, uint8_t* mask, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (!h->has_constraints) return fail(h, BX_ERR_STATE, "bx_set_constraints has not been called");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  BX_CUDA(h, cudaMemsetAsync(h->d_fault.p, 0, 4, s));
+  BX_CUDA(h, launch_constraints(space_dev(h), h->cons, rows, q, mask, s));
+  int fault = 0;
+  BX_CUDA(h, cudaMemcpyAsync(&fault, h->d_fault.p, 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  if (fault)
+    return fail(h, BX_ERR_UNSUPPORTED,
+                "constraint arithmetic left the exact int64/2^53 envelope of the device evaluator");
+  return BX_OK;
+}
+
+int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const double* z,
+                   const double* thetas, int32_t c, double* out, void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
+    return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
+  cudaSetDevice(h->device);
+  const size_t bytes = ((size_t)n * (n + 1) / 2 + n) * sizeof(double);
+  double* scratch = nullptr;
+  if (bytes > 200 * 1024) {
+    BX_CUDA(h, h->d_lml_scratch.ensure(lml_scratch_doubles(n, c) * sizeof(double)));
+    scratch = h->d_lml_scratch.as<double>();
+  }
+  BX_CUDA(h, launch_lml(sq, n, D, z, thetas, c, out, scratch, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_pairwise_sq(bx_handle* h, const uint32_t* a, int32_t qa, const uint32_t* b, int32_t qb,
+                   double* out, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  cudaSetDevice(h->device);
+  BX_CUDA(h, launch_pairwise_sq(space_dev(h), a, qa, b, qb, out, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+}  // extern "C"

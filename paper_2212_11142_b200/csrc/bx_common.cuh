@@ -1,0 +1,277 @@
+// bx_common.cuh — internal types and device helpers shared by the sm_100a kernels.
+//
+// Encoded rows, parameter descriptors and the handle's device-resident model state.  Every
+// helper cites the reference expression (file:line under /root/reference/pkg/src/boxtune) whose
+// value it reproduces.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/bx_sm100.h"
+
+namespace bx {
+
+constexpr int kRealGrid = 64;          // space.py:23 REAL_NEIGHBOR_GRID
+constexpr double kSqrt5 = 2.23606797749978969640917366873128;  // surrogate.py:35 math.sqrt(5.0)
+constexpr double kInvSqrt2Pi = 0.398942280401432702863218082712;  // acquisition.py:27
+
+// ---- device-resident state owned by a handle -------------------------------------------------
+
+struct SpaceDev {
+  const bx_param_desc* params;  // [n_params]
+  const double* coord_lut;      // coordinates per domain index / real grid point
+  const int32_t* rank_lut;      // categorical label rank (Python sort order)
+  const int32_t* feat_param;    // [n_features] parameter of each feature column
+  const int32_t* feat_sub;      // [n_features] sub-column (one-hot label / permutation element)
+  const int32_t* slot_param;    // [n_slots] neighbour slot -> parameter
+  const int32_t* slot_move;     // [n_slots] neighbour slot -> move id inside the parameter
+  int32_t n_params;
+  int32_t row_words;
+  int32_t n_features;
+  int32_t n_slots;
+};
+
+// Per-parameter training plane for the cross-covariance.  For numeric kinds plane[j] holds the
+// training coordinate divided by the lengthscale (double); categorical: domain index (as int64
+// in the same 8 bytes); permutation: packed u64.  Kendall additionally keeps the pair-order
+// masks (two u64 words for m <= 16).
+struct GpDev {
+  int32_t n;             // training points
+  int32_t ncols_pad;     // n rounded up to 4 (DMMA k-step)
+  int32_t rows_pad;      // (n + 1) rounded up to 16 (augmented rows: L^-1 then alpha)
+  int32_t lda;           // row stride of A (doubles)
+  const double* A;       // [rows_pad x lda]: rows 0..n-1 = L^-1 (lower), row n = alpha
+  const uint64_t* planes;   // [n_params x n] 8-byte training planes
+  const uint64_t* kmask;    // [n_params x n x 2] Kendall pair masks (only for Kendall params)
+  const double* inv_l;      // [n_params] 1 / lengthscale
+  const double* inv_l2;     // [n_params] 1 / lengthscale^2 (surrogate.py:222)
+  const double* disc_tab;   // discrete contribution tables: (raw / mx) / l^2 per raw value
+  const int32_t* disc_off;  // [n_params] offset of the parameter's table in disc_tab
+  double outputscale;
+  double y_mean, y_std;
+};
+
+// Forest nodes repacked breadth-first so that the two children of a node are adjacent.
+struct RfNode {
+  double thr;     // split threshold (internal) -- feasibility.py:86 `x <= threshold`
+  double val;     // feasible fraction stored at every node (feasibility.py:105)
+  int32_t feat;   // feature column, -1 for a leaf
+  int32_t child;  // index of the left child; right child = child + 1
+};
+
+struct ForestDev {
+  const RfNode* nodes;
+  const int32_t* roots;
+  int32_t n_trees;
+  int32_t max_depth;
+  int32_t has_trees;     // 0 -> constant model
+  double constant;       // single-class shortcut (feasibility.py:73-74)
+};
+
+struct EvalSetDev {
+  const uint32_t* rows;       // [count x row_words]
+  const int32_t* table;       // open-addressing hash table of row ids, -1 = empty
+  int32_t count;
+  int32_t table_mask;         // size - 1 (power of two)
+};
+
+struct CotDev {
+  int32_t n_groups;
+  const int32_t* group_kind;        // 0 tree, 1 real singleton, 2 permutation singleton
+  const int32_t* group_param_begin;
+  const int32_t* group_params;
+  const int32_t* group_root;
+  const int32_t* child_begin;   // first child node id
+  const int32_t* child_count;
+  const int32_t* node_value;    // domain index of the node's value
+};
+
+struct ConstraintDev {
+  int32_t n_constraints;
+  const int32_t* prog_begin;
+  const int32_t* code;
+  const double* consts;
+  const int32_t* vtag;      // per (param, domain index): 0 int, 1 float (ordinal value types)
+  const int64_t* vint;      // per (param, domain index) integer value
+  const double* vflt;       // per (param, domain index) float value
+  const int32_t* voff;      // [n_params] offset into the value tables
+  const int32_t* str_id;    // per (param, domain index) string id of categorical labels
+  int32_t* fault;           // set to 1 when a value leaves the exactly-representable envelope
+};
+
+// ---- row accessors ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t row_word(const uint32_t* row, int w) { return row[w]; }
+
+__device__ __forceinline__ double row_f64(const uint32_t* row, int w) {
+  uint64_t bits = (uint64_t)row[w] | ((uint64_t)row[w + 1] << 32);
+  return __longlong_as_double((long long)bits);
+}
+
+__device__ __forceinline__ uint64_t row_u64(const uint32_t* row, int w) {
+  return (uint64_t)row[w] | ((uint64_t)row[w + 1] << 32);
+}
+
+__device__ __forceinline__ void put_u64(uint32_t* row, int w, uint64_t v) {
+  row[w] = (uint32_t)v;
+  row[w + 1] = (uint32_t)(v >> 32);
+}
+
+__device__ __forceinline__ void put_f64(uint32_t* row, int w, double v) {
+  put_u64(row, w, (uint64_t)__double_as_longlong(v));
+}
+
+// element (minus one) at position i of a packed permutation of size m
+__device__ __forceinline__ int perm_at(uint64_t p, int m, int i) {
+  return (int)((p >> (4 * (m - 1 - i))) & 0xFull);
+}
+
+// position of element e (0-based, i.e. value e+1) -- feasibility.py:48 argsort of the values
+__device__ __forceinline__ int perm_pos(uint64_t p, int m, int e) {
+  uint64_t mask = (m >= 16) ? ~0ull : ((1ull << (4 * m)) - 1ull);
+  uint64_t y = (p ^ (0x1111111111111111ull * (uint64_t)e)) & mask;
+  uint64_t z = ~(y | (y >> 1) | (y >> 2) | (y >> 3)) & 0x1111111111111111ull & mask;
+  int bit = __ffsll((long long)z) - 1;
+  return m - 1 - (bit >> 2);
+}
+
+// Kendall pair-order masks: bit (i,j), i<j, set iff a_i < a_j (surrogate.py:213)
+__device__ __forceinline__ void kendall_mask(uint64_t p, int m, uint64_t& lo, uint64_t& hi) {
+  lo = 0; hi = 0;
+  int b = 0;
+  for (int i = 0; i < m; ++i) {
+    int ai = perm_at(p, m, i);
+    for (int j = i + 1; j < m; ++j, ++b) {
+      if (ai < perm_at(p, m, j)) {
+        if (b < 64) lo |= 1ull << b; else hi |= 1ull << (b - 64);
+      }
+    }
+  }
+}
+
+// raw (un-normalised) permutation semimetric between two packed permutations.
+// surrogate.py:201-218 (_perm_sq_distances) / 54-72 (scalar definitions)
+__device__ __forceinline__ int perm_raw(int metric, int m, uint64_t a, uint64_t b, uint64_t alo,
+                                        uint64_t ahi, uint64_t blo, uint64_t bhi) {
+  if (metric == BX_KENDALL) return __popcll(alo ^ blo) + __popcll(ahi ^ bhi);
+  if (metric == BX_NAIVE) return a != b ? 1 : 0;
+  if (metric == BX_HAMMING) {
+    uint64_t x = a ^ b;
+    uint64_t t = (x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x1111111111111111ull;
+    return __popcll(t);
+  }
+  int s = 0;  // spearman: sum of squared element differences
+  for (int i = 0; i < m; ++i) {
+    int d = perm_at(a, m, i) - perm_at(b, m, i);
+    s += d * d;
+  }
+  return s;
+}
+
+// numeric coordinate of parameter p in a row (surrogate.py:163-170 via host LUT)
+__device__ __forceinline__ double row_coord(const bx_param_desc& p, const double* coord_lut,
+                                            const uint32_t* row) {
+  if (p.kind == BX_REAL) return row_f64(row, p.word + 2);
+  return coord_lut[p.coord + (int)row[p.word]];
+}
+
+// Python tuple order of two encoded configurations (acquisition.py:91, :109-110):
+// returns -1, 0, 1.
+__device__ __forceinline__ int key_cmp(const bx_param_desc* params, int n_params,
+                                       const int32_t* rank_lut, const uint32_t* a,
+                                       const uint32_t* b) {
+  for (int k = 0; k < n_params; ++k) {
+    const bx_param_desc& p = params[k];
+    if (p.kind == BX_REAL) {
+      double x = row_f64(a, p.word), y = row_f64(b, p.word);
+      if (x < y) return -1;
+      if (x > y) return 1;
+    } else if (p.kind == BX_PERMUTATION) {
+      uint64_t x = row_u64(a, p.word), y = row_u64(b, p.word);
+      if (x < y) return -1;
+      if (x > y) return 1;
+    } else if (p.kind == BX_CATEGORICAL) {
+      int x = rank_lut[p.rank + (int)a[p.word]], y = rank_lut[p.rank + (int)b[p.word]];
+      if (x < y) return -1;
+      if (x > y) return 1;
+    } else {
+      uint32_t x = a[p.word], y = b[p.word];
+      if (x < y) return -1;
+      if (x > y) return 1;
+    }
+  }
+  return 0;
+}
+
+__device__ __forceinline__ uint64_t row_hash(const uint32_t* row, int words) {
+  uint64_t h = 1469598103934665603ull;
+  for (int w = 0; w < words; ++w) {
+    h ^= row[w];
+    h *= 1099511628211ull;
+    h ^= h >> 29;
+  }
+  return h;
+}
+
+__device__ __forceinline__ bool is_evaluated(const EvalSetDev& ev, const uint32_t* row, int words) {
+  if (ev.count == 0) return false;
+  uint64_t h = row_hash(row, words);
+  int slot = (int)(h & (uint64_t)ev.table_mask);
+  for (int probe = 0; probe <= ev.table_mask; ++probe) {
+    int id = ev.table[slot];
+    if (id < 0) return false;
+    const uint32_t* r = ev.rows + (size_t)id * words;
+    bool eq = true;
+    for (int w = 0; w < words; ++w) eq &= (r[w] == row[w]);
+    if (eq) return true;
+    slot = (slot + 1) & ev.table_mask;
+  }
+  return false;
+}
+
+// ---- launch helpers implemented in the .cu files -------------------------------------------
+
+struct ScoreArgs {
+  SpaceDev space;
+  GpDev gp;
+  ForestDev forest;
+  EvalSetDev evald;
+  const uint32_t* rows;
+  int64_t q;
+  int64_t index_base;
+  double f_model;
+  double eps_f;
+  int32_t k;
+  int32_t flags;
+  int32_t use_forest;
+  const double* probs_in;   // feasibility p from rf kernel (NULL without a forest)
+  double* values_out;       // optional
+  double* probs_out;        // optional
+  double* mean_out;         // optional (bx_gp_predict)
+  double* var_out;          // optional
+  bx_score_summary* partials;  // [gridDim.x] per-CTA summaries (NULL -> no summary)
+};
+
+cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* grid_used);
+cudaError_t launch_summary_merge(const bx_score_summary* partials, int n_partials,
+                                 const SpaceDev& space, int k, int64_t q,
+                                 bx_score_summary* out, cudaStream_t s);
+cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
+                      int pairwise, double* probs, cudaStream_t s);
+cudaError_t launch_neighbors(const SpaceDev& space, const CotDev* cot, const uint32_t* rows,
+                             int count, uint32_t* out_rows, uint8_t* out_valid, cudaStream_t s);
+cudaError_t launch_cot_contains(const SpaceDev& space, const CotDev& cot, const uint32_t* rows,
+                                int64_t q, uint8_t* mask, cudaStream_t s);
+cudaError_t launch_constraints(const SpaceDev& space, const ConstraintDev& c, const uint32_t* rows,
+                               int64_t q, uint8_t* mask, cudaStream_t s);
+cudaError_t launch_lml(const double* sq, int n, int D, const double* z, const double* thetas,
+                       int c, double* out, double* scratch, cudaStream_t s);
+cudaError_t launch_pairwise_sq(const SpaceDev& space, const uint32_t* a, int qa, const uint32_t* b,
+                               int qb, double* out, cudaStream_t s);
+cudaError_t launch_gp_planes(const SpaceDev& space, const uint32_t* train_rows, int n,
+                             const double* inv_l, uint64_t* planes, uint64_t* kmask,
+                             cudaStream_t s);
+cudaError_t launch_tri_inverse(const double* L, int n, double* A, int lda, cudaStream_t s);
+
+}  // namespace bx

@@ -1,0 +1,227 @@
+// gp_linalg.cu — once-per-iteration GP state and the batched coarse marginal likelihood.
+//
+//   gp_planes_kernel     training planes for the cross-covariance (surrogate.py:163-218)
+//   tri_inverse_kernel   L^-1 by column forward substitution (the TRSM of surrogate.py:323 done once)
+//   pairwise_sq_kernel   pairwise_sq_distances (surrogate.py:173-198), bit-exact
+//   lml_kernel           _batched_coarse_lml (surrogate.py:420-456): one CTA per hyperparameter
+//                        candidate, Gram build + right-looking Cholesky in shared memory (packed
+//                        lower triangle) or in an L2-resident global scratch when n is large,
+//                        -inf when a pivot is not positive (LAPACK potrf info > 0).
+#include "bx_common.cuh"
+
+namespace bx {
+
+namespace {
+
+__global__ void gp_planes_kernel(SpaceDev sp, const uint32_t* train, int n, const double* inv_l,
+                                 uint64_t* planes, uint64_t* kmask) {
+  const int64_t total = (int64_t)sp.n_params * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(t / n), j = (int)(t % n);
+    const bx_param_desc& p = sp.params[k];
+    const uint32_t* row = train + (size_t)j * sp.row_words;
+    uint64_t v;
+    if (p.kind == BX_PERMUTATION) {
+      v = row_u64(row, p.word);
+      uint64_t lo = 0, hi = 0;
+      if (p.metric == BX_KENDALL) kendall_mask(v, p.size, lo, hi);
+      kmask[((size_t)k * n + j) * 2] = lo;
+      kmask[((size_t)k * n + j) * 2 + 1] = hi;
+    } else if (p.kind == BX_CATEGORICAL) {
+      v = row[p.word];
+    } else {
+      v = (uint64_t)__double_as_longlong(row_coord(p, sp.coord_lut, row) * inv_l[k]);
+    }
+    planes[(size_t)k * n + j] = v;
+  }
+}
+
+__global__ void tri_inverse_kernel(const double* L, int n, double* A, int lda) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  A[(size_t)j * lda + j] = 1.0 / L[(size_t)j * n + j];
+  for (int i = j + 1; i < n; ++i) {
+    double s = 0.0;
+    const double* Li = L + (size_t)i * n;
+    for (int k = j; k < i; ++k) s = fma(Li[k], A[(size_t)k * lda + j], s);
+    A[(size_t)i * lda + j] = -s / Li[i];
+  }
+}
+
+__global__ void pairwise_sq_kernel(SpaceDev sp, const uint32_t* a, int qa, const uint32_t* b, int qb,
+                                   double* out) {
+  const int64_t total = (int64_t)qa * qb;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int ia = (int)(t / qb), ib = (int)(t % qb);
+    const uint32_t* ra = a + (size_t)ia * sp.row_words;
+    const uint32_t* rb = b + (size_t)ib * sp.row_words;
+    for (int k = 0; k < sp.n_params; ++k) {
+      const bx_param_desc& p = sp.params[k];
+      double v;
+      if (p.kind == BX_CATEGORICAL) {
+        v = ra[p.word] != rb[p.word] ? 1.0 : 0.0;  // surrogate.py:193
+      } else if (p.kind == BX_PERMUTATION) {
+        const uint64_t x = row_u64(ra, p.word), y = row_u64(rb, p.word);
+        uint64_t xl = 0, xh = 0, yl = 0, yh = 0;
+        if (p.metric == BX_KENDALL) {
+          kendall_mask(x, p.size, xl, xh);
+          kendall_mask(y, p.size, yl, yh);
+        }
+        const int raw = perm_raw(p.metric, p.size, x, y, xl, xh, yl, yh);
+        v = __ddiv_rn((double)raw, p.raw_mx);  // surrogate.py:218
+      } else {
+        const double d = __dsub_rn(row_coord(p, sp.coord_lut, ra), row_coord(p, sp.coord_lut, rb));
+        v = __dmul_rn(d, d);  // surrogate.py:187-188
+      }
+      out[((size_t)k * qa + ia) * qb + ib] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ size_t tri_idx(int i, int k) { return (size_t)i * (i + 1) / 2 + k; }
+
+constexpr int kLmlThreads = 256;
+
+// One CTA per hyperparameter candidate.
+__global__ void __launch_bounds__(kLmlThreads) lml_kernel(const double* sq, int n, int D,
+                                                          const double* z, const double* thetas,
+                                                          double* out, double* scratch,
+                                                          int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x;
+  const size_t tri = (size_t)n * (n + 1) / 2;
+  double* K = use_smem ? reinterpret_cast<double*>(smem_raw) : scratch + (size_t)c * (tri + n);
+  double* u = use_smem ? K + tri : scratch + (size_t)c * (tri + n) + tri;
+  __shared__ double inv_sq[BX_MAX_PARAMS];
+  __shared__ double red[kLmlThreads / 32];
+  __shared__ int failed;
+  const double* th = thetas + (size_t)c * (2 + D);
+  const double sigma = exp(th[0]);
+  const double noise = fmax(exp(th[1]), 1e-6);  // NOISE_FLOOR
+  for (int k = tid; k < D; k += blockDim.x) inv_sq[k] = exp(-2.0 * th[2 + k]);
+  if (tid == 0) failed = 0;
+  __syncthreads();
+
+  // Gram (lower triangle): sigma * (1 + sqrt5 d + 5/3 W) * exp(-sqrt5 d)   (surrogate.py:430-434)
+  for (size_t t = tid; t < tri; t += blockDim.x) {
+    int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (tri_idx(i + 1, 0) <= t) ++i;
+    while (tri_idx(i, 0) > t) --i;
+    const int k2 = (int)(t - tri_idx(i, 0));
+    double W = 0.0;
+    for (int k = 0; k < D; ++k) W = fma(sq[((size_t)k * n + i) * n + k2], inv_sq[k], W);
+    const double d = sqrt(fmax(W, 0.0));
+    double v = sigma * (1.0 + kSqrt5 * d + (5.0 / 3.0) * W) * exp(-kSqrt5 * d);
+    if (i == k2) v += noise + 1e-9;  // JITTER
+    K[t] = v;
+  }
+  for (int i = tid; i < n; i += blockDim.x) u[i] = z[i];
+  __syncthreads();
+
+  // right-looking Cholesky, lower
+  for (int j = 0; j < n; ++j) {
+    const double piv = K[tri_idx(j, j)];
+    if (!(piv > 0.0)) {  // potrf: ajj <= 0 or NaN -> info > 0
+      if (tid == 0) failed = 1;
+      break;
+    }
+    const double ljj = sqrt(piv);
+    __syncthreads();
+    if (tid == 0) K[tri_idx(j, j)] = ljj;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) K[tri_idx(i, j)] /= ljj;
+    __syncthreads();
+    const int m = n - j - 1;  // trailing size
+    const size_t work = (size_t)m * (m + 1) / 2;
+    for (size_t t = tid; t < work; t += blockDim.x) {
+      int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while (tri_idx(r + 1, 0) <= t) ++r;
+      while (tri_idx(r, 0) > t) --r;
+      const int cc = (int)(t - tri_idx(r, 0));
+      const int i = j + 1 + r, k = j + 1 + cc;
+      K[tri_idx(i, k)] -= K[tri_idx(i, j)] * K[tri_idx(k, j)];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (failed) {
+    if (tid == 0) out[c] = -INFINITY;
+    return;
+  }
+  // u = L^-1 z (column sweep)
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    const double uj = u[j] / K[tri_idx(j, j)];
+    __syncthreads();
+    if (tid == 0) u[j] = uj;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) u[i] -= K[tri_idx(i, j)] * uj;
+  }
+  __syncthreads();
+  double quad = 0.0, logdet = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    quad = fma(u[i], u[i], quad);
+    logdet += log(K[tri_idx(i, i)]);
+  }
+  for (int off = 16; off; off >>= 1) {
+    quad += __shfl_xor_sync(0xffffffffu, quad, off);
+    logdet += __shfl_xor_sync(0xffffffffu, logdet, off);
+  }
+  __shared__ double red2[kLmlThreads / 32];
+  if ((tid & 31) == 0) { red[tid >> 5] = quad; red2[tid >> 5] = logdet; }
+  __syncthreads();
+  if (tid == 0) {
+    double q = 0.0, l = 0.0;
+    for (int w = 0; w < kLmlThreads / 32; ++w) { q += red[w]; l += red2[w]; }
+    // surrogate.py:453-455
+    out[c] = -0.5 * q - 0.5 * (2.0 * l) - 0.5 * n * log(2.0 * 3.14159265358979323846);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+size_t lml_scratch_doubles(int n, int c) { return (size_t)c * ((size_t)n * (n + 1) / 2 + n); }
+
+cudaError_t launch_lml(const double* sq, int n, int D, const double* z, const double* thetas, int c,
+                       double* out, double* scratch, cudaStream_t s) {
+  if (c <= 0) return cudaSuccess;
+  const size_t bytes = ((size_t)n * (n + 1) / 2 + n) * sizeof(double);
+  const int use_smem = bytes <= 200 * 1024;
+  if (use_smem) {
+    cudaError_t e = cudaFuncSetAttribute(lml_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess) return e;
+  }
+  lml_kernel<<<c, kLmlThreads, use_smem ? bytes : 0, s>>>(sq, n, D, z, thetas, out, scratch, use_smem);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pairwise_sq(const SpaceDev& space, const uint32_t* a, int qa, const uint32_t* b,
+                               int qb, double* out, cudaStream_t s) {
+  if ((int64_t)qa * qb <= 0) return cudaSuccess;
+  pairwise_sq_kernel<<<grid_for((int64_t)qa * qb, 256), 256, 0, s>>>(space, a, qa, b, qb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gp_planes(const SpaceDev& space, const uint32_t* train_rows, int n,
+                             const double* inv_l, uint64_t* planes, uint64_t* kmask,
+                             cudaStream_t s) {
+  gp_planes_kernel<<<grid_for((int64_t)space.n_params * n, 256), 256, 0, s>>>(
+      space, train_rows, n, inv_l, planes, kmask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tri_inverse(const double* L, int n, double* A, int lda, cudaStream_t s) {
+  tri_inverse_kernel<<<(n + 63) / 64, 64, 0, s>>>(L, n, A, lda);
+  return cudaGetLastError();
+}
+
+}  // namespace bx

@@ -1,0 +1,293 @@
+"""Device-resident acquisition state and typed wrappers around every libbx_sm100 entry point.
+
+`Scorer` owns one native handle on one CUDA device.  It uploads the per-iteration model state
+(space tables, GP posterior, forest, evaluated set, chain of trees, constraint bytecode) and runs
+the hot-path kernels on torch-allocated device buffers, on torch's current stream.  All model
+objects are read through the attributes the reference defines, so the reference's own `GPModel`,
+`FeasibilityModel`, `ChainOfTrees` and `SearchSpace` are accepted as they are.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .constraints import Program, flatten_cot
+from .layout import SpaceLayout
+
+
+def _ptr(a) -> C.c_void_p:
+    if isinstance(a, torch.Tensor):
+        return C.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    if a is None:
+        return C.c_void_p(0)
+    return C.c_void_p(a)
+
+
+def _host(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype))
+
+
+@dataclass
+class Candidate:
+    value: float
+    prob: float
+    index: int
+    row: np.ndarray  # uint32 [row_words]
+
+
+@dataclass
+class Summary:
+    n_scored: int
+    n_finite: int
+    top: list          # [Candidate], stable argsort(-values)[:k] with -inf excluded
+    best: Candidate | None       # tracker over values (unevaluated, finite)
+    best_prob: Candidate | None  # tracker over probabilities (unevaluated)
+
+
+def _cand(c: N.Cand, words: int) -> Candidate | None:
+    if c.index < 0:
+        return None
+    return Candidate(float(c.value), float(c.prob), int(c.index),
+                     np.ctypeslib.as_array(c.row)[:words].copy())
+
+
+class Scorer:
+    """One device's worth of acquisition state."""
+
+    def __init__(self, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2212_11142_b200 needs a CUDA device (there is no CPU path)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._lib = N.lib()
+        with torch.cuda.device(self.device):
+            h = self._lib.bx_create(self.device)
+        if not h:
+            raise RuntimeError(f"bx_create({self.device}) failed")
+        self.h = C.c_void_p(h)
+        self.layout: SpaceLayout | None = None
+        self._space_key = None
+        self.has_forest = False
+        self.n_slots = 0
+        self.space_gen = 0  # bumped whenever the space tables (and so every model upload) change
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.bx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers --------------------------------------------------------------------------------
+    def _check(self, code):
+        N.check(self.h, code)
+
+    @property
+    def stream(self) -> C.c_void_p:
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def to_device(self, rows: np.ndarray) -> torch.Tensor:
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        t = torch.from_numpy(rows.view(np.int32))
+        return t.to(f"cuda:{self.device}", non_blocking=False)
+
+    # -- model state ----------------------------------------------------------------------------
+    def layout_for(self, space) -> SpaceLayout:
+        """The resident layout when it already describes `space`, else a fresh upload."""
+        if self.layout is not None and self.layout.space is space:
+            return self.layout
+        return self.set_space(space, True)
+
+    def set_space(self, space, use_transforms: bool = True) -> SpaceLayout:
+        key = (id(space), bool(use_transforms))
+        if self._space_key == key and self.layout is not None and self.layout.space is space:
+            return self.layout
+        lay = SpaceLayout(space, use_transforms)
+        self._check(self._lib.bx_set_space(self.h, C.cast(lay.params, C.c_void_p), lay.n_params,
+                                           lay.row_words, _ptr(lay.coord_lut), len(lay.coord_lut),
+                                           _ptr(lay.rank_lut), len(lay.rank_lut), lay.n_features))
+        self.layout = lay
+        self._space_key = key
+        self.space_gen += 1
+        self.n_slots = self._lib.bx_neighbor_slots(self.h)
+        self._cot_key = None
+        self._cons_key = None
+        return lay
+
+    def set_gp(self, gp):
+        """Upload a GPModel (reference surrogate.py:264-332, or GPState) - L, alpha, encodings."""
+        lay = self.set_space(gp.space, getattr(gp, "use_transforms", True))
+        rows = lay.encode(gp.configs)
+        L = np.tril(np.asarray(gp._cho[0], dtype=np.float64))  # upper triangle is stale K (:300)
+        L = np.ascontiguousarray(L)
+        alpha = _host(gp.alpha, np.float64)
+        h = gp.hyperparameters
+        ls = _host(h.lengthscales, np.float64)
+        self._check(self._lib.bx_set_gp(self.h, _ptr(rows), len(rows), _ptr(L), _ptr(alpha),
+                                        float(h.outputscale), _ptr(ls), float(gp.y_mean),
+                                        float(gp.y_std), self.stream))
+        self.gp = gp
+
+    def set_forest(self, feas):
+        """Upload a FeasibilityModel (feasibility.py:54-71) or clear it (None)."""
+        if feas is None:
+            self._check(self._lib.bx_clear_forest(self.h))
+            self.has_forest = False
+            return
+        if feas.constant is not None:
+            self._check(self._lib.bx_set_forest(self.h, None, None, None, None, None, 0, None, 0,
+                                                int(feas.max_depth), float(feas.constant)))
+            self.has_forest = True
+            return
+        if feas.roots is None or len(feas.roots) == 0:
+            raise N.NativeError(N.BX_ERR_NO_TREES, "feasibility model has no trees")
+        f = _host(feas.feature, np.int32)
+        t = _host(feas.threshold, np.float64)
+        lft = _host(feas.left, np.int32)
+        rgt = _host(feas.right, np.int32)
+        v = _host(feas.value, np.float64)
+        roots = _host(feas.roots, np.int32)
+        self._check(self._lib.bx_set_forest(self.h, _ptr(f), _ptr(t), _ptr(lft), _ptr(rgt), _ptr(v),
+                                            len(f), _ptr(roots), len(roots), int(feas.max_depth),
+                                            float("nan")))
+        self.has_forest = True
+
+    def set_evaluated(self, configs):
+        configs = list(configs)
+        rows = self.layout.encode(configs) if configs else np.zeros((0, self.layout.row_words), np.uint32)
+        self._check(self._lib.bx_set_evaluated(self.h, _ptr(rows), len(rows)))
+
+    def set_evaluated_rows(self, rows: np.ndarray):
+        rows = np.ascontiguousarray(rows, np.uint32)
+        self._check(self._lib.bx_set_evaluated(self.h, _ptr(rows), len(rows)))
+
+    def set_cot(self, cot):
+        key = id(cot)
+        if getattr(self, "_cot_key", None) == key:
+            return
+        t = flatten_cot(cot, self.layout)
+        self._check(self._lib.bx_set_cot(self.h, t.n_groups, _ptr(t.group_kind),
+                                         _ptr(t.group_param_begin), _ptr(t.group_params),
+                                         _ptr(t.group_root), t.n_nodes, _ptr(t.child_begin),
+                                         _ptr(t.child_count), _ptr(t.node_value)))
+        self._cot_tables = t
+        self._cot_key = key
+
+    def set_constraints(self, space):
+        key = id(space)
+        if getattr(self, "_cons_key", None) == key:
+            return
+        p = Program(space, self.layout)
+        self._check(self._lib.bx_set_constraints(
+            self.h, p.n, _ptr(p.prog_begin), _ptr(p.code), p.code_len, _ptr(p.consts_arr),
+            len(p.consts), _ptr(p.value_tag), _ptr(p.value_int), _ptr(p.value_float),
+            _ptr(p.value_str), p.n_values))
+        self._program = p
+        self._cons_key = key
+
+    # -- hot path -------------------------------------------------------------------------------
+    def _summary(self, s: N.ScoreSummary) -> Summary:
+        w = self.layout.row_words
+        top = [_cand(s.top[i], w) for i in range(s.n_top)]
+        return Summary(int(s.n_scored), int(s.n_finite), top, _cand(s.best, w), _cand(s.best_prob, w))
+
+    def score(self, rows: torch.Tensor, f_model: float, eps_f: float = 0.0, k: int = 10,
+              want_values: bool = False, summary: bool = True, rf_pairwise: bool | None = None,
+              index_base: int = 0):
+        """bx_score over device rows.  Returns (Summary | None, values | None, probs | None)."""
+        q = rows.shape[0]
+        flags = 0
+        if rf_pairwise if rf_pairwise is not None else q == 1:
+            flags |= N.BX_SCORE_RF_PAIRWISE
+        if not summary:
+            flags |= N.BX_SCORE_NO_SUMMARY
+        values = probs = None
+        if want_values:
+            values = torch.empty(q, dtype=torch.float64, device=rows.device)
+            probs = torch.empty(q, dtype=torch.float64, device=rows.device)
+        s = N.ScoreSummary()
+        self._check(self._lib.bx_score(self.h, _ptr(rows), q, index_base, float(f_model), float(eps_f),
+                                       int(k), flags, _ptr(values), _ptr(probs),
+                                       C.byref(s) if summary else None, self.stream))
+        return (self._summary(s) if summary else None), values, probs
+
+    def score_host(self, rows: np.ndarray | torch.Tensor, f_model: float, eps_f: float = 0.0,
+                   k: int = 10, index_base: int = 0) -> Summary:
+        """bx_score_host: the pool stays in (pinned) host memory; copies overlap the scoring."""
+        q = rows.shape[0]
+        s = N.ScoreSummary()
+        self._check(self._lib.bx_score_host(self.h, _ptr(rows), q, index_base, float(f_model),
+                                            float(eps_f), int(k), 0, C.byref(s), self.stream))
+        return self._summary(s)
+
+    def predict(self, rows: torch.Tensor):
+        q = rows.shape[0]
+        mean = torch.empty(q, dtype=torch.float64, device=rows.device)
+        var = torch.empty(q, dtype=torch.float64, device=rows.device)
+        self._check(self._lib.bx_gp_predict(self.h, _ptr(rows), q, _ptr(mean), _ptr(var), self.stream))
+        return mean, var
+
+    def rf_predict(self, rows: torch.Tensor, pairwise: bool | None = None):
+        q = rows.shape[0]
+        probs = torch.empty(q, dtype=torch.float64, device=rows.device)
+        pw = (q == 1) if pairwise is None else pairwise
+        self._check(self._lib.bx_rf_predict(self.h, _ptr(rows), q, N.BX_SCORE_RF_PAIRWISE if pw else 0,
+                                            _ptr(probs), self.stream))
+        return probs
+
+    def neighbors(self, rows: torch.Tensor, use_cot: bool):
+        count = rows.shape[0]
+        w = self.layout.row_words
+        out = torch.empty((count * self.n_slots, w), dtype=torch.int32, device=rows.device)
+        valid = torch.empty(count * self.n_slots, dtype=torch.uint8, device=rows.device)
+        self._check(self._lib.bx_neighbors(self.h, _ptr(rows), count, int(bool(use_cot)), _ptr(out),
+                                           _ptr(valid), self.stream))
+        return out, valid
+
+    def cot_contains(self, rows: torch.Tensor) -> torch.Tensor:
+        mask = torch.empty(rows.shape[0], dtype=torch.uint8, device=rows.device)
+        self._check(self._lib.bx_cot_contains(self.h, _ptr(rows), rows.shape[0], _ptr(mask), self.stream))
+        return mask
+
+    def constraints_eval(self, rows: torch.Tensor) -> torch.Tensor:
+        mask = torch.empty(rows.shape[0], dtype=torch.uint8, device=rows.device)
+        self._check(self._lib.bx_constraints_eval(self.h, _ptr(rows), rows.shape[0], _ptr(mask),
+                                                  self.stream))
+        return mask
+
+    def pairwise_sq(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.layout.n_params, a.shape[0], b.shape[0]), dtype=torch.float64,
+                          device=a.device)
+        self._check(self._lib.bx_pairwise_sq(self.h, _ptr(a), a.shape[0], _ptr(b), b.shape[0],
+                                             _ptr(out), self.stream))
+        return out
+
+    def lml_batched(self, sq: torch.Tensor, z: torch.Tensor, thetas: torch.Tensor) -> torch.Tensor:
+        D, n, _ = sq.shape
+        c = thetas.shape[0]
+        out = torch.empty(c, dtype=torch.float64, device=sq.device)
+        self._check(self._lib.bx_lml_batched(self.h, _ptr(sq.contiguous()), n, D, _ptr(z.contiguous()),
+                                             _ptr(thetas.contiguous()), c, _ptr(out), self.stream))
+        return out
+
+
+_SCORERS: dict = {}
+
+
+def scorer(device: int | None = None) -> Scorer:
+    """Process-wide Scorer per device (one handle per device, reused across iterations)."""
+    dev = torch.cuda.current_device() if device is None else int(device)
+    s = _SCORERS.get(dev)
+    if s is None:
+        s = _SCORERS[dev] = Scorer(dev)
+    return s

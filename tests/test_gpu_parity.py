@@ -1,0 +1,158 @@
+"""GPU parity: libbx_sm100 through the package API vs the reference's golden outputs and the oracle.
+
+Bars (BASELINE.json north_star): bit-exact for forest probabilities, neighbour sets, chain-of-trees
+and constraint masks and pairwise distances; mean / variance / EI within 1e-5 relative (with an
+absolute floor of 1e-9 x the largest magnitude, because standardised quantities cross zero);
+identical selected configuration.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from golden_io import CASES, TRACES, Ctx, cot_for, load, model, oracle_model, to_cfg
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+def close(got, want, rtol=RTOL, floor=1e-9):
+    got, want = np.asarray(got), np.asarray(want)
+    atol = floor * max(float(np.max(np.abs(want))), 1e-300)
+    np.testing.assert_allclose(got, want, rtol=rtol, atol=atol)
+
+
+@pytest.fixture(scope="module")
+def sc():
+    from paper_2212_11142_b200.device import scorer
+    return scorer()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_predict(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    gp, _ = model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"]]
+    mean, var = A.predict_batch(gp, cands)
+    close(mean, arr["mean"])
+    close(var, arr["var"])
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_scores(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    gp, feas = model(meta, arr, space)
+    ctx = Ctx(gp, feas, meta["f_best"], meta["eps_f"])
+    cands = [to_cfg(space, c) for c in meta["cands"]]
+    values, probs = A.scores(ctx, cands)
+    assert np.array_equal(probs, arr["probs"])
+    assert np.array_equal(np.isneginf(values), np.isneginf(arr["values"]))
+    fin = np.isfinite(arr["values"])
+    close(values[fin], arr["values"][fin])
+
+
+@pytest.mark.parametrize("case", ["mixed_fit", "mixed_metrics", "C3", "C4"])
+def test_forest_bit_exact(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    _, feas = model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"]]
+    assert np.array_equal(A.predict_proba_batch(feas, cands), arr["probs"])
+    single = np.array([A.predict_proba_batch(feas, [c])[0] for c in cands[:64]])
+    assert np.array_equal(single, arr["probs_q1"])
+    lay = sc.layout
+    assert np.array_equal(lay.features(lay.encode(cands[:256])), arr["rf_X"])
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_neighbors(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    cot = cot_for(case)
+    for start, plain in zip(meta["nbr_starts"], meta["nbr_plain"]):
+        assert A.neighbors(space, to_cfg(space, start)) == [to_cfg(space, c) for c in plain]
+    if cot is not None:
+        for start, filt in zip(meta["nbr_starts"], meta["nbr_cot"]):
+            assert A.neighbors(space, to_cfg(space, start), cot) == [to_cfg(space, c) for c in filt]
+
+
+@pytest.mark.parametrize("case", ["C2", "C3"])
+def test_masks(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    cot = cot_for(case)
+    probe = [to_cfg(space, c) for c in meta["cot_probe"]]
+    assert np.array_equal(A.contains_batch(cot, probe), arr["cot_mask"])
+    assert np.array_equal(A.constraints_batch(space, probe), arr["cons_mask"].all(1))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_pairwise_and_lml(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    og, _ = oracle_model(meta, arr, space)
+    lay = sc.set_space(space, meta["use_transforms"])
+    rows = sc.to_device(lay.encode(og.configs))
+    sq = sc.pairwise_sq(rows, rows).cpu().numpy()
+    assert np.array_equal(sq, oracle.pairwise_sq(space, og.configs, og.configs, og.use_transforms))
+    assert np.array_equal(sq[:, :16, :16], arr["sq_train_head"])
+    lml = A.batched_coarse_lml(sq, arr["lml_z"], arr["lml_thetas"])
+    want = arr["lml"]
+    assert np.array_equal(np.isfinite(lml), np.isfinite(want))
+    fin = np.isfinite(want)
+    np.testing.assert_allclose(lml[fin], want[fin], rtol=1e-9, atol=1e-7)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_summary_consistent_with_values(case, sc):
+    """Fused top-k / tracker reductions equal the host reductions over the same values."""
+    meta, arr, space = load(case)
+    gp, feas = model(meta, arr, space)
+    sc.set_gp(gp)
+    sc.set_forest(feas)
+    ev = {to_cfg(space, c) for c in meta["evaluated"]}
+    sc.set_evaluated(list(ev))
+    cands = [to_cfg(space, c) for c in meta["cands"]]
+    rows = sc.to_device(sc.layout.encode(cands))
+    f_model = gp.objective_to_model(meta["f_best"])
+    summ, values, probs = sc.score(rows, f_model, meta["eps_f"], k=10, want_values=True)
+    v = values.cpu().numpy()
+    order = [i for i in np.argsort(-v, kind="stable")[:10] if v[i] != -np.inf]
+    assert [c.index for c in summ.top] == order
+    assert summ.n_finite == int(np.sum(v != -np.inf))
+    best = None
+    for i, c in enumerate(cands):
+        if v[i] == -np.inf or c in ev:
+            continue
+        if best is None or v[i] > v[best] or (v[i] == v[best] and c < cands[best]):
+            best = i
+    assert (summ.best.index if summ.best else None) == best
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "C3"])
+def test_selection(case, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(case)
+    gp, feas = model(meta, arr, space)
+    pool = [to_cfg(space, c) for c in meta["sel_pool"]]
+    ev = {to_cfg(space, c) for c in meta["evaluated"]}
+    ctx = Ctx(gp, feas, meta["f_best"], meta["eps_f"], np.random.default_rng(0), ev)
+    got = A.optimize_acquisition(ctx, space, cot_for(case), sample_fn=lambda n, r: pool)
+    assert got == to_cfg(space, meta["sel_chosen"])
+
+
+@pytest.mark.parametrize("trace", TRACES)
+def test_engine_trace(trace, sc):
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load(trace)
+    cot = cot_for(trace)
+    for i, it in enumerate(meta["iters"]):
+        gp, feas = model(it, arr, space, prefix=f"it{i}_")
+        pool = [to_cfg(space, c) for c in it["pool"]]
+        ev = {to_cfg(space, c) for c in it["evaluated"]}
+        ctx = Ctx(gp, feas, it["f_best"], it["eps_f"], np.random.default_rng(0), ev)
+        got = A.optimize_acquisition(ctx, space, cot, sample_fn=lambda n, r, pool=pool: pool)
+        assert got == to_cfg(space, it["chosen"]), f"iteration {i}"
