@@ -173,8 +173,17 @@ int bx_set_constraints(bx_handle* h, int32_t n_constraints, const int32_t* host_
 /* ---- hot path --------------------------------------------------------------------------- */
 enum bx_score_flags {
   BX_SCORE_RF_PAIRWISE = 1,   /* numpy pairwise-8 tree sum (what predict_proba does at q == 1) */
-  BX_SCORE_NO_SUMMARY = 2     /* skip the top-k / tracker reduction                             */
+  BX_SCORE_NO_SUMMARY = 2,    /* skip the top-k / tracker reduction                             */
+  BX_SCORE_TIMING = 4         /* record per-kernel CUDA-event durations (bx_last_timing)        */
 };
+
+/* Durations (ms, CUDA events on the call's stream) of the forest, fused-score and merge kernels
+   of the last bx_score call made with BX_SCORE_TIMING. */
+int bx_last_timing(bx_handle* h, float* rf_ms, float* score_ms, float* merge_ms);
+
+/* Diagnostic (no reference counterpart): measured FP64 peaks of the DFMA pipe and of the DMMA
+   m8n8k4 tensor path on `device`, in TFLOP/s - the roofline denominator of the contraction. */
+int bx_probe_fp64(int device, double* dfma_tflops, double* dmma_tflops);
 
 /* Score dev_rows[0..q) (encoded, device).  f_model = objective_to_model(best feasible value);
    eps_f = feasibility limit.  Writes values/probs when non-NULL (device, q doubles each) and,

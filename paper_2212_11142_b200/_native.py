@@ -29,8 +29,9 @@ EXPORTED = (
     "bx_set_space", "bx_set_gp", "bx_set_forest", "bx_clear_forest", "bx_set_evaluated",
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_cot_contains",
-    "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq",
+    "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64",
 )
+BX_SCORE_TIMING = 4
 
 
 class ParamDesc(C.Structure):
@@ -86,6 +87,8 @@ _SIGS = {
     "bx_constraints_eval": (C.c_int, [_p, _p, _i64, _p, _p]),
     "bx_lml_batched": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _p, _p]),
     "bx_pairwise_sq": (C.c_int, [_p, _p, _i32, _p, _i32, _p, _p]),
+    "bx_last_timing": (C.c_int, [_p, _p, _p, _p]),
+    "bx_probe_fp64": (C.c_int, [C.c_int, _p, _p]),
 }
 
 

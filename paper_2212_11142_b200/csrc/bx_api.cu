@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -10,7 +11,7 @@
 #include "bx_common.cuh"
 
 namespace bx {
-int score_smem_bytes(int cpw, int ncols, int n_params, int row_words);
+int score_max_partials(int sm_count);
 size_t lml_scratch_doubles(int n, int c);
 }  // namespace bx
 
@@ -59,7 +60,10 @@ struct bx_handle {
   // forest
   bool has_forest = false;
   ForestDev forest{};
-  DevBuf d_nodes, d_roots;
+  DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_real_thr, d_code_param, d_code_sub;
+  bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
+  std::vector<int32_t> feat_param_host, feat_sub_host;
+  std::vector<double> coord_host;
   // evaluated
   int ev_count = 0, ev_mask = 0;
   DevBuf d_ev_rows, d_ev_table;
@@ -75,6 +79,8 @@ struct bx_handle {
   DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[2];
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // rf / score / merge timing
+  float t_ms[3] = {0, 0, 0};
 };
 
 namespace {
@@ -173,6 +179,9 @@ int check_gp(bx_handle* h) {
 
 }  // namespace
 
+static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
+                              const std::vector<int32_t>& roots, int max_depth);
+
 extern "C" {
 
 int bx_abi_version(void) { return BX_ABI_VERSION; }
@@ -182,12 +191,15 @@ bx_handle* bx_create(int device) {
   bx_handle* h = new (std::nothrow) bx_handle();
   if (!h) return nullptr;
   h->device = device;
+  const char* generic = getenv("BX_FOREST_GENERIC");
+  h->no_coded_forest = generic && generic[0] == '1';
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
   }
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&h->ev_t[i]);
   return h;
 }
 
@@ -202,13 +214,16 @@ void bx_destroy(bx_handle* h) {
                     &h->d_child_begin, &h->d_child_count, &h->d_child_value, &h->d_prog_begin, &h->d_code,
                     &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
-                    &h->d_host_rows[0], &h->d_host_rows[1]};
+                    &h->d_host_rows[0], &h->d_host_rows[1], &h->d_cnodes, &h->d_leaf_val,
+                    &h->d_real_thr, &h->d_code_param, &h->d_code_sub};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
     if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
   }
+  for (int i = 0; i < 4; ++i)
+    if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
   delete h;
 }
 
@@ -260,6 +275,9 @@ int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, in
   BX_CUDA(h, upload(h->d_slot_param, sparam.data(), sparam.size()));
   BX_CUDA(h, upload(h->d_slot_move, smove.data(), smove.size()));
   h->params.assign(params, params + n_params);
+  h->feat_param_host = fparam;
+  h->feat_sub_host = fsub;
+  h->coord_host.assign(coord_lut, coord_lut + coord_len);
   h->rank_host.assign(rank_lut, rank_lut + rank_len);
   h->n_params = n_params;
   h->row_words = row_words;
@@ -389,9 +407,111 @@ int bx_set_forest(bx_handle* h, const int32_t* feature, const double* threshold,
   h->forest.max_depth = max_depth;
   h->forest.has_trees = 1;
   h->forest.constant = 0.0;
+  h->forest.coded = 0;
   h->has_forest = true;
+  if (!h->no_coded_forest) {
+    r = build_coded_forest(h, nodes, new_roots, max_depth);
+    if (r) return r;
+  }
   return BX_OK;
 }
+
+// Integer-coded node table for rf_coded_kernel (see CodedForestDev).  Falls back to the generic
+// kernel (coded = 0) whenever an assumption does not hold: a leaf deeper than max_depth, a
+// non-monotone coordinate table, or a field overflow.
+}  // extern "C"
+
+static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
+                              const std::vector<int32_t>& roots, int max_depth) {
+  const int D = h->n_params;
+  std::vector<int32_t> slot_base(D), code_param, code_sub;
+  for (int k = 0; k < D; ++k) {
+    const bx_param_desc& p = h->params[k];
+    slot_base[k] = (int)code_param.size();
+    const int cnt = p.kind == BX_PERMUTATION ? p.size : 1;
+    for (int e = 0; e < cnt; ++e) {
+      code_param.push_back(k);
+      code_sub.push_back(e);
+    }
+    if (p.kind == BX_INTEGER || p.kind == BX_ORDINAL)
+      for (int i = 1; i < p.size; ++i)
+        if (!(h->coord_host[p.coord + i - 1] <= h->coord_host[p.coord + i])) return BX_OK;
+  }
+  if ((int)code_param.size() > 64) return BX_OK;
+  // depth of every node (breadth-first layout: children after parents)
+  std::vector<int> depth(nodes.size(), -1);
+  for (int32_t r : roots) depth[r] = 0;
+  for (size_t u = 0; u < nodes.size(); ++u) {
+    if (depth[u] < 0) return BX_OK;
+    if (nodes[u].feat >= 0) {
+      if (depth[u] + 1 > max_depth) return BX_OK;  // traversal would stop on an internal node
+      depth[nodes[u].child] = depth[nodes[u].child + 1] = depth[u] + 1;
+    }
+  }
+  std::vector<uint64_t> coded(nodes.size());
+  std::vector<double> leaf_val, real_thr;
+  for (size_t u = 0; u < nodes.size(); ++u) {
+    const RfNode& nd = nodes[u];
+    uint64_t type, slot = 0, arg;
+    if (nd.feat < 0) {
+      type = 0;
+      arg = leaf_val.size();
+      leaf_val.push_back(nd.val);
+    } else {
+      const int k = h->feat_param_host[nd.feat], sub = h->feat_sub_host[nd.feat];
+      const bx_param_desc& p = h->params[k];
+      const double t = nd.thr;
+      if (p.kind == BX_REAL) {
+        type = 3;
+        slot = slot_base[k];
+        arg = real_thr.size();
+        real_thr.push_back(t);
+      } else if (p.kind == BX_CATEGORICAL) {
+        type = 2;
+        slot = slot_base[k];
+        if (sub >= (1 << 22)) return BX_OK;
+        arg = (uint64_t)sub | ((uint64_t)(1.0 <= t) << 22) | ((uint64_t)(0.0 <= t) << 23);
+      } else {
+        type = 1;
+        int cut1 = 0;  // number of codes whose feature value is <= t
+        if (p.kind == BX_PERMUTATION) {
+          slot = slot_base[k] + sub;
+          for (int i = 0; i < p.size; ++i) cut1 += ((double)i <= t) ? 1 : 0;
+        } else {
+          slot = slot_base[k];
+          for (int i = 0; i < p.size; ++i) cut1 += (h->coord_host[p.coord + i] <= t) ? 1 : 0;
+        }
+        arg = (uint64_t)cut1;
+      }
+    }
+    if (arg >= (1u << 24) || nd.child < -1) return BX_OK;
+    const uint64_t child = nd.feat < 0 ? 0 : (uint64_t)(uint32_t)nd.child;
+    coded[u] = type | (slot << 2) | (arg << 8) | (child << 32);
+  }
+  if (leaf_val.empty()) leaf_val.push_back(0.0);
+  if (real_thr.empty()) real_thr.push_back(0.0);
+  BX_CUDA(h, upload(h->d_cnodes, coded.data(), coded.size()));
+  BX_CUDA(h, upload(h->d_leaf_val, leaf_val.data(), leaf_val.size()));
+  BX_CUDA(h, upload(h->d_real_thr, real_thr.data(), real_thr.size()));
+  BX_CUDA(h, upload(h->d_code_param, code_param.data(), code_param.size()));
+  BX_CUDA(h, upload(h->d_code_sub, code_sub.data(), code_sub.size()));
+  CodedForestDev& cf = h->forest.cf;
+  cf.nodes = h->d_cnodes.as<uint64_t>();
+  cf.leaf_val = h->d_leaf_val.as<double>();
+  cf.real_thr = h->d_real_thr.as<double>();
+  cf.roots = h->forest.roots;
+  cf.code_param = h->d_code_param.as<int32_t>();
+  cf.code_sub = h->d_code_sub.as<int32_t>();
+  cf.n_nodes = (int)coded.size();
+  cf.n_codes = (int)code_param.size();
+  cf.n_trees = h->forest.n_trees;
+  cf.max_depth = max_depth;
+  cf.nodes_in_smem = coded.size() * 8 <= 160 * 1024 ? 1 : 0;
+  h->forest.coded = 1;
+  return BX_OK;
+}
+
+extern "C" {
 
 int bx_clear_forest(bx_handle* h) {
   if (!h) return BX_ERR_ARG;
@@ -519,8 +639,8 @@ int bx_set_constraints(bx_handle* h, int32_t n_constraints, const int32_t* prog_
 
 static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
                       double f_model, double eps_f, int32_t k, int32_t flags, double* values,
-                      double* probs_out, bx_score_summary* partials, int* grid_used,
-                      cudaStream_t s) {
+                      double* probs_out, Partial* partials, int* n_partials, cudaStream_t s,
+                      bool timing) {
   ScoreArgs a{};
   a.space = space_dev(h);
   a.gp = gp_dev(h);
@@ -537,13 +657,16 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   a.values_out = values;
   a.probs_out = probs_out;
   a.partials = partials;
+  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
   if (h->has_forest && h->forest.has_trees) {
     BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
     BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                          h->d_probs.as<double>(), s));
     a.probs_in = h->d_probs.as<double>();
   }
-  BX_CUDA(h, launch_score(a, h->sm_count, s, grid_used));
+  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+  BX_CUDA(h, launch_score(a, h->sm_count, s, n_partials));
+  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
   return BX_OK;
 }
 
@@ -557,22 +680,40 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool want = !(flags & BX_SCORE_NO_SUMMARY) && summary != nullptr;
-  bx_score_summary* partials = nullptr;
+  const bool timing = (flags & BX_SCORE_TIMING) != 0;
+  Partial* partials = nullptr;
   if (want) {
-    BX_CUDA(h, h->d_partials.ensure(sizeof(bx_score_summary) * (size_t)h->sm_count * 8));
+    BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)score_max_partials(h->sm_count)));
     BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
-    partials = h->d_partials.as<bx_score_summary>();
+    partials = h->d_partials.as<Partial>();
   }
-  int grid = 0;
-  r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags, values, probs, partials, &grid, s);
+  int np = 0;
+  r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags, values, probs, partials, &np, s,
+                 timing);
   if (r) return r;
   if (want) {
-    BX_CUDA(h, launch_summary_merge(partials, grid, space_dev(h), k, q,
+    BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                                cudaMemcpyDeviceToHost, s));
-    BX_CUDA(h, cudaStreamSynchronize(s));
+  } else if (timing) {
+    BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
   }
+  if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
+  if (timing) {
+    cudaEventElapsedTime(&h->t_ms[0], h->ev_t[0], h->ev_t[1]);
+    cudaEventElapsedTime(&h->t_ms[1], h->ev_t[1], h->ev_t[2]);
+    cudaEventElapsedTime(&h->t_ms[2], h->ev_t[2], h->ev_t[3]);
+  }
+  return BX_OK;
+}
+
+int bx_last_timing(bx_handle* h, float* rf_ms, float* score_ms, float* merge_ms) {
+  if (!h) return BX_ERR_ARG;
+  if (rf_ms) *rf_ms = h->t_ms[0];
+  if (score_ms) *score_ms = h->t_ms[1];
+  if (merge_ms) *merge_ms = h->t_ms[2];
   return BX_OK;
 }
 
@@ -589,37 +730,40 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   const int W = h->row_words;
   const int64_t chunk = 1 << 18;
   const int64_t n_chunks = (q + chunk - 1) / chunk;
-  const size_t per_chunk_partials = (size_t)h->sm_count * 8;
-  BX_CUDA(h, h->d_partials.ensure(sizeof(bx_score_summary) * per_chunk_partials * (size_t)n_chunks));
+  const size_t per_chunk = (size_t)score_max_partials(h->sm_count);
+  BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
   for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
-  // merge the per-chunk partials as a compact list: record how many partials each chunk wrote
-  int total_partials = 0;
-  bx_score_summary* base = h->d_partials.as<bx_score_summary>();
+  int total = 0;
+  Partial* base = h->d_partials.as<Partial>();
   BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
   BX_CUDA(h, cudaEventRecord(h->ev_done[1], s));
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int b = (int)(c & 1);
     const int64_t off = c * chunk;
     const int64_t len = (q - off) < chunk ? (q - off) : chunk;
-    // the copy into buffer b waits until the kernel that last read buffer b is done
+    // the copy into buffer b waits until the kernels that last read buffer b are done
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
     BX_CUDA(h, cudaMemcpyAsync(h->d_host_rows[b].p, host_rows + (size_t)off * W, (size_t)len * W * 4,
                                cudaMemcpyHostToDevice, h->copy_stream));
     BX_CUDA(h, cudaEventRecord(h->ev_copy[b], h->copy_stream));
     BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
-    int grid = 0;
+    int np = 0;
     r = score_impl(h, h->d_host_rows[b].as<uint32_t>(), len, index_base + off, f_model, eps_f, k,
-                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total_partials, &grid, s);
+                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total, &np, s, false);
     if (r) return r;
-    total_partials += grid;
+    total += np;
     BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
   }
-  BX_CUDA(h, launch_summary_merge(base, total_partials, space_dev(h), k, q,
+  BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
                                   h->d_summary.as<bx_score_summary>(), s));
   BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                              cudaMemcpyDeviceToHost, s));
   BX_CUDA(h, cudaStreamSynchronize(s));
+  // the pool is host-resident: the top-k rows come straight from the caller's buffer
+  for (int i = 0; i < summary->n_top; ++i)
+    std::memcpy(summary->top[i].row, host_rows + (size_t)(summary->top[i].index - index_base) * W,
+                (size_t)W * 4);
   return BX_OK;
 }
 
@@ -638,8 +782,8 @@ int bx_gp_predict(bx_handle* h, const uint32_t* rows, int64_t q, double* mean, d
   a.f_model = 0.0;
   a.mean_out = mean;
   a.var_out = var;
-  int grid = 0;
-  BX_CUDA(h, launch_score(a, h->sm_count, (cudaStream_t)stream, &grid));
+  int np = 0;
+  BX_CUDA(h, launch_score(a, h->sm_count, (cudaStream_t)stream, &np));
   return BX_OK;
 }
 

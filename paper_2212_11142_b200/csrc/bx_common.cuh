@@ -60,13 +60,37 @@ struct RfNode {
   int32_t child;  // index of the left child; right child = child + 1
 };
 
+// Integer-coded forest (the fast path).  Every split `x <= threshold` on an encode_configs column
+// becomes an exact test on a per-candidate code: a finite numeric column compares its domain index
+// with the largest index whose coordinate is <= threshold (coordinates are monotone in the index);
+// a one-hot column tests label equality with precomputed left/right outcomes; a permutation
+// position column compares the integer position with floor-like cut; a real column keeps the f64
+// comparison against a side table.  One 64-bit word per node:
+//   [1:0] type (0 leaf, 1 int cut, 2 label test, 3 real)  [7:2] code slot  [31:8] argument
+//   [63:32] left child (right child = left + 1)
+struct CodedForestDev {
+  const uint64_t* nodes;     // [n_nodes]
+  const double* leaf_val;    // leaf values (argument of a leaf node)
+  const double* real_thr;    // thresholds of real splits
+  const int32_t* roots;      // [n_trees]
+  const int32_t* code_param; // [n_codes] parameter of each code slot
+  const int32_t* code_sub;   // [n_codes] permutation element (or 0)
+  int32_t n_nodes;
+  int32_t n_codes;
+  int32_t n_trees;
+  int32_t max_depth;
+  int32_t nodes_in_smem;     // node table copied to shared memory
+};
+
 struct ForestDev {
   const RfNode* nodes;
   const int32_t* roots;
   int32_t n_trees;
   int32_t max_depth;
   int32_t has_trees;     // 0 -> constant model
+  int32_t coded;         // 1 -> use `cf` (integer-coded fast path)
   double constant;       // single-class shortcut (feasibility.py:73-74)
+  CodedForestDev cf;
 };
 
 struct EvalSetDev {
@@ -230,6 +254,29 @@ __device__ __forceinline__ bool is_evaluated(const EvalSetDev& ev, const uint32_
   return false;
 }
 
+// ---- per-warp partial summaries of a score launch --------------------------------------------
+
+struct TopRec {
+  double value;
+  double prob;
+  int64_t index;
+};
+
+// Compact partial summary written by every warp of bx_score's kernel and merged afterwards.
+// Top-k entries carry no row (rows are gathered by index at the end); the two tracker bests keep
+// their rows because their tie-break compares configurations.
+struct Partial {
+  int64_t n_scored;
+  int64_t n_finite;
+  int32_t n_top;
+  int32_t pad;
+  TopRec top[BX_MAX_K];
+  TopRec best;
+  TopRec best_prob;
+  uint32_t best_row[BX_MAX_ROW_WORDS];
+  uint32_t best_prob_row[BX_MAX_ROW_WORDS];
+};
+
 // ---- launch helpers implemented in the .cu files -------------------------------------------
 
 struct ScoreArgs {
@@ -250,12 +297,15 @@ struct ScoreArgs {
   double* probs_out;        // optional
   double* mean_out;         // optional (bx_gp_predict)
   double* var_out;          // optional
-  bx_score_summary* partials;  // [gridDim.x] per-CTA summaries (NULL -> no summary)
+  Partial* partials;        // [gridDim.x * warps] per-warp summaries (NULL -> no summary)
 };
 
-cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* grid_used);
-cudaError_t launch_summary_merge(const bx_score_summary* partials, int n_partials,
-                                 const SpaceDev& space, int k, int64_t q,
+// launch_score returns the number of partials it wrote in *n_partials.
+cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials);
+// Merge partials into *out.  When pool_rows is non-NULL the rows of the top-k entries are
+// gathered from it (index - index_base); otherwise the caller fills them.
+cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const SpaceDev& space,
+                                 int k, const uint32_t* pool_rows, int64_t index_base,
                                  bx_score_summary* out, cudaStream_t s);
 cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
                       int pairwise, double* probs, cudaStream_t s);

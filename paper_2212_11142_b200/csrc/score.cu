@@ -7,9 +7,11 @@
 //   phase B  [v ; mean] = [L^-1 ; alpha^T] K*^T on the FP64 tensor pipe (DMMA m8n8k4),
 //            block-triangular over 16-row blocks, ss = sum_i v_i^2             (:322-325)
 //   phase C  de-standardise, EI (acquisition.py:40-51), x p, -inf below eps_f (:70-79)
-// then one thread folds the tile into the CTA's running summary: stable top-k by
-// (value desc, index asc) (acquisition.py:188), and the two _Tracker reductions
-// (value desc / prob desc, ties -> smallest configuration, evaluated skipped; :97-111).
+// then the warp folds its candidates into a warp-private summary: stable top-k by
+// (value desc, index asc) (acquisition.py:188) and the two _Tracker reductions (value desc /
+// prob desc, ties -> smallest configuration, evaluated skipped; :97-111).  A ballot against the
+// warp's current thresholds skips the sequential insert for almost every candidate.  The partial
+// summaries are merged by merge_kernel.
 #include "bx_common.cuh"
 
 namespace bx {
@@ -30,10 +32,10 @@ __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, doub
 __host__ __device__ __forceinline__ int ks_stride(int ncols) { return ((ncols + 15) / 16) * 16 + 4; }
 
 struct SmemLayout {
-  int ks_off, cand_off, tile_off, sum_off, par_off, total;
+  int par_off, ks_off, cand_off, tile_off, sum_off, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int cpw, int ncols, int n_params, int row_words) {
+__host__ __device__ inline SmemLayout smem_layout(int cpw, int ncols, int n_params) {
   SmemLayout L;
   int off = 0;
   L.par_off = off;
@@ -43,133 +45,66 @@ __host__ __device__ inline SmemLayout smem_layout(int cpw, int ncols, int n_para
   off += kWarps * cpw * ks_stride(ncols) * 8;
   L.cand_off = off;  // per warp: [n_params][cpw] 8-byte values + Kendall masks [n_params][cpw][2]
   off += kWarps * n_params * cpw * 8 * 3;
-  L.tile_off = off;  // per tile: value, prob (doubles), flags (int) for 4*cpw candidates
-  off += kWarps * cpw * (8 + 8 + 8 + 8 + 4);
+  L.tile_off = off;  // per warp tile: ss, mean (doubles)
+  off += kWarps * cpw * 16;
   off = (off + 15) & ~15;
   L.sum_off = off;
-  off += (int)sizeof(bx_score_summary);
+  off += kWarps * (int)sizeof(Partial);
   L.total = off;
-  (void)row_words;
   return L;
 }
 
-__device__ void summary_init(bx_score_summary* s, int k) {
+__device__ void partial_init(Partial* s) {
   s->n_scored = 0;
   s->n_finite = 0;
-  s->k = k;
   s->n_top = 0;
-  s->best.value = -INFINITY;
-  s->best.prob = -INFINITY;
-  s->best.index = -1;
-  s->best_prob.value = -INFINITY;
-  s->best_prob.prob = -INFINITY;
-  s->best_prob.index = -1;
+  s->best = TopRec{-INFINITY, -INFINITY, -1};
+  s->best_prob = TopRec{-INFINITY, -INFINITY, -1};
 }
 
-__device__ __forceinline__ void copy_row(uint32_t* dst, const uint32_t* src, int words) {
-  for (int w = 0; w < words; ++w) dst[w] = src[w];
+__device__ __forceinline__ bool top_before(double v, int64_t g, const TopRec& r) {
+  return v > r.value || (v == r.value && g < r.index);
 }
 
-// Fold one scored candidate into a summary (single thread).
-__device__ void summary_add(bx_score_summary* s, const bx_param_desc* params, int n_params,
+__device__ void top_insert(TopRec* top, int& n_top, int k, const TopRec& rec) {
+  if (k <= 0) return;
+  if (n_top == k && !top_before(rec.value, rec.index, top[k - 1])) return;
+  int pos = n_top < k ? n_top : k - 1;
+  while (pos > 0 && top_before(rec.value, rec.index, top[pos - 1])) {
+    top[pos] = top[pos - 1];
+    --pos;
+  }
+  top[pos] = rec;
+  if (n_top < k) ++n_top;
+}
+
+// Fold one scored candidate into a partial (single lane).
+__device__ void partial_add(Partial* s, int k, const bx_param_desc* params, int n_params,
                             const int32_t* rank_lut, int words, double v, double p, int64_t g,
                             bool evaluated, const uint32_t* row) {
-  s->n_scored += 1;
   if (v != -INFINITY) {
-    s->n_finite += 1;
-    // stable top-k by (value desc, index asc)
-    int k = s->k, nt = s->n_top;
-    bool enters = nt < k;
-    if (!enters) {
-      const bx_cand& last = s->top[nt - 1];
-      enters = v > last.value || (v == last.value && g < last.index);
-    }
-    if (enters) {
-      int pos = nt < k ? nt : k - 1;
-      while (pos > 0) {
-        const bx_cand& prev = s->top[pos - 1];
-        if (v > prev.value || (v == prev.value && g < prev.index)) {
-          s->top[pos] = prev;
-          --pos;
-        } else {
-          break;
-        }
-      }
-      s->top[pos].value = v;
-      s->top[pos].prob = p;
-      s->top[pos].index = g;
-      copy_row(s->top[pos].row, row, words);
-      if (nt < k) s->n_top = nt + 1;
-    }
+    int nt = s->n_top;
+    top_insert(s->top, nt, k, TopRec{v, p, g});
+    s->n_top = nt;
     if (!evaluated) {
       bool take = v > s->best.value;
       if (!take && v == s->best.value)
-        take = s->best.index < 0 || key_cmp(params, n_params, rank_lut, row, s->best.row) < 0;
+        take = s->best.index < 0 || key_cmp(params, n_params, rank_lut, row, s->best_row) < 0;
       if (take) {
-        s->best.value = v;
-        s->best.prob = p;
-        s->best.index = g;
-        copy_row(s->best.row, row, words);
+        s->best = TopRec{v, p, g};
+        for (int w = 0; w < words; ++w) s->best_row[w] = row[w];
       }
     }
   }
   if (!evaluated && p != -INFINITY) {
     bool take = p > s->best_prob.prob;
     if (!take && p == s->best_prob.prob)
-      take = s->best_prob.index < 0 ||
-             key_cmp(params, n_params, rank_lut, row, s->best_prob.row) < 0;
+      take = s->best_prob.index < 0 || key_cmp(params, n_params, rank_lut, row, s->best_prob_row) < 0;
     if (take) {
-      s->best_prob.value = v;
-      s->best_prob.prob = p;
-      s->best_prob.index = g;
-      copy_row(s->best_prob.row, row, words);
+      s->best_prob = TopRec{v, p, g};
+      for (int w = 0; w < words; ++w) s->best_prob_row[w] = row[w];
     }
   }
-}
-
-// Merge summary `b` into `a` (single thread).  Same orders as summary_add.
-__device__ void summary_merge(bx_score_summary* a, const bx_score_summary* b,
-                              const bx_param_desc* params, int n_params, const int32_t* rank_lut,
-                              int words) {
-  a->n_scored += b->n_scored;
-  a->n_finite += b->n_finite;
-  for (int i = 0; i < b->n_top; ++i) {
-    const bx_cand& c = b->top[i];
-    int k = a->k, nt = a->n_top;
-    bool enters = nt < k;
-    if (!enters) {
-      const bx_cand& last = a->top[nt - 1];
-      enters = c.value > last.value || (c.value == last.value && c.index < last.index);
-    }
-    if (!enters) break;  // b->top is sorted: nothing later can enter
-    int pos = nt < k ? nt : k - 1;
-    while (pos > 0) {
-      const bx_cand& prev = a->top[pos - 1];
-      if (c.value > prev.value || (c.value == prev.value && c.index < prev.index)) {
-        a->top[pos] = prev;
-        --pos;
-      } else {
-        break;
-      }
-    }
-    a->top[pos] = c;
-    if (nt < k) a->n_top = nt + 1;
-  }
-  if (b->best.index >= 0) {
-    bool take = b->best.value > a->best.value;
-    if (!take && b->best.value == a->best.value)
-      take = a->best.index < 0 ||
-             key_cmp(params, n_params, rank_lut, b->best.row, a->best.row) < 0;
-    if (take) a->best = b->best;
-  }
-  if (b->best_prob.index >= 0) {
-    bool take = b->best_prob.prob > a->best_prob.prob;
-    if (!take && b->best_prob.prob == a->best_prob.prob)
-      take = a->best_prob.index < 0 ||
-             key_cmp(params, n_params, rank_lut, b->best_prob.row, a->best_prob.row) < 0;
-    if (take) a->best_prob = b->best_prob;
-  }
-  (void)words;
 }
 
 // Matern-5/2 correlation times outputscale at squared weighted distance W (surrogate.py:142-145,
@@ -188,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
   const int n = a.gp.n;
   const int ncols = a.gp.ncols_pad;  // multiple of 16
   const int S = ks_stride(ncols);
-  const SmemLayout L = smem_layout(CPW, ncols, n_params, words);
+  const SmemLayout L = smem_layout(CPW, ncols, n_params);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par_off);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -198,18 +133,15 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
   double* ks = reinterpret_cast<double*>(smem + L.ks_off) + (size_t)warp * CPW * S;
   uint64_t* cval = reinterpret_cast<uint64_t*>(smem + L.cand_off) + (size_t)warp * n_params * CPW * 3;
   uint64_t* cmask = cval + n_params * CPW;  // [n_params][CPW][2]
-  constexpr int TC = kWarps * CPW;
-  double* t_value = reinterpret_cast<double*>(smem + L.tile_off);
-  double* t_prob = t_value + TC;
-  double* t_ss = t_prob + TC;
-  double* t_mean = t_ss + TC;
-  int* t_flag = reinterpret_cast<int*>(t_mean + TC);
-  bx_score_summary* summ = reinterpret_cast<bx_score_summary*>(smem + L.sum_off);
+  double* t_ss = reinterpret_cast<double*>(smem + L.tile_off) + warp * CPW * 2;
+  double* t_mean = t_ss + CPW;
+  Partial* summ = reinterpret_cast<Partial*>(smem + L.sum_off) + warp;
   const bool want_summary = a.partials != nullptr;
-  if (want_summary && tid == 0) summary_init(summ, a.k);
+  if (want_summary && lane == 0) partial_init(summ);
   __syncthreads();
 
   const double sigma = a.gp.outputscale;
+  constexpr int TC = kWarps * CPW;
   const int64_t n_tiles = (a.q + TC - 1) / TC;
 
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -295,6 +227,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
     __syncwarp();
 
     // ---- phase B: [L^-1; alpha] K*^T with DMMA, block-triangular ------------------------------
+    // Two accumulator sets (even / odd k-steps) double the independent DMMA chains.
     constexpr int NT = CPW / 8;
     double ss[NT][2], mn[NT][2];
 #pragma unroll
@@ -303,11 +236,13 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
     const int n_rb = a.gp.rows_pad / 16;
     for (int rb = 0; rb < n_rb; ++rb) {
       const int ext = min(ncols, 16 * (rb + 1));
-      double acc[2][NT][2];
+      double acc[2][2][NT][2];
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) acc[h][m][t][0] = acc[h][m][t][1] = 0.0;
       const double* A0 = a.gp.A + (size_t)(16 * rb + fr) * a.gp.lda + fk;
       const double* A1 = A0 + (size_t)8 * a.gp.lda;
       const double* B0 = ks + fr * S + fk;
@@ -325,19 +260,22 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int t = 0; t < NT; ++t) dmma8x8x4(acc[m][t][0], acc[m][t][1], ra[m][s], rbv[t][s]);
+            for (int t = 0; t < NT; ++t)
+              dmma8x8x4(acc[s & 1][m][t][0], acc[s & 1][m][t][1], ra[m][s], rbv[t][s]);
       }
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int row = 16 * rb + 8 * m + fr;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
+          const double v0 = acc[0][m][t][0] + acc[1][m][t][0];
+          const double v1 = acc[0][m][t][1] + acc[1][m][t][1];
           if (row < n) {
-            ss[t][0] = fma(acc[m][t][0], acc[m][t][0], ss[t][0]);
-            ss[t][1] = fma(acc[m][t][1], acc[m][t][1], ss[t][1]);
+            ss[t][0] = fma(v0, v0, ss[t][0]);
+            ss[t][1] = fma(v1, v1, ss[t][1]);
           } else if (row == n) {
-            mn[t][0] = acc[m][t][0];
-            mn[t][1] = acc[m][t][1];
+            mn[t][0] = v0;
+            mn[t][1] = v1;
           }
         }
       }
@@ -357,98 +295,203 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
       for (int t = 0; t < NT; ++t)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int c = warp * CPW + t * 8 + 2 * fk + e;
+          const int c = t * 8 + 2 * fk + e;
           t_ss[c] = ss[t][e];
           t_mean[c] = mn[t][e];
         }
     }
     __syncwarp();
 
-    // ---- phase C: epilogue per candidate ----------------------------------------------------
-    if (lane < CPW) {
-      const int c = warp * CPW + lane;
-      const int64_t gi = cbase + lane;
-      double value = -INFINITY, prob = -INFINITY;
-      int flag = 0;
-      if (gi < a.q) {
-        flag = 1;
-        const double var_s = fmax(sigma - t_ss[c], 0.0);          // surrogate.py:324-325
-        const double mean = a.gp.y_mean + a.gp.y_std * t_mean[c];  // :328
-        const double var = (a.gp.y_std * a.gp.y_std) * var_s;
-        if (a.mean_out) a.mean_out[gi] = mean;
-        if (a.var_out) a.var_out[gi] = var;
-        // expected_improvement_vec (acquisition.py:40-51)
-        const double s = sqrt(fmax(var, 0.0));
-        const double delta = a.f_model - mean;
-        double ei = fmax(delta, 0.0);
-        if (s > 0.0) {
-          const double z = delta / s;
-          const double phi = kInvSqrt2Pi * exp(-0.5 * z * z);
-          ei = delta * normcdf(z) + s * phi;
-        }
-        ei = fmax(ei, 0.0);
-        if (a.use_forest) {
-          prob = a.forest.has_trees ? a.probs_in[gi] : a.forest.constant;
-          value = (prob < a.eps_f) ? -INFINITY : ei * prob;  // acquisition.py:78
-        } else {
-          prob = 1.0;
-          value = ei;
-        }
-        if (a.values_out) a.values_out[gi] = value;
-        if (a.probs_out) a.probs_out[gi] = prob;
-        if (want_summary && is_evaluated(a.evald, a.rows + (size_t)gi * words, words)) flag = 2;
+    // ---- phase C: epilogue per candidate (lane c < CPW) ------------------------------------
+    const int64_t gi = cbase + lane;
+    double value = -INFINITY, prob = -INFINITY;
+    bool valid = false, evaluated = false;
+    if (lane < CPW && gi < a.q) {
+      valid = true;
+      const double var_s = fmax(sigma - t_ss[lane], 0.0);          // surrogate.py:324-325
+      const double mean = a.gp.y_mean + a.gp.y_std * t_mean[lane];  // :328
+      const double var = (a.gp.y_std * a.gp.y_std) * var_s;
+      if (a.mean_out) a.mean_out[gi] = mean;
+      if (a.var_out) a.var_out[gi] = var;
+      // expected_improvement_vec (acquisition.py:40-51)
+      const double s = sqrt(fmax(var, 0.0));
+      const double delta = a.f_model - mean;
+      double ei = fmax(delta, 0.0);
+      if (s > 0.0) {
+        const double z = delta / s;
+        const double phi = kInvSqrt2Pi * exp(-0.5 * z * z);
+        ei = delta * normcdf(z) + s * phi;
       }
-      t_value[c] = value;
-      t_prob[c] = prob;
-      t_flag[c] = flag;
+      ei = fmax(ei, 0.0);
+      if (a.use_forest) {
+        prob = a.forest.has_trees ? a.probs_in[gi] : a.forest.constant;
+        value = (prob < a.eps_f) ? -INFINITY : ei * prob;  // acquisition.py:78
+      } else {
+        prob = 1.0;
+        value = ei;
+      }
+      if (a.values_out) a.values_out[gi] = value;
+      if (a.probs_out) a.probs_out[gi] = prob;
+      if (want_summary) evaluated = is_evaluated(a.evald, a.rows + (size_t)gi * words, words);
     }
     if (want_summary) {
-      __syncthreads();
-      if (tid == 0) {
-        const int64_t tbase = tile * TC;
-        for (int c = 0; c < TC; ++c) {
-          if (t_flag[c] == 0) continue;
-          const int64_t gi = tbase + c;
-          summary_add(summ, params, n_params, a.space.rank_lut, words, t_value[c], t_prob[c],
-                      a.index_base + gi, t_flag[c] == 2, a.rows + (size_t)gi * words);
-        }
+      // conservative filter against the warp's current thresholds (they only tighten)
+      bool pass = false;
+      if (valid) {
+        const bool fin = value != -INFINITY;
+        const bool top_ok = fin && a.k > 0 && (summ->n_top < a.k || value >= summ->top[a.k - 1].value);
+        const bool best_ok = fin && !evaluated && value >= summ->best.value;
+        const bool prob_ok = !evaluated && prob >= summ->best_prob.prob;
+        pass = top_ok || best_ok || prob_ok;
       }
-      __syncthreads();
-    } else {
-      __syncwarp();
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      const unsigned fmask = __ballot_sync(0xffffffffu, valid && value != -INFINITY);
+      const unsigned pmask = __ballot_sync(0xffffffffu, pass);
+      const unsigned emask = __ballot_sync(0xffffffffu, evaluated);
+      if (lane == 0) {
+        summ->n_scored += __popc(vmask);
+        summ->n_finite += __popc(fmask);
+      }
+      unsigned m = pmask;
+      while (m) {
+        const int c = __ffs(m) - 1;
+        m &= m - 1;
+        const double vc = __shfl_sync(0xffffffffu, value, c);
+        const double pc = __shfl_sync(0xffffffffu, prob, c);
+        if (lane == 0)
+          partial_add(summ, a.k, params, n_params, a.space.rank_lut, words, vc, pc,
+                      a.index_base + cbase + c, (emask >> c) & 1u, a.rows + (size_t)(cbase + c) * words);
+        __syncwarp();
+      }
     }
+    __syncwarp();
   }
 
   if (want_summary) {
-    __syncthreads();
-    // copy the CTA summary out (int32 granularity)
+    __syncwarp();
     const int32_t* src = reinterpret_cast<const int32_t*>(summ);
-    int32_t* dst = reinterpret_cast<int32_t*>(a.partials + blockIdx.x);
-    for (int i = tid; i < (int)(sizeof(bx_score_summary) / 4); i += kThreads) dst[i] = src[i];
+    int32_t* dst = reinterpret_cast<int32_t*>(a.partials + (size_t)blockIdx.x * kWarps + warp);
+    for (int i = lane; i < (int)(sizeof(Partial) / 4); i += 32) dst[i] = src[i];
   }
 }
 
-__global__ void merge_kernel(const bx_score_summary* partials, int n_partials, SpaceDev space, int k,
-                             bx_score_summary* out) {
-  __shared__ bx_score_summary acc;
+// ---- merge --------------------------------------------------------------------------------
+constexpr int kMergeThreads = 32;
+
+__device__ bool rec_better_key(const TopRec& a, const uint32_t* arow, const TopRec& b,
+                               const uint32_t* brow, bool by_prob, const bx_param_desc* params,
+                               int n_params, const int32_t* rank_lut) {
+  if (a.index < 0) return false;
+  if (b.index < 0) return true;
+  const double x = by_prob ? a.prob : a.value, y = by_prob ? b.prob : b.value;
+  if (x != y) return x > y;
+  return key_cmp(params, n_params, rank_lut, arow, brow) < 0;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const Partial* parts, int n_parts,
+                                                              SpaceDev space, int k,
+                                                              const uint32_t* pool_rows,
+                                                              int64_t index_base,
+                                                              bx_score_summary* out) {
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
-  for (int i = threadIdx.x; i < space.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
+  __shared__ TopRec lists[kMergeThreads][BX_MAX_K];
+  __shared__ int counts[kMergeThreads];
+  __shared__ int best_at[kMergeThreads], prob_at[kMergeThreads];
+  __shared__ long long scored[kMergeThreads], finite[kMergeThreads];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < space.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(space.params)[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    summary_init(&acc, k);
-    for (int p = 0; p < n_partials; ++p)
-      summary_merge(&acc, partials + p, params, space.n_params, space.rank_lut, space.row_words);
+  int nt = 0, bi = -1, pi = -1;
+  long long sc = 0, fi = 0;
+  for (int p = tid; p < n_parts; p += blockDim.x) {
+    const Partial& P = parts[p];
+    sc += P.n_scored;
+    fi += P.n_finite;
+    for (int i = 0; i < P.n_top; ++i) {
+      const TopRec r = P.top[i];
+      if (nt == k && !top_before(r.value, r.index, lists[tid][k - 1])) break;
+      top_insert(lists[tid], nt, k, r);
+    }
+    if (P.best.index >= 0 &&
+        (bi < 0 || rec_better_key(P.best, P.best_row, parts[bi].best, parts[bi].best_row, false,
+                                  params, space.n_params, space.rank_lut)))
+      bi = p;
+    if (P.best_prob.index >= 0 &&
+        (pi < 0 || rec_better_key(P.best_prob, P.best_prob_row, parts[pi].best_prob,
+                                  parts[pi].best_prob_row, true, params, space.n_params,
+                                  space.rank_lut)))
+      pi = p;
+  }
+  counts[tid] = nt;
+  best_at[tid] = bi;
+  prob_at[tid] = pi;
+  scored[tid] = sc;
+  finite[tid] = fi;
+  __syncthreads();
+  if (tid == 0) {
+    TopRec top[BX_MAX_K];
+    int n = 0;
+    long long S = 0, F = 0;
+    int b = -1, pb = -1;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      S += scored[t];
+      F += finite[t];
+      for (int i = 0; i < counts[t]; ++i) {
+        if (n == k && !top_before(lists[t][i].value, lists[t][i].index, top[k - 1])) break;
+        top_insert(top, n, k, lists[t][i]);
+      }
+      const int cb = best_at[t];
+      if (cb >= 0 && (b < 0 || rec_better_key(parts[cb].best, parts[cb].best_row, parts[b].best,
+                                              parts[b].best_row, false, params, space.n_params,
+                                              space.rank_lut)))
+        b = cb;
+      const int cp = prob_at[t];
+      if (cp >= 0 && (pb < 0 || rec_better_key(parts[cp].best_prob, parts[cp].best_prob_row,
+                                               parts[pb].best_prob, parts[pb].best_prob_row, true,
+                                               params, space.n_params, space.rank_lut)))
+        pb = cp;
+    }
+    out->n_scored = S;
+    out->n_finite = F;
+    out->k = k;
+    out->n_top = n;
+    for (int i = 0; i < n; ++i) {
+      out->top[i].value = top[i].value;
+      out->top[i].prob = top[i].prob;
+      out->top[i].index = top[i].index;
+    }
+    const int W = space.row_words;
+    out->best.index = -1;
+    out->best.value = out->best.prob = -INFINITY;
+    if (b >= 0) {
+      out->best.value = parts[b].best.value;
+      out->best.prob = parts[b].best.prob;
+      out->best.index = parts[b].best.index;
+      for (int w = 0; w < W; ++w) out->best.row[w] = parts[b].best_row[w];
+    }
+    out->best_prob.index = -1;
+    out->best_prob.value = out->best_prob.prob = -INFINITY;
+    if (pb >= 0) {
+      out->best_prob.value = parts[pb].best_prob.value;
+      out->best_prob.prob = parts[pb].best_prob.prob;
+      out->best_prob.index = parts[pb].best_prob.index;
+      for (int w = 0; w < W; ++w) out->best_prob.row[w] = parts[pb].best_prob_row[w];
+    }
   }
   __syncthreads();
-  const int32_t* src = reinterpret_cast<const int32_t*>(&acc);
-  int32_t* dst = reinterpret_cast<int32_t*>(out);
-  for (int i = threadIdx.x; i < (int)(sizeof(bx_score_summary) / 4); i += blockDim.x) dst[i] = src[i];
+  if (pool_rows) {  // gather the rows of the top-k entries
+    const int W = space.row_words;
+    for (int t = tid; t < out->n_top * W; t += blockDim.x) {
+      const int i = t / W, w = t % W;
+      out->top[i].row[w] = pool_rows[(size_t)(out->top[i].index - index_base) * W + w];
+    }
+  }
 }
 
 template <int CPW>
-cudaError_t launch_score_t(const ScoreArgs& a, int sm_count, cudaStream_t s, int* grid_used) {
-  const SmemLayout L = smem_layout(CPW, a.gp.ncols_pad, a.space.n_params, a.space.row_words);
+cudaError_t launch_score_t(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials) {
+  const SmemLayout L = smem_layout(CPW, a.gp.ncols_pad, a.space.n_params);
   cudaError_t e = cudaFuncSetAttribute(score_kernel<CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        L.total);
   if (e != cudaSuccess) return e;
@@ -461,32 +504,28 @@ cudaError_t launch_score_t(const ScoreArgs& a, int sm_count, cudaStream_t s, int
   int64_t grid = (int64_t)sm_count * per_sm;
   if (tiles < grid) grid = tiles;
   if (grid < 1) grid = 1;
-  *grid_used = (int)grid;
+  *n_partials = (int)grid * kWarps;
   score_kernel<CPW><<<(int)grid, kThreads, L.total, s>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-int score_smem_bytes(int cpw, int ncols, int n_params, int row_words) {
-  return smem_layout(cpw, ncols, n_params, row_words).total;
+int score_smem_bytes(int cpw, int ncols, int n_params) {
+  return smem_layout(cpw, ncols, n_params).total;
 }
 
-cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* grid_used) {
-  // 8 candidates per warp keeps two CTAs per SM resident up to n ~ 300; 16 per warp halves the
-  // B-fragment traffic per DMMA when the tile still fits.
-  const int big = score_smem_bytes(16, a.gp.ncols_pad, a.space.n_params, a.space.row_words);
-  const int small = score_smem_bytes(8, a.gp.ncols_pad, a.space.n_params, a.space.row_words);
-  if (small > 227 * 1024) return cudaErrorInvalidValue;
-  (void)big;
-  return launch_score_t<8>(a, sm_count, s, grid_used);
+int score_max_partials(int sm_count) { return sm_count * 16 * kWarps; }
+
+cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials) {
+  if (score_smem_bytes(8, a.gp.ncols_pad, a.space.n_params) > 227 * 1024) return cudaErrorInvalidValue;
+  return launch_score_t<8>(a, sm_count, s, n_partials);
 }
 
-cudaError_t launch_summary_merge(const bx_score_summary* partials, int n_partials,
-                                 const SpaceDev& space, int k, int64_t q, bx_score_summary* out,
-                                 cudaStream_t s) {
-  (void)q;
-  merge_kernel<<<1, 32, 0, s>>>(partials, n_partials, space, k, out);
+cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const SpaceDev& space,
+                                 int k, const uint32_t* pool_rows, int64_t index_base,
+                                 bx_score_summary* out, cudaStream_t s) {
+  merge_kernel<<<1, kMergeThreads, 0, s>>>(partials, n_partials, space, k, pool_rows, index_base, out);
   return cudaGetLastError();
 }
 

@@ -203,10 +203,10 @@ class Scorer:
 
     def score(self, rows: torch.Tensor, f_model: float, eps_f: float = 0.0, k: int = 10,
               want_values: bool = False, summary: bool = True, rf_pairwise: bool | None = None,
-              index_base: int = 0):
+              index_base: int = 0, timing: bool = False):
         """bx_score over device rows.  Returns (Summary | None, values | None, probs | None)."""
         q = rows.shape[0]
-        flags = 0
+        flags = N.BX_SCORE_TIMING if timing else 0
         if rf_pairwise if rf_pairwise is not None else q == 1:
             flags |= N.BX_SCORE_RF_PAIRWISE
         if not summary:
@@ -220,6 +220,13 @@ class Scorer:
                                        int(k), flags, _ptr(values), _ptr(probs),
                                        C.byref(s) if summary else None, self.stream))
         return (self._summary(s) if summary else None), values, probs
+
+    def last_timing(self) -> dict:
+        """CUDA-event durations (ms) of the forest / fused-score / merge kernels of the last
+        score(..., timing=True) call."""
+        t = [C.c_float(), C.c_float(), C.c_float()]
+        self._check(self._lib.bx_last_timing(self.h, *(C.byref(x) for x in t)))
+        return {"rf_ms": t[0].value, "score_ms": t[1].value, "merge_ms": t[2].value}
 
     def score_host(self, rows: np.ndarray | torch.Tensor, f_model: float, eps_f: float = 0.0,
                    k: int = 10, index_base: int = 0) -> Summary:

@@ -67,6 +67,30 @@ def test_forest_bit_exact(case, sc):
     assert np.array_equal(lay.features(lay.encode(cands[:256])), arr["rf_X"])
 
 
+@pytest.mark.parametrize("case", ["mixed_fit", "mixed_metrics", "C3", "C4"])
+def test_forest_generic_kernel_matches_coded(case, monkeypatch):
+    """The integer-coded fast path and the generic f64 traversal give identical bits."""
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    _, feas = model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"]]
+    monkeypatch.setenv("BX_FOREST_GENERIC", "1")
+    generic = Scorer()
+    monkeypatch.delenv("BX_FOREST_GENERIC")
+    coded = Scorer()
+    out = []
+    for s in (generic, coded):
+        s.set_space(space, feas.use_transforms)
+        s.set_forest(feas)
+        rows = s.to_device(s.layout.encode(cands))
+        out.append(s.rf_predict(rows, pairwise=False).cpu().numpy())
+        out.append(np.array([s.rf_predict(rows[i:i + 1]).item() for i in range(32)]))
+    generic.close()
+    coded.close()
+    assert np.array_equal(out[0], arr["probs"]) and np.array_equal(out[2], arr["probs"])
+    assert np.array_equal(out[1], arr["probs_q1"][:32]) and np.array_equal(out[3], arr["probs_q1"][:32])
+
+
 @pytest.mark.parametrize("case", CASES)
 def test_neighbors(case, sc):
     from paper_2212_11142_b200 import acquisition as A

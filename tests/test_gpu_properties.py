@@ -1,0 +1,126 @@
+"""GPU properties at BASELINE sizes (1M-candidate pools) and edge cases the reference tests."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from golden_io import Ctx, cot_for, load, model, oracle_model, to_cfg
+from paper_2212_11142_b200 import scenarios
+from paper_2212_11142_b200.space import sample_uniform
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3():
+    from paper_2212_11142_b200.device import scorer
+    meta, arr, space = load("C3")
+    gp, feas = model(meta, arr, space)
+    sc = scorer()
+    sc.set_gp(gp)
+    sc.set_forest(feas)
+    rows_h = scenarios.sample_rows_cot(sc.layout, cot_for("C3"), 1 << 20, np.random.default_rng(9))
+    return sc, meta, arr, space, gp, feas, rows_h
+
+
+def test_host_and_device_pools_agree_at_full_size(c3):
+    """bx_score (device pool) and bx_score_host (chunked pinned host pool) give identical
+    summaries; the top-k equals the stable argsort of the per-candidate values."""
+    sc, meta, arr, space, gp, feas, rows_h = c3
+    f = gp.objective_to_model(meta["f_best"])
+    rows = sc.to_device(rows_h)
+    a, values, probs = sc.score(rows, f, meta["eps_f"], k=10, want_values=True)
+    pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
+    b = sc.score_host(pinned.numpy().view(np.uint32), f, meta["eps_f"], k=10)
+    assert [c.index for c in a.top] == [c.index for c in b.top]
+    assert [c.value for c in a.top] == [c.value for c in b.top]
+    assert all(np.array_equal(x.row, y.row) for x, y in zip(a.top, b.top))
+    assert (a.n_scored, a.n_finite) == (b.n_scored, b.n_finite) == (1 << 20, a.n_finite)
+    v = values.cpu().numpy()
+    order = [i for i in np.argsort(-v, kind="stable")[:10] if v[i] != -np.inf]
+    assert [c.index for c in a.top] == order
+    assert a.n_finite == int(np.sum(v != -np.inf))
+    for c in a.top:
+        assert np.array_equal(c.row, rows_h[c.index])
+
+
+def test_deterministic_and_batch_independent(c3):
+    """The value of a candidate does not depend on its batch or position (so the hill climb's
+    comparisons are consistent across batches)."""
+    sc, meta, arr, space, gp, feas, rows_h = c3
+    f = gp.objective_to_model(meta["f_best"])
+    rows = sc.to_device(rows_h[:200_003])
+    _, v1, p1 = sc.score(rows, f, meta["eps_f"], want_values=True, summary=False)
+    _, v2, p2 = sc.score(rows, f, meta["eps_f"], want_values=True, summary=False)
+    _, v3, p3 = sc.score(rows[777:5777], f, meta["eps_f"], want_values=True, summary=False)
+    assert torch.equal(v1, v2) and torch.equal(p1, p2)
+    assert torch.equal(v1[777:5777], v3) and torch.equal(p1[777:5777], p3)
+
+
+def test_full_size_sample_against_oracle(c3):
+    """A 4096-candidate sample of the 1M pool (including its tail) against the oracle."""
+    sc, meta, arr, space, gp, feas, rows_h = c3
+    og, of = oracle_model(meta, arr, space)
+    f = gp.objective_to_model(meta["f_best"])
+    idx = np.concatenate([np.arange(2048), np.arange((1 << 20) - 2048, 1 << 20)])
+    sub = rows_h[idx]
+    _, v, p = sc.score(sc.to_device(sub), f, meta["eps_f"], want_values=True, summary=False)
+    cfgs = sc.layout.decode(sub)
+    ov, op = oracle.scores(og, of, cfgs, meta["f_best"], meta["eps_f"])
+    assert np.array_equal(p.cpu().numpy(), op)
+    v = v.cpu().numpy()
+    fin = np.isfinite(ov)
+    assert np.array_equal(fin, np.isfinite(v))
+    np.testing.assert_allclose(v[fin], ov[fin], rtol=1e-5, atol=1e-9 * np.abs(ov[fin]).max())
+
+
+def test_single_and_empty_batches(c3):
+    sc, meta, arr, space, gp, feas, rows_h = c3
+    f = gp.objective_to_model(meta["f_best"])
+    s, v, p = sc.score(sc.to_device(rows_h[:1]), f, meta["eps_f"], k=10, want_values=True)
+    assert s.n_scored == 1 and len(s.top) == (1 if v.item() != -np.inf else 0)
+    from paper_2212_11142_b200._native import NativeError
+    with pytest.raises(NativeError):
+        sc.score(sc.to_device(rows_h[:0]), f, meta["eps_f"])
+
+
+def test_constraint_kernel_python_semantics():
+    """Division/modulo by zero -> False, floor modulo, int/float promotion, categorical equality."""
+    from paper_2212_11142_b200 import acquisition as A
+    from test_host import tricky_space
+    sp = tricky_space()
+    cfgs = sample_uniform(sp, 5000, np.random.default_rng(4))
+    want = np.array([all(oracle.eval_constraint(e, sp.as_dict(c)) is True for e in sp.constraints)
+                     for c in cfgs])
+    assert np.array_equal(A.constraints_batch(sp, cfgs), want)
+
+
+def test_all_minus_inf_falls_back_to_max_probability():
+    """acquisition.py:179-184: every value below eps_f -> best unevaluated probability."""
+    from paper_2212_11142_b200 import acquisition as A
+    meta, arr, space = load("mixed_fit")
+    gp, feas = model(meta, arr, space)
+    og, of = oracle_model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"][:500]]
+    ev = set(cands[:50])
+    ctx = Ctx(gp, feas, meta["f_best"], 0.999, np.random.default_rng(0), ev)
+    got = A.optimize_acquisition(ctx, space, None, sample_fn=lambda n, r: cands)
+    want = oracle.optimize(og, of, space, cands, meta["f_best"], 0.999, ev)
+    assert got == want
+
+
+def test_space_exhausted_raises():
+    from paper_2212_11142_b200 import acquisition as A
+    from paper_2212_11142_b200.constraints import build_cot
+    from paper_2212_11142_b200.models import GPState, Hyper
+    from paper_2212_11142_b200.space import Parameter, SearchSpace
+    sp = SearchSpace([Parameter.ordinal("a", [1, 2, 4]), Parameter.categorical("c", ["x", "y"])],
+                     ["a >= 1"])
+    cot = build_cot(sp)
+    allc = list(cot.enumerate())
+    gp = GPState.fit(sp, allc[:3], [1.0, 2.0, 3.0], Hyper(1.0, 1e-3, (0.5, 0.5)))
+    ctx = Ctx(gp, None, 1.0, 0.0, np.random.default_rng(0), set(allc))
+    with pytest.raises(A.SpaceExhausted):
+        A.optimize_acquisition(ctx, sp, cot)
+    ctx = Ctx(gp, None, 1.0, 0.0, np.random.default_rng(0), set(allc[:5]))
+    assert A.optimize_acquisition(ctx, sp, cot) == allc[5]
