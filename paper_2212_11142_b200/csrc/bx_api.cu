@@ -79,8 +79,16 @@ struct bx_handle {
   DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[2];
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
-  cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};  // rf / score / merge timing
+  cudaEvent_t ev_t[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // rf / gp / merge timing
   float t_ms[3] = {0, 0, 0};
+  // register-resident fused GP path (gp_fused.cu)
+  bool use_fused = false;
+  bool no_fused = false;  // BX_GP_GENERIC debug switch (env)
+  int mt = 0, rows8 = 0, n_kendall = 0;
+  int32_t kendall_param[BX_MAX_PARAMS] = {0};
+  DevBuf d_panels, d_ei;
+  cudaStream_t rf_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_rf = nullptr;
 };
 
 namespace {
@@ -170,6 +178,32 @@ int check_space(bx_handle* h) {
   return BX_OK;
 }
 
+int max_partials(int sm_count) {
+  const int a = score_max_partials(sm_count), b = summary_max_partials(sm_count);
+  return a > b ? a : b;
+}
+
+FusedArgs fused_args(const bx_handle* h, const uint32_t* rows, int64_t q, double f_model) {
+  FusedArgs f{};
+  f.space = space_dev(h);
+  f.gp = gp_dev(h);
+  f.panels = h->d_panels.as<double>();
+  f.rows = rows;
+  f.q = q;
+  f.f_model = f_model;
+  f.mt = h->mt;
+  f.n_kendall = h->n_kendall;
+  for (int i = 0; i < h->n_kendall; ++i) f.kendall_param[i] = h->kendall_param[i];
+  f.n_num = f.n_cat = f.n_perm = 0;
+  for (int k = 0; k < h->n_params; ++k) {
+    const int kind = h->params[k].kind;
+    if (kind == BX_CATEGORICAL) f.cat_param[f.n_cat++] = k;
+    else if (kind == BX_PERMUTATION) f.perm_param[f.n_perm++] = k;
+    else f.num_param[f.n_num++] = k;
+  }
+  return f;
+}
+
 int check_gp(bx_handle* h) {
   int r = check_space(h);
   if (r) return r;
@@ -199,7 +233,12 @@ bx_handle* bx_create(int device) {
     cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
   }
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&h->ev_t[i]);
+  for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
+  const char* gpg = getenv("BX_GP_GENERIC");
+  h->no_fused = gpg && gpg[0] == '1';
+  cudaStreamCreateWithFlags(&h->rf_stream, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_rf, cudaEventDisableTiming);
   return h;
 }
 
@@ -222,8 +261,13 @@ void bx_destroy(bx_handle* h) {
     if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
     if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
   }
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 5; ++i)
     if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
+  h->d_panels.release();
+  h->d_ei.release();
+  if (h->rf_stream) cudaStreamDestroy(h->rf_stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_rf) cudaEventDestroy(h->ev_rf);
   delete h;
 }
 
@@ -345,6 +389,24 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
   BX_CUDA(h, launch_tri_inverse(h->d_L.as<double>(), n, h->d_A.as<double>(), h->gp_lda, s));
   BX_CUDA(h, launch_gp_planes(space_dev(h), h->d_train.as<uint32_t>(), n, h->d_inv_l.as<double>(),
                               h->d_planes.as<uint64_t>(), h->d_kmask.as<uint64_t>(), s));
+  // register-resident path: n + 1 rows must fit 8 * 32 register rows and the smem budget
+  h->use_fused = false;
+  h->n_kendall = 0;
+  for (int k = 0; k < D; ++k)
+    if (h->params[k].kind == BX_PERMUTATION && h->params[k].metric == BX_KENDALL)
+      h->kendall_param[h->n_kendall++] = k;
+  const int mt = ((n + 1 + 31) / 32) * 4;  // m-tiles, a multiple of 4
+  if (!h->no_fused && 8 * mt <= fused_max_rows()) {
+    const size_t smem = fused_smem_bytes(n, D, h->n_kendall, 8 * mt);
+    if (smem <= 200 * 1024) {
+      h->mt = mt;
+      h->rows8 = 8 * mt;
+      BX_CUDA(h, h->d_panels.ensure(panels_doubles(h->gp_ncols, h->rows8) * 8));
+      BX_CUDA(h, launch_build_panels(h->d_A.as<double>(), h->gp_lda, h->gp_rows, h->gp_ncols,
+                                     h->rows8, h->d_panels.as<double>(), s));
+      h->use_fused = true;
+    }
+  }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
   h->outputscale = outputscale;
   h->y_mean = y_mean;
@@ -657,16 +719,54 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   a.values_out = values;
   a.probs_out = probs_out;
   a.partials = partials;
+  const bool forest = h->has_forest && h->forest.has_trees;
+  if (forest) BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
+  if (h->use_fused) {
+    // forest on the side stream, GP on the caller's stream, joined before the summary
+    BX_CUDA(h, cudaEventRecord(h->ev_fork, s));
+    BX_CUDA(h, cudaStreamWaitEvent(h->rf_stream, h->ev_fork, 0));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], h->rf_stream));
+    if (forest)
+      BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
+                           h->d_probs.as<double>(), h->rf_stream));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], h->rf_stream));
+    BX_CUDA(h, cudaEventRecord(h->ev_rf, h->rf_stream));
+    BX_CUDA(h, h->d_ei.ensure((size_t)q * 8));
+    FusedArgs f = fused_args(h, rows, q, f_model);
+    f.ei_out = h->d_ei.as<double>();
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
+    BX_CUDA(h, launch_gp_fused(f, h->sm_count, s));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
+    BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_rf, 0));
+    SummaryArgs m{};
+    m.space = a.space;
+    m.evald = a.evald;
+    m.rows = rows;
+    m.q = q;
+    m.index_base = index_base;
+    m.ei = h->d_ei.as<double>();
+    m.probs_in = forest ? h->d_probs.as<double>() : nullptr;
+    m.use_forest = h->has_forest ? 1 : 0;
+    m.has_trees = forest ? 1 : 0;
+    m.constant = h->forest.constant;
+    m.eps_f = eps_f;
+    m.k = k;
+    m.values_out = values;
+    m.probs_out = probs_out;
+    m.partials = partials;
+    BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));
+    return BX_OK;
+  }
   if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
-  if (h->has_forest && h->forest.has_trees) {
-    BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
+  if (forest) {
     BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                          h->d_probs.as<double>(), s));
     a.probs_in = h->d_probs.as<double>();
   }
   if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
-  BX_CUDA(h, launch_score(a, h->sm_count, s, n_partials));
   if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
+  BX_CUDA(h, launch_score(a, h->sm_count, s, n_partials));
+  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
   return BX_OK;
 }
 
@@ -683,7 +783,7 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   const bool timing = (flags & BX_SCORE_TIMING) != 0;
   Partial* partials = nullptr;
   if (want) {
-    BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)score_max_partials(h->sm_count)));
+    BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
     BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
     partials = h->d_partials.as<Partial>();
   }
@@ -694,17 +794,17 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   if (want) {
     BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                                cudaMemcpyDeviceToHost, s));
   } else if (timing) {
-    BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
+    BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
   }
   if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
   if (timing) {
     cudaEventElapsedTime(&h->t_ms[0], h->ev_t[0], h->ev_t[1]);
-    cudaEventElapsedTime(&h->t_ms[1], h->ev_t[1], h->ev_t[2]);
-    cudaEventElapsedTime(&h->t_ms[2], h->ev_t[2], h->ev_t[3]);
+    cudaEventElapsedTime(&h->t_ms[1], h->ev_t[2], h->ev_t[3]);
+    cudaEventElapsedTime(&h->t_ms[2], h->ev_t[3], h->ev_t[4]);
   }
   return BX_OK;
 }
@@ -730,7 +830,7 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   const int W = h->row_words;
   const int64_t chunk = 1 << 18;
   const int64_t n_chunks = (q + chunk - 1) / chunk;
-  const size_t per_chunk = (size_t)score_max_partials(h->sm_count);
+  const size_t per_chunk = (size_t)max_partials(h->sm_count);
   BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
   for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
@@ -783,6 +883,13 @@ int bx_gp_predict(bx_handle* h, const uint32_t* rows, int64_t q, double* mean, d
   a.mean_out = mean;
   a.var_out = var;
   int np = 0;
+  if (h->use_fused) {
+    FusedArgs f = fused_args(h, rows, q, 0.0);
+    f.mean_out = mean;
+    f.var_out = var;
+    BX_CUDA(h, launch_gp_fused(f, h->sm_count, (cudaStream_t)stream));
+    return BX_OK;
+  }
   BX_CUDA(h, launch_score(a, h->sm_count, (cudaStream_t)stream, &np));
   return BX_OK;
 }

@@ -300,6 +300,55 @@ struct ScoreArgs {
   Partial* partials;        // [gridDim.x * warps] per-warp summaries (NULL -> no summary)
 };
 
+// Register-resident GP kernel (gp_fused.cu): writes EI (or mean/var) per candidate.
+struct FusedArgs {
+  SpaceDev space;
+  GpDev gp;
+  const double* panels;   // panel-major padded copy of A (launch_build_panels)
+  const uint32_t* rows;
+  int64_t q;
+  double f_model;
+  double* ei_out;
+  double* mean_out;
+  double* var_out;
+  int32_t mt;             // m-tiles held in registers (8 * mt >= n + 1)
+  int32_t n_kendall;
+  int32_t kendall_param[BX_MAX_PARAMS];
+  // parameters grouped by kind so the distance loops carry no per-parameter dispatch
+  int32_t n_num, n_cat, n_perm;
+  int32_t num_param[BX_MAX_PARAMS];
+  int32_t cat_param[BX_MAX_PARAMS];
+  int32_t perm_param[BX_MAX_PARAMS];
+};
+
+// Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).
+struct SummaryArgs {
+  SpaceDev space;
+  EvalSetDev evald;
+  const uint32_t* rows;
+  int64_t q;
+  int64_t index_base;
+  const double* ei;
+  const double* probs_in;  // NULL -> constant / no forest
+  int32_t use_forest;
+  int32_t has_trees;
+  double constant;
+  double eps_f;
+  int32_t k;
+  double* values_out;
+  double* probs_out;
+  Partial* partials;
+};
+
+int fused_max_rows();
+size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8);
+size_t panels_doubles(int ncols_pad, int rows8);
+cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
+                                double* panels, cudaStream_t s);
+cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_summary(const SummaryArgs& a, int sm_count, cudaStream_t s, int* n_partials);
+int summary_max_partials(int sm_count);
+
 // launch_score returns the number of partials it wrote in *n_partials.
 cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials);
 // Merge partials into *out.  When pool_rows is non-NULL the rows of the top-k entries are

@@ -115,6 +115,49 @@ __device__ __forceinline__ double coded_leaf(const CodedForestDev& cf, const uin
   return cf.leaf_val[(uint32_t)(nodes[cur] >> 8) & 0xFFFFFFu];
 }
 
+// G trees walked in lockstep (independent dependency chains: G node loads in flight per thread);
+// the leaf values are still added strictly in tree order.
+template <int G>
+__device__ __forceinline__ void coded_leaves(const CodedForestDev& cf, const uint64_t* nodes,
+                                             const CodeView& cv, int t0, double* out) {
+  int cur[G];
+  bool live[G];
+#pragma unroll
+  for (int s = 0; s < G; ++s) {
+    cur[s] = cf.roots[t0 + s];
+    live[s] = true;
+  }
+  for (int it = 0; it <= cf.max_depth; ++it) {
+    bool any = false;
+#pragma unroll
+    for (int s = 0; s < G; ++s) {
+      if (!live[s]) continue;
+      const uint64_t nd = nodes[cur[s]];
+      const int type = (int)(nd & 3u);
+      if (type == 0) {
+        live[s] = false;
+        continue;
+      }
+      any = true;
+      const int slot = (int)((nd >> 2) & 63u);
+      const uint32_t arg = (uint32_t)(nd >> 8) & 0xFFFFFFu;
+      bool left;
+      if (type == 1) {
+        left = cv.code[slot * kRfThreads + cv.t] < (int)arg;
+      } else if (type == 2) {
+        const bool eq = cv.code[slot * kRfThreads + cv.t] == (int)(arg & 0x3FFFFFu);
+        left = eq ? ((arg >> 22) & 1u) : ((arg >> 23) & 1u);
+      } else {
+        left = cv.real[slot * kRfThreads + cv.t] <= cf.real_thr[arg];
+      }
+      cur[s] = (int)(nd >> 32) + (left ? 0 : 1);
+    }
+    if (!any) break;
+  }
+#pragma unroll
+  for (int s = 0; s < G; ++s) out[s] = cf.leaf_val[(uint32_t)(nodes[cur[s]] >> 8) & 0xFFFFFFu];
+}
+
 __device__ double coded_pairwise(const CodedForestDev& cf, const uint64_t* nodes, const CodeView& cv,
                                  int t0, int cnt) {
   if (cnt < 8) {
