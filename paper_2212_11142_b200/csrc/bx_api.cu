@@ -60,7 +60,7 @@ struct bx_handle {
   // forest
   bool has_forest = false;
   ForestDev forest{};
-  DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_real_thr, d_code_param, d_code_sub;
+  DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
   std::vector<double> coord_host;
@@ -84,6 +84,7 @@ struct bx_handle {
   // register-resident fused GP path (gp_fused.cu)
   bool use_fused = false;
   bool no_fused = false;  // BX_GP_GENERIC debug switch (env)
+  bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
   DevBuf d_panels, d_ei;
@@ -201,6 +202,8 @@ FusedArgs fused_args(const bx_handle* h, const uint32_t* rows, int64_t q, double
     else if (kind == BX_PERMUTATION) f.perm_param[f.n_perm++] = k;
     else f.num_param[f.n_num++] = k;
   }
+  for (int j = 0; j < 64; ++j) f.exp2tab[j] = (double)exp2l((long double)j / 64.0L);
+  f.precise = h->matern_precise ? 1 : 0;
   return f;
 }
 
@@ -236,6 +239,8 @@ bx_handle* bx_create(int device) {
   for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
   const char* gpg = getenv("BX_GP_GENERIC");
   h->no_fused = gpg && gpg[0] == '1';
+  const char* mp = getenv("BX_MATERN_PRECISE");
+  h->matern_precise = mp && mp[0] == '1';
   cudaStreamCreateWithFlags(&h->rf_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_rf, cudaEventDisableTiming);
@@ -254,7 +259,7 @@ void bx_destroy(bx_handle* h) {
                     &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
                     &h->d_host_rows[0], &h->d_host_rows[1], &h->d_cnodes, &h->d_leaf_val,
-                    &h->d_real_thr, &h->d_code_param, &h->d_code_sub};
+                    &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -490,7 +495,9 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
   for (int k = 0; k < D; ++k) {
     const bx_param_desc& p = h->params[k];
     slot_base[k] = (int)code_param.size();
-    const int cnt = p.kind == BX_PERMUTATION ? p.size : 1;
+    // one code per encode_configs column: a one-hot label and a permutation position each get
+    // their own slot, so every non-real split is `code < cut`
+    const int cnt = (p.kind == BX_PERMUTATION || p.kind == BX_CATEGORICAL) ? p.size : 1;
     for (int e = 0; e < cnt; ++e) {
       code_param.push_back(k);
       code_sub.push_back(e);
@@ -511,49 +518,57 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     }
   }
   std::vector<uint64_t> coded(nodes.size());
+  std::vector<uint32_t> leaf_idx(nodes.size(), 0);
   std::vector<double> leaf_val, real_thr;
+  bool has_real = false;
   for (size_t u = 0; u < nodes.size(); ++u) {
     const RfNode& nd = nodes[u];
-    uint64_t type, slot = 0, arg;
+    uint64_t type, slot = 0, arg, child;
     if (nd.feat < 0) {
-      type = 0;
-      arg = leaf_val.size();
+      // leaf: `code[0] >= 0xFFFFFF` never holds and the left child is the leaf itself, so a walk
+      // that reached it stays; its value index lives in leaf_idx
+      type = 2;
+      arg = 0xFFFFFF;
+      leaf_idx[u] = (uint32_t)leaf_val.size();
       leaf_val.push_back(nd.val);
+      child = (uint64_t)u;
+      coded[u] = arg | (type << 30) | (child << 32);
+      continue;
     } else {
       const int k = h->feat_param_host[nd.feat], sub = h->feat_sub_host[nd.feat];
       const bx_param_desc& p = h->params[k];
       const double t = nd.thr;
+      child = (uint64_t)(uint32_t)nd.child;
       if (p.kind == BX_REAL) {
-        type = 3;
+        type = 1;
         slot = slot_base[k];
         arg = real_thr.size();
         real_thr.push_back(t);
-      } else if (p.kind == BX_CATEGORICAL) {
-        type = 2;
-        slot = slot_base[k];
-        if (sub >= (1 << 22)) return BX_OK;
-        arg = (uint64_t)sub | ((uint64_t)(1.0 <= t) << 22) | ((uint64_t)(0.0 <= t) << 23);
+        has_real = true;
       } else {
-        type = 1;
-        int cut1 = 0;  // number of codes whose feature value is <= t
+        type = 0;
+        int cut1 = 0;  // number of code values whose feature value is <= t
+        slot = slot_base[k] + ((p.kind == BX_PERMUTATION || p.kind == BX_CATEGORICAL) ? sub : 0);
         if (p.kind == BX_PERMUTATION) {
-          slot = slot_base[k] + sub;
           for (int i = 0; i < p.size; ++i) cut1 += ((double)i <= t) ? 1 : 0;
+        } else if (p.kind == BX_CATEGORICAL) {
+          cut1 = (0.0 <= t ? 1 : 0) + (1.0 <= t ? 1 : 0);  // one-hot code in {0, 1}
         } else {
-          slot = slot_base[k];
           for (int i = 0; i < p.size; ++i) cut1 += (h->coord_host[p.coord + i] <= t) ? 1 : 0;
         }
         arg = (uint64_t)cut1;
       }
     }
-    if (arg >= (1u << 24) || nd.child < -1) return BX_OK;
-    const uint64_t child = nd.feat < 0 ? 0 : (uint64_t)(uint32_t)nd.child;
-    coded[u] = type | (slot << 2) | (arg << 8) | (child << 32);
+    if (arg >= (1u << 24) || slot >= 64) return BX_OK;
+    coded[u] = arg | (slot << 24) | (type << 30) | (child << 32);
   }
+  h->forest.cf.has_real = has_real ? 1 : 0;
   if (leaf_val.empty()) leaf_val.push_back(0.0);
   if (real_thr.empty()) real_thr.push_back(0.0);
   BX_CUDA(h, upload(h->d_cnodes, coded.data(), coded.size()));
   BX_CUDA(h, upload(h->d_leaf_val, leaf_val.data(), leaf_val.size()));
+  BX_CUDA(h, upload(h->d_leaf_idx, leaf_idx.data(), leaf_idx.size()));
+  h->forest.cf.leaf_idx = h->d_leaf_idx.as<uint32_t>();
   BX_CUDA(h, upload(h->d_real_thr, real_thr.data(), real_thr.size()));
   BX_CUDA(h, upload(h->d_code_param, code_param.data(), code_param.size()));
   BX_CUDA(h, upload(h->d_code_sub, code_sub.data(), code_sub.size()));
@@ -568,7 +583,8 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
   cf.n_codes = (int)code_param.size();
   cf.n_trees = h->forest.n_trees;
   cf.max_depth = max_depth;
-  cf.nodes_in_smem = coded.size() * 8 <= 160 * 1024 ? 1 : 0;
+  cf.n_leaves = (int)leaf_val.size();
+  cf.nodes_in_smem = 0;  // decided at launch from the smem budget
   h->forest.coded = 1;
   return BX_OK;
 }
@@ -699,10 +715,34 @@ int bx_set_constraints(bx_handle* h, int32_t n_constraints, const int32_t* prog_
 
 // ---- scoring --------------------------------------------------------------------------------
 
+// Summary pass over the EI / probability buffers of the last fused scoring launch.
+static SummaryArgs last_summary_args(bx_handle* h, const uint32_t* rows, int64_t q,
+                                     int64_t index_base, double eps_f, int32_t k, double* values,
+                                     double* probs_out, Partial* partials) {
+  const bool forest = h->has_forest && h->forest.has_trees;
+  SummaryArgs m{};
+  m.space = space_dev(h);
+  m.evald = eval_dev(h);
+  m.rows = rows;
+  m.q = q;
+  m.index_base = index_base;
+  m.ei = h->d_ei.as<double>();
+  m.probs_in = forest ? h->d_probs.as<double>() : nullptr;
+  m.use_forest = h->has_forest ? 1 : 0;
+  m.has_trees = forest ? 1 : 0;
+  m.constant = h->forest.constant;
+  m.eps_f = eps_f;
+  m.k = k;
+  m.values_out = values;
+  m.probs_out = probs_out;
+  m.partials = partials;
+  return m;
+}
+
 static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
                       double f_model, double eps_f, int32_t k, int32_t flags, double* values,
                       double* probs_out, Partial* partials, int* n_partials, cudaStream_t s,
-                      bool timing) {
+                      bool timing, bool track_prob = false) {
   ScoreArgs a{};
   a.space = space_dev(h);
   a.gp = gp_dev(h);
@@ -738,22 +778,8 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     BX_CUDA(h, launch_gp_fused(f, h->sm_count, s));
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_rf, 0));
-    SummaryArgs m{};
-    m.space = a.space;
-    m.evald = a.evald;
-    m.rows = rows;
-    m.q = q;
-    m.index_base = index_base;
-    m.ei = h->d_ei.as<double>();
-    m.probs_in = forest ? h->d_probs.as<double>() : nullptr;
-    m.use_forest = h->has_forest ? 1 : 0;
-    m.has_trees = forest ? 1 : 0;
-    m.constant = h->forest.constant;
-    m.eps_f = eps_f;
-    m.k = k;
-    m.values_out = values;
-    m.probs_out = probs_out;
-    m.partials = partials;
+    SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
+    m.track_prob = track_prob ? 1 : 0;
     BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));
     return BX_OK;
   }
@@ -801,6 +827,17 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
     BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
   }
   if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
+  if (want && summary->n_finite == 0 && h->use_fused) {
+    // every value is -inf: only now is the probability tracker needed (acquisition.py:179-184)
+    SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs, partials);
+    m.track_prob = 1;
+    BX_CUDA(h, launch_summary(m, h->sm_count, s, &np));
+    BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
+                                    h->d_summary.as<bx_score_summary>(), s));
+    BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
+                               cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));
+  }
   if (timing) {
     cudaEventElapsedTime(&h->t_ms[0], h->ev_t[0], h->ev_t[1]);
     cudaEventElapsedTime(&h->t_ms[1], h->ev_t[2], h->ev_t[3]);
@@ -834,8 +871,10 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
   for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
-  int total = 0;
   Partial* base = h->d_partials.as<Partial>();
+  // pass 1 without the probability tracker; pass 2 (with it) only if every value is -inf
+  for (int pass = 0; pass < 2; ++pass) {
+  int total = 0;
   BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
   BX_CUDA(h, cudaEventRecord(h->ev_done[1], s));
   for (int64_t c = 0; c < n_chunks; ++c) {
@@ -850,7 +889,8 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
     int np = 0;
     r = score_impl(h, h->d_host_rows[b].as<uint32_t>(), len, index_base + off, f_model, eps_f, k,
-                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total, &np, s, false);
+                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total, &np, s, false,
+                   pass == 1);
     if (r) return r;
     total += np;
     BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
@@ -860,6 +900,8 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                              cudaMemcpyDeviceToHost, s));
   BX_CUDA(h, cudaStreamSynchronize(s));
+  if (summary->n_finite != 0 || !h->use_fused) break;
+  }
   // the pool is host-resident: the top-k rows come straight from the caller's buffer
   for (int i = 0; i < summary->n_top; ++i)
     std::memcpy(summary->top[i].row, host_rows + (size_t)(summary->top[i].index - index_base) * W,

@@ -60,26 +60,30 @@ struct RfNode {
   int32_t child;  // index of the left child; right child = child + 1
 };
 
-// Integer-coded forest (the fast path).  Every split `x <= threshold` on an encode_configs column
-// becomes an exact test on a per-candidate code: a finite numeric column compares its domain index
-// with the largest index whose coordinate is <= threshold (coordinates are monotone in the index);
-// a one-hot column tests label equality with precomputed left/right outcomes; a permutation
-// position column compares the integer position with floor-like cut; a real column keeps the f64
-// comparison against a side table.  One 64-bit word per node:
-//   [1:0] type (0 leaf, 1 int cut, 2 label test, 3 real)  [7:2] code slot  [31:8] argument
-//   [63:32] left child (right child = left + 1)
+// Integer-coded forest (the fast path).  Every encode_configs column gets a per-candidate integer
+// code (domain index of a finite numeric parameter, 0/1 for a one-hot label column, element
+// position for a permutation column) and every split `x <= threshold` on it becomes the exact
+// test `code < cut` with cut = #{code values whose feature value <= threshold} (coordinates are
+// monotone in the domain index).  Real columns keep the f64 comparison against a side table.
+// One 64-bit word per node:
+//   [23:0] argument (cut / real-threshold index / leaf-value index)   [29:24] code slot
+//   [31:30] type (0 integer cut, 1 real, 2 leaf)   [63:32] left child (right = left + 1; a leaf
+//   points at itself, so a finished walk stays put)
 struct CodedForestDev {
   const uint64_t* nodes;     // [n_nodes]
-  const double* leaf_val;    // leaf values (argument of a leaf node)
+  const uint32_t* leaf_idx;  // [n_nodes] leaf-value index of leaf nodes
+  const double* leaf_val;    // [n_leaves]
   const double* real_thr;    // thresholds of real splits
   const int32_t* roots;      // [n_trees]
   const int32_t* code_param; // [n_codes] parameter of each code slot
-  const int32_t* code_sub;   // [n_codes] permutation element (or 0)
+  const int32_t* code_sub;   // [n_codes] label / permutation element (or 0)
   int32_t n_nodes;
+  int32_t n_leaves;
   int32_t n_codes;
   int32_t n_trees;
   int32_t max_depth;
-  int32_t nodes_in_smem;     // node table copied to shared memory
+  int32_t has_real;
+  int32_t nodes_in_smem;     // node table + leaf values copied to shared memory
 };
 
 struct ForestDev {
@@ -319,6 +323,8 @@ struct FusedArgs {
   int32_t num_param[BX_MAX_PARAMS];
   int32_t cat_param[BX_MAX_PARAMS];
   int32_t perm_param[BX_MAX_PARAMS];
+  double exp2tab[64];     // 2^(j/64), correctly rounded (host long double)
+  int32_t precise;        // 1 -> libm sqrt/exp in the Matérn (BX_MATERN_PRECISE=1)
 };
 
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).
@@ -335,6 +341,7 @@ struct SummaryArgs {
   double constant;
   double eps_f;
   int32_t k;
+  int32_t track_prob;      // also run the probability tracker (only needed when all values are -inf)
   double* values_out;
   double* probs_out;
   Partial* partials;

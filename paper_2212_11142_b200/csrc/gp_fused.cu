@@ -63,6 +63,48 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// sigma * matern52(sqrt(W)) with 18 FP64 operations instead of the ~47 of sqrt() + exp():
+//   d  = W * y,  y = rsqrt(W) from MUFU.RSQ64H refined by one Newton step (rel. err ~2^-46)
+//   e^x, x = -sqrt5 d: x = (64 k + j) ln2/64 + r, |r| <= ln2/128, 2^(j/64) from a 64-entry table,
+//        degree-5 Taylor in r (truncation < 4e-17), 2^k folded into the table value's exponent
+//   K  = (sigma + sigma sqrt5 d + sigma 5/3 W) e
+// The table is exact to 1/2 ulp (host-computed with long double), so K* is within a few ulp of
+// the reference's sigma * (1 + sqrt5 d + 5/3 d^2) * exp(-sqrt5 d) (surrogate.py:142-145, 321).
+struct MaternConst {
+  double s0, s1, s2;  // sigma, sigma*sqrt5, sigma*5/3
+};
+
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+__device__ __forceinline__ double kstar_fast(double W, const MaternConst& mc, const double* exp2tab) {
+  const double w = fmax(W, 1e-300);                 // W = 0 -> d ~ 1e-150 -> K* = sigma exactly
+  double y = rsqrt_approx(w);
+  y = y * fma(-0.5 * w * y, y, 1.5);                // Newton step for 1/sqrt(w)
+  const double d = w * y;
+  const double x = -kSqrt5 * d;
+  // k = rint(x * 64 / ln2) via the 1.5 * 2^52 shifter
+  const double t = fma(x, 92.332482616893656877, 6755399441055744.0);
+  const int k = __double2loint(t);
+  const double kf = t - 6755399441055744.0;
+  double r = fma(kf, -0.010830424696223417, x);     // ln2/64 split: hi (exact product) ...
+  r = fma(kf, -2.572804622327669e-14, r);           // ... and lo
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = fma(r, p, 1.0);
+  // 2^(j/64) * 2^(k >> 6): add the integer exponent to the table entry's exponent field
+  const double tj = exp2tab[k & 63];
+  const int hi = __double2hiint(tj) + ((k >> 6) << 20);
+  const double scale = __hiloint2double(hi, __double2loint(tj));
+  const double e = (x < -700.0) ? 0.0 : p * scale;
+  return fma(mc.s2, W, fma(mc.s1, d, mc.s0)) * e;
+}
+
 __device__ __forceinline__ double kstar(double W, double sigma) {
   const double d = sqrt(fmax(W, 0.0));
   const double e = exp(-kSqrt5 * d);
@@ -70,7 +112,7 @@ __device__ __forceinline__ double kstar(double W, double sigma) {
 }
 
 struct FusedLayout {
-  int par, planes, kmask, abuf, cand, tile, bar, total;
+  int par, planes, kmask, abuf, cand, tile, bar, exp2, total;
 };
 
 __host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params, int n_kendall,
@@ -93,6 +135,8 @@ __host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params,
   off += nw * 16 * 8;
   L.bar = off;
   off += 2 * 8;
+  L.exp2 = off;
+  off += 64 * 8;
   L.total = off;
   return L;
 }
@@ -120,6 +164,9 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
   double* t_ss = reinterpret_cast<double*>(smem + L.tile) + warp * 16;
   double* t_mean = t_ss + 8;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
+  double* s_exp2 = reinterpret_cast<double*>(smem + L.exp2);
+  for (int i = tid; i < 64; i += blockDim.x) s_exp2[i] = a.exp2tab[i];
+  const MaternConst mc{a.gp.outputscale, a.gp.outputscale * kSqrt5, a.gp.outputscale * (5.0 / 3.0)};
 
   for (int i = tid; i < n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
@@ -229,7 +276,10 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       }
       double kv[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) kv[s] = (chunk * kKC + 4 * s + fk < n) ? kstar(W[s], sigma) : 0.0;
+      for (int s = 0; s < 4; ++s)
+        kv[s] = (chunk * kKC + 4 * s + fk < n)
+                    ? (a.precise ? kstar(W[s], sigma) : kstar_fast(W[s], mc, s_exp2))
+                    : 0.0;
 
       mbar_wait(&bars[buf], phase[buf]);
       phase[buf] ^= 1u;

@@ -48,13 +48,13 @@ __global__ void __launch_bounds__(kSumThreads) summary_kernel(SummaryArgs a) {
     // thresholds snapshot (warp-uniform reads of lane 0's partial)
     const bool top_open = a.k > 0 && summ->n_top < a.k;
     const double kth = (a.k > 0 && !top_open) ? summ->top[a.k - 1].value : -INFINITY;
+    const bool prob_ok = a.track_prob && prob >= summ->best_prob.prob;
     const bool maybe = valid && ((fin && a.k > 0 && (top_open || value >= kth)) ||
-                                 (fin && value >= summ->best.value) || prob >= summ->best_prob.prob);
+                                 (fin && value >= summ->best.value) || prob_ok);
     bool evaluated = false;
     if (maybe && a.evald.count > 0) evaluated = is_evaluated(a.evald, a.rows + (size_t)gi * words, words);
     const bool pass = maybe && ((fin && a.k > 0 && (top_open || value >= kth)) ||
-                                (!evaluated && ((fin && value >= summ->best.value) ||
-                                                prob >= summ->best_prob.prob)));
+                                (!evaluated && ((fin && value >= summ->best.value) || prob_ok)));
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
     const unsigned fmask = __ballot_sync(0xffffffffu, fin);
     unsigned pmask = __ballot_sync(0xffffffffu, pass);
@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kSumThreads) summary_kernel(SummaryArgs a) {
       const double pc = __shfl_sync(0xffffffffu, prob, c);
       if (lane == 0)
         partial_add(summ, a.k, params, a.space.n_params, a.space.rank_lut, words, vc, pc,
-                    a.index_base + base + c, (emask >> c) & 1u, a.rows + (size_t)(base + c) * words);
+                    a.index_base + base + c, (emask >> c) & 1u, a.rows + (size_t)(base + c) * words,
+                    a.track_prob != 0);
       __syncwarp();
     }
   }

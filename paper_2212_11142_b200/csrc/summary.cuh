@@ -30,7 +30,7 @@ __device__ inline void top_insert(TopRec* top, int& n_top, int k, const TopRec& 
 // Fold one scored candidate into a partial (single lane).
 __device__ inline void partial_add(Partial* s, int k, const bx_param_desc* params, int n_params,
                             const int32_t* rank_lut, int words, double v, double p, int64_t g,
-                            bool evaluated, const uint32_t* row) {
+                            bool evaluated, const uint32_t* row, bool track_prob = true) {
   if (v != -INFINITY) {
     int nt = s->n_top;
     top_insert(s->top, nt, k, TopRec{v, p, g});
@@ -45,7 +45,7 @@ __device__ inline void partial_add(Partial* s, int k, const bx_param_desc* param
       }
     }
   }
-  if (!evaluated && p != -INFINITY) {
+  if (track_prob && !evaluated && p != -INFINITY) {
     bool take = p > s->best_prob.prob;
     if (!take && p == s->best_prob.prob)
       take = s->best_prob.index < 0 || key_cmp(params, n_params, rank_lut, row, s->best_prob_row) < 0;
