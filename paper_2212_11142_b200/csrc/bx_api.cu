@@ -400,7 +400,7 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
   for (int k = 0; k < D; ++k)
     if (h->params[k].kind == BX_PERMUTATION && h->params[k].metric == BX_KENDALL)
       h->kendall_param[h->n_kendall++] = k;
-  const int mt = ((n + 1 + 31) / 32) * 4;  // m-tiles, a multiple of 4
+  const int mt = ((n + 1 + 15) / 16) * 2;  // m-tiles of 8 rows covering rows 0..n, even count
   if (!h->no_fused && 8 * mt <= fused_max_rows()) {
     const size_t smem = fused_smem_bytes(n, D, h->n_kendall, 8 * mt);
     if (smem <= 200 * 1024) {

@@ -184,7 +184,6 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
 
   const double sigma = a.gp.outputscale;
   const int n_chunks = a.gp.ncols_pad / kKC;      // ncols_pad: multiple of 16
-  const int mt_hi = (n + 1 + 7) / 8;               // m-tiles holding rows 0..n
   const int64_t n_tiles = (a.q + 8 * nw - 1) / (8 * nw);
   const int c = lane >> 2, fk = lane & 3;
   uint32_t phase[2] = {0, 0};
@@ -412,13 +411,21 @@ size_t panels_doubles(int ncols_pad, int rows8) { return (size_t)(ncols_pad / kK
 
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s) {
   switch (a.mt) {
+    case 2: return launch_mt<2>(a, sm_count, s);
     case 4: return launch_mt<4>(a, sm_count, s);
+    case 6: return launch_mt<6>(a, sm_count, s);
     case 8: return launch_mt<8>(a, sm_count, s);
+    case 10: return launch_mt<10>(a, sm_count, s);
     case 12: return launch_mt<12>(a, sm_count, s);
+    case 14: return launch_mt<14>(a, sm_count, s);
     case 16: return launch_mt<16>(a, sm_count, s);
+    case 18: return launch_mt<18>(a, sm_count, s);
     case 20: return launch_mt<20>(a, sm_count, s);
+    case 22: return launch_mt<22>(a, sm_count, s);
     case 24: return launch_mt<24>(a, sm_count, s);
+    case 26: return launch_mt<26>(a, sm_count, s);
     case 28: return launch_mt<28>(a, sm_count, s);
+    case 30: return launch_mt<30>(a, sm_count, s);
     case 32: return launch_mt<32>(a, sm_count, s);
     default: return cudaErrorInvalidValue;
   }

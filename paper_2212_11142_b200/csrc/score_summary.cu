@@ -76,10 +76,14 @@ __global__ void __launch_bounds__(kSumThreads) summary_kernel(SummaryArgs a) {
     }
   }
   if (want) {
-    __syncwarp();
-    const int32_t* src = reinterpret_cast<const int32_t*>(summ);
-    int32_t* dst = reinterpret_cast<int32_t*>(a.partials + (size_t)blockIdx.x * kSumWarps + warp);
-    for (int i = lane; i < (int)(sizeof(Partial) / 4); i += 32) dst[i] = src[i];
+    __syncthreads();  // fold the block's warp partials into one
+    if (tid == 0)
+      for (int w = 1; w < kSumWarps; ++w)
+        partial_merge(&parts[0], &parts[w], a.k, params, a.space.n_params, a.space.rank_lut, words);
+    __syncthreads();
+    const int32_t* src = reinterpret_cast<const int32_t*>(&parts[0]);
+    int32_t* dst = reinterpret_cast<int32_t*>(a.partials + blockIdx.x);
+    for (int i = tid; i < (int)(sizeof(Partial) / 4); i += kSumThreads) dst[i] = src[i];
   }
 }
 
@@ -91,7 +95,7 @@ cudaError_t launch_summary(const SummaryArgs& a, int sm_count, cudaStream_t s, i
   int64_t blocks = (a.q + kSumThreads - 1) / kSumThreads;
   if (blocks > (int64_t)sm_count * 2) blocks = (int64_t)sm_count * 2;
   if (blocks < 1) blocks = 1;
-  *n_partials = (int)blocks * kSumWarps;
+  *n_partials = (int)blocks;
   summary_kernel<<<(int)blocks, kSumThreads, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -57,3 +57,36 @@ __device__ inline void partial_add(Partial* s, int k, const bx_param_desc* param
 }
 
 }  // namespace bx
+
+namespace bx {
+// Merge partial `b` into `a` (single lane); same total orders as partial_add.
+__device__ inline void partial_merge(Partial* a, const Partial* b, int k, const bx_param_desc* params,
+                                     int n_params, const int32_t* rank_lut, int words) {
+  a->n_scored += b->n_scored;
+  a->n_finite += b->n_finite;
+  int nt = a->n_top;
+  for (int i = 0; i < b->n_top; ++i) {
+    if (nt == k && !top_before(b->top[i].value, b->top[i].index, a->top[k - 1])) break;
+    top_insert(a->top, nt, k, b->top[i]);
+  }
+  a->n_top = nt;
+  if (b->best.index >= 0) {
+    bool take = a->best.index < 0 || b->best.value > a->best.value;
+    if (!take && b->best.value == a->best.value)
+      take = key_cmp(params, n_params, rank_lut, b->best_row, a->best_row) < 0;
+    if (take) {
+      a->best = b->best;
+      for (int w = 0; w < words; ++w) a->best_row[w] = b->best_row[w];
+    }
+  }
+  if (b->best_prob.index >= 0) {
+    bool take = a->best_prob.index < 0 || b->best_prob.prob > a->best_prob.prob;
+    if (!take && b->best_prob.prob == a->best_prob.prob)
+      take = key_cmp(params, n_params, rank_lut, b->best_prob_row, a->best_prob_row) < 0;
+    if (take) {
+      a->best_prob = b->best_prob;
+      for (int w = 0; w < words; ++w) a->best_prob_row[w] = b->best_prob_row[w];
+    }
+  }
+}
+}  // namespace bx
