@@ -61,6 +61,8 @@ struct bx_handle {
   bool has_forest = false;
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
+  DevBuf d_knodes, d_kvid, d_kuval;
+  bool no_fused_forest = false;  // BX_FOREST_SEPARATE debug switch (env)
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
   std::vector<double> coord_host;
@@ -241,6 +243,11 @@ bx_handle* bx_create(int device) {
   h->no_fused = gpg && gpg[0] == '1';
   const char* mp = getenv("BX_MATERN_PRECISE");
   h->matern_precise = mp && mp[0] == '1';
+  // The forest walk fused into the GP kernel is correct but measured slower than the concurrent
+  // stand-alone kernel (the per-panel CTA barrier aligns every warp's integer phase), so it is
+  // opt-in: BX_FOREST_FUSED=1.
+  const char* fs = getenv("BX_FOREST_FUSED");
+  h->no_fused_forest = !(fs && fs[0] == '1');
   cudaStreamCreateWithFlags(&h->rf_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_rf, cudaEventDisableTiming);
@@ -259,7 +266,8 @@ void bx_destroy(bx_handle* h) {
                     &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
                     &h->d_host_rows[0], &h->d_host_rows[1], &h->d_cnodes, &h->d_leaf_val,
-                    &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx};
+                    &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
+                    &h->d_knodes, &h->d_kvid, &h->d_kuval};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -586,6 +594,53 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
   cf.n_leaves = (int)leaf_val.size();
   cf.nodes_in_smem = 0;  // decided at launch from the smem budget
   h->forest.coded = 1;
+
+  // compact 32-bit form for the walk fused into the GP kernel (CompactForestDev)
+  CompactForestDev& kf = h->forest.kf;
+  kf = CompactForestDev{};
+  bool ok = !has_real;
+  for (size_t c = 0; ok && c < code_param.size(); ++c) {
+    const bx_param_desc& p = h->params[code_param[c]];
+    if ((p.kind == BX_INTEGER || p.kind == BX_ORDINAL) && p.size > 511) ok = false;
+  }
+  std::vector<uint32_t> knodes(nodes.size());
+  std::vector<uint16_t> vid(nodes.size(), 0);
+  std::vector<double> uval;
+  for (size_t u = 0; ok && u < nodes.size(); ++u) {
+    const uint32_t lo = (uint32_t)coded[u];
+    const uint32_t type = lo >> 30;
+    if (type == 2) {
+      const double v = leaf_val[leaf_idx[u]];
+      size_t id = 0;
+      while (id < uval.size() && std::memcmp(&uval[id], &v, 8) != 0) ++id;
+      if (id == uval.size()) uval.push_back(v);
+      if (id > 65535) { ok = false; break; }
+      vid[u] = (uint16_t)id;
+      knodes[u] = 0x80000000u | (511u << 16);  // stays: code < 511 always
+      continue;
+    }
+    const uint32_t slot = (lo >> 24) & 63u, cut = lo & 0xFFFFFFu;
+    const uint64_t off = (uint64_t)(coded[u] >> 32) - u;
+    if (cut > 511 || off == 0 || off > 65535) { ok = false; break; }
+    knodes[u] = (slot << 25) | (cut << 16) | (uint32_t)off;
+  }
+  if (ok) {
+    BX_CUDA(h, upload(h->d_knodes, knodes.data(), knodes.size()));
+    BX_CUDA(h, upload(h->d_kvid, vid.data(), vid.size()));
+    BX_CUDA(h, upload(h->d_kuval, uval.data(), uval.size()));
+    kf.nodes = h->d_knodes.as<uint32_t>();
+    kf.vid = h->d_kvid.as<uint16_t>();
+    kf.uval = h->d_kuval.as<double>();
+    kf.roots = h->forest.roots;
+    kf.code_param = cf.code_param;
+    kf.code_sub = cf.code_sub;
+    kf.n_nodes = (int)knodes.size();
+    kf.n_uvals = (int)uval.size();
+    kf.n_trees = cf.n_trees;
+    kf.max_depth = max_depth;
+    kf.n_codes = cf.n_codes;
+    kf.enabled = 1;
+  }
   return BX_OK;
 }
 
@@ -762,22 +817,32 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   const bool forest = h->has_forest && h->forest.has_trees;
   if (forest) BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
   if (h->use_fused) {
-    // forest on the side stream, GP on the caller's stream, joined before the summary
-    BX_CUDA(h, cudaEventRecord(h->ev_fork, s));
-    BX_CUDA(h, cudaStreamWaitEvent(h->rf_stream, h->ev_fork, 0));
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], h->rf_stream));
-    if (forest)
+    // The forest walk runs inside the GP kernel (FP64 and integer/LSU work interleave in the same
+    // warps) unless the numpy pairwise order (q == 1) or the table budget rules it out; then it
+    // runs on the side stream and is joined before the summary.
+    const CompactForestDev& kf = h->forest.kf;
+    const bool fuse_rf = forest && kf.enabled && !(flags & BX_SCORE_RF_PAIRWISE) &&
+                         !h->no_fused_forest &&
+                         fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
+                             220 * 1024;
+    // The stand-alone forest kernel and the GP kernel each fill every SM's shared memory, so
+    // they cannot co-reside: run them back to back on the caller's stream (which also makes the
+    // per-kernel CUDA-event timing exact).
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+    if (forest && !fuse_rf)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
-                           h->d_probs.as<double>(), h->rf_stream));
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], h->rf_stream));
-    BX_CUDA(h, cudaEventRecord(h->ev_rf, h->rf_stream));
+                           h->d_probs.as<double>(), s));
+    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
     BX_CUDA(h, h->d_ei.ensure((size_t)q * 8));
     FusedArgs f = fused_args(h, rows, q, f_model);
     f.ei_out = h->d_ei.as<double>();
+    if (fuse_rf) {
+      f.kf = kf;
+      f.probs_out = h->d_probs.as<double>();
+    }
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
     BX_CUDA(h, launch_gp_fused(f, h->sm_count, s));
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
-    BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_rf, 0));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
     BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));

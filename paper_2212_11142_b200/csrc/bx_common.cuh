@@ -86,6 +86,22 @@ struct CodedForestDev {
   int32_t nodes_in_smem;     // node table + leaf values copied to shared memory
 };
 
+// Compact forest for the GP kernel's fused walk (gp_fused.cu): 32-bit nodes
+//   internal: [31] 0, [30:25] code slot, [24:16] cut, [15:0] left-child offset (right = left + 1)
+//   leaf:     [31] 1, [30:0] 0 (offset 0 -> the walk stays); value = uval[vid[node]]
+// Available when there are no real splits, every cut and code fits 9 bits and every tree has
+// fewer than 65536 nodes.
+struct CompactForestDev {
+  const uint32_t* nodes;
+  const uint16_t* vid;       // [n_nodes] unique-value id of leaves
+  const double* uval;        // [n_uvals] distinct leaf values
+  const int32_t* roots;
+  const int32_t* code_param;
+  const int32_t* code_sub;
+  int32_t n_nodes, n_uvals, n_trees, max_depth, n_codes;
+  int32_t enabled;
+};
+
 struct ForestDev {
   const RfNode* nodes;
   const int32_t* roots;
@@ -95,6 +111,7 @@ struct ForestDev {
   int32_t coded;         // 1 -> use `cf` (integer-coded fast path)
   double constant;       // single-class shortcut (feasibility.py:73-74)
   CodedForestDev cf;
+  CompactForestDev kf;
 };
 
 struct EvalSetDev {
@@ -325,6 +342,8 @@ struct FusedArgs {
   int32_t perm_param[BX_MAX_PARAMS];
   double exp2tab[64];     // 2^(j/64), correctly rounded (host long double)
   int32_t precise;        // 1 -> libm sqrt/exp in the Matérn (BX_MATERN_PRECISE=1)
+  CompactForestDev kf;    // kf.enabled -> walk the forest inside the kernel, write probs_out
+  double* probs_out;
 };
 
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).
@@ -349,6 +368,8 @@ struct SummaryArgs {
 
 int fused_max_rows();
 size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8);
+size_t fused_smem_bytes_forest(int n, int n_params, int n_kendall, int rows8,
+                               const CompactForestDev& kf);
 size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);

@@ -19,8 +19,8 @@ namespace bx {
 
 namespace {
 
-constexpr int kKC = 16;        // panel width (columns of A per TMA copy)
-constexpr int kKCP = kKC + 4;  // padded panel row (doubles): fragment loads hit 2 wavefronts
+constexpr int kKC = 16;        // panel width (columns of A per TMA copy; 32 measured no faster)
+constexpr int kKCP = kKC + 4;  // padded panel row (doubles): == 4 (mod 16), fragment loads hit 2 wavefronts
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -112,11 +112,13 @@ __device__ __forceinline__ double kstar(double W, double sigma) {
 }
 
 struct FusedLayout {
-  int par, planes, kmask, abuf, cand, tile, bar, exp2, total;
+  int par, planes, kmask, abuf, cand, tile, bar, exp2, rf_nodes, rf_vid, rf_uval, rf_roots, rf_codes,
+      total;
 };
 
 __host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params, int n_kendall,
-                                                    int rows8) {
+                                                    int rows8, int kf_nodes = 0, int kf_uvals = 0,
+                                                    int kf_trees = 0, int kf_codes = 0) {
   FusedLayout L;
   int off = 0;
   L.par = off;
@@ -137,6 +139,17 @@ __host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params,
   off += 2 * 8;
   L.exp2 = off;
   off += 64 * 8;
+  // fused forest walk (CompactForestDev): nodes, leaf value ids, distinct values, roots, codes
+  L.rf_nodes = off;
+  off += kf_nodes * 4;
+  L.rf_vid = off;
+  off += (kf_nodes * 2 + 15) & ~15;
+  L.rf_uval = off;
+  off += kf_uvals * 8;
+  L.rf_roots = off;
+  off += (kf_trees * 4 + 15) & ~15;
+  L.rf_codes = off;  // per warp: [8 candidates][n_codes] int32
+  off += nw * 8 * kf_codes * 4;
   L.total = off;
   return L;
 }
@@ -154,7 +167,24 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
   const int n_params = a.space.n_params, words = a.space.row_words;
   const int n = a.gp.n;
   const int rows8 = 8 * MT;
-  const FusedLayout L = fused_layout(nw, n, n_params, a.n_kendall, rows8);
+  const CompactForestDev& kf = a.kf;
+  const bool rf = kf.enabled != 0;
+  const FusedLayout L = rf ? fused_layout(nw, n, n_params, a.n_kendall, rows8, kf.n_nodes, kf.n_uvals,
+                                          kf.n_trees, kf.n_codes)
+                           : fused_layout(nw, n, n_params, a.n_kendall, rows8);
+  uint32_t* rf_nodes = reinterpret_cast<uint32_t*>(smem + L.rf_nodes);
+  uint16_t* rf_vid = reinterpret_cast<uint16_t*>(smem + L.rf_vid);
+  double* rf_uval = reinterpret_cast<double*>(smem + L.rf_uval);
+  int32_t* rf_roots = reinterpret_cast<int32_t*>(smem + L.rf_roots);
+  int32_t* rf_codes = reinterpret_cast<int32_t*>(smem + L.rf_codes) + warp * 8 * kf.n_codes;
+  if (rf) {
+    for (int i = tid; i < kf.n_nodes; i += blockDim.x) {
+      rf_nodes[i] = kf.nodes[i];
+      rf_vid[i] = kf.vid[i];
+    }
+    for (int i = tid; i < kf.n_uvals; i += blockDim.x) rf_uval[i] = kf.uval[i];
+    for (int i = tid; i < kf.n_trees; i += blockDim.x) rf_roots[i] = kf.roots[i];
+  }
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -183,7 +213,7 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
   __syncthreads();
 
   const double sigma = a.gp.outputscale;
-  const int n_chunks = a.gp.ncols_pad / kKC;      // ncols_pad: multiple of 16
+  const int n_chunks = (a.gp.ncols_pad + kKC - 1) / kKC;
   const int64_t n_tiles = (a.q + 8 * nw - 1) / (8 * nw);
   const int c = lane >> 2, fk = lane & 3;
   uint32_t phase[2] = {0, 0};
@@ -224,20 +254,65 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       cmask[(k * 8 + cc) * 2] = lo;
       cmask[(k * 8 + cc) * 2 + 1] = hi;
     }
+    if (rf) {  // forest codes of the 8 candidates (one per encode_configs column)
+      for (int idx = lane; idx < 8 * kf.n_codes; idx += 32) {
+        const int cc = idx / kf.n_codes, s = idx % kf.n_codes;
+        const int64_t gi = cbase + cc;
+        int v = 0;
+        if (gi < a.q) {
+          const uint32_t* row = a.rows + (size_t)gi * words;
+          const bx_param_desc& p = params[kf.code_param[s]];
+          if (p.kind == BX_PERMUTATION) v = perm_pos(row_u64(row, p.word), p.size, kf.code_sub[s]);
+          else if (p.kind == BX_CATEGORICAL) v = (int)row[p.word] == kf.code_sub[s] ? 1 : 0;
+          else v = (int)row[p.word];
+        }
+        rf_codes[idx] = v;
+      }
+    }
     __syncwarp();
 
     double acc[MT][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+    // forest walk interleaved with the chunks: lane (c, fk) walks trees 4r + fk; lane (c, 0)
+    // keeps the running sum of candidate c in tree order (feasibility.py:89, q >= 2 order)
+    const int rounds = rf ? (kf.n_trees + 3) / 4 : 0;
+    const int rounds_per_chunk = (rounds + n_chunks - 1) / n_chunks;
+    int round = 0;
+    double psum = 0.0;
+    const int32_t* my_codes = rf_codes + c * kf.n_codes;
 
     for (int chunk = 0; chunk < n_chunks; ++chunk) {
       const int buf = chunk & 1;
-      // K* for this lane's four columns of the panel: j = 16 chunk + 4 ks + fk (B fragments)
+      for (int rr = 0; rr < rounds_per_chunk && round < rounds; ++rr, ++round) {
+        const int t = 4 * round + fk;
+        int cur = rf_roots[t < kf.n_trees ? t : 0];
+        for (int it = 0; it <= kf.max_depth; ++it) {
+          const uint32_t nd = rf_nodes[cur];
+          const uint32_t off = nd & 0xFFFFu;
+          if (__all_sync(0xffffffffu, off == 0u)) break;  // every lane sits on a leaf
+          cur += (int)off + (my_codes[(nd >> 25) & 63u] >= (int)((nd >> 16) & 511u) ? 1 : 0);
+        }
+        const double v = rf_uval[rf_vid[cur]];
+        const double v1 = __shfl_down_sync(0xffffffffu, v, 1);
+        const double v2 = __shfl_down_sync(0xffffffffu, v, 2);
+        const double v3 = __shfl_down_sync(0xffffffffu, v, 3);
+        if (fk == 0) {
+          const int t0 = 4 * round;
+          psum = (round == 0) ? v : __dadd_rn(psum, v);
+          if (t0 + 1 < kf.n_trees) psum = __dadd_rn(psum, v1);
+          if (t0 + 2 < kf.n_trees) psum = __dadd_rn(psum, v2);
+          if (t0 + 3 < kf.n_trees) psum = __dadd_rn(psum, v3);
+        }
+      }
+      for (int half = 0; half < kKC / 16; ++half) {
+      const int jb = chunk * kKC + 16 * half;
+      // K* for this lane's four columns of the half panel: j = jb + 4 ks + fk (B fragments)
       double W[4] = {0.0, 0.0, 0.0, 0.0};
       int jj[4];
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        const int j = chunk * kKC + 4 * s + fk;
+        const int j = jb + 4 * s + fk;
         jj[s] = j < n ? j : 0;
       }
       for (int i = 0; i < a.n_num; ++i) {
@@ -276,17 +351,19 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       double kv[4];
 #pragma unroll
       for (int s = 0; s < 4; ++s)
-        kv[s] = (chunk * kKC + 4 * s + fk < n)
+        kv[s] = (jb + 4 * s + fk < n)
                     ? (a.precise ? kstar(W[s], sigma) : kstar_fast(W[s], mc, s_exp2))
                     : 0.0;
 
-      mbar_wait(&bars[buf], phase[buf]);
-      phase[buf] ^= 1u;
+      if (half == 0) {
+        mbar_wait(&bars[buf], phase[buf]);
+        phase[buf] ^= 1u;
+      }
       const double* As = abuf + (size_t)buf * rows8 * kKCP;
 #pragma unroll
-      for (int ks = 0; ks < kKC / 4; ++ks) {
-        const int mt_lo = (chunk * kKC + ks * 4) >> 3;  // m-tiles above are zero in these columns
-        const double* Af = As + (size_t)c * kKCP + ks * 4 + fk;  // A row 8*m + c
+      for (int ks = 0; ks < 4; ++ks) {
+        const int mt_lo = (jb + ks * 4) >> 3;  // m-tiles above are zero in these columns
+        const double* Af = As + (size_t)c * kKCP + 16 * half + ks * 4 + fk;  // A row 8*m + c
         const double b = kv[ks];
         // enter the unrolled m-tile sequence at mt_lo (Duff's device: one indirect branch)
 #define BX_DM(m)                                                              \
@@ -303,6 +380,7 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
         }
 #undef BX_DM
       }
+      }  // half
       __syncthreads();  // everyone is done with this buffer
       if (tid == 0 && chunk + 2 < n_chunks) issue(chunk + 2, buf);
     }
@@ -334,8 +412,10 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       t_mean[2 * fk + 1] = mn1;
     }
     __syncwarp();
+    const double prob = __shfl_sync(0xffffffffu, psum, (lane & 7) * 4);  // lane c <- lane 4c
     if (lane < 8) {
       const int64_t gi = cbase + lane;
+      if (rf && gi < a.q) a.probs_out[gi] = __ddiv_rn(prob, (double)kf.n_trees);
       if (gi < a.q) {
         const double var_s = fmax(sigma - t_ss[lane], 0.0);          // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * t_mean[lane];  // :328
@@ -361,7 +441,11 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
 template <int MT>
 cudaError_t launch_mt(const FusedArgs& a, int sm_count, cudaStream_t s) {
   constexpr int nw = warps_for<MT>();
-  const FusedLayout L = fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT);
+  const CompactForestDev& kf = a.kf;
+  const FusedLayout L = kf.enabled ? fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT,
+                                                  kf.n_nodes, kf.n_uvals, kf.n_trees, kf.n_codes)
+                                   : fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT);
+  if (L.total > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(gp_fused_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        L.total);
   if (e != cudaSuccess) return e;
@@ -385,18 +469,25 @@ size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8) {
   return fused_layout(16, n, n_params, n_kendall, rows8).total;  // upper bound over warp counts
 }
 
+size_t fused_smem_bytes_forest(int n, int n_params, int n_kendall, int rows8,
+                               const CompactForestDev& kf) {
+  return fused_layout(16, n, n_params, n_kendall, rows8, kf.n_nodes, kf.n_uvals, kf.n_trees,
+                      kf.n_codes)
+      .total;
+}
+
 // Panel-major padded copy of A for the TMA stream: panel c holds columns [16c, 16c+16) of rows
 // [0, rows8), each row padded to kKCP doubles.
 __global__ void build_panels_kernel(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                     double* panels) {
-  const int64_t total = (int64_t)(ncols_pad / kKC) * rows8 * kKCP;
+  const int64_t total = (int64_t)((ncols_pad + kKC - 1) / kKC) * rows8 * kKCP;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int chunk = (int)(t / ((int64_t)rows8 * kKCP));
     const int rem = (int)(t % ((int64_t)rows8 * kKCP));
     const int r = rem / kKCP, cc = rem % kKCP;
     double v = 0.0;
-    if (cc < kKC && r < rows_src) v = A[(size_t)r * lda + chunk * kKC + cc];
+    if (cc < kKC && r < rows_src && chunk * kKC + cc < ncols_pad) v = A[(size_t)r * lda + chunk * kKC + cc];
     panels[t] = v;
   }
 }
@@ -407,7 +498,9 @@ cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncol
   return cudaGetLastError();
 }
 
-size_t panels_doubles(int ncols_pad, int rows8) { return (size_t)(ncols_pad / kKC) * rows8 * kKCP; }
+size_t panels_doubles(int ncols_pad, int rows8) {
+  return (size_t)((ncols_pad + kKC - 1) / kKC) * rows8 * kKCP;
+}
 
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s) {
   switch (a.mt) {

@@ -44,6 +44,8 @@ def main(case="C3", q=1 << 20, reps=5):
             ts.append(a.elapsed_time(b))
         ms = min(ts)
         print(f"{case} n={gp._cho[0].shape[0]} q={q} {name:18s} {ms:8.3f} ms  {q / ms * 1e3:,.0f} cand/s")
+    sc.score(rows, f_model, meta["eps_f"], k=10, timing=True)
+    print("kernel timing (ms):", {k: round(v, 3) for k, v in sc.last_timing().items()})
     pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
     sc.score_host(pinned.numpy().view(np.uint32), f_model, meta["eps_f"], k=10)
     torch.cuda.synchronize()
