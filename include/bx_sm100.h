@@ -227,6 +227,17 @@ int bx_constraints_eval(bx_handle* h, const uint32_t* dev_rows, int64_t q, uint8
 int bx_lml_batched(bx_handle* h, const double* dev_sq, int32_t n, int32_t D, const double* dev_z,
                    const double* dev_thetas, int32_t c, double* dev_out, void* stream);
 
+/* Log marginal posterior and its gradient (_lml_core, surrogate.py:356-400) for c hyperparameter
+   settings at once, one CTA each.  dev_params: c rows of (sigma, noise, l_1..l_D) in natural
+   units (noise floored at 1e-6 as the reference does).  use_prior adds the Gamma(prior_shape,
+   prior_rate) lengthscale log-density.  Writes dev_value[c], dev_grad[c x (2+D)] (d/dlog sigma,
+   d/dlog noise, d/dlog l_i) when want_grad, and dev_ok[c] = 0 where the Cholesky factorisation
+   fails (the reference raises LinAlgError there; value -inf, gradient 0). */
+int bx_lml_core(bx_handle* h, const double* dev_sq, int32_t n, int32_t D, const double* dev_z,
+                const double* dev_params, int32_t c, double prior_shape, double prior_rate,
+                int32_t use_prior, int32_t want_grad, double* dev_value, double* dev_grad,
+                int32_t* dev_ok, void* stream);
+
 /* Per-parameter squared distances between rows (pairwise_sq_distances, surrogate.py:173-198),
    dev_out: D x qa x qb f64. */
 int bx_pairwise_sq(bx_handle* h, const uint32_t* dev_a, int32_t qa, const uint32_t* dev_b,

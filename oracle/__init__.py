@@ -16,5 +16,5 @@ constraints, forest leaves) agree exactly.
 from .gp import OracleGP, expected_improvement, pairwise_sq, predict, scores  # noqa: F401
 from .forest import OracleForest, features, predict_proba  # noqa: F401
 from .moves import cot_contains, eval_constraint, neighbors  # noqa: F401
-from .lml import coarse_lml, prior_term  # noqa: F401
+from .lml import coarse_lml, lml_core, prior_term  # noqa: F401
 from .search import optimize  # noqa: F401

@@ -30,6 +30,7 @@ EXPORTED = (
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_cot_contains",
     "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64",
+    "bx_lml_core",
 )
 BX_SCORE_TIMING = 4
 
@@ -89,6 +90,7 @@ _SIGS = {
     "bx_pairwise_sq": (C.c_int, [_p, _p, _i32, _p, _i32, _p, _p]),
     "bx_last_timing": (C.c_int, [_p, _p, _p, _p]),
     "bx_probe_fp64": (C.c_int, [C.c_int, _p, _p]),
+    "bx_lml_core": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _f64, _f64, _i32, _i32, _p, _p, _p, _p]),
 }
 
 

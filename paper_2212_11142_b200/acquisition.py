@@ -311,6 +311,40 @@ def _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted):
     return remaining[best]
 
 
+_SQ_CACHE: dict = {}
+
+
+def _device_sq(sc, sq_dists):
+    """The (D, n, n) distance tensor on the device, cached across the ~200 objective calls of one
+    gp_fit (the reference passes the same array object every time, surrogate.py:512)."""
+    arr = np.ascontiguousarray(sq_dists, dtype=np.float64)
+    key = (id(sq_dists), arr.shape, arr.ctypes.data)
+    hit = _SQ_CACHE.get("k")
+    if hit is not None and hit[0] == key and hit[2] is sq_dists:
+        return hit[1]
+    t = torch.as_tensor(arr, device=f"cuda:{sc.device}")
+    _SQ_CACHE["k"] = (key, t, sq_dists)
+    return t
+
+
+def lml_core(sq_dists, z, sigma, noise, lengthscales, want_grad=False, prior=None):
+    """`_lml_core` (surrogate.py:356-400) on the GPU: value, or (value, grad) with the gradient
+    with respect to (log sigma, log noise, log l_1..l_D).  Raises numpy.linalg.LinAlgError when
+    the Gram matrix is not positive definite, as the reference's np.linalg.cholesky does."""
+    sc = scorer()
+    dev = f"cuda:{sc.device}"
+    sq = _device_sq(sc, sq_dists)
+    zz = torch.as_tensor(np.ascontiguousarray(z, dtype=np.float64), device=dev)
+    prm = np.concatenate([[float(sigma), float(noise)], np.asarray(lengthscales, dtype=np.float64)])
+    params = torch.as_tensor(prm[None, :], device=dev)
+    value, grad, ok = sc.lml_core(sq, zz, params, want_grad, prior)
+    if int(ok.item()) == 0:
+        raise np.linalg.LinAlgError("Matrix is not positive definite")
+    if not want_grad:
+        return float(value.item())
+    return float(value.item()), grad[0].cpu().numpy()
+
+
 def batched_coarse_lml(sq_dists, z, thetas):
     """`_batched_coarse_lml` (surrogate.py:420-456) on the GPU: one CTA per hyperparameter
     candidate, -inf where the Cholesky factorisation fails."""

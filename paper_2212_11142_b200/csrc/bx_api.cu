@@ -89,7 +89,7 @@ struct bx_handle {
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
-  DevBuf d_panels, d_ei;
+  DevBuf d_panels, d_ei, d_grad_scratch;
   cudaStream_t rf_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_rf = nullptr;
 };
@@ -278,6 +278,7 @@ void bx_destroy(bx_handle* h) {
     if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
   h->d_panels.release();
   h->d_ei.release();
+  h->d_grad_scratch.release();
   if (h->rf_stream) cudaStreamDestroy(h->rf_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_rf) cudaEventDestroy(h->ev_rf);
@@ -1072,6 +1073,21 @@ int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const d
     scratch = h->d_lml_scratch.as<double>();
   }
   BX_CUDA(h, launch_lml(sq, n, D, z, thetas, c, out, scratch, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const double* z,
+                const double* params, int32_t c, double prior_shape, double prior_rate,
+                int32_t use_prior, int32_t want_grad, double* value, double* grad, int32_t* ok,
+                void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
+    return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
+  if (want_grad && !grad) return fail(h, BX_ERR_ARG, "want_grad needs a gradient buffer");
+  cudaSetDevice(h->device);
+  BX_CUDA(h, h->d_grad_scratch.ensure(lml_grad_scratch_doubles(n, c) * sizeof(double)));
+  BX_CUDA(h, launch_lml_grad(sq, n, D, z, params, c, prior_shape, prior_rate, use_prior, want_grad,
+                             value, grad, ok, h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
   return BX_OK;
 }
 

@@ -179,6 +179,172 @@ __global__ void __launch_bounds__(kLmlThreads) lml_kernel(const double* sq, int 
   }
 }
 
+// ---- _lml_core with gradient (surrogate.py:356-400), one CTA per hyperparameter setting ------
+// params row: (sigma, noise, l_1 .. l_D) in natural units, as _lml_core receives them.
+// Scratch per CTA: K (n x n), L (n x n), X = L^-1 (n x n), u, alpha (n).
+constexpr int kGradThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(kGradThreads) lml_grad_kernel(const double* sq, int n, int D,
+                                                                const double* z, const double* prm,
+                                                                double prior_k, double prior_rate,
+                                                                int use_prior, int want_grad,
+                                                                double* out_value, double* out_grad,
+                                                                int* out_ok, double* scratch) {
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const size_t nn = (size_t)n * n;
+  double* K = scratch + (size_t)c * (3 * nn + 2 * n);
+  double* L = K + nn;
+  double* X = L + nn;
+  double* u = X + nn;
+  double* al = u + n;
+  __shared__ double inv_l2[BX_MAX_PARAMS];
+  __shared__ double red[kGradThreads / 32];
+  __shared__ int failed;
+  const double* p = prm + (size_t)c * (2 + D);
+  const double sigma = p[0];
+  const double noise = fmax(p[1], 1e-6);  // NOISE_FLOOR
+  for (int k = tid; k < D; k += blockDim.x) inv_l2[k] = 1.0 / (p[2 + k] * p[2 + k]);
+  if (tid == 0) failed = 0;
+  __syncthreads();
+  // K and Ky = K + (noise + jitter) I  (surrogate.py:365-371)
+  for (size_t t = tid; t < nn; t += blockDim.x) {
+    const int i = (int)(t / n), j = (int)(t % n);
+    double W = 0.0;
+    for (int k = 0; k < D; ++k) W = fma(sq[(size_t)k * nn + t], inv_l2[k], W);
+    const double d = sqrt(fmax(W, 0.0));
+    const double E = exp(-kSqrt5 * d);
+    const double kv = sigma * ((1.0 + kSqrt5 * d + (5.0 / 3.0) * W) * E);
+    K[t] = kv;
+    L[t] = (i == j) ? kv + noise + 1e-9 : kv;
+  }
+  __syncthreads();
+  // right-looking Cholesky on the lower triangle of L
+  for (int j = 0; j < n; ++j) {
+    const double piv = L[(size_t)j * n + j];
+    if (!(piv > 0.0)) {
+      if (tid == 0) failed = 1;
+      break;
+    }
+    const double ljj = sqrt(piv);
+    __syncthreads();
+    if (tid == 0) L[(size_t)j * n + j] = ljj;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) L[(size_t)i * n + j] /= ljj;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int t = tid; t < m * m; t += blockDim.x) {
+      const int i = j + 1 + t / m, k = j + 1 + t % m;
+      if (k <= i) L[(size_t)i * n + k] -= L[(size_t)i * n + j] * L[(size_t)k * n + j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (failed) {
+    if (tid == 0) {
+      out_ok[c] = 0;
+      out_value[c] = -INFINITY;
+    }
+    if (want_grad)
+      for (int k = tid; k < 2 + D; k += blockDim.x) out_grad[(size_t)c * (2 + D) + k] = 0.0;
+    return;
+  }
+  // u = L^-1 z, alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374)
+  for (int i = tid; i < n; i += blockDim.x) u[i] = z[i];
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    const double uj = u[j] / L[(size_t)j * n + j];
+    __syncthreads();
+    if (tid == 0) u[j] = uj;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) u[i] -= L[(size_t)i * n + j] * uj;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) al[i] = u[i];
+  for (int j = n - 1; j >= 0; --j) {
+    __syncthreads();
+    const double aj = al[j] / L[(size_t)j * n + j];
+    __syncthreads();
+    if (tid == 0) al[j] = aj;
+    for (int i = tid; i < j; i += blockDim.x) al[i] -= L[(size_t)j * n + i] * aj;
+  }
+  __syncthreads();
+  double za = 0.0, ld = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    za = fma(z[i], al[i], za);
+    ld += log(L[(size_t)i * n + i]);
+  }
+  za = block_sum(za, red);
+  ld = block_sum(ld, red);
+  double value = -0.5 * za - ld - 0.5 * n * log(2.0 * 3.14159265358979323846);
+  if (use_prior) {  // Gamma(k, rate) log density per lengthscale (surrogate.py:380-383)
+    double sl = 0.0, sll = 0.0;
+    for (int k = 0; k < D; ++k) {
+      sl += p[2 + k];
+      sll += log(p[2 + k]);
+    }
+    value += D * (prior_k * log(prior_rate) - lgamma(prior_k)) + (prior_k - 1.0) * sll - prior_rate * sl;
+  }
+  if (tid == 0) {
+    out_ok[c] = 1;
+    out_value[c] = value;
+  }
+  if (!want_grad) return;
+  // X = L^-1, one column per thread (forward substitution)
+  for (int j = tid; j < n; j += blockDim.x) {
+    for (int i = 0; i < j; ++i) X[(size_t)i * n + j] = 0.0;
+    X[(size_t)j * n + j] = 1.0 / L[(size_t)j * n + j];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s = fma(L[(size_t)i * n + k], X[(size_t)k * n + j], s);
+      X[(size_t)i * n + j] = -s / L[(size_t)i * n + i];
+    }
+  }
+  __syncthreads();
+  // M = alpha alpha^T - X^T X; gradient sums (surrogate.py:386-399)
+  double g0 = 0.0, g1 = 0.0;
+  double gl[BX_MAX_PARAMS];
+  for (int k = 0; k < D; ++k) gl[k] = 0.0;
+  for (size_t t = tid; t < nn; t += blockDim.x) {
+    const int a = (int)(t / n), b = (int)(t % n);
+    const int k0 = a > b ? a : b;
+    double kinv = 0.0;
+    for (int k = k0; k < n; ++k) kinv = fma(X[(size_t)k * n + a], X[(size_t)k * n + b], kinv);
+    const double M = al[a] * al[b] - kinv;
+    g0 = fma(M, K[t], g0);
+    if (a == b) g1 += M;
+    double W = 0.0;
+    for (int k = 0; k < D; ++k) W = fma(sq[(size_t)k * nn + t], inv_l2[k], W);
+    const double d = sqrt(fmax(W, 0.0));
+    const double MG = M * ((1.0 + kSqrt5 * d) * exp(-kSqrt5 * d));
+    for (int k = 0; k < D; ++k) gl[k] = fma(MG, sq[(size_t)k * nn + t], gl[k]);
+  }
+  g0 = block_sum(g0, red);
+  g1 = block_sum(g1, red);
+  double* g = out_grad + (size_t)c * (2 + D);
+  if (tid == 0) {
+    g[0] = 0.5 * g0;
+    g[1] = 0.5 * noise * g1;
+  }
+  const double scale = (5.0 / 6.0) * sigma;
+  for (int k = 0; k < D; ++k) {
+    const double s = block_sum(gl[k], red);
+    if (tid == 0) {
+      const double l = p[2 + k];
+      double gk = (scale / (l * l)) * s;
+      if (use_prior) gk += (prior_k - 1.0) - prior_rate * l;
+      g[2 + k] = gk;
+    }
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -189,6 +355,18 @@ int grid_for(int64_t work, int threads) {
 }  // namespace
 
 size_t lml_scratch_doubles(int n, int c) { return (size_t)c * ((size_t)n * (n + 1) / 2 + n); }
+
+size_t lml_grad_scratch_doubles(int n, int c) { return (size_t)c * (3 * (size_t)n * n + 2 * (size_t)n); }
+
+cudaError_t launch_lml_grad(const double* sq, int n, int D, const double* z, const double* prm,
+                            int c, double prior_k, double prior_rate, int use_prior, int want_grad,
+                            double* out_value, double* out_grad, int* out_ok, double* scratch,
+                            cudaStream_t s) {
+  if (c <= 0) return cudaSuccess;
+  lml_grad_kernel<<<c, kGradThreads, 0, s>>>(sq, n, D, z, prm, prior_k, prior_rate, use_prior,
+                                              want_grad, out_value, out_grad, out_ok, scratch);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_lml(const double* sq, int n, int D, const double* z, const double* thetas, int c,
                        double* out, double* scratch, cudaStream_t s) {

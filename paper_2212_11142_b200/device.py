@@ -279,6 +279,21 @@ class Scorer:
                                              _ptr(out), self.stream))
         return out
 
+    def lml_core(self, sq: torch.Tensor, z: torch.Tensor, params: torch.Tensor, want_grad: bool,
+                 prior=None):
+        """bx_lml_core: (values[c], grads[c, 2+D] | None, ok[c]) for rows (sigma, noise, l...)."""
+        D, n, _ = sq.shape
+        c = params.shape[0]
+        dev = sq.device
+        value = torch.empty(c, dtype=torch.float64, device=dev)
+        grad = torch.empty((c, 2 + D), dtype=torch.float64, device=dev) if want_grad else None
+        ok = torch.empty(c, dtype=torch.int32, device=dev)
+        k, rate = (float(prior.shape), float(prior.rate)) if prior is not None else (0.0, 0.0)
+        self._check(self._lib.bx_lml_core(self.h, _ptr(sq.contiguous()), n, D, _ptr(z.contiguous()),
+                                          _ptr(params.contiguous()), c, k, rate, int(prior is not None),
+                                          int(want_grad), _ptr(value), _ptr(grad), _ptr(ok), self.stream))
+        return value, grad, ok
+
     def lml_batched(self, sq: torch.Tensor, z: torch.Tensor, thetas: torch.Tensor) -> torch.Tensor:
         D, n, _ = sq.shape
         c = thetas.shape[0]

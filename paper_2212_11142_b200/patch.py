@@ -17,6 +17,7 @@ TARGETS = (
     ("acquisition", "_scores", gpu.scores),
     ("acquisition", "neighbors", gpu.neighbors),
     ("surrogate", "_batched_coarse_lml", gpu.batched_coarse_lml),
+    ("surrogate", "_lml_core", gpu.lml_core),
 )
 METHODS = (
     ("surrogate", "GPModel", "predict_batch", gpu.predict_batch),

@@ -137,6 +137,18 @@ def score_case(case, desc, n_train, q, seed, *, rf_rule=None, eps=0.0, hyper="fi
     arrays["lml_z"] = z
     arrays["lml"] = ref_sur._batched_coarse_lml(sq, z, th)
     arrays["lml_prior"] = ref_sur._prior_term(th, ref_sur.LengthscalePrior())
+    # _lml_core value + gradient (the L-BFGS-B objective) at the first 8 coarse settings
+    core_v, core_g, core_ok = [], [], []
+    for t in th[:8]:
+        try:
+            v, g = ref_sur._lml_core(sq, z, math.exp(t[0]), math.exp(t[1]), np.exp(t[2:]),
+                                     want_grad=True, prior=ref_sur.LengthscalePrior())
+            core_v.append(v), core_g.append(g), core_ok.append(True)
+        except np.linalg.LinAlgError:
+            core_v.append(-np.inf), core_g.append(np.zeros(2 + space.dimension)), core_ok.append(False)
+    arrays["core_value"] = np.array(core_v)
+    arrays["core_grad"] = np.array(core_g)
+    arrays["core_ok"] = np.array(core_ok)
     if extra:
         extra(space, cot, gp, feas, ctx, cands, meta, arrays, rng)
     save(case, meta, arrays)

@@ -131,6 +131,30 @@ def test_pairwise_and_lml(case, sc):
 
 
 @pytest.mark.parametrize("case", CASES)
+def test_lml_core_gradient(case, sc):
+    """_lml_core value and gradient (surrogate.py:356-400) vs the reference's own numbers."""
+    from paper_2212_11142_b200 import acquisition as A
+
+    class Prior:
+        shape, rate = 2.0, 2.0
+
+    meta, arr, space = load(case)
+    og, _ = oracle_model(meta, arr, space)
+    sq = oracle.pairwise_sq(space, og.configs, og.configs, og.use_transforms)
+    for t, v, g, ok in zip(arr["lml_thetas"][:8], arr["core_value"], arr["core_grad"], arr["core_ok"]):
+        args = (sq, arr["lml_z"], np.exp(t[0]), np.exp(t[1]), np.exp(t[2:]))
+        if not ok:
+            with pytest.raises(np.linalg.LinAlgError):
+                A.lml_core(*args, want_grad=True, prior=Prior())
+            continue
+        val, grad = A.lml_core(*args, want_grad=True, prior=Prior())
+        assert val == pytest.approx(v, rel=1e-9, abs=1e-7)
+        np.testing.assert_allclose(grad, g, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(g).max()))
+        assert A.lml_core(*args, want_grad=False, prior=None) == pytest.approx(
+            oracle.lml_core(*args, want_grad=False, prior=None), rel=1e-9, abs=1e-7)
+
+
+@pytest.mark.parametrize("case", CASES)
 def test_summary_consistent_with_values(case, sc):
     """Fused top-k / tracker reductions equal the host reductions over the same values."""
     meta, arr, space = load(case)

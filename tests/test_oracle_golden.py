@@ -79,6 +79,21 @@ def test_pairwise_and_lml(case):
     np.testing.assert_allclose(oracle.prior_term(arr["lml_thetas"]), arr["lml_prior"], rtol=1e-13)
 
 
+@pytest.mark.parametrize("case", CASES)
+def test_lml_core_value_and_gradient(case):
+    meta, arr, space = load(case)
+    og, _ = oracle_model(meta, arr, space)
+    sq = oracle.pairwise_sq(space, og.configs, og.configs, og.use_transforms)
+    for t, v, g, ok in zip(arr["lml_thetas"][:8], arr["core_value"], arr["core_grad"], arr["core_ok"]):
+        if not ok:
+            with pytest.raises(np.linalg.LinAlgError):
+                oracle.lml_core(sq, arr["lml_z"], np.exp(t[0]), np.exp(t[1]), np.exp(t[2:]), True)
+            continue
+        val, grad = oracle.lml_core(sq, arr["lml_z"], np.exp(t[0]), np.exp(t[1]), np.exp(t[2:]), True)
+        assert val == pytest.approx(v, rel=1e-9, abs=1e-7)
+        np.testing.assert_allclose(grad, g, rtol=1e-6, atol=1e-6 * max(1.0, np.abs(g).max()))
+
+
 @pytest.mark.parametrize("case", ["C1", "C2", "C3"])
 def test_selection_matches_reference(case):
     meta, arr, space = load(case)
