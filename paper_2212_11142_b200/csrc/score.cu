@@ -322,120 +322,6 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
   }
 }
 
-// ---- merge --------------------------------------------------------------------------------
-constexpr int kMergeThreads = 32;
-
-__device__ bool rec_better_key(const TopRec& a, const uint32_t* arow, const TopRec& b,
-                               const uint32_t* brow, bool by_prob, const bx_param_desc* params,
-                               int n_params, const int32_t* rank_lut) {
-  if (a.index < 0) return false;
-  if (b.index < 0) return true;
-  const double x = by_prob ? a.prob : a.value, y = by_prob ? b.prob : b.value;
-  if (x != y) return x > y;
-  return key_cmp(params, n_params, rank_lut, arow, brow) < 0;
-}
-
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const Partial* parts, int n_parts,
-                                                              SpaceDev space, int k,
-                                                              const uint32_t* pool_rows,
-                                                              int64_t index_base,
-                                                              bx_score_summary* out) {
-  __shared__ bx_param_desc params[BX_MAX_PARAMS];
-  __shared__ TopRec lists[kMergeThreads][BX_MAX_K];
-  __shared__ int counts[kMergeThreads];
-  __shared__ int best_at[kMergeThreads], prob_at[kMergeThreads];
-  __shared__ long long scored[kMergeThreads], finite[kMergeThreads];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < space.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
-    reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(space.params)[i];
-  __syncthreads();
-  int nt = 0, bi = -1, pi = -1;
-  long long sc = 0, fi = 0;
-  for (int p = tid; p < n_parts; p += blockDim.x) {
-    const Partial& P = parts[p];
-    sc += P.n_scored;
-    fi += P.n_finite;
-    for (int i = 0; i < P.n_top; ++i) {
-      const TopRec r = P.top[i];
-      if (nt == k && !top_before(r.value, r.index, lists[tid][k - 1])) break;
-      top_insert(lists[tid], nt, k, r);
-    }
-    if (P.best.index >= 0 &&
-        (bi < 0 || rec_better_key(P.best, P.best_row, parts[bi].best, parts[bi].best_row, false,
-                                  params, space.n_params, space.rank_lut)))
-      bi = p;
-    if (P.best_prob.index >= 0 &&
-        (pi < 0 || rec_better_key(P.best_prob, P.best_prob_row, parts[pi].best_prob,
-                                  parts[pi].best_prob_row, true, params, space.n_params,
-                                  space.rank_lut)))
-      pi = p;
-  }
-  counts[tid] = nt;
-  best_at[tid] = bi;
-  prob_at[tid] = pi;
-  scored[tid] = sc;
-  finite[tid] = fi;
-  __syncthreads();
-  if (tid == 0) {
-    TopRec top[BX_MAX_K];
-    int n = 0;
-    long long S = 0, F = 0;
-    int b = -1, pb = -1;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      S += scored[t];
-      F += finite[t];
-      for (int i = 0; i < counts[t]; ++i) {
-        if (n == k && !top_before(lists[t][i].value, lists[t][i].index, top[k - 1])) break;
-        top_insert(top, n, k, lists[t][i]);
-      }
-      const int cb = best_at[t];
-      if (cb >= 0 && (b < 0 || rec_better_key(parts[cb].best, parts[cb].best_row, parts[b].best,
-                                              parts[b].best_row, false, params, space.n_params,
-                                              space.rank_lut)))
-        b = cb;
-      const int cp = prob_at[t];
-      if (cp >= 0 && (pb < 0 || rec_better_key(parts[cp].best_prob, parts[cp].best_prob_row,
-                                               parts[pb].best_prob, parts[pb].best_prob_row, true,
-                                               params, space.n_params, space.rank_lut)))
-        pb = cp;
-    }
-    out->n_scored = S;
-    out->n_finite = F;
-    out->k = k;
-    out->n_top = n;
-    for (int i = 0; i < n; ++i) {
-      out->top[i].value = top[i].value;
-      out->top[i].prob = top[i].prob;
-      out->top[i].index = top[i].index;
-    }
-    const int W = space.row_words;
-    out->best.index = -1;
-    out->best.value = out->best.prob = -INFINITY;
-    if (b >= 0) {
-      out->best.value = parts[b].best.value;
-      out->best.prob = parts[b].best.prob;
-      out->best.index = parts[b].best.index;
-      for (int w = 0; w < W; ++w) out->best.row[w] = parts[b].best_row[w];
-    }
-    out->best_prob.index = -1;
-    out->best_prob.value = out->best_prob.prob = -INFINITY;
-    if (pb >= 0) {
-      out->best_prob.value = parts[pb].best_prob.value;
-      out->best_prob.prob = parts[pb].best_prob.prob;
-      out->best_prob.index = parts[pb].best_prob.index;
-      for (int w = 0; w < W; ++w) out->best_prob.row[w] = parts[pb].best_prob_row[w];
-    }
-  }
-  __syncthreads();
-  if (pool_rows) {  // gather the rows of the top-k entries
-    const int W = space.row_words;
-    for (int t = tid; t < out->n_top * W; t += blockDim.x) {
-      const int i = t / W, w = t % W;
-      out->top[i].row[w] = pool_rows[(size_t)(out->top[i].index - index_base) * W + w];
-    }
-  }
-}
-
 template <int CPW>
 cudaError_t launch_score_t(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials) {
   const SmemLayout L = smem_layout(CPW, a.gp.ncols_pad, a.space.n_params);
@@ -469,11 +355,5 @@ cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* 
   return launch_score_t<8>(a, sm_count, s, n_partials);
 }
 
-cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const SpaceDev& space,
-                                 int k, const uint32_t* pool_rows, int64_t index_base,
-                                 bx_score_summary* out, cudaStream_t s) {
-  merge_kernel<<<1, kMergeThreads, 0, s>>>(partials, n_partials, space, k, pool_rows, index_base, out);
-  return cudaGetLastError();
-}
 
 }  // namespace bx
