@@ -155,7 +155,8 @@ int bx_set_evaluated(bx_handle* h, const uint32_t* host_rows, int32_t count);
 int bx_set_cot(bx_handle* h, int32_t n_groups, const int32_t* host_group_kind,
                const int32_t* host_group_param_begin, const int32_t* host_group_params,
                const int32_t* host_group_root, int32_t n_nodes, const int32_t* host_child_begin,
-               const int32_t* host_child_count, const int32_t* host_node_value);
+               const int32_t* host_child_count, const int32_t* host_node_value,
+               const int64_t* host_node_leaf_count /* nullable: needed by bx_generate mode 1 */);
 int bx_clear_cot(bx_handle* h);
 
 /* Known constraints as stack bytecode (opcode table in paper_2212_11142_b200/constraints.py).
@@ -197,6 +198,19 @@ int bx_score(bx_handle* h, const uint32_t* dev_rows, int64_t q, int64_t index_ba
 int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t index_base,
                   double f_model, double eps_f, int32_t k, int32_t flags,
                   bx_score_summary* host_summary, void* stream);
+
+/* Device-side candidate generation: q rows for global indices
+   index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the
+   dense space (sample_uniform's distribution, space.py:312-332), mode 1 = leaf-uniform over the
+   chain of trees (sample_leaf_uniform's, constraints.py:471-523; needs bx_set_cot leaf counts). */
+int bx_generate(bx_handle* h, uint64_t seed, int64_t index_base, int64_t q, int32_t mode,
+                uint32_t* dev_rows, void* stream);
+
+/* Score a device-generated pool of q candidates chunk by chunk without materialising it (pools of
+   10^9 and beyond); the summary's top-k rows are regenerated from their indices. */
+int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t q, int32_t mode,
+                       double f_model, double eps_f, int32_t k, bx_score_summary* host_summary,
+                       void* stream);
 
 /* Posterior mean / latent variance, de-standardised (predict_batch, include_noise=False). */
 int bx_gp_predict(bx_handle* h, const uint32_t* dev_rows, int64_t q, double* dev_mean,

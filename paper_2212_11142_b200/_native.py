@@ -30,7 +30,7 @@ EXPORTED = (
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_cot_contains",
     "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64",
-    "bx_lml_core",
+    "bx_lml_core", "bx_generate", "bx_score_generated",
 )
 BX_SCORE_TIMING = 4
 
@@ -75,7 +75,7 @@ _SIGS = {
     "bx_set_forest": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _f64]),
     "bx_clear_forest": (C.c_int, [_p]),
     "bx_set_evaluated": (C.c_int, [_p, _p, _i32]),
-    "bx_set_cot": (C.c_int, [_p, _i32, _p, _p, _p, _p, _i32, _p, _p, _p]),
+    "bx_set_cot": (C.c_int, [_p, _i32, _p, _p, _p, _p, _i32, _p, _p, _p, _p]),
     "bx_clear_cot": (C.c_int, [_p]),
     "bx_set_constraints": (C.c_int, [_p, _i32, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _i32]),
     "bx_score": (C.c_int, [_p, _p, _i64, _i64, _f64, _f64, _i32, _i32, _p, _p, _p, _p]),
@@ -91,6 +91,8 @@ _SIGS = {
     "bx_last_timing": (C.c_int, [_p, _p, _p, _p]),
     "bx_probe_fp64": (C.c_int, [C.c_int, _p, _p]),
     "bx_lml_core": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _f64, _f64, _i32, _i32, _p, _p, _p, _p]),
+    "bx_generate": (C.c_int, [_p, C.c_uint64, _i64, _i64, _i32, _p, _p]),
+    "bx_score_generated": (C.c_int, [_p, C.c_uint64, _i64, _i64, _i32, _f64, _f64, _i32, _p, _p]),
 }
 
 

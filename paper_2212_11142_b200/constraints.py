@@ -537,13 +537,14 @@ class CotTables:
     child_begin: np.ndarray        # [n_nodes] first child node id
     child_count: np.ndarray        # [n_nodes]
     node_value: np.ndarray         # [n_nodes] domain index of the node's value (-1 for roots)
+    leaf_count: np.ndarray = None  # [n_nodes] leaves below each node (leaf-uniform generation)
 
 
 def flatten_cot(cot, layout) -> CotTables:
     """Breadth-first node tables of a ChainOfTrees (the reference's or ours).  Children of a node
     get consecutive ids, in creation order = ascending domain index (constraints.py:621)."""
     kinds, pbeg, plist, roots = [], [0], [], []
-    begin, count, value = [], [], []
+    begin, count, value, leaves = [], [], [], []
     for g in cot.groups:
         plist.extend(int(i) for i in g.indices)
         pbeg.append(len(plist))
@@ -564,9 +565,10 @@ def flatten_cot(cot, layout) -> CotTables:
         for node, depth in order:
             begin.append(nxt)
             count.append(len(node.children))
+            leaves.append(int(node.leaf_count))
             nxt += len(node.children)
             value.append(-1 if depth < 0 else layout.slots[g.indices[depth]].index[node.value])
     return CotTables(len(kinds), np.asarray(kinds, np.int32), np.asarray(pbeg, np.int32),
                      np.asarray(plist or [0], np.int32), np.asarray(roots or [0], np.int32),
                      len(value), np.asarray(begin or [0], np.int32), np.asarray(count or [0], np.int32),
-                     np.asarray(value or [0], np.int32))
+                     np.asarray(value or [0], np.int32), np.asarray(leaves or [0], np.int64))

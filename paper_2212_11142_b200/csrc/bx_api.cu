@@ -89,7 +89,8 @@ struct bx_handle {
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
-  DevBuf d_panels, d_ei, d_grad_scratch;
+  DevBuf d_panels, d_ei, d_grad_scratch, d_leaf_count, d_gen_rows;
+  bool has_leaf_count = false;
   cudaStream_t rf_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_rf = nullptr;
 };
@@ -279,6 +280,8 @@ void bx_destroy(bx_handle* h) {
   h->d_panels.release();
   h->d_ei.release();
   h->d_grad_scratch.release();
+  h->d_leaf_count.release();
+  h->d_gen_rows.release();
   if (h->rf_stream) cudaStreamDestroy(h->rf_stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_rf) cudaEventDestroy(h->ev_rf);
@@ -681,7 +684,8 @@ int bx_set_evaluated(bx_handle* h, const uint32_t* rows, int32_t count) {
 int bx_set_cot(bx_handle* h, int32_t n_groups, const int32_t* group_kind,
                const int32_t* group_param_begin, const int32_t* group_params,
                const int32_t* group_root, int32_t n_nodes, const int32_t* child_begin,
-               const int32_t* child_count, const int32_t* node_value) {
+               const int32_t* child_count, const int32_t* node_value,
+               const int64_t* node_leaf_count) {
   int r = check_space(h);
   if (r) return r;
   if (n_groups < 0 || n_nodes < 0) return fail(h, BX_ERR_ARG, "bad chain-of-trees sizes");
@@ -709,6 +713,8 @@ int bx_set_cot(bx_handle* h, int32_t n_groups, const int32_t* group_kind,
   h->cot.child_begin = h->d_child_begin.as<int32_t>();
   h->cot.child_count = h->d_child_count.as<int32_t>();
   h->cot.node_value = h->d_child_value.as<int32_t>();
+  h->has_leaf_count = node_leaf_count != nullptr;
+  if (node_leaf_count) BX_CUDA(h, upload(h->d_leaf_count, node_leaf_count, n_nodes));
   h->has_cot = true;
   return BX_OK;
 }
@@ -1073,6 +1079,82 @@ int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const d
     scratch = h->d_lml_scratch.as<double>();
   }
   BX_CUDA(h, launch_lml(sq, n, D, z, thetas, c, out, scratch, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+static int check_generate(bx_handle* h, int32_t mode) {
+  int r = check_space(h);
+  if (r) return r;
+  if (mode != 0 && mode != 1) return fail(h, BX_ERR_ARG, "generation mode %d not in {0, 1}", mode);
+  if (mode == 1 && !(h->has_cot && h->has_leaf_count))
+    return fail(h, BX_ERR_STATE, "mode 1 needs bx_set_cot with node leaf counts");
+  return BX_OK;
+}
+
+int bx_generate(bx_handle* h, uint64_t seed, int64_t index_base, int64_t q, int32_t mode,
+                uint32_t* rows, void* stream) {
+  int r = check_generate(h, mode);
+  if (r) return r;
+  cudaSetDevice(h->device);
+  CotDev cot = h->has_cot ? h->cot : CotDev{};
+  BX_CUDA(h, launch_generate(space_dev(h), cot, h->d_leaf_count.as<int64_t>(), mode, seed, index_base,
+                             q, rows, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t q, int32_t mode,
+                       double f_model, double eps_f, int32_t k, bx_score_summary* summary,
+                       void* stream) {
+  int r = check_gp(h);
+  if (r) return r;
+  r = check_generate(h, mode);
+  if (r) return r;
+  if (q < 1) return fail(h, BX_ERR_ARG, "empty candidate pool");
+  if (!summary) return fail(h, BX_ERR_ARG, "bx_score_generated needs a summary");
+  if (k < 0 || k > BX_MAX_K) return fail(h, BX_ERR_ARG, "k=%d outside [0, %d]", k, BX_MAX_K);
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int W = h->row_words;
+  const int64_t chunk = 1 << 22;
+  const int64_t n_chunks = (q + chunk - 1) / chunk;
+  const size_t per_chunk = (size_t)max_partials(h->sm_count);
+  BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
+  BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
+  BX_CUDA(h, h->d_gen_rows.ensure((size_t)chunk * W * 4));
+  CotDev cot = h->has_cot ? h->cot : CotDev{};
+  Partial* base = h->d_partials.as<Partial>();
+  for (int pass = 0; pass < 2; ++pass) {
+    int total = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      const int64_t off = c * chunk;
+      const int64_t len = (q - off) < chunk ? (q - off) : chunk;
+      BX_CUDA(h, launch_generate(space_dev(h), cot, h->d_leaf_count.as<int64_t>(), mode, seed,
+                                 index_base + off, len, h->d_gen_rows.as<uint32_t>(), s));
+      int np = 0;
+      r = score_impl(h, h->d_gen_rows.as<uint32_t>(), len, index_base + off, f_model, eps_f, k, 0,
+                     nullptr, nullptr, base + total, &np, s, false, pass == 1);
+      if (r) return r;
+      total += np;
+    }
+    BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
+                                    h->d_summary.as<bx_score_summary>(), s));
+    BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
+                               cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));
+    if (summary->n_finite != 0 || !h->use_fused) break;
+  }
+  // regenerate the top-k rows from their global indices
+  int64_t idx[BX_MAX_K];
+  for (int i = 0; i < summary->n_top; ++i) idx[i] = summary->top[i].index;
+  if (summary->n_top > 0) {
+    BX_CUDA(h, launch_generate_indexed(space_dev(h), cot, h->d_leaf_count.as<int64_t>(), mode, seed,
+                                       idx, summary->n_top, h->d_gen_rows.as<uint32_t>(), s));
+    std::vector<uint32_t> rows((size_t)summary->n_top * W);
+    BX_CUDA(h, cudaMemcpyAsync(rows.data(), h->d_gen_rows.p, rows.size() * 4, cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));
+    for (int i = 0; i < summary->n_top; ++i)
+      std::memcpy(summary->top[i].row, rows.data() + (size_t)i * W, (size_t)W * 4);
+  }
   return BX_OK;
 }
 

@@ -394,6 +394,13 @@ cudaError_t launch_constraints(const SpaceDev& space, const ConstraintDev& c, co
                                int64_t q, uint8_t* mask, cudaStream_t s);
 cudaError_t launch_lml(const double* sq, int n, int D, const double* z, const double* thetas,
                        int c, double* out, double* scratch, cudaStream_t s);
+cudaError_t launch_generate(const SpaceDev& space, const CotDev& cot, const int64_t* leaf_count,
+                            int mode, uint64_t seed, int64_t index_base, int64_t q, uint32_t* rows,
+                            cudaStream_t s);
+cudaError_t launch_generate_indexed(const SpaceDev& space, const CotDev& cot,
+                                    const int64_t* leaf_count, int mode, uint64_t seed,
+                                    const int64_t* host_indices, int count, uint32_t* rows,
+                                    cudaStream_t s);
 cudaError_t launch_lml_grad(const double* sq, int n, int D, const double* z, const double* prm,
                             int c, double prior_k, double prior_rate, int use_prior, int want_grad,
                             double* out_value, double* out_grad, int* out_ok, double* scratch,

@@ -179,7 +179,7 @@ class Scorer:
         self._check(self._lib.bx_set_cot(self.h, t.n_groups, _ptr(t.group_kind),
                                          _ptr(t.group_param_begin), _ptr(t.group_params),
                                          _ptr(t.group_root), t.n_nodes, _ptr(t.child_begin),
-                                         _ptr(t.child_count), _ptr(t.node_value)))
+                                         _ptr(t.child_count), _ptr(t.node_value), _ptr(t.leaf_count)))
         self._cot_tables = t
         self._cot_key = key
 
@@ -235,6 +235,22 @@ class Scorer:
         s = N.ScoreSummary()
         self._check(self._lib.bx_score_host(self.h, _ptr(rows), q, index_base, float(f_model),
                                             float(eps_f), int(k), 0, C.byref(s), self.stream))
+        return self._summary(s)
+
+    def generate(self, q: int, seed: int, mode: int = 0, index_base: int = 0) -> torch.Tensor:
+        """bx_generate: q device-generated rows (mode 0 uniform, 1 chain-of-trees leaf-uniform)."""
+        out = torch.empty((q, self.layout.row_words), dtype=torch.int32, device=f"cuda:{self.device}")
+        self._check(self._lib.bx_generate(self.h, C.c_uint64(seed), index_base, q, mode, _ptr(out),
+                                          self.stream))
+        return out
+
+    def score_generated(self, q: int, seed: int, f_model: float, eps_f: float = 0.0, k: int = 10,
+                        mode: int = 0, index_base: int = 0) -> Summary:
+        """bx_score_generated: score a device-generated pool of q candidates chunk by chunk."""
+        s = N.ScoreSummary()
+        self._check(self._lib.bx_score_generated(self.h, C.c_uint64(seed), index_base, q, mode,
+                                                 float(f_model), float(eps_f), int(k), C.byref(s),
+                                                 self.stream))
         return self._summary(s)
 
     def predict(self, rows: torch.Tensor):
