@@ -119,6 +119,11 @@ void bx_destroy(bx_handle* h);
 const char* bx_last_error(bx_handle* h);
 int bx_abi_version(void);
 int bx_device_sm_count(bx_handle* h);
+/* Which posterior kernel the current model state runs (valid after bx_set_gp):
+   BX_GP_TENSOR (tcgen05 int8 split product), BX_GP_DMMA (register-resident FP64 DMMA) or
+   BX_GP_GENERIC (shared-memory FP64 kernel for n + 1 > 256). */
+enum { BX_GP_GENERIC = 0, BX_GP_DMMA = 1, BX_GP_TENSOR = 2 };
+int bx_gp_kernel(bx_handle* h);
 
 /* ---- model state (once per BO iteration) ------------------------------------------------ */
 /* Space tables.  coord_lut / rank_lut are host arrays indexed by bx_param_desc offsets;

@@ -86,6 +86,12 @@ struct bx_handle {
   // register-resident fused GP path (gp_fused.cu)
   bool use_fused = false;
   bool no_fused = false;  // BX_GP_GENERIC debug switch (env)
+  // tensor-core posterior (gp_tc.cu): digit-sliced [L^-1; alpha^T] + row scales
+  bool use_tc = false;
+  bool no_tc = false;     // BX_GP_DMMA=1 forces the FP64 DMMA kernel
+  int tc_nsl = 0, tc_nch = 0;
+  double tc_kscale = 0;
+  DevBuf d_mdig, d_rowscale;
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
@@ -210,6 +216,23 @@ FusedArgs fused_args(const bx_handle* h, const uint32_t* rows, int64_t q, double
   return f;
 }
 
+// the posterior kernels that take FusedArgs (tensor-core or register-resident DMMA)
+bool fused_path(const bx_handle* h) { return h->use_tc || h->use_fused; }
+
+cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_t s) {
+  if (h->use_tc) {
+    TcArgs t{};
+    t.f = f;
+    t.mdig = h->d_mdig.as<unsigned char>();
+    t.rowscale = h->d_rowscale.as<double>();
+    t.n_slices = h->tc_nsl;
+    t.n_chunks = h->tc_nch;
+    t.kscale = h->tc_kscale;
+    return launch_gp_tc(t, h->sm_count, s);
+  }
+  return launch_gp_fused(f, h->sm_count, s);
+}
+
 int check_gp(bx_handle* h) {
   int r = check_space(h);
   if (r) return r;
@@ -242,6 +265,8 @@ bx_handle* bx_create(int device) {
   for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
   const char* gpg = getenv("BX_GP_GENERIC");
   h->no_fused = gpg && gpg[0] == '1';
+  const char* dm = getenv("BX_GP_DMMA");
+  h->no_tc = h->no_fused || (dm && dm[0] == '1');
   const char* mp = getenv("BX_MATERN_PRECISE");
   h->matern_precise = mp && mp[0] == '1';
   // The forest walk fused into the GP kernel is correct but measured slower than the concurrent
@@ -278,6 +303,8 @@ void bx_destroy(bx_handle* h) {
   for (int i = 0; i < 5; ++i)
     if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
   h->d_panels.release();
+  h->d_mdig.release();
+  h->d_rowscale.release();
   h->d_ei.release();
   h->d_grad_scratch.release();
   h->d_leaf_count.release();
@@ -291,6 +318,11 @@ void bx_destroy(bx_handle* h) {
 const char* bx_last_error(bx_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int bx_device_sm_count(bx_handle* h) { return h ? h->sm_count : 0; }
+
+int bx_gp_kernel(bx_handle* h) {
+  if (!h) return BX_GP_GENERIC;
+  return h->use_tc ? BX_GP_TENSOR : h->use_fused ? BX_GP_DMMA : BX_GP_GENERIC;
+}
 
 int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, int32_t row_words,
                  const double* coord_lut, int32_t coord_len, const int32_t* rank_lut,
@@ -423,6 +455,20 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
                                      h->rows8, h->d_panels.as<double>(), s));
       h->use_fused = true;
     }
+  }
+  // tensor-core path: n <= 255 (8 row chunks) and the shared-memory budget
+  h->use_tc = false;
+  if (!h->no_tc && n <= 255 && tc_smem_bytes(n, D, h->n_kendall) <= 227 * 1024) {
+    int E = 0;
+    frexp(outputscale, &E);  // sigma < 2^E = sc
+    h->tc_nsl = (n + 31) / 32;
+    h->tc_nch = n / 32 + 1;
+    h->tc_kscale = ldexp(1.0, 40 - E);
+    BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
+    BX_CUDA(h, h->d_rowscale.ensure(2 * 256 * 8));
+    BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
+                                 h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), s));
+    h->use_tc = true;
   }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
   h->outputscale = outputscale;
@@ -823,12 +869,12 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   a.partials = partials;
   const bool forest = h->has_forest && h->forest.has_trees;
   if (forest) BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
-  if (h->use_fused) {
+  if (fused_path(h)) {
     // The forest walk runs inside the GP kernel (FP64 and integer/LSU work interleave in the same
     // warps) unless the numpy pairwise order (q == 1) or the table budget rules it out; then it
     // runs on the side stream and is joined before the summary.
     const CompactForestDev& kf = h->forest.kf;
-    const bool fuse_rf = forest && kf.enabled && !(flags & BX_SCORE_RF_PAIRWISE) &&
+    const bool fuse_rf = forest && kf.enabled && !(flags & BX_SCORE_RF_PAIRWISE) && !h->use_tc &&
                          !h->no_fused_forest &&
                          fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
                              220 * 1024;
@@ -848,7 +894,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
       f.probs_out = h->d_probs.as<double>();
     }
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
-    BX_CUDA(h, launch_gp_fused(f, h->sm_count, s));
+    BX_CUDA(h, launch_posterior(h, f, s));
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
@@ -899,7 +945,7 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
     BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
   }
   if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
-  if (want && summary->n_finite == 0 && h->use_fused) {
+  if (want && summary->n_finite == 0 && fused_path(h)) {
     // every value is -inf: only now is the probability tracker needed (acquisition.py:179-184)
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs, partials);
     m.track_prob = 1;
@@ -972,7 +1018,7 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                              cudaMemcpyDeviceToHost, s));
   BX_CUDA(h, cudaStreamSynchronize(s));
-  if (summary->n_finite != 0 || !h->use_fused) break;
+  if (summary->n_finite != 0 || !fused_path(h)) break;
   }
   // the pool is host-resident: the top-k rows come straight from the caller's buffer
   for (int i = 0; i < summary->n_top; ++i)
@@ -997,11 +1043,11 @@ int bx_gp_predict(bx_handle* h, const uint32_t* rows, int64_t q, double* mean, d
   a.mean_out = mean;
   a.var_out = var;
   int np = 0;
-  if (h->use_fused) {
+  if (fused_path(h)) {
     FusedArgs f = fused_args(h, rows, q, 0.0);
     f.mean_out = mean;
     f.var_out = var;
-    BX_CUDA(h, launch_gp_fused(f, h->sm_count, (cudaStream_t)stream));
+    BX_CUDA(h, launch_posterior(h, f, (cudaStream_t)stream));
     return BX_OK;
   }
   BX_CUDA(h, launch_score(a, h->sm_count, (cudaStream_t)stream, &np));
@@ -1141,7 +1187,7 @@ int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t 
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                                cudaMemcpyDeviceToHost, s));
     BX_CUDA(h, cudaStreamSynchronize(s));
-    if (summary->n_finite != 0 || !h->use_fused) break;
+    if (summary->n_finite != 0 || !fused_path(h)) break;
   }
   // regenerate the top-k rows from their global indices
   int64_t idx[BX_MAX_K];

@@ -221,6 +221,10 @@ class Scorer:
                                        C.byref(s) if summary else None, self.stream))
         return (self._summary(s) if summary else None), values, probs
 
+    def gp_kernel(self) -> str:
+        """Posterior kernel the current model state runs: "tensor", "dmma" or "generic"."""
+        return {0: "generic", 1: "dmma", 2: "tensor"}[self._lib.bx_gp_kernel(self.h)]
+
     def last_timing(self) -> dict:
         """CUDA-event durations (ms) of the forest / fused-score / merge kernels of the last
         score(..., timing=True) call."""

@@ -204,3 +204,35 @@ def test_engine_trace(trace, sc):
         ctx = Ctx(gp, feas, it["f_best"], it["eps_f"], np.random.default_rng(0), ev)
         got = A.optimize_acquisition(ctx, space, cot, sample_fn=lambda n, r, pool=pool: pool)
         assert got == to_cfg(space, it["chosen"]), f"iteration {i}"
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_posterior_kernels_agree(case, monkeypatch):
+    """The tensor-core split product (gp_tc.cu) against the FP64 DMMA kernel (gp_fused.cu) on a
+    generated pool much larger than the golden one; both must also meet the golden bar above."""
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    gp, _ = model(meta, arr, space)
+    monkeypatch.setenv("BX_GP_DMMA", "1")
+    ref = Scorer()
+    ref.set_space(space)
+    ref.set_gp(gp)
+    monkeypatch.delenv("BX_GP_DMMA")
+    tc = Scorer()
+    tc.set_space(space)
+    tc.set_gp(gp)
+    assert ref.gp_kernel() == "dmma"
+    assert tc.gp_kernel() == ("tensor" if len(gp.configs) <= 255 else "dmma")
+    rows = tc.generate(300_001, seed=7)
+    m1, v1 = (x.cpu().numpy() for x in tc.predict(rows))
+    m0, v0 = (x.cpu().numpy() for x in ref.predict(rows))
+    close(m1, m0, rtol=1e-7)
+    close(v1, v0, rtol=1e-6)
+    # and at the golden candidates, against the reference's numbers
+    lay = tc.layout
+    gold = tc.to_device(lay.encode([to_cfg(space, c) for c in meta["cands"]]))
+    m2, v2 = (x.cpu().numpy() for x in tc.predict(gold))
+    close(m2, arr["mean"])
+    close(v2, arr["var"])
+    ref.close()
+    tc.close()
