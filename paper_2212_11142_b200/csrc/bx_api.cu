@@ -228,7 +228,23 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.n_slices = h->tc_nsl;
     t.n_chunks = h->tc_nch;
     t.kscale = h->tc_kscale;
-    return launch_gp_tc(t, h->sm_count, s);
+    const char* trace = getenv("BX_TC_TRACE");  // profiling aid: dump CTA 0's role timeline
+    if (!trace || !trace[0]) return launch_gp_tc(t, h->sm_count, s);
+    const size_t bytes = 4 * 4096 * 2 * sizeof(long long);
+    std::vector<long long> host(bytes / sizeof(long long));
+    long long* dev = nullptr;
+    cudaError_t e = cudaMalloc(&dev, bytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dev, 0, bytes, s);
+    t.trace = dev;
+    if (e == cudaSuccess) e = launch_gp_tc(t, h->sm_count, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host.data(), dev, bytes, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(dev);
+    if (FILE* f = fopen(trace, "wb")) {
+      fwrite(host.data(), 1, bytes, f);
+      fclose(f);
+    }
+    return e;
   }
   return launch_gp_fused(f, h->sm_count, s);
 }

@@ -354,6 +354,7 @@ struct TcArgs {
   int32_t n_slices;           // ceil(n / 32) column slices of K*
   int32_t n_chunks;           // floor(n / 32) + 1 row chunks of [L^-1; alpha^T]
   double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
+  long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
 };
 
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).

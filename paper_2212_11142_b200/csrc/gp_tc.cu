@@ -18,7 +18,7 @@
 // Chunks run from the last to the first, so column slice k of the candidate digits is dead after
 // chunk k and the producers refill it for the next tile while the MMAs finish the smaller chunks.
 // CTA = 16 warps, one per SM, persistent over tiles:
-//   warp 0  lane 0 : MMA issuer (20 UTCIMMA 128x32x32 per chunk and slice)
+//   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*32 x 32 per chunk and slice, b = K* digit)
 //   warp 1  lane 0 : TMA producer: one 6 KB bulk copy per (chunk, slice) block, 4-stage ring
 //   warps 4-7      : epilogue, thread = candidate = TMEM lane: tcgen05.ld of the 6 groups,
 //                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction
@@ -86,10 +86,23 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
          ((uint64_t)(256 >> 4) << 32) | ((uint64_t)1 << 46);
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
-               ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+// Issued by a whole convergent warp; elect.sync picks the one thread that issues, which keeps the
+// compiler from wrapping every MMA in a per-thread serialisation loop.
+template <uint32_t kIdesc>
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n\t}\n"
+               ::"r"(d), "l"(a), "l"(b), "r"(acc), "n"(kIdesc));
+}
+__device__ __forceinline__ void tc_commit_warp(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n"
+               ::"r"(su32(bar)) : "memory");
+}
+// s32 accumulate, A (candidate digits) unsigned, B (matrix digits) signed, both K-major, M = 128
+template <int N>
+constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
@@ -98,6 +111,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
                  "=r"(v[7])
                : "r"(addr));
 }
+
+// role timeline of CTA 0 for BX_TC_TRACE: [role][4096][clock, code << 16 | sub]
+#define TC_TRACE(role, code, sub)                                                          \
+  do {                                                                                     \
+    if (ta.trace && blockIdx.x == 0 && tr_n < 4096) {                                      \
+      ta.trace[((role) * 4096 + tr_n) * 2] = clock64();                                    \
+      ta.trace[((role) * 4096 + tr_n) * 2 + 1] = ((long long)(code) << 16) | (long long)(sub); \
+      ++tr_n;                                                                              \
+    }                                                                                      \
+  } while (0)
 
 struct TcLayout {
   int par, planes, kmask, cval, cmask, exp2, rowscale, cdig, mat, bars, total;
@@ -133,6 +156,7 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   return L;
 }
 
+template <bool kPrecise>
 __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const FusedArgs& a = ta.f;
@@ -193,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  int tr_n = 0;
   const int64_t n_tiles = (a.q + kM - 1) / kM;
   const int my_tiles = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
@@ -208,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
               mb_wait(&mat_empty[s], (ph >> s) & 1u);
               ph ^= 1u << s;
             }
+            TC_TRACE(3, 1, c * 16 + ks);
             mb_expect(&mat_full[s], kMatBlock);
             bulk_g2s(mat + (size_t)s * kMatBlock, ta.mdig + ((size_t)c * nsl + ks) * kMatBlock, kMatBlock,
                      &mat_full[s]);
@@ -216,50 +242,45 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           }
     }
   } else if (warp == 0) {
-    // ---- MMA issuer ------------------------------------------------------------------------
-    if (lane == 0) {
-      // s32 accumulate, A (candidate digits) unsigned, B (matrix digits) signed, both K-major
-      const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
-                             ((uint32_t)(kM >> 4) << 24);
-      uint32_t ph_m = 0, ph_e = 0, ph_c = 0;  // parity bits per stage / accumulator
-      int s = 0, chunk_no = 0;
-      for (int t = 0; t < my_tiles; ++t) {
-        mb_wait(cand_full, ph_c);
-        ph_c ^= 1u;
-        tc_fence_after();
-        for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
-          const int buf = chunk_no & 1;
-          if (chunk_no >= 2) {
-            mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
-            ph_e ^= 1u << buf;
-            tc_fence_after();
-          }
-          const uint32_t dbase = tmem + (uint32_t)(buf * kAccCols);
-          unsigned started = 0;
-          for (int ks = 0; ks <= min(c, nsl - 1); ++ks) {
-            mb_wait(&mat_full[s], (ph_m >> s) & 1u);
-            ph_m ^= 1u << s;
-            tc_fence_after();
-            const unsigned char* Bs = mat + (size_t)s * kMatBlock;
-            const unsigned char* As = cdig + (size_t)ks * kDB * kCandBlock;
-#pragma unroll
-            for (int da = 0; da < kDA; ++da) {
-#pragma unroll
-              for (int db = 0; db < kDB; ++db) {
-                if (da + db < kGroups) {
-                  const int g = da + db;
-                  mma_i8(dbase + (uint32_t)(g * kN), sdesc(As + db * kCandBlock), sdesc(Bs + da * kN * 32),
-                         idesc, (started >> g) & 1u);
-                  started |= 1u << g;
-                }
-              }
-            }
-            tc_commit(&mat_empty[s]);  // the stage is free once these MMAs retire
-            s = (s + 1 == kStages) ? 0 : s + 1;
-          }
-          tc_commit(&acc_full[buf]);
-          if (c < nsl) tc_commit(&slice_empty[c]);  // chunks below c never read slice c
+    // ---- MMA issuer (whole warp, one elected thread issues) ---------------------------------
+    // The B tile of a (chunk, slice) block stacks the six matrix digits (6 x 32 rows), so one MMA
+    // per candidate digit b covers every group t = a + b <= 5 at once: N = (6 - b) * 32 rows
+    // starting at matrix digit 0, accumulated at TMEM column b * 32 (group-major accumulator).
+    const uint64_t adesc0 = sdesc(cdig), bdesc0 = sdesc(mat);
+    uint32_t ph_m = 0, ph_e = 0, ph_c = 0;  // parity bits per stage / accumulator
+    int s = 0, chunk_no = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      if (lane == 0) TC_TRACE(1, 1, t);
+      mb_wait(cand_full, ph_c);
+      ph_c ^= 1u;
+      tc_fence_after();
+      if (lane == 0) TC_TRACE(1, 2, t);
+      for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
+        const int buf = chunk_no & 1;
+        if (chunk_no >= 2) {
+          mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
+          ph_e ^= 1u << buf;
+          tc_fence_after();
         }
+        const uint32_t dbase = tmem + (uint32_t)(buf * kAccCols);
+        for (int ks = 0; ks <= min(c, nsl - 1); ++ks) {
+          mb_wait(&mat_full[s], (ph_m >> s) & 1u);
+          ph_m ^= 1u << s;
+          tc_fence_after();
+          const uint64_t bd = bdesc0 + (uint64_t)((s * kMatBlock) >> 4);
+          const uint64_t ad = adesc0 + (uint64_t)((ks * kDB * kCandBlock) >> 4);
+          const uint32_t acc = ks > 0 ? 1u : 0u;
+          mma_i8<idesc_i8<6 * kN>()>(dbase, ad, bd, acc);
+          mma_i8<idesc_i8<5 * kN>()>(dbase + 1 * kN, ad + (1 * kCandBlock >> 4), bd, 1u);
+          mma_i8<idesc_i8<4 * kN>()>(dbase + 2 * kN, ad + (2 * kCandBlock >> 4), bd, 1u);
+          mma_i8<idesc_i8<3 * kN>()>(dbase + 3 * kN, ad + (3 * kCandBlock >> 4), bd, 1u);
+          mma_i8<idesc_i8<2 * kN>()>(dbase + 4 * kN, ad + (4 * kCandBlock >> 4), bd, 1u);
+          tc_commit_warp(&mat_empty[s]);  // the stage is free once these MMAs retire
+          s = (s + 1 == kStages) ? 0 : s + 1;
+        }
+        tc_commit_warp(&acc_full[buf]);
+        if (c < nsl) tc_commit_warp(&slice_empty[c]);  // chunks below c never read slice c
+        if (lane == 0) TC_TRACE(1, 3, c);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -277,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);
         ph_f ^= 1u << buf;
         tc_fence_after();
+        if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
         const uint32_t base = tmem + lane_base + (uint32_t)(buf * kAccCols);
         for (int r0 = 0; r0 < kN && kN * c + r0 <= n; r0 += 8) {
           uint32_t g[kGroups][8];
@@ -300,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mb_arrive(&acc_empty[buf]);
+        if (lane == 0 && warp == 4) TC_TRACE(2, 2, c);
       }
       const int64_t gi = tile * kM + r;
       if (gi < a.q) {
@@ -330,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       asm volatile("bar.sync 1, 256;" ::: "memory");  // every producer is done with the last tile
+      if (pt == 0) TC_TRACE(0, 1, t);
       for (int idx = pt; idx < n_params * kM; idx += 256) {
         const int k = idx / kM, cc = idx % kM;
         const int64_t gi = tile * kM + cc;
@@ -354,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const int64_t gi = tile * kM + c;
+      if (pt == 0) TC_TRACE(0, 2, t);
       for (int ks = nsl - 1; ks >= 0; --ks) {
         const int j0 = 32 * ks + 16 * half;  // warp-uniform
         double W[16];
@@ -394,7 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           }
           kend += kd ? 1 : 0;
         }
-        // K* -> 40-bit fixed point -> five base-256 digits, 4 columns per 32-bit word
+        // K* -> 40-bit fixed point -> five base-256 digits, 4 columns per 32-bit word.  Straight-line
+        // code (padding columns are evaluated on the zero planes and masked afterwards) so the 16
+        // independent Matérn chains interleave.
+        const int nvalid = (gi < a.q) ? n - j0 : 0;
         uint32_t dw[kDB][4];
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
@@ -402,10 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             const int u = 4 * qd + v;
-            double kv = 0.0;
-            if (j0 + u < n && gi < a.q) kv = a.precise ? kstar(W[u], sigma) : kstar_fast(W[u], mc, s_exp2);
+            const double kv = kPrecise ? kstar(W[u], sigma) : kstar_fast(W[u], mc, s_exp2);
             unsigned long long X = __double2ull_rz(kv * kscale);
             X = X < 0xFFFFFFFFFFull ? X : 0xFFFFFFFFFFull;
+            X = u < nvalid ? X : 0ull;
             lo[v] = (uint32_t)X;
             hi[v] = (uint32_t)(X >> 32);
           }
@@ -418,8 +446,11 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           dw[3][qd] = __byte_perm(p01, p23, 0x7632);  // bits 8..15
           dw[4][qd] = __byte_perm(p01, p23, 0x5410);  // bits 0..7
         }
+        if (pt == 0) TC_TRACE(0, 3, ks);
         if (t > 0 && pt == 0) mb_wait(&slice_empty[ks], (uint32_t)((t - 1) & 1));
+        if (pt == 0) TC_TRACE(0, 4, ks);
         asm volatile("bar.sync 2, 256;" ::: "memory");  // the MMAs no longer read this slice
+        if (pt == 0) TC_TRACE(0, 5, ks);
 #pragma unroll
         for (int b = 0; b < kDB; ++b)
           *reinterpret_cast<uint4*>(cdig + ((size_t)ks * kDB + b) * kCandBlock + kmaj(c, 16 * half)) =
@@ -428,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (pt == 0) mb_arrive(cand_full);
+      if (pt == 0) TC_TRACE(0, 6, t);
     }
   }
   tc_fence_before();
@@ -499,13 +531,14 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
   const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(gp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  auto kernel = a.f.precise ? gp_tc_kernel<true> : gp_tc_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.f.q + kM - 1) / kM;
   int64_t grid = sm_count;
   if (tiles < grid) grid = tiles;
   if (grid < 1) grid = 1;
-  gp_tc_kernel<<<(int)grid, kThreads, L.total, s>>>(a);
+  kernel<<<(int)grid, kThreads, L.total, s>>>(a);
   return cudaGetLastError();
 }
 
