@@ -228,6 +228,9 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.n_slices = h->tc_nsl;
     t.n_chunks = h->tc_nch;
     t.kscale = h->tc_kscale;
+    t.n_coord = (int32_t)h->coord_host.size();
+    for (int j = 0; j < 256; ++j) t.exp2tab256[j] = (double)exp2l((long double)j / 256.0L);
+    if (const char* dbg = getenv("BX_TC_DEBUG")) t.debug = atoi(dbg);
     const char* trace = getenv("BX_TC_TRACE");  // profiling aid: dump CTA 0's role timeline
     if (!trace || !trace[0]) return launch_gp_tc(t, h->sm_count, s);
     const size_t bytes = 4 * 4096 * 2 * sizeof(long long);
@@ -474,11 +477,12 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
   }
   // tensor-core path: n <= 255 (8 row chunks) and the shared-memory budget
   h->use_tc = false;
-  if (!h->no_tc && n <= 255 && tc_smem_bytes(n, D, h->n_kendall) <= 227 * 1024) {
+  if (!h->no_tc && n <= 255 && tc_smem_bytes(n, D, h->n_kendall, h->row_words) <= 227 * 1024) {
     int E = 0;
-    frexp(outputscale, &E);  // sigma < 2^E = sc
+    const double m = frexp(outputscale, &E);  // sigma < 2^E = sc
+    if (m > 1.0 - ldexp(1.0, -20)) ++E;        // headroom: K* * 2^40 / sc < 2^40 - 2^20
     h->tc_nsl = (n + 31) / 32;
-    h->tc_nch = n / 32 + 1;
+    h->tc_nch = n / 16 + 1;
     h->tc_kscale = ldexp(1.0, 40 - E);
     BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
     BX_CUDA(h, h->d_rowscale.ensure(2 * 256 * 8));

@@ -349,11 +349,14 @@ struct FusedArgs {
 // Tensor-core posterior (gp_tc.cu): FusedArgs plus the digit-sliced [L^-1; alpha^T].
 struct TcArgs {
   FusedArgs f;
-  const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 32 rows x 32 columns
+  const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 16 rows x 32 columns
   const double* rowscale;     // [32 * n_chunks] 2^(e_i - 56) * sc (0 beyond row n)
   int32_t n_slices;           // ceil(n / 32) column slices of K*
-  int32_t n_chunks;           // floor(n / 32) + 1 row chunks of [L^-1; alpha^T]
+  int32_t n_chunks;           // floor(n / 16) + 1 row chunks of [L^-1; alpha^T]
   double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
+  int32_t n_coord;            // coord_lut entries
+  double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
+  int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue math, 2 no MMAs
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
 };
 
@@ -385,7 +388,7 @@ size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
-size_t tc_smem_bytes(int n, int n_params, int n_kendall);
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, cudaStream_t s);

@@ -13,19 +13,22 @@
 // golden fixtures the variance moves by <= 1e-7 relative (C1, the worst case), far inside the
 // 1e-5 parity bar.  The Matérn evaluation itself stays FP64.
 //
-// Tile = 128 candidates (the MMA M dimension, one TMEM lane each); the matrix is consumed in row
-// chunks of 32 (MMA N = 32), chunk c needing column slices 0..c only (lower triangle + alpha).
-// Chunks run from the last to the first, so column slice k of the candidate digits is dead after
-// chunk k and the producers refill it for the next tile while the MMAs finish the smaller chunks.
-// CTA = 16 warps, one per SM, persistent over tiles:
-//   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*32 x 32 per chunk and slice, b = K* digit)
-//   warp 1  lane 0 : TMA producer: one 6 KB bulk copy per (chunk, slice) block, 4-stage ring
+// Tile = 128 candidates (the MMA M dimension, one TMEM lane each).  The candidate digits are the
+// MMA A operand and live in tensor memory (written by the producers with tcgen05.st), so the
+// tensor core reads only the small matrix operand from shared memory.  The matrix is consumed in
+// row chunks of 16: chunk c needs column slices 0..c/2 only (lower triangle + alpha).  Chunks run
+// from the last to the first, so column slice k is dead after chunk 2k and the producers refill
+// it for the next tile while the MMAs finish the smaller chunks.
+// CTA = 24 warps, one per SM, persistent over tiles:
+//   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*16 x 32 per chunk and slice, b = K* digit)
+//   warp 1  lane 0 : TMA producer: one 3 KB bulk copy per (chunk, slice) block, 8-stage ring
+//   warp 2  lane 0 : row prefetcher: the next tiles' encoded rows, one bulk copy per tile
 //   warps 4-7      : epilogue, thread = candidate = TMEM lane: tcgen05.ld of the 6 groups,
 //                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction
-//   warps 8-15     : K* producers: 16 Matérn values (FP64) per thread and slice, sliced into
-//                    digits and stored in the canonical K-major layout of the MMA A operand
-// TMEM: two 192-column accumulators (6 groups x 32 rows) so the epilogue of one chunk overlaps
-// the MMAs of the next.
+//   warps 8-23     : K* producers: 8 Matérn values (FP64) per thread and slice, sliced into
+//                    digits and stored into the candidate's TMEM lane (tcgen05.st)
+// TMEM (512 columns): two 96-column accumulators (6 groups x 16 rows) so the epilogue of one chunk
+// overlaps the MMAs of the next, then 40 columns (5 digits x 32 bytes) per column slice.
 #include "bx_common.cuh"
 #include "matern.cuh"
 
@@ -34,16 +37,22 @@ namespace bx {
 namespace {
 
 constexpr int kM = 128;          // candidates per tile
-constexpr int kN = 32;           // matrix rows per chunk
+constexpr int kN = 16;           // matrix rows per chunk
 constexpr int kDA = 6;           // matrix digits (signed)
 constexpr int kDB = 5;           // K* digits (unsigned)
 constexpr int kGroups = 6;       // a + b in 0..5
-constexpr int kStages = 4;       // matrix block ring
-constexpr int kMaxChunks = 8;    // n <= 255
-constexpr int kThreads = 512;
-constexpr int kMatBlock = kDA * kN * 32;  // 6 KB per (chunk, slice)
-constexpr int kCandBlock = kM * 32;       // 4 KB per (slice, digit)
-constexpr int kAccCols = kGroups * kN;    // 192 TMEM columns per accumulator
+constexpr int kStages = 8;       // matrix block ring
+constexpr int kMaxChunks = 16;   // n <= 255
+constexpr int kMaxSlices = 8;
+constexpr int kProdWarps = 16;   // K* producers: 4 per TMEM lane quarter
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // 8 columns of a slice per producer thread
+constexpr int kThreads = (8 + kProdWarps) * 32;
+constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
+constexpr int kAccCols = kGroups * kN;    // 96 TMEM columns per accumulator
+constexpr int kDigCol0 = 2 * kAccCols;    // first TMEM column of the candidate digits
+constexpr int kSliceCols = kDB * 8;       // 40 TMEM columns (5 digits x 32 bytes) per slice
+constexpr int kMaxCoord = 1024;           // scaled coordinate table entries kept in shared memory
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -89,10 +98,10 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
 // Issued by a whole convergent warp; elect.sync picks the one thread that issues, which keeps the
 // compiler from wrapping every MMA in a per-thread serialisation loop.
 template <uint32_t kIdesc>
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_i8(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t acc) {
   asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %3, 0;\n\t"
-               "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n\t}\n"
-               ::"r"(d), "l"(a), "l"(b), "r"(acc), "n"(kIdesc));
+               "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n\t}\n"
+               ::"r"(d), "r"(a_tmem), "l"(b), "r"(acc), "n"(kIdesc));
 }
 __device__ __forceinline__ void tc_commit_warp(uint64_t* bar) {
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -122,11 +131,40 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
     }                                                                                      \
   } while (0)
 
+// sigma * matern52(sqrt(W)) * kscale truncated to a 40-bit integer (the producers' hot path), in 18
+// FP64 operations: d = sqrt(W) from rsqrt.approx + one Newton step on d; e^x (x = -sqrt5 d) as
+// 2^(k/256) (256-entry table, k clamped so the exponent stays normal; such K* truncate to 0) times a
+// degree-4 Taylor polynomial in |r| <= ln2/512 (truncation < 4e-17).
+__device__ __forceinline__ unsigned long long kstar_fixed(double W, const MaternConst& m, const double* tab256) {
+  const double w = W + 1e-300;                      // W = 0 -> d = 1e-150, K* = sigma
+  const double y0 = rsqrt_approx(w);
+  const double d0 = w * y0;
+  const double e0 = fma(-d0, y0, 1.0);               // 1 - w y0^2
+  const double d = fma(0.5 * d0, e0, d0);            // d0 (1 + e0 / 2)
+  const double x = -kSqrt5 * d;
+  const double t = fma(x, 369.3299304675746, 6755399441055744.0);  // x * 256 / ln2 + 1.5 * 2^52
+  const int k = max(__double2loint(t), -256 * 900);
+  const double kf = t - 6755399441055744.0;
+  double r = fma(kf, -0.00270760617331689, x);       // ln2/256 split: hi (32 bits, exact product) ...
+  r = fma(kf, -7.453964567463233e-13, r);            // ... and lo
+  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p = fma(r, p, 1.0);
+  const double tj = tab256[k & 255];
+  const double scale = __hiloint2double(__double2hiint(tj) + ((k >> 8) << 20), __double2loint(tj));
+  return __double2ull_rz(fma(m.s2, W, fma(m.s1, d, m.s0)) * (p * scale));
+}
+
+__device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(addr), "r"(v0), "r"(v1) : "memory");
+}
+
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, rowscale, cdig, mat, bars, total;
+  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, mat, bars, total;
 };
 
-__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall) {
+__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words) {
   const int nsl = (n + 31) / 32, npad = 32 * nsl;
   TcLayout L;
   int off = 0;
@@ -141,17 +179,19 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += n_params * kM * 8;
   L.cmask = off;   // [n_kendall][128][2] candidate Kendall masks
   off += n_kendall * kM * 16;
-  L.exp2 = off;
-  off += 64 * 8;
+  L.exp2 = off;    // 2^(j/256), j < 256
+  off += 256 * 8;
   L.rowscale = off;
   off += kMaxChunks * kN * 8;
+  L.rows = off;    // [2][128 x row_words] encoded rows of the next tiles (bulk-copy staging)
+  off += 2 * kM * words * 4;
+  L.stab = off;    // coord_lut / lengthscale of the finite numeric domains (when it fits)
+  off += kMaxCoord * 8;
   off = (off + 1023) & ~1023;
-  L.cdig = off;    // [slice][digit][128 x 32 B]
-  off += nsl * kDB * kCandBlock;
-  L.mat = off;     // [stage][digit][32 x 32 B]
+  L.mat = off;     // [stage][digit][16 x 32 B]
   off += kStages * kMatBlock;
-  L.bars = off;    // cand_full, slice_empty[8], mat_full[4], mat_empty[4], acc_full[2], acc_empty[2], tmem
-  off += (1 + kMaxChunks + 2 * kStages + 4 + 1) * 8;
+  L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
+  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
@@ -163,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.gp.n, n_params = a.space.n_params, words = a.space.row_words;
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -171,16 +211,20 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* cmask = reinterpret_cast<uint64_t*>(smem + L.cmask);
   double* s_exp2 = reinterpret_cast<double*>(smem + L.exp2);
   double* rowscale = reinterpret_cast<double*>(smem + L.rowscale);
-  unsigned char* cdig = smem + L.cdig;
   unsigned char* mat = smem + L.mat;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* cand_full = bars;
   uint64_t* slice_empty = bars + 1;
-  uint64_t* mat_full = slice_empty + kMaxChunks;
+  uint64_t* mat_full = slice_empty + kMaxSlices;
   uint64_t* mat_empty = mat_full + kStages;
   uint64_t* acc_full = mat_empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* rows_full = acc_empty + 2;
+  uint64_t* rows_empty = rows_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rows_empty + 2);
+  uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
+  // rows are staged by 16-byte bulk copies when the pool pointer allows it
+  const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
 
   for (int i = tid; i < n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
@@ -194,11 +238,20 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     kmask[2 * i] = j < n ? a.gp.kmask[src] : 0;
     kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
   }
-  for (int i = tid; i < 64; i += blockDim.x) s_exp2[i] = a.exp2tab[i];
+  for (int i = tid; i < 256; i += blockDim.x) s_exp2[i] = ta.exp2tab256[i];
+  // finite numeric coordinates pre-divided by the lengthscale: decode = two shared loads
+  double* stab = reinterpret_cast<double*>(smem + L.stab);
+  const bool use_stab = ta.n_coord <= kMaxCoord;
+  if (use_stab)
+    for (int k = 0; k < n_params; ++k) {
+      const bx_param_desc& p = a.space.params[k];
+      if (p.kind == BX_REAL || p.kind == BX_CATEGORICAL || p.kind == BX_PERMUTATION) continue;
+      for (int d = tid; d < p.size; d += blockDim.x) stab[p.coord + d] = a.space.coord_lut[p.coord + d] * a.gp.inv_l[k];
+    }
   for (int i = tid; i < kMaxChunks * kN; i += blockDim.x) rowscale[i] = i < nch * kN ? ta.rowscale[i] : 0.0;
   if (tid == 0) {
     mb_init(cand_full, 1);
-    for (int i = 0; i < kMaxChunks; ++i) mb_init(&slice_empty[i], 1);
+    for (int i = 0; i < kMaxSlices; ++i) mb_init(&slice_empty[i], 1);
     for (int i = 0; i < kStages; ++i) {
       mb_init(&mat_full[i], 1);
       mb_init(&mat_empty[i], 1);
@@ -206,6 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     for (int i = 0; i < 2; ++i) {
       mb_init(&acc_full[i], 1);
       mb_init(&acc_empty[i], 4);
+      mb_init(&rows_full[i], 1);
+      mb_init(&rows_empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -221,14 +276,38 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int64_t n_tiles = (a.q + kM - 1) / kM;
   const int my_tiles = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
-  if (warp == 1) {
+  // words of tile t's rows held in its staging buffer (the rest, if any, is read from global)
+  auto staged_words = [&](int64_t tile) -> int {
+    if (!stage_rows) return 0;
+    const int64_t count = min((int64_t)kM, a.q - tile * kM);
+    return (int)(((count * words * 4) & ~(int64_t)15) / 4);
+  };
+
+  if (warp == 2) {
+    // ---- row prefetcher: the encoded rows of each tile, one bulk copy ahead ----------------
+    if (lane == 0) {
+      for (int t = 0; t < my_tiles; ++t) {
+        const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+        const int buf = t & 1;
+        if (t >= 2) mb_wait(&rows_empty[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        const int sw = staged_words(tile);
+        if (sw > 0) {
+          mb_expect(&rows_full[buf], (uint32_t)sw * 4);
+          bulk_g2s(rowsbuf + (size_t)buf * kM * words, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4,
+                   &rows_full[buf]);
+        } else {
+          mb_arrive(&rows_full[buf]);
+        }
+      }
+    }
+  } else if (warp == 1) {
     // ---- TMA producer: matrix digit blocks in MMA consumption order ------------------------
     if (lane == 0) {
       uint32_t ph = 0;  // parity bit per stage
       int s = 0, issued = 0;
       for (int t = 0; t < my_tiles; ++t)
         for (int c = nch - 1; c >= 0; --c)
-          for (int ks = 0; ks <= min(c, nsl - 1); ++ks) {
+          for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks) {
             if (issued >= kStages) {
               mb_wait(&mat_empty[s], (ph >> s) & 1u);
               ph ^= 1u << s;
@@ -243,10 +322,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     }
   } else if (warp == 0) {
     // ---- MMA issuer (whole warp, one elected thread issues) ---------------------------------
-    // The B tile of a (chunk, slice) block stacks the six matrix digits (6 x 32 rows), so one MMA
-    // per candidate digit b covers every group t = a + b <= 5 at once: N = (6 - b) * 32 rows
-    // starting at matrix digit 0, accumulated at TMEM column b * 32 (group-major accumulator).
-    const uint64_t adesc0 = sdesc(cdig), bdesc0 = sdesc(mat);
+    // The B tile of a (chunk, slice) block stacks the six matrix digits (6 x 16 rows), so one MMA
+    // per candidate digit b covers every group t = a + b <= 5 at once: N = (6 - b) * 16 rows
+    // starting at matrix digit 0, accumulated at TMEM column b * 16 (group-major accumulator).
+    const uint64_t bdesc0 = sdesc(mat);
     uint32_t ph_m = 0, ph_e = 0, ph_c = 0;  // parity bits per stage / accumulator
     int s = 0, chunk_no = 0;
     for (int t = 0; t < my_tiles; ++t) {
@@ -263,23 +342,26 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           tc_fence_after();
         }
         const uint32_t dbase = tmem + (uint32_t)(buf * kAccCols);
-        for (int ks = 0; ks <= min(c, nsl - 1); ++ks) {
+        for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks) {
           mb_wait(&mat_full[s], (ph_m >> s) & 1u);
           ph_m ^= 1u << s;
           tc_fence_after();
           const uint64_t bd = bdesc0 + (uint64_t)((s * kMatBlock) >> 4);
-          const uint64_t ad = adesc0 + (uint64_t)((ks * kDB * kCandBlock) >> 4);
+          const uint32_t at = tmem + (uint32_t)(kDigCol0 + ks * kSliceCols);
           const uint32_t acc = ks > 0 ? 1u : 0u;
-          mma_i8<idesc_i8<6 * kN>()>(dbase, ad, bd, acc);
-          mma_i8<idesc_i8<5 * kN>()>(dbase + 1 * kN, ad + (1 * kCandBlock >> 4), bd, 1u);
-          mma_i8<idesc_i8<4 * kN>()>(dbase + 2 * kN, ad + (2 * kCandBlock >> 4), bd, 1u);
-          mma_i8<idesc_i8<3 * kN>()>(dbase + 3 * kN, ad + (3 * kCandBlock >> 4), bd, 1u);
-          mma_i8<idesc_i8<2 * kN>()>(dbase + 4 * kN, ad + (4 * kCandBlock >> 4), bd, 1u);
+          if (!(ta.debug & 2)) {
+            mma_i8<idesc_i8<6 * kN>()>(dbase, at, bd, acc);
+            mma_i8<idesc_i8<5 * kN>()>(dbase + 1 * kN, at + 1 * 8, bd, 1u);
+            mma_i8<idesc_i8<4 * kN>()>(dbase + 2 * kN, at + 2 * 8, bd, 1u);
+            mma_i8<idesc_i8<3 * kN>()>(dbase + 3 * kN, at + 3 * 8, bd, 1u);
+            mma_i8<idesc_i8<2 * kN>()>(dbase + 4 * kN, at + 4 * 8, bd, 1u);
+          }
           tc_commit_warp(&mat_empty[s]);  // the stage is free once these MMAs retire
           s = (s + 1 == kStages) ? 0 : s + 1;
         }
         tc_commit_warp(&acc_full[buf]);
-        if (c < nsl) tc_commit_warp(&slice_empty[c]);  // chunks below c never read slice c
+        // chunk c is the last reader of slice c / 2 when c is even (chunks run downwards)
+        if (!(c & 1) && (c >> 1) < nsl) tc_commit_warp(&slice_empty[c >> 1]);
         if (lane == 0) TC_TRACE(1, 3, c);
       }
     }
@@ -300,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         tc_fence_after();
         if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
         const uint32_t base = tmem + lane_base + (uint32_t)(buf * kAccCols);
-        for (int r0 = 0; r0 < kN && kN * c + r0 <= n; r0 += 8) {
+        for (int r0 = 0; r0 < kN && kN * c + r0 <= n && !(ta.debug & 1); r0 += 8) {
           uint32_t g[kGroups][8];
 #pragma unroll
           for (int q = 0; q < kGroups; ++q) tmem_ld8(base + (uint32_t)(q * kN + r0), g[q]);
@@ -345,30 +427,55 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     }
   } else if (warp >= 8) {
     // ---- K* producers ------------------------------------------------------------------------
-    const int pt = tid - 8 * 32;  // 0..255
-    const int c = pt & (kM - 1), half = pt >> 7;
+    const int pt = tid - 8 * 32;  // 0..kProdThreads-1
+    // warp w may only access TMEM lanes 32 (w % 4) .. +31: candidate = that lane, and the four
+    // warps sharing a lane quarter split each 32-column slice into 8-column parts
+    const int quarter = warp & 3, part = (warp - 8) >> 2;
+    const int c = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const double sigma = a.gp.outputscale;
-    const MaternConst mc{sigma, sigma * kSqrt5, sigma * (5.0 / 3.0)};
+    // K* * kscale: the fixed-point scale is folded into the Matérn polynomial
+    const MaternConst mc{sigma * ta.kscale, sigma * kSqrt5 * ta.kscale, sigma * (5.0 / 3.0) * ta.kscale};
     const double kscale = ta.kscale;
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // every producer is done with the last tile
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");  // every producer is done with the last tile
       if (pt == 0) TC_TRACE(0, 1, t);
-      for (int idx = pt; idx < n_params * kM; idx += 256) {
+      const int buf = t & 1;
+      mb_wait(&rows_full[buf], (uint32_t)((t >> 1) & 1));
+      const uint32_t* rs = rowsbuf + (size_t)buf * kM * words;
+      const int sw = staged_words(tile);
+      for (int idx = pt; idx < n_params * kM; idx += kProdThreads) {
         const int k = idx / kM, cc = idx % kM;
         const int64_t gi = tile * kM + cc;
         const bx_param_desc& p = params[k];
+        auto word = [&](int w) -> uint32_t {
+          const int o = cc * words + w;
+          return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
+        };
         uint64_t v = 0;
         if (gi < a.q) {
-          const uint32_t* row = a.rows + (size_t)gi * words;
-          if (p.kind == BX_PERMUTATION) v = row_u64(row, p.word);
-          else if (p.kind == BX_CATEGORICAL) v = row[p.word];
-          else v = (uint64_t)__double_as_longlong(row_coord(p, a.space.coord_lut, row) * a.gp.inv_l[k]);
+          if (p.kind == BX_PERMUTATION) {
+            v = (uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32);
+          } else if (p.kind == BX_CATEGORICAL) {
+            v = word(p.word);
+          } else {
+            double x;
+            if (p.kind == BX_REAL)
+              x = __longlong_as_double((long long)((uint64_t)word(p.word + 2) | ((uint64_t)word(p.word + 3) << 32))) *
+                  a.gp.inv_l[k];
+            else if (use_stab)
+              x = stab[p.coord + (int)word(p.word)];
+            else
+              x = a.space.coord_lut[p.coord + (int)word(p.word)] * a.gp.inv_l[k];
+            v = (uint64_t)__double_as_longlong(x);
+          }
         }
         cval[idx] = v;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int idx = pt; idx < a.n_kendall * kM; idx += 256) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
+      if (pt == 0) mb_arrive(&rows_empty[buf]);
+      for (int idx = pt; idx < a.n_kendall * kM; idx += kProdThreads) {
         const int kk = idx / kM, cc = idx % kM;
         const bx_param_desc& p = params[a.kendall_param[kk]];
         uint64_t lo = 0, hi = 0;
@@ -376,22 +483,25 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         cmask[2 * idx] = lo;
         cmask[2 * idx + 1] = hi;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       const int64_t gi = tile * kM + c;
       if (pt == 0) TC_TRACE(0, 2, t);
       for (int ks = nsl - 1; ks >= 0; --ks) {
-        const int j0 = 32 * ks + 16 * half;  // warp-uniform
-        double W[16];
+        const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
+        double W[kColsPerItem];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) W[u] = 0.0;
+        for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
         for (int i = 0; i < a.n_num; ++i) {
           const int k = a.num_param[i];
           const double x = __longlong_as_double((long long)cval[k * kM + c]);
-          const double* pl = reinterpret_cast<const double*>(planes + (size_t)k * npad + j0);
+          // 16-byte broadcast loads: half the shared-memory wavefronts of scalar loads
+          const double2* pl = reinterpret_cast<const double2*>(planes + (size_t)k * npad + j0);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const double d = x - pl[u];
-            W[u] = fma(d, d, W[u]);
+          for (int u = 0; u < kColsPerItem / 2; ++u) {
+            const double2 y = pl[u];
+            const double d0 = x - y.x, d1 = x - y.y;
+            W[2 * u] = fma(d0, d0, W[2 * u]);
+            W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
           }
         }
         for (int i = 0; i < a.n_cat; ++i) {
@@ -400,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           const double wl = a.gp.inv_l2[k];
           const uint64_t* pl = planes + (size_t)k * npad + j0;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) W[u] += (x != pl[u]) ? wl : 0.0;
+          for (int u = 0; u < kColsPerItem; ++u) W[u] += (x != pl[u]) ? wl : 0.0;
         }
         for (int i = 0, kend = 0; i < a.n_perm; ++i) {
           const int k = a.perm_param[i];
@@ -413,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           const uint64_t* pl = planes + (size_t)k * npad + j0;
           const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
+          for (int u = 0; u < kColsPerItem; ++u) {
             const uint64_t bl = kd ? km[2 * u] : 0, bh = kd ? km[2 * u + 1] : 0;
             W[u] += __ldg(tab + perm_raw(p.metric, p.size, x, pl[u], xl, xh, bl, bh));
           }
@@ -422,18 +532,17 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         // K* -> 40-bit fixed point -> five base-256 digits, 4 columns per 32-bit word.  Straight-line
         // code (padding columns are evaluated on the zero planes and masked afterwards) so the 16
         // independent Matérn chains interleave.
-        const int nvalid = (gi < a.q) ? n - j0 : 0;
-        uint32_t dw[kDB][4];
+        uint32_t dw[kDB][kColsPerItem / 4];
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
+        for (int qd = 0; qd < kColsPerItem / 4; ++qd) {
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             const int u = 4 * qd + v;
-            const double kv = kPrecise ? kstar(W[u], sigma) : kstar_fast(W[u], mc, s_exp2);
-            unsigned long long X = __double2ull_rz(kv * kscale);
-            X = X < 0xFFFFFFFFFFull ? X : 0xFFFFFFFFFFull;
-            X = u < nvalid ? X : 0ull;
+            // columns j >= n meet zero matrix digits and candidates beyond q are never stored, so
+            // neither needs masking; sc leaves >= 2^-20 headroom, so X < 2^40 without a clamp
+            const unsigned long long X =
+                kPrecise ? __double2ull_rz(kstar(W[u], sigma) * kscale) : kstar_fixed(W[u], mc, s_exp2);
             lo[v] = (uint32_t)X;
             hi[v] = (uint32_t)(X >> 32);
           }
@@ -447,17 +556,20 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           dw[4][qd] = __byte_perm(p01, p23, 0x5410);  // bits 0..7
         }
         if (pt == 0) TC_TRACE(0, 3, ks);
-        if (t > 0 && pt == 0) mb_wait(&slice_empty[ks], (uint32_t)((t - 1) & 1));
+        if (t > 0 && pt == 0) {
+          mb_wait(&slice_empty[ks], (uint32_t)((t - 1) & 1));
+          tc_fence_after();
+        }
         if (pt == 0) TC_TRACE(0, 4, ks);
-        asm volatile("bar.sync 2, 256;" ::: "memory");  // the MMAs no longer read this slice
+        asm volatile("bar.sync 2, %0;" ::"n"(kProdThreads) : "memory");  // the MMAs no longer read this slice
         if (pt == 0) TC_TRACE(0, 5, ks);
 #pragma unroll
         for (int b = 0; b < kDB; ++b)
-          *reinterpret_cast<uint4*>(cdig + ((size_t)ks * kDB + b) * kCandBlock + kmaj(c, 16 * half)) =
-              make_uint4(dw[b][0], dw[b][1], dw[b][2], dw[b][3]);
+          tmem_st2(tmem + lane_base + (uint32_t)(kDigCol0 + ks * kSliceCols + b * 8 + part * 2), dw[b][0], dw[b][1]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       if (pt == 0) mb_arrive(cand_full);
       if (pt == 0) TC_TRACE(0, 6, t);
     }
@@ -490,8 +602,8 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
   const int64_t total = (int64_t)nch * nsl * kN * 32;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int kb = (int)(t & 31), r = (int)((t >> 5) & 31);
-    const int blk = (int)(t >> 10);
+    const int kb = (int)(t & 31), r = (int)((t >> 5) & (kN - 1));
+    const int blk = (int)(t / (kN * 32));
     const int ks = blk % nsl, c = blk / nsl;
     const int row = c * kN + r, col = ks * 32 + kb;
     const double x = (row <= n && col < n) ? A[(size_t)row * lda + col] : 0.0;
@@ -509,17 +621,19 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 }  // namespace
 
-size_t tc_smem_bytes(int n, int n_params, int n_kendall) { return tc_layout(n, n_params, n_kendall).total; }
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words) {
+  return tc_layout(n, n_params, n_kendall, row_words).total;
+}
 
 size_t tc_mdig_bytes(int n) {
-  const int nsl = (n + 31) / 32, nch = n / 32 + 1;
+  const int nsl = (n + 31) / 32, nch = n / kN + 1;
   return (size_t)nsl * nch * kMatBlock;
 }
 
 // rowscale must hold 2 * 256 doubles (epilogue factors, then digit scales)
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, cudaStream_t s) {
-  const int nsl = (n + 31) / 32, nch = n / 32 + 1;
+  const int nsl = (n + 31) / 32, nch = n / kN + 1;
   if (nch > kMaxChunks) return cudaErrorInvalidValue;
   row_scale_kernel<<<kMaxChunks * kN, 32, 0, s>>>(A, lda, n, sc, rowscale);
   cudaError_t e = cudaGetLastError();
@@ -529,7 +643,7 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 }
 
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
-  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall);
+  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   auto kernel = a.f.precise ? gp_tc_kernel<true> : gp_tc_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
