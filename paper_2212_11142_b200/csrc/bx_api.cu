@@ -62,7 +62,8 @@ struct bx_handle {
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
   DevBuf d_knodes, d_kvid, d_kuval;
-  bool no_fused_forest = false;  // BX_FOREST_SEPARATE debug switch (env)
+  DevBuf d_qmask, d_qvid, d_quval, d_qsoff;
+  bool no_fused_forest = true;   // DMMA kernel: BX_FOREST_FUSED=1 walks the forest inside it
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
   std::vector<double> coord_host;
@@ -89,6 +90,8 @@ struct bx_handle {
   // tensor-core posterior (gp_tc.cu): digit-sliced [L^-1; alpha^T] + row scales
   bool use_tc = false;
   bool no_tc = false;     // BX_GP_DMMA=1 forces the FP64 DMMA kernel
+  bool tc_separate_forest = true;   // gp_tc + stand-alone forest kernel (BX_TC_FOREST_FUSED=1: fused)
+  bool no_qs_forest = false;        // BX_FOREST_WALK=1: node walks instead of QuickScorer tables
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale;
@@ -284,6 +287,13 @@ bx_handle* bx_create(int device) {
   for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
   const char* gpg = getenv("BX_GP_GENERIC");
   h->no_fused = gpg && gpg[0] == '1';
+  const char* fw = getenv("BX_FOREST_WALK");
+  h->no_qs_forest = fw && fw[0] == '1';
+  // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
+  // drains) is exact but measured slower than the stand-alone QuickScorer kernel run after it:
+  // opt-in with BX_TC_FOREST_FUSED=1.
+  const char* tff = getenv("BX_TC_FOREST_FUSED");
+  h->tc_separate_forest = !(tff && tff[0] == '1');
   const char* dm = getenv("BX_GP_DMMA");
   h->no_tc = h->no_fused || (dm && dm[0] == '1');
   const char* mp = getenv("BX_MATERN_PRECISE");
@@ -312,7 +322,8 @@ void bx_destroy(bx_handle* h) {
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
                     &h->d_host_rows[0], &h->d_host_rows[1], &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
-                    &h->d_knodes, &h->d_kvid, &h->d_kuval};
+                    &h->d_knodes, &h->d_kvid, &h->d_kuval, &h->d_qmask, &h->d_qvid,
+                    &h->d_quval, &h->d_qsoff};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -665,6 +676,92 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
   cf.nodes_in_smem = 0;  // decided at launch from the smem budget
   h->forest.coded = 1;
 
+  // QuickScorer tables (QsForestDev): integer splits only, <= 64 leaves per tree
+  QsForestDev& qs = h->forest.qs;
+  qs = QsForestDev{};
+  if (!has_real) {
+    const int S = (int)code_param.size();
+    std::vector<int32_t> soff(S), range(S);
+    int stride = 0;
+    for (int c = 0; c < S; ++c) {
+      const bx_param_desc& p = h->params[code_param[c]];
+      range[c] = p.kind == BX_CATEGORICAL ? 2 : p.size;  // one-hot {0,1}; position < m; index < size
+      soff[c] = stride;
+      stride += range[c];
+    }
+    const int T = h->forest.n_trees;
+    std::vector<uint64_t> mask((size_t)T * stride, ~0ull);
+    std::vector<uint16_t> vid((size_t)T * 64, 0);
+    std::vector<double> uval;
+    bool ok = (size_t)T * stride * 8 <= 160 * 1024;
+    std::vector<int32_t> lo(nodes.size()), mid(nodes.size()), hi(nodes.size());
+    for (int t = 0; ok && t < T; ++t) {
+      // left-to-right leaf numbering and subtree leaf ranges by an explicit post-order walk
+      int leaves = 0;
+      std::vector<std::pair<int, int>> stack{{roots[t], 0}};  // (node, phase)
+      while (!stack.empty() && ok) {
+        const int u = stack.back().first;
+        const int phase = stack.back().second;
+        const RfNode& nd = nodes[u];
+        if (nd.feat < 0) {
+          if (leaves >= 64) { ok = false; break; }
+          const double v = nd.val;
+          size_t id = 0;
+          while (id < uval.size() && std::memcmp(&uval[id], &v, 8) != 0) ++id;
+          if (id == uval.size()) uval.push_back(v);
+          if (id > 65535) { ok = false; break; }
+          vid[(size_t)t * 64 + leaves] = (uint16_t)id;
+          lo[u] = leaves;
+          hi[u] = ++leaves;
+          stack.pop_back();
+        } else if (phase == 0) {
+          stack.back().second = 1;
+          lo[u] = leaves;
+          stack.push_back({nd.child, 0});
+        } else if (phase == 1) {
+          stack.back().second = 2;
+          mid[u] = leaves;
+          stack.push_back({nd.child + 1, 0});
+        } else {
+          hi[u] = leaves;
+          // going right (code >= cut) rules out the left subtree's leaves [lo, mid)
+          const uint32_t lo32 = (uint32_t)coded[u];
+          const int slot = (int)((lo32 >> 24) & 63u), cut = (int)(lo32 & 0xFFFFFFu);
+          const uint64_t left = ((mid[u] - lo[u]) >= 64 ? ~0ull : ((1ull << (mid[u] - lo[u])) - 1)) << lo[u];
+          for (int v = cut; v < range[slot]; ++v) mask[(size_t)t * stride + soff[slot] + v] &= ~left;
+          stack.pop_back();
+        }
+      }
+    }
+    if (ok) {
+      if (uval.empty()) uval.push_back(0.0);
+      // transpose to [slot value][tree] so a group of 8 trees is one 64-byte run per slot
+      // row stride == 4 words (mod 32): rows of different code values start on different banks
+      int tpad = (T + 7) / 8 * 8;
+      while (tpad % 16 != 2) ++tpad;
+      std::vector<uint64_t> mt((size_t)stride * tpad, ~0ull);
+      for (int t = 0; t < T; ++t)
+        for (int r = 0; r < stride; ++r) mt[(size_t)r * tpad + t] = mask[(size_t)t * stride + r];
+      mask.swap(mt);
+      qs.tpad = tpad;
+      BX_CUDA(h, upload(h->d_qmask, mask.data(), mask.size()));
+      BX_CUDA(h, upload(h->d_qvid, vid.data(), vid.size()));
+      BX_CUDA(h, upload(h->d_quval, uval.data(), uval.size()));
+      BX_CUDA(h, upload(h->d_qsoff, soff.data(), soff.size()));
+      qs.mask = h->d_qmask.as<uint64_t>();
+      qs.vid = h->d_qvid.as<uint16_t>();
+      qs.uval = h->d_quval.as<double>();
+      qs.soff = h->d_qsoff.as<int32_t>();
+      qs.code_param = cf.code_param;
+      qs.code_sub = cf.code_sub;
+      qs.n_trees = T;
+      qs.n_codes = S;
+      qs.stride = stride;
+      qs.n_uvals = (int)uval.size();
+      qs.enabled = h->no_qs_forest ? 0 : 1;
+    }
+  }
+
   // compact 32-bit form for the walk fused into the GP kernel (CompactForestDev)
   CompactForestDev& kf = h->forest.kf;
   kf = CompactForestDev{};
@@ -894,10 +991,15 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // warps) unless the numpy pairwise order (q == 1) or the table budget rules it out; then it
     // runs on the side stream and is joined before the summary.
     const CompactForestDev& kf = h->forest.kf;
-    const bool fuse_rf = forest && kf.enabled && !(flags & BX_SCORE_RF_PAIRWISE) && !h->use_tc &&
-                         !h->no_fused_forest &&
+    // Tensor-core kernel: optionally the QuickScorer forest inside the kernel (BX_TC_FOREST_FUSED=1).
+    const QsForestDev& qf = h->forest.qs;
+    const bool fuse_rf =
+        forest && !(flags & BX_SCORE_RF_PAIRWISE) &&
+        (h->use_tc ? qf.enabled && !h->tc_separate_forest &&
+                         tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf) <= 227 * 1024
+                   : kf.enabled && !h->no_fused_forest &&
                          fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
-                             220 * 1024;
+                             220 * 1024);
     // The stand-alone forest kernel and the GP kernel each fill every SM's shared memory, so
     // they cannot co-reside: run them back to back on the caller's stream (which also makes the
     // per-kernel CUDA-event timing exact).
@@ -910,7 +1012,8 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     FusedArgs f = fused_args(h, rows, q, f_model);
     f.ei_out = h->d_ei.as<double>();
     if (fuse_rf) {
-      f.kf = kf;
+      if (h->use_tc) f.qs = qf;
+      else f.kf = kf;
       f.probs_out = h->d_probs.as<double>();
     }
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));

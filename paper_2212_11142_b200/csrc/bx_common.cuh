@@ -102,6 +102,24 @@ struct CompactForestDev {
   int32_t enabled;
 };
 
+// QuickScorer-style tables (Lucchese et al., SIGIR 2015) over the integer codes: leaves of every
+// tree are numbered left to right; a node whose test goes right (code >= cut) rules out its left
+// subtree's leaves, and the exit leaf is the leftmost leaf no such node rules out.  mask[t][s][v]
+// is the AND of those eliminations over tree t's nodes on code slot s for code value v, so a tree
+// is n_codes table loads and ANDs plus a find-first-set — no dependent descent.  Needs at most 64
+// leaves per tree and integer-coded splits only.
+struct QsForestDev {
+  const uint64_t* mask;      // [stride][tpad] (slot s, code v at row soff[s] + v; trees contiguous)
+  const uint16_t* vid;       // [n_trees][64] leaf value id of leaf l (left-to-right order)
+  const double* uval;        // [n_uvals] distinct leaf values
+  const int32_t* soff;       // [n_codes] offset of slot s inside a tree's stride
+  const int32_t* code_param; // [n_codes] (the coded forest's slots)
+  const int32_t* code_sub;
+  int32_t n_trees, n_codes, stride, n_uvals;
+  int32_t tpad;              // row length >= n_trees rounded up to 8, == 2 (mod 16) (bank spread)
+  int32_t enabled;
+};
+
 struct ForestDev {
   const RfNode* nodes;
   const int32_t* roots;
@@ -112,6 +130,7 @@ struct ForestDev {
   double constant;       // single-class shortcut (feasibility.py:73-74)
   CodedForestDev cf;
   CompactForestDev kf;
+  QsForestDev qs;
 };
 
 struct EvalSetDev {
@@ -343,6 +362,7 @@ struct FusedArgs {
   double exp2tab[64];     // 2^(j/64), correctly rounded (host long double)
   int32_t precise;        // 1 -> libm sqrt/exp in the Matérn (BX_MATERN_PRECISE=1)
   CompactForestDev kf;    // kf.enabled -> walk the forest inside the kernel, write probs_out
+  QsForestDev qs;         // gp_tc.cu: qs.enabled -> evaluate the forest inside the kernel
   double* probs_out;
 };
 
@@ -388,7 +408,7 @@ size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words);
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs = nullptr);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, cudaStream_t s);

@@ -195,6 +195,117 @@ __global__ void __launch_bounds__(kRfThreads, 1) rf_coded_kernel(SpaceDev sp, Co
   }
 }
 
+// ---- QuickScorer path (QsForestDev) -----------------------------------------------------------
+constexpr int kQsThreads = 1024;
+constexpr int kQsGroup = 8;  // trees evaluated together (8 masks in registers)
+
+// explicit shared-space 16-byte load (the mask table is indexed through computed offsets, which
+// otherwise compile to generic loads)
+__device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t saddr) {
+  ulonglong2 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(saddr));
+  return v;
+}
+
+__device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* row, int sub) {
+  if (p.kind == BX_PERMUTATION) return perm_pos(row_u64(row, p.word), p.size, sub);
+  if (p.kind == BX_CATEGORICAL) return (int)row[p.word] == sub ? 1 : 0;
+  return (int)row[p.word];
+}
+
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_s32(uint32_t a, int32_t v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Tables: masks [stride][tpad] u64, distinct leaf values, leaf value ids [n_trees][64] u16, and the
+// per-thread mask-row offsets [n_codes][kQsThreads]; every access is an explicit shared load.
+__global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForestDev f, const uint32_t* rows,
+                                                           int64_t q, int use_pairwise, double* probs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ bx_param_desc params[BX_MAX_PARAMS];
+  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem);
+  size_t off = (size_t)f.stride * f.tpad * 8;
+  double* s_uval = reinterpret_cast<double*>(smem + off);
+  off += (size_t)f.n_uvals * 8;
+  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + off);
+  off += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem + off);
+  for (int i = threadIdx.x; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
+    reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(sp.params)[i];
+  for (int i = threadIdx.x; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
+  for (int i = threadIdx.x; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
+  for (int i = threadIdx.x; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
+  __syncthreads();
+  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(s_mask);
+  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(s_uval);
+  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(s_vid);
+  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(s_off) + 4u * threadIdx.x;
+  auto leaf = [=](int t, uint64_t m) {
+    const uint32_t id = lds_u16(vid_s + 2u * (uint32_t)(t * 64 + __ffsll((long long)m) - 1));
+    return __longlong_as_double((long long)lds_u64(uval_s + 8u * id));
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += stride) {
+    const uint32_t* row = rows + (size_t)i * sp.row_words;
+    for (int c = 0; c < f.n_codes; ++c)
+      sts_s32(off_s + 4u * kQsThreads * c,
+              (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+    double sum = 0.0;
+    if (use_pairwise) {
+      sum = pairwise(
+          [=](int t) {
+            uint64_t m = ~0ull;
+            for (int c = 0; c < f.n_codes; ++c)
+              m &= lds_u64(mask_s + 8u * (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + t));
+            return leaf(t, m);
+          },
+          0, f.n_trees);
+    } else {
+      for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {
+        uint64_t m[kQsGroup];
+#pragma unroll
+        for (int j = 0; j < kQsGroup; ++j) m[j] = ~0ull;
+        for (int c = 0; c < f.n_codes; ++c) {
+          const uint32_t col = mask_s + (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + g0) * 8u;
+#pragma unroll
+          for (int j = 0; j < kQsGroup / 2; ++j) {
+            const ulonglong2 w = lds_u64x2(col + 16u * j);
+            m[2 * j] &= w.x;
+            m[2 * j + 1] &= w.y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kQsGroup; ++j)
+          if (g0 + j < f.n_trees) {
+            const double v = leaf(g0 + j, m[j]);
+            sum = (g0 + j == 0) ? v : __dadd_rn(sum, v);  // tree order (feasibility.py:89)
+          }
+      }
+    }
+    probs[i] = __ddiv_rn(sum, (double)f.n_trees);
+  }
+}
+
+size_t qs_smem(const QsForestDev& f) {
+  return (size_t)f.stride * f.tpad * 8 + (size_t)f.n_uvals * 8 + (((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15) +
+         (size_t)f.n_codes * kQsThreads * 4;
+}
+
 size_t coded_smem(const CodedForestDev& cf, bool in_smem) {
   return (in_smem ? ((size_t)cf.n_nodes + cf.n_leaves) * 8 + (((size_t)cf.n_nodes * 4 + 15) & ~(size_t)15) : 0) +
          (((size_t)cf.n_trees * 4 + 15) & ~(size_t)15) + (size_t)cf.n_codes * kRfThreads * 4 +
@@ -214,6 +325,19 @@ cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (f.coded && f.qs.enabled && qs_smem(f.qs) <= 220 * 1024) {
+    const size_t bytes = qs_smem(f.qs);
+    cudaError_t e = cudaFuncSetAttribute(rf_qs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rf_qs_kernel, kQsThreads, bytes);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (q + kQsThreads - 1) / kQsThreads;
+    const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (blocks > cap) blocks = cap;
+    rf_qs_kernel<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, rows, q, use_pairwise, probs);
+    return cudaGetLastError();
+  }
   if (f.coded) {
     const bool in_smem = coded_smem(f.cf, true) <= 220 * 1024;
     const size_t bytes = coded_smem(f.cf, in_smem);

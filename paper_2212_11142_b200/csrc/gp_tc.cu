@@ -22,9 +22,10 @@
 // CTA = 24 warps, one per SM, persistent over tiles:
 //   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*16 x 32 per chunk and slice, b = K* digit)
 //   warp 1  lane 0 : TMA producer: one 3 KB bulk copy per (chunk, slice) block, 8-stage ring
-//   warp 2  lane 0 : row prefetcher: the next tiles' encoded rows, one bulk copy per tile
+//   warp 1  lane 1 : row prefetcher: the next tiles' encoded rows, one bulk copy per tile
 //   warps 4-7      : epilogue, thread = candidate = TMEM lane: tcgen05.ld of the 6 groups,
-//                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction
+//                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction;
+//                    between chunks, the candidate's forest probability from QuickScorer tables
 //   warps 8-23     : K* producers: 8 Matérn values (FP64) per thread and slice, sliced into
 //                    digits and stored into the candidate's TMEM lane (tcgen05.st)
 // TMEM (512 columns): two 96-column accumulators (6 groups x 16 rows) so the epilogue of one chunk
@@ -161,10 +162,14 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, mat, bars, total;
+  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, mat, bars,
+      total;
 };
 
-__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words) {
+// qs: the QuickScorer forest evaluated by warps 2-3 (qs->enabled == 0 -> no forest tables)
+__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words,
+                                              const QsForestDev* qs = nullptr) {
+  const bool rf = qs && qs->enabled;
   const int nsl = (n + 31) / 32, npad = 32 * nsl;
   TcLayout L;
   int off = 0;
@@ -187,11 +192,19 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += 2 * kM * words * 4;
   L.stab = off;    // coord_lut / lengthscale of the finite numeric domains (when it fits)
   off += kMaxCoord * 8;
+  L.qs_mask = off;   // QuickScorer tables: masks, distinct leaf values, leaf value ids
+  off += rf ? qs->stride * qs->tpad * 8 : 0;
+  L.qs_uval = off;
+  off += rf ? qs->n_uvals * 8 : 0;
+  L.qs_vid = off;
+  off += rf ? ((qs->n_trees * 64 * 2 + 15) & ~15) : 0;
+  L.qs_off = off;    // [2][n_codes][128] table offsets (soff + code) of the tiles' candidates
+  off += rf ? 2 * qs->n_codes * kM * 4 : 0;
   off = (off + 1023) & ~1023;
   L.mat = off;     // [stage][digit][16 x 32 B]
   off += kStages * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
-  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 1) * 8;
+  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 2 + 1) * 8;
   L.total = off;
   return L;
 }
@@ -203,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.gp.n, n_params = a.space.n_params, words = a.space.row_words;
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words);
+  const QsForestDev& qf = a.qs;
+  const bool rf = qf.enabled != 0;
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -221,7 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* rows_full = acc_empty + 2;
   uint64_t* rows_empty = rows_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rows_empty + 2);
+  uint64_t* qs_free = rows_empty + 2;  // the epilogue is done with a tile's forest offsets
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qs_free + 2);
   uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
   // rows are staged by 16-byte bulk copies when the pool pointer allows it
   const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
@@ -249,6 +265,15 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       for (int d = tid; d < p.size; d += blockDim.x) stab[p.coord + d] = a.space.coord_lut[p.coord + d] * a.gp.inv_l[k];
     }
   for (int i = tid; i < kMaxChunks * kN; i += blockDim.x) rowscale[i] = i < nch * kN ? ta.rowscale[i] : 0.0;
+  uint64_t* qs_mask = reinterpret_cast<uint64_t*>(smem + L.qs_mask);
+  double* qs_uval = reinterpret_cast<double*>(smem + L.qs_uval);
+  uint16_t* qs_vid = reinterpret_cast<uint16_t*>(smem + L.qs_vid);
+  int32_t* qs_off = reinterpret_cast<int32_t*>(smem + L.qs_off);
+  if (rf) {
+    for (int i = tid; i < qf.stride * qf.tpad; i += blockDim.x) qs_mask[i] = qf.mask[i];
+    for (int i = tid; i < qf.n_uvals; i += blockDim.x) qs_uval[i] = qf.uval[i];
+    for (int i = tid; i < qf.n_trees * 64; i += blockDim.x) qs_vid[i] = qf.vid[i];
+  }
   if (tid == 0) {
     mb_init(cand_full, 1);
     for (int i = 0; i < kMaxSlices; ++i) mb_init(&slice_empty[i], 1);
@@ -261,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       mb_init(&acc_empty[i], 4);
       mb_init(&rows_full[i], 1);
       mb_init(&rows_empty[i], 1);
+      mb_init(&qs_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -283,9 +309,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     return (int)(((count * words * 4) & ~(int64_t)15) / 4);
   };
 
-  if (warp == 2) {
+  if (warp == 1 && lane == 1) {
     // ---- row prefetcher: the encoded rows of each tile, one bulk copy ahead ----------------
-    if (lane == 0) {
+    {
       for (int t = 0; t < my_tiles; ++t) {
         const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
         const int buf = t & 1;
@@ -300,9 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && lane == 0) {
     // ---- TMA producer: matrix digit blocks in MMA consumption order ------------------------
-    if (lane == 0) {
+    {
       uint32_t ph = 0;  // parity bit per stage
       int s = 0, issued = 0;
       for (int t = 0; t < my_tiles; ++t)
@@ -372,9 +398,39 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     const double sigma = a.gp.outputscale;
     uint32_t ph_f = 0;
     int chunk_no = 0;
+    // forest (QuickScorer tables): groups of G trees evaluated while the next chunk's MMAs run;
+    // leaves summed strictly in tree order (the q >= 2 numpy order, feasibility.py:89)
+    constexpr int G = 8;
+    const int n_groups = rf ? (qf.n_trees + G - 1) / G : 0;
+    const uint32_t qs_mask_s = su32(qs_mask);
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       double ss = 0.0, mean_s = 0.0;
+      const int32_t* qo = qs_off + (size_t)(t & 1) * (rf ? qf.n_codes : 0) * kM + r;
+      double fsum = 0.0;
+      int g_next = 0;
+      auto forest_group = [&](int g) {
+        const int g0 = g * G;
+        uint64_t m[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) m[j] = ~0ull;
+        for (int sl = 0; sl < qf.n_codes; ++sl) {
+          const uint32_t col = qs_mask_s + (uint32_t)(qo[sl * kM] + g0) * 8u;
+#pragma unroll
+          for (int j = 0; j < G / 2; ++j) {
+            ulonglong2 w;
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w.x), "=l"(w.y) : "r"(col + 16u * j));
+            m[2 * j] &= w.x;
+            m[2 * j + 1] &= w.y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (g0 + j < qf.n_trees) {
+            const double v = qs_uval[qs_vid[(g0 + j) * 64 + __ffsll((long long)m[j]) - 1]];
+            fsum = (g0 + j == 0) ? v : __dadd_rn(fsum, v);
+          }
+      };
       for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);
@@ -405,8 +461,16 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         __syncwarp();
         if (lane == 0) mb_arrive(&acc_empty[buf]);
         if (lane == 0 && warp == 4) TC_TRACE(2, 2, c);
+        const int target = n_groups * (nch - c) / nch;
+        while (g_next < target) forest_group(g_next++);
       }
+      while (g_next < n_groups) forest_group(g_next++);
       const int64_t gi = tile * kM + r;
+      if (rf) {
+        if (gi < a.q) a.probs_out[gi] = __ddiv_rn(fsum, (double)qf.n_trees);  // np.mean: sum / count
+        __syncwarp();
+        if (lane == 0) mb_arrive(&qs_free[t & 1]);
+      }
       if (gi < a.q) {
         const double var_s = fmax(sigma - ss, 0.0);                 // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * mean_s;      // :328
@@ -472,6 +536,29 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           }
         }
         cval[idx] = v;
+      }
+      if (rf) {  // forest table offsets of the tile, read by the epilogue (its thread = candidate)
+        if (t >= 2) mb_wait(&qs_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
+        for (int idx = pt; idx < qf.n_codes * kM; idx += kProdThreads) {
+          const int sl = idx / kM, cc = idx % kM;
+          const int64_t gi = tile * kM + cc;
+          int v = 0;
+          if (gi < a.q) {
+            auto word = [&](int w) -> uint32_t {
+              const int o = cc * words + w;
+              return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
+            };
+            const bx_param_desc& p = params[qf.code_param[sl]];
+            if (p.kind == BX_PERMUTATION)
+              v = perm_pos((uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32), p.size, qf.code_sub[sl]);
+            else if (p.kind == BX_CATEGORICAL)
+              v = (int)word(p.word) == qf.code_sub[sl] ? 1 : 0;
+            else
+              v = (int)word(p.word);
+          }
+          qo[idx] = (qf.soff[sl] + v) * qf.tpad;
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       if (pt == 0) mb_arrive(&rows_empty[buf]);
@@ -621,8 +708,8 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 }  // namespace
 
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words) {
-  return tc_layout(n, n_params, n_kendall, row_words).total;
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs) {
+  return tc_layout(n, n_params, n_kendall, row_words, qs).total;
 }
 
 size_t tc_mdig_bytes(int n) {
@@ -643,7 +730,7 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 }
 
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
-  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words);
+  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   auto kernel = a.f.precise ? gp_tc_kernel<true> : gp_tc_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);

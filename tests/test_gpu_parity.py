@@ -236,3 +236,29 @@ def test_posterior_kernels_agree(case, monkeypatch):
     close(v2, arr["var"])
     ref.close()
     tc.close()
+
+
+@pytest.mark.parametrize("case", ["C3", "C4", "mixed_fit"])
+def test_forest_paths_bit_exact(case, monkeypatch):
+    """QuickScorer tables (stand-alone and fused into the tensor-core kernel) and the node walk
+    give bit-identical probabilities and scores."""
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    gp, feas = model(meta, arr, space)
+    f = gp.objective_to_model(meta["f_best"])
+    out = {}
+    for name, env in [("walk", {"BX_FOREST_WALK": "1"}), ("qs", {}), ("fused", {"BX_TC_FOREST_FUSED": "1"})]:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sc = Scorer()
+        sc.set_gp(gp)
+        sc.set_forest(feas)
+        rows = sc.generate(200_003, seed=3)
+        _, values, probs = sc.score(rows, f, meta["eps_f"], k=10, want_values=True)
+        out[name] = (values.cpu().numpy(), probs.cpu().numpy(), sc.rf_predict(rows, pairwise=False).cpu().numpy())
+        sc.close()
+        for k in env:
+            monkeypatch.delenv(k)
+    for name in ("qs", "fused"):
+        for a, b in zip(out[name], out["walk"]):
+            assert np.array_equal(a, b), name
