@@ -1106,8 +1106,11 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->row_words;
+  // geometric chunk sizes (2^16, 2^17, then 2^18): the first copy, which nothing overlaps, is short
   const int64_t chunk = 1 << 18;
-  const int64_t n_chunks = (q + chunk - 1) / chunk;
+  auto chunk_len = [&](int64_t c) -> int64_t { return c >= 2 ? chunk : (chunk >> (2 - c)); };
+  int64_t n_chunks = 0;
+  for (int64_t off = 0; off < q; off += chunk_len(n_chunks), ++n_chunks) {}
   const size_t per_chunk = (size_t)max_partials(h->sm_count);
   BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
@@ -1118,10 +1121,10 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   int total = 0;
   BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
   BX_CUDA(h, cudaEventRecord(h->ev_done[1], s));
-  for (int64_t c = 0; c < n_chunks; ++c) {
+  int64_t off = 0;
+  for (int64_t c = 0; c < n_chunks; off += chunk_len(c), ++c) {
     const int b = (int)(c & 1);
-    const int64_t off = c * chunk;
-    const int64_t len = (q - off) < chunk ? (q - off) : chunk;
+    const int64_t len = (q - off) < chunk_len(c) ? (q - off) : chunk_len(c);
     // the copy into buffer b waits until the kernels that last read buffer b are done
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
     BX_CUDA(h, cudaMemcpyAsync(h->d_host_rows[b].p, host_rows + (size_t)off * W, (size_t)len * W * 4,

@@ -376,7 +376,8 @@ struct TcArgs {
   double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
   int32_t n_coord;            // coord_lut entries
   double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
-  int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue math, 2 no MMAs
+  int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
+                              // 4 epilogue TMEM reads without the arithmetic
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
 };
 

@@ -37,16 +37,27 @@ __global__ void gp_planes_kernel(SpaceDev sp, const uint32_t* train, int n, cons
   }
 }
 
-__global__ void tri_inverse_kernel(const double* L, int n, double* A, int lda) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per column j of L^-1: x_i = -(sum_{k=j}^{i-1} L_ik x_k) / L_ii, the dot product split
+// across the lanes and reduced with shuffles; the column lives in shared memory.
+constexpr int kInvWarps = 8;
+__global__ void __launch_bounds__(kInvWarps * 32) tri_inverse_kernel(const double* L, int n, double* A, int lda) {
+  extern __shared__ double xcol[];  // [warps][n]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= n) return;
-  A[(size_t)j * lda + j] = 1.0 / L[(size_t)j * n + j];
+  double* x = xcol + (size_t)warp * n;
+  if (lane == 0) x[j] = 1.0 / L[(size_t)j * n + j];
+  __syncwarp();
   for (int i = j + 1; i < n; ++i) {
-    double s = 0.0;
     const double* Li = L + (size_t)i * n;
-    for (int k = j; k < i; ++k) s = fma(Li[k], A[(size_t)k * lda + j], s);
-    A[(size_t)i * lda + j] = -s / Li[i];
+    double s = 0.0;
+    for (int k = j + lane; k < i; k += 32) s = fma(Li[k], x[k], s);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) x[i] = -s / Li[i];
+    __syncwarp();
   }
+  for (int i = j + lane; i < n; i += 32) A[(size_t)i * lda + j] = x[i];
 }
 
 __global__ void pairwise_sq_kernel(SpaceDev sp, const uint32_t* a, int qa, const uint32_t* b, int qb,
@@ -398,7 +409,15 @@ cudaError_t launch_gp_planes(const SpaceDev& space, const uint32_t* train_rows, 
 }
 
 cudaError_t launch_tri_inverse(const double* L, int n, double* A, int lda, cudaStream_t s) {
-  tri_inverse_kernel<<<(n + 63) / 64, 64, 0, s>>>(L, n, A, lda);
+  int warps = kInvWarps;
+  while (warps > 1 && (size_t)warps * n * 8 > 200 * 1024) warps >>= 1;
+  const size_t smem = (size_t)warps * n * 8;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;  // n > 25600
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(tri_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  tri_inverse_kernel<<<(n + warps - 1) / warps, warps * 32, smem, s>>>(L, n, A, lda);
   return cudaGetLastError();
 }
 

@@ -186,8 +186,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += n_kendall * kM * 16;
   L.exp2 = off;    // 2^(j/256), j < 256
   off += 256 * 8;
-  L.rowscale = off;
-  off += kMaxChunks * kN * 8;
+  L.rowscale = off;  // [2][256]: row factors, then the same with the alpha / padding rows zeroed
+  off += 2 * kMaxChunks * kN * 8;
   L.rows = off;    // [2][128 x row_words] encoded rows of the next tiles (bulk-copy staging)
   off += 2 * kM * words * 4;
   L.stab = off;    // coord_lut / lengthscale of the finite numeric domains (when it fits)
@@ -209,7 +209,9 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   return L;
 }
 
-template <bool kPrecise>
+// ND > 0: all-numeric space with exactly ND parameters — the distance loop is unrolled at compile
+// time and the candidate coordinates stay in registers for the whole tile.  ND == 0: any space.
+template <bool kPrecise, int ND>
 __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const FusedArgs& a = ta.f;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* cmask = reinterpret_cast<uint64_t*>(smem + L.cmask);
   double* s_exp2 = reinterpret_cast<double*>(smem + L.exp2);
   double* rowscale = reinterpret_cast<double*>(smem + L.rowscale);
+  double* rowscale_ss = rowscale + kMaxChunks * kN;
   unsigned char* mat = smem + L.mat;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* cand_full = bars;
@@ -264,7 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       if (p.kind == BX_REAL || p.kind == BX_CATEGORICAL || p.kind == BX_PERMUTATION) continue;
       for (int d = tid; d < p.size; d += blockDim.x) stab[p.coord + d] = a.space.coord_lut[p.coord + d] * a.gp.inv_l[k];
     }
-  for (int i = tid; i < kMaxChunks * kN; i += blockDim.x) rowscale[i] = i < nch * kN ? ta.rowscale[i] : 0.0;
+  for (int i = tid; i < kMaxChunks * kN; i += blockDim.x) {
+    rowscale[i] = i < nch * kN ? ta.rowscale[i] : 0.0;
+    rowscale_ss[i] = i < n ? ta.rowscale[i] : 0.0;  // sum-of-squares rows: L^-1 only
+  }
   uint64_t* qs_mask = reinterpret_cast<uint64_t*>(smem + L.qs_mask);
   double* qs_uval = reinterpret_cast<double*>(smem + L.qs_uval);
   uint16_t* qs_vid = reinterpret_cast<uint16_t*>(smem + L.qs_vid);
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     for (int i = tid; i < qf.n_trees * 64; i += blockDim.x) qs_vid[i] = qf.vid[i];
   }
   if (tid == 0) {
-    mb_init(cand_full, 1);
+    mb_init(cand_full, kProdWarps);
     for (int i = 0; i < kMaxSlices; ++i) mb_init(&slice_empty[i], 1);
     for (int i = 0; i < kStages; ++i) {
       mb_init(&mat_full[i], 1);
@@ -445,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
+            if (ta.debug & 4) break;  // timing experiment: TMEM reads only
             const int row = kN * c + r0 + j;
             long long Z = (long long)(int32_t)g[0][j] << 40;
             Z += (long long)(int32_t)g[1][j] << 32;
@@ -452,9 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             Z += (long long)(int32_t)g[3][j] << 16;
             Z += (long long)(int32_t)g[4][j] << 8;
             Z += (long long)(int32_t)g[5][j];
-            const double v = (double)Z * rowscale[row];
-            if (row < n) ss = fma(v, v, ss);
-            else if (row == n) mean_s = v;
+            const double zd = (double)Z;
+            const double v = zd * rowscale_ss[row];  // 0 for the alpha row and the padding rows
+            ss = fma(v, v, ss);
+            if (row == n) mean_s = zd * rowscale[row];  // only in the alpha row's chunk
           }
         }
         tc_fence_before();
@@ -573,12 +581,31 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       const int64_t gi = tile * kM + c;
       if (pt == 0) TC_TRACE(0, 2, t);
+      double xr[ND > 0 ? ND : 1];
+      if constexpr (ND > 0) {
+#pragma unroll
+        for (int k = 0; k < ND; ++k) xr[k] = __longlong_as_double((long long)cval[k * kM + c]);
+      }
       for (int ks = nsl - 1; ks >= 0; --ks) {
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
         double W[kColsPerItem];
 #pragma unroll
         for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
-        for (int i = 0; i < a.n_num; ++i) {
+        if constexpr (ND > 0) {
+          const double2* pl0 = reinterpret_cast<const double2*>(planes + j0);
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            const double2* pl = pl0 + (size_t)k * (npad / 2);
+#pragma unroll
+            for (int u = 0; u < kColsPerItem / 2; ++u) {
+              const double2 y = pl[u];
+              const double d0 = xr[k] - y.x, d1 = xr[k] - y.y;
+              W[2 * u] = fma(d0, d0, W[2 * u]);
+              W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
+            }
+          }
+        }
+        for (int i = 0; i < (ND > 0 ? 0 : a.n_num); ++i) {
           const int k = a.num_param[i];
           const double x = __longlong_as_double((long long)cval[k * kM + c]);
           // 16-byte broadcast loads: half the shared-memory wavefronts of scalar loads
@@ -591,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
           }
         }
-        for (int i = 0; i < a.n_cat; ++i) {
+        for (int i = 0; i < (ND > 0 ? 0 : a.n_cat); ++i) {
           const int k = a.cat_param[i];
           const uint64_t x = cval[k * kM + c];
           const double wl = a.gp.inv_l2[k];
@@ -599,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
 #pragma unroll
           for (int u = 0; u < kColsPerItem; ++u) W[u] += (x != pl[u]) ? wl : 0.0;
         }
-        for (int i = 0, kend = 0; i < a.n_perm; ++i) {
+        for (int i = 0, kend = 0; i < (ND > 0 ? 0 : a.n_perm); ++i) {
           const int k = a.perm_param[i];
           const bx_param_desc& p = params[k];
           const uint64_t x = cval[k * kM + c];
@@ -643,21 +670,19 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           dw[4][qd] = __byte_perm(p01, p23, 0x5410);  // bits 0..7
         }
         if (pt == 0) TC_TRACE(0, 3, ks);
-        if (t > 0 && pt == 0) {
+        if (t > 0) {  // every producer waits for the MMAs to release the slice (no CTA barrier)
           mb_wait(&slice_empty[ks], (uint32_t)((t - 1) & 1));
           tc_fence_after();
         }
         if (pt == 0) TC_TRACE(0, 4, ks);
-        asm volatile("bar.sync 2, %0;" ::"n"(kProdThreads) : "memory");  // the MMAs no longer read this slice
-        if (pt == 0) TC_TRACE(0, 5, ks);
 #pragma unroll
         for (int b = 0; b < kDB; ++b)
           tmem_st2(tmem + lane_base + (uint32_t)(kDigCol0 + ks * kSliceCols + b * 8 + part * 2), dw[b][0], dw[b][1]);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
-      if (pt == 0) mb_arrive(cand_full);
+      __syncwarp();
+      if (lane == 0) mb_arrive(cand_full);  // one arrival per producer warp
       if (pt == 0) TC_TRACE(0, 6, t);
     }
   }
@@ -732,7 +757,18 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
   const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
-  auto kernel = a.f.precise ? gp_tc_kernel<true> : gp_tc_kernel<false>;
+  // all-numeric spaces with up to 16 parameters get the unrolled distance loop
+  const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;
+  const int nd = numeric ? a.f.n_num : 0;
+  auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
+  switch (nd) {
+#define BX_ND(d) \
+    case d: kernel = gp_tc_kernel<false, d>; break;
+    BX_ND(1) BX_ND(2) BX_ND(3) BX_ND(4) BX_ND(5) BX_ND(6) BX_ND(7) BX_ND(8)
+    BX_ND(9) BX_ND(10) BX_ND(11) BX_ND(12) BX_ND(13) BX_ND(14) BX_ND(15) BX_ND(16)
+#undef BX_ND
+    default: break;
+  }
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.f.q + kM - 1) / kM;
