@@ -92,6 +92,7 @@ struct bx_handle {
   bool no_tc = false;     // BX_GP_DMMA=1 forces the FP64 DMMA kernel
   bool tc_separate_forest = true;   // gp_tc + stand-alone forest kernel (BX_TC_FOREST_FUSED=1: fused)
   bool no_qs_forest = false;        // BX_FOREST_WALK=1: node walks instead of QuickScorer tables
+  bool rf_after_gp = false;         // last score_impl ran the forest + summary kernel after the posterior
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale;
@@ -1003,11 +1004,16 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // The stand-alone forest kernel and the GP kernel each fill every SM's shared memory, so
     // they cannot co-reside: run them back to back on the caller's stream (which also makes the
     // per-kernel CUDA-event timing exact).
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
-    if (forest && !fuse_rf)
+    // QuickScorer forest + summary in one kernel after the posterior (it reads the EI): used
+    // whenever a summary is wanted and the tables fit.
+    const bool rf_summ = forest && !fuse_rf && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
+                         h->use_tc && qs_summary_available(h->forest);
+    h->rf_after_gp = rf_summ;
+    if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+    if (forest && !fuse_rf && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                            h->d_probs.as<double>(), s));
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+    if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
     BX_CUDA(h, h->d_ei.ensure((size_t)q * 8));
     FusedArgs f = fused_args(h, rows, q, f_model);
     f.ei_out = h->d_ei.as<double>();
@@ -1021,6 +1027,12 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
+    if (rf_summ) {
+      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+      BX_CUDA(h, launch_rf_summary(a.space, h->forest, m, h->sm_count, s, n_partials));
+      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+      return BX_OK;
+    }
     BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));
     return BX_OK;
   }
@@ -1072,7 +1084,8 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
     // every value is -inf: only now is the probability tracker needed (acquisition.py:179-184)
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs, partials);
     m.track_prob = 1;
-    BX_CUDA(h, launch_summary(m, h->sm_count, s, &np));
+    if (h->rf_after_gp) BX_CUDA(h, launch_rf_summary(space_dev(h), h->forest, m, h->sm_count, s, &np));
+    else BX_CUDA(h, launch_summary(m, h->sm_count, s, &np));
     BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
@@ -1082,7 +1095,7 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   if (timing) {
     cudaEventElapsedTime(&h->t_ms[0], h->ev_t[0], h->ev_t[1]);
     cudaEventElapsedTime(&h->t_ms[1], h->ev_t[2], h->ev_t[3]);
-    cudaEventElapsedTime(&h->t_ms[2], h->ev_t[3], h->ev_t[4]);
+    cudaEventElapsedTime(&h->t_ms[2], h->rf_after_gp ? h->ev_t[1] : h->ev_t[3], h->ev_t[4]);
   }
   return BX_OK;
 }
@@ -1116,6 +1129,9 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
   for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
   Partial* base = h->d_partials.as<Partial>();
+  // the summary kernel of the fused paths writes at most 2 partials per SM
+  const int64_t np_max = fused_path(h) ? 2 * (int64_t)h->sm_count : (int64_t)per_chunk;
+  const bool running = np_max + 1 <= 1024 && (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 96 * 1024;
   // pass 1 without the probability tracker; pass 2 (with it) only if every value is -inf
   for (int pass = 0; pass < 2; ++pass) {
   int total = 0;
@@ -1132,11 +1148,16 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     BX_CUDA(h, cudaEventRecord(h->ev_copy[b], h->copy_stream));
     BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
     int np = 0;
+    // running merge: the chunk's partials land at base + 1 and are folded into base[0]
+    Partial* dst = running ? base + 1 : base + total;
     r = score_impl(h, h->d_host_rows[b].as<uint32_t>(), len, index_base + off, f_model, eps_f, k,
-                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, base + total, &np, s, false,
+                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, dst, &np, s, false,
                    pass == 1);
     if (r) return r;
-    total += np;
+    if (running)
+      BX_CUDA(h, c == 0 ? launch_partial_merge(base + 1, np, space_dev(h), k, base, s)
+                        : launch_partial_merge(base, np + 1, space_dev(h), k, base, s));
+    total = running ? 1 : total + np;
     BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
   }
   BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
@@ -1295,6 +1316,9 @@ int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t 
   BX_CUDA(h, h->d_gen_rows.ensure((size_t)chunk * W * 4));
   CotDev cot = h->has_cot ? h->cot : CotDev{};
   Partial* base = h->d_partials.as<Partial>();
+  // the summary kernel of the fused paths writes at most 2 partials per SM
+  const int64_t np_max = fused_path(h) ? 2 * (int64_t)h->sm_count : (int64_t)per_chunk;
+  const bool running = np_max + 1 <= 1024 && (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 96 * 1024;
   for (int pass = 0; pass < 2; ++pass) {
     int total = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {
@@ -1303,10 +1327,14 @@ int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t 
       BX_CUDA(h, launch_generate(space_dev(h), cot, h->d_leaf_count.as<int64_t>(), mode, seed,
                                  index_base + off, len, h->d_gen_rows.as<uint32_t>(), s));
       int np = 0;
+      Partial* dst = running ? base + 1 : base + total;
       r = score_impl(h, h->d_gen_rows.as<uint32_t>(), len, index_base + off, f_model, eps_f, k, 0,
-                     nullptr, nullptr, base + total, &np, s, false, pass == 1);
+                     nullptr, nullptr, dst, &np, s, false, pass == 1);
       if (r) return r;
-      total += np;
+      if (running)
+        BX_CUDA(h, c == 0 ? launch_partial_merge(base + 1, np, space_dev(h), k, base, s)
+                          : launch_partial_merge(base, np + 1, space_dev(h), k, base, s));
+      total = running ? 1 : total + np;
     }
     BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
                                     h->d_summary.as<bx_score_summary>(), s));

@@ -421,9 +421,14 @@ int summary_max_partials(int sm_count);
 cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials);
 // Merge partials into *out.  When pool_rows is non-NULL the rows of the top-k entries are
 // gathered from it (index - index_base); otherwise the caller fills them.
+cudaError_t launch_partial_merge(const Partial* partials, int n_partials, const SpaceDev& space, int k,
+                                 Partial* acc_out, cudaStream_t s);
 cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const SpaceDev& space,
                                  int k, const uint32_t* pool_rows, int64_t index_base,
                                  bx_score_summary* out, cudaStream_t s);
+bool qs_summary_available(const ForestDev& f);
+cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
+                              cudaStream_t s, int* n_partials);
 cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
                       int pairwise, double* probs, cudaStream_t s);
 cudaError_t launch_neighbors(const SpaceDev& space, const CotDev* cot, const uint32_t* rows,

@@ -12,6 +12,7 @@
 // mean over trees: sequential over trees for q >= 2 (the (T, q) reduction over axis 0), numpy's
 // pairwise_sum (8 accumulators, 128-element blocks) for q == 1.
 #include "bx_common.cuh"
+#include "summary.cuh"
 
 namespace bx {
 
@@ -301,6 +302,110 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
   }
 }
 
+// QuickScorer forest fused with the acquisition summary (the work of summary_kernel): runs after the
+// posterior kernel, reads its EI, applies value = -inf if p < eps_f else EI * p (acquisition.py:
+// 77-79) and keeps per-warp partials (stable top-k, both trackers) merged into one per block.
+__global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, QsForestDev f, SummaryArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ bx_param_desc params[BX_MAX_PARAMS];
+  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem);
+  size_t off = (size_t)f.stride * f.tpad * 8;
+  double* s_uval = reinterpret_cast<double*>(smem + off);
+  off += (size_t)f.n_uvals * 8;
+  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + off);
+  off += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem + off);
+  off += (size_t)f.n_codes * kQsThreads * 4;
+  Partial* parts = reinterpret_cast<Partial*>(smem + ((off + 15) & ~(size_t)15));  // [warps]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
+    reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(sp.params)[i];
+  for (int i = tid; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
+  for (int i = tid; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
+  for (int i = tid; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
+  Partial* summ = &parts[warp];
+  if (lane == 0) partial_init(summ);
+  __syncthreads();
+  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(s_mask);
+  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(s_uval);
+  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(s_vid);
+  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(s_off) + 4u * tid;
+  const int words = sp.row_words;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + warp * 32; base < a.q; base += stride) {
+    const int64_t i = base + lane;
+    const bool valid = i < a.q;
+    double value = -INFINITY, prob = -INFINITY;
+    if (valid) {
+      const uint32_t* row = a.rows + (size_t)i * words;
+      for (int c = 0; c < f.n_codes; ++c)
+        sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+      double sum = 0.0;
+      for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {
+        uint64_t m[kQsGroup];
+#pragma unroll
+        for (int j = 0; j < kQsGroup; ++j) m[j] = ~0ull;
+        for (int c = 0; c < f.n_codes; ++c) {
+          const uint32_t col = mask_s + (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + g0) * 8u;
+#pragma unroll
+          for (int j = 0; j < kQsGroup / 2; ++j) {
+            const ulonglong2 w = lds_u64x2(col + 16u * j);
+            m[2 * j] &= w.x;
+            m[2 * j + 1] &= w.y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kQsGroup; ++j)
+          if (g0 + j < f.n_trees) {
+            const uint32_t id = lds_u16(vid_s + 2u * (uint32_t)((g0 + j) * 64 + __ffsll((long long)m[j]) - 1));
+            const double v = __longlong_as_double((long long)lds_u64(uval_s + 8u * id));
+            sum = (g0 + j == 0) ? v : __dadd_rn(sum, v);  // tree order (feasibility.py:89)
+          }
+      }
+      prob = __ddiv_rn(sum, (double)f.n_trees);
+      value = (prob < a.eps_f) ? -INFINITY : a.ei[i] * prob;
+      if (a.values_out) a.values_out[i] = value;
+      if (a.probs_out) a.probs_out[i] = prob;
+    }
+    const bool fin = valid && value != -INFINITY;
+    const bool top_open = a.k > 0 && summ->n_top < a.k;
+    const double kth = (a.k > 0 && !top_open) ? summ->top[a.k - 1].value : -INFINITY;
+    const bool prob_ok = a.track_prob && prob >= summ->best_prob.prob;
+    const bool maybe = valid && ((fin && a.k > 0 && (top_open || value >= kth)) ||
+                                 (fin && value >= summ->best.value) || prob_ok);
+    bool evaluated = false;
+    if (maybe && a.evald.count > 0) evaluated = is_evaluated(a.evald, a.rows + (size_t)i * words, words);
+    const bool pass = maybe && ((fin && a.k > 0 && (top_open || value >= kth)) ||
+                                (!evaluated && ((fin && value >= summ->best.value) || prob_ok)));
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    const unsigned fmask = __ballot_sync(0xffffffffu, fin);
+    unsigned pmask = __ballot_sync(0xffffffffu, pass);
+    const unsigned emask = __ballot_sync(0xffffffffu, evaluated);
+    if (lane == 0) {
+      summ->n_scored += __popc(vmask);
+      summ->n_finite += __popc(fmask);
+    }
+    while (pmask) {
+      const int c = __ffs(pmask) - 1;
+      pmask &= pmask - 1;
+      const double vc = __shfl_sync(0xffffffffu, value, c);
+      const double pc = __shfl_sync(0xffffffffu, prob, c);
+      if (lane == 0)
+        partial_add(summ, a.k, params, sp.n_params, sp.rank_lut, words, vc, pc, a.index_base + base + c,
+                    (emask >> c) & 1u, a.rows + (size_t)(base + c) * words, a.track_prob != 0);
+      __syncwarp();
+    }
+  }
+  __syncthreads();  // fold the block's warp partials into one
+  if (tid == 0)
+    for (int w = 1; w < kQsThreads / 32; ++w)
+      partial_merge(&parts[0], &parts[w], a.k, params, sp.n_params, sp.rank_lut, words);
+  __syncthreads();
+  const int32_t* src = reinterpret_cast<const int32_t*>(&parts[0]);
+  int32_t* dst = reinterpret_cast<int32_t*>(a.partials + blockIdx.x);
+  for (int i = tid; i < (int)(sizeof(Partial) / 4); i += kQsThreads) dst[i] = src[i];
+}
+
 size_t qs_smem(const QsForestDev& f) {
   return (size_t)f.stride * f.tpad * 8 + (size_t)f.n_uvals * 8 + (((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15) +
          (size_t)f.n_codes * kQsThreads * 4;
@@ -317,7 +422,30 @@ auto pick_real(bool real) {
   return real ? rf_coded_kernel<SMEM, true> : rf_coded_kernel<SMEM, false>;
 }
 
+size_t qs_summary_smem(const QsForestDev& f) {
+  return ((qs_smem(f) + 15) & ~(size_t)15) + (size_t)(kQsThreads / 32) * sizeof(Partial);
+}
+
 }  // namespace
+
+bool qs_summary_available(const ForestDev& f) {
+  return f.coded && f.has_trees && f.qs.enabled && qs_summary_smem(f.qs) <= 227 * 1024;
+}
+
+// Forest + summary in one kernel (after the posterior kernel wrote a.ei); a.partials receives one
+// partial per block (<= SM count).
+cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
+                              cudaStream_t s, int* n_partials) {
+  const size_t bytes = qs_summary_smem(f.qs);
+  cudaError_t e = cudaFuncSetAttribute(rf_qs_summary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (a.q + kQsThreads - 1) / kQsThreads;
+  if (blocks > sm_count) blocks = sm_count;
+  if (blocks < 1) blocks = 1;
+  *n_partials = (int)blocks;
+  rf_qs_summary_kernel<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
                       int use_pairwise, double* probs, cudaStream_t s) {
