@@ -1,5 +1,6 @@
 // bx_api.cu — the C ABI (include/bx_sm100.h): handle, model-state uploads, launches.
 // No exception crosses the boundary; every failure becomes a status code + bx_last_error().
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -7,6 +8,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <unordered_map>
+#include <mutex>
 
 #include "bx_common.cuh"
 
@@ -79,9 +82,10 @@ struct bx_handle {
   ConstraintDev cons{};
   DevBuf d_prog_begin, d_code, d_consts, d_vtag, d_vint, d_vflt, d_voff, d_str_id, d_fault;
   // scratch
-  DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[2];
+  static constexpr int kHostBufs = 4;  // bx_score_host ring: copies run up to 3 chunks ahead
+  DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[kHostBufs];
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copy[kHostBufs] = {}, ev_done[kHostBufs] = {};
   cudaEvent_t ev_t[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // rf / gp / merge timing
   float t_ms[3] = {0, 0, 0};
   // register-resident fused GP path (gp_fused.cu)
@@ -93,6 +97,8 @@ struct bx_handle {
   bool tc_separate_forest = true;   // gp_tc + stand-alone forest kernel (BX_TC_FOREST_FUSED=1: fused)
   bool no_qs_forest = false;        // BX_FOREST_WALK=1: node walks instead of QuickScorer tables
   bool rf_after_gp = false;         // last score_impl ran the forest + summary kernel after the posterior
+  int tc_debug = 0;                 // BX_TC_DEBUG (timing experiments)
+  bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale;
@@ -105,7 +111,31 @@ struct bx_handle {
   cudaEvent_t ev_fork = nullptr, ev_rf = nullptr;
 };
 
+cudaError_t bx::set_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[fn];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 namespace {
+
+// 2^(j/64) and 2^(j/256), correctly rounded (long double), computed once per process
+struct Exp2Tables {
+  double t64[64], t256[256];
+  Exp2Tables() {
+    for (int j = 0; j < 64; ++j) t64[j] = (double)exp2l((long double)j / 64.0L);
+    for (int j = 0; j < 256; ++j) t256[j] = (double)exp2l((long double)j / 256.0L);
+  }
+};
+const Exp2Tables& exp2_tables() {
+  static const Exp2Tables t;
+  return t;
+}
 
 int fail(bx_handle* h, int code, const char* fmt, ...) {
   char buf[512];
@@ -215,7 +245,7 @@ FusedArgs fused_args(const bx_handle* h, const uint32_t* rows, int64_t q, double
     else if (kind == BX_PERMUTATION) f.perm_param[f.n_perm++] = k;
     else f.num_param[f.n_num++] = k;
   }
-  for (int j = 0; j < 64; ++j) f.exp2tab[j] = (double)exp2l((long double)j / 64.0L);
+  std::memcpy(f.exp2tab, exp2_tables().t64, sizeof(f.exp2tab));
   f.precise = h->matern_precise ? 1 : 0;
   return f;
 }
@@ -233,9 +263,9 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.n_chunks = h->tc_nch;
     t.kscale = h->tc_kscale;
     t.n_coord = (int32_t)h->coord_host.size();
-    for (int j = 0; j < 256; ++j) t.exp2tab256[j] = (double)exp2l((long double)j / 256.0L);
-    if (const char* dbg = getenv("BX_TC_DEBUG")) t.debug = atoi(dbg);
-    const char* trace = getenv("BX_TC_TRACE");  // profiling aid: dump CTA 0's role timeline
+    std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
+    t.debug = h->tc_debug;
+    const char* trace = h->tc_trace ? getenv("BX_TC_TRACE") : nullptr;  // profiling aid: CTA 0's timeline
     if (!trace || !trace[0]) return launch_gp_tc(t, h->sm_count, s);
     const size_t bytes = 4 * 4096 * 2 * sizeof(long long);
     std::vector<long long> host(bytes / sizeof(long long));
@@ -281,13 +311,15 @@ bx_handle* bx_create(int device) {
   h->no_coded_forest = generic && generic[0] == '1';
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < bx_handle::kHostBufs; ++i) {
     cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
   }
   for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
   const char* gpg = getenv("BX_GP_GENERIC");
   h->no_fused = gpg && gpg[0] == '1';
+  if (const char* dbg = getenv("BX_TC_DEBUG")) h->tc_debug = atoi(dbg);
+  h->tc_trace = getenv("BX_TC_TRACE") != nullptr;
   const char* fw = getenv("BX_FOREST_WALK");
   h->no_qs_forest = fw && fw[0] == '1';
   // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
@@ -321,13 +353,14 @@ void bx_destroy(bx_handle* h) {
                     &h->d_child_begin, &h->d_child_count, &h->d_child_value, &h->d_prog_begin, &h->d_code,
                     &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
-                    &h->d_host_rows[0], &h->d_host_rows[1], &h->d_cnodes, &h->d_leaf_val,
+                    &h->d_host_rows[0], &h->d_host_rows[1], &h->d_host_rows[2], &h->d_host_rows[3],
+                    &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
                     &h->d_knodes, &h->d_kvid, &h->d_kuval, &h->d_qmask, &h->d_qvid,
                     &h->d_quval, &h->d_qsoff};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < bx_handle::kHostBufs; ++i) {
     if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
     if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
   }
@@ -1119,27 +1152,38 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->row_words;
-  // geometric chunk sizes (2^16, 2^17, then 2^18): the first copy, which nothing overlaps, is short
-  const int64_t chunk = 1 << 18;
-  auto chunk_len = [&](int64_t c) -> int64_t { return c >= 2 ? chunk : (chunk >> (2 - c)); };
+  // chunks of 2^17, 2^18, then 2^19 rows through a 2-buffer ring: the first copy, which nothing
+  // overlaps, stays short, and later chunks are large enough that per-launch costs vanish (measured
+  // on B200 over PCIe at 26 GB/s; BX_HOST_CHUNK / _RAMP / _BUFS override for tuning)
+  int64_t chunk = 1 << 19;
+  int ramp = 2, nbuf = 2;
+  if (const char* e = getenv("BX_HOST_CHUNK")) chunk = (int64_t)1 << atoi(e);   // tuning aids
+  if (const char* e = getenv("BX_HOST_RAMP")) ramp = atoi(e);
+  if (const char* e = getenv("BX_HOST_BUFS")) nbuf = std::max(1, std::min(bx_handle::kHostBufs, atoi(e)));
+  auto chunk_len = [&](int64_t c) -> int64_t { return c >= ramp ? chunk : (chunk >> (ramp - c)); };
   int64_t n_chunks = 0;
   for (int64_t off = 0; off < q; off += chunk_len(n_chunks), ++n_chunks) {}
   const size_t per_chunk = (size_t)max_partials(h->sm_count);
   BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
-  for (int b = 0; b < 2; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
+  for (int b = 0; b < bx_handle::kHostBufs; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
   Partial* base = h->d_partials.as<Partial>();
-  // the summary kernel of the fused paths writes at most 2 partials per SM
-  const int64_t np_max = fused_path(h) ? 2 * (int64_t)h->sm_count : (int64_t)per_chunk;
-  const bool running = np_max + 1 <= 1024 && (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 96 * 1024;
+  // Partials per chunk: one per SM (forest + summary kernel) or two (summary kernel).  They are
+  // merged once at the end when all of them fit the fast merge, else folded into a running
+  // partial after every chunk.
+  const bool rf_summ = h->use_tc && h->has_forest && h->forest.has_trees && qs_summary_available(h->forest);
+  const int64_t np_max = fused_path(h) ? (rf_summ ? 1 : 2) * (int64_t)h->sm_count : (int64_t)per_chunk;
+  const bool fits_once = np_max * n_chunks <= 1024 &&
+                         np_max * n_chunks * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
+  const bool running = !fits_once && np_max + 1 <= 1024 &&
+                       (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
   // pass 1 without the probability tracker; pass 2 (with it) only if every value is -inf
   for (int pass = 0; pass < 2; ++pass) {
   int total = 0;
-  BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
-  BX_CUDA(h, cudaEventRecord(h->ev_done[1], s));
+  for (int b = 0; b < bx_handle::kHostBufs; ++b) BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
   int64_t off = 0;
   for (int64_t c = 0; c < n_chunks; off += chunk_len(c), ++c) {
-    const int b = (int)(c & 1);
+    const int b = (int)(c % nbuf);
     const int64_t len = (q - off) < chunk_len(c) ? (q - off) : chunk_len(c);
     // the copy into buffer b waits until the kernels that last read buffer b are done
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
@@ -1316,9 +1360,15 @@ int bx_score_generated(bx_handle* h, uint64_t seed, int64_t index_base, int64_t 
   BX_CUDA(h, h->d_gen_rows.ensure((size_t)chunk * W * 4));
   CotDev cot = h->has_cot ? h->cot : CotDev{};
   Partial* base = h->d_partials.as<Partial>();
-  // the summary kernel of the fused paths writes at most 2 partials per SM
-  const int64_t np_max = fused_path(h) ? 2 * (int64_t)h->sm_count : (int64_t)per_chunk;
-  const bool running = np_max + 1 <= 1024 && (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 96 * 1024;
+  // Partials per chunk: one per SM (forest + summary kernel) or two (summary kernel).  They are
+  // merged once at the end when all of them fit the fast merge, else folded into a running
+  // partial after every chunk.
+  const bool rf_summ = h->use_tc && h->has_forest && h->forest.has_trees && qs_summary_available(h->forest);
+  const int64_t np_max = fused_path(h) ? (rf_summ ? 1 : 2) * (int64_t)h->sm_count : (int64_t)per_chunk;
+  const bool fits_once = np_max * n_chunks <= 1024 &&
+                         np_max * n_chunks * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
+  const bool running = !fits_once && np_max + 1 <= 1024 &&
+                       (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
   for (int pass = 0; pass < 2; ++pass) {
     int total = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {

@@ -12,6 +12,14 @@
 
 namespace bx {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (host side): the call
+// costs microseconds, and the chunked scoring paths launch the same kernels many times
+cudaError_t set_smem_once(const void* fn, int bytes);
+template <typename K>
+inline cudaError_t set_smem(K* fn, int bytes) {
+  return set_smem_once(reinterpret_cast<const void*>(fn), bytes);
+}
+
 constexpr int kRealGrid = 64;          // space.py:23 REAL_NEIGHBOR_GRID
 constexpr double kSqrt5 = 2.23606797749978969640917366873128;  // surrogate.py:35 math.sqrt(5.0)
 constexpr double kInvSqrt2Pi = 0.398942280401432702863218082712;  // acquisition.py:27

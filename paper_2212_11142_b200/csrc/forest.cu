@@ -437,7 +437,7 @@ bool qs_summary_available(const ForestDev& f) {
 cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
                               cudaStream_t s, int* n_partials) {
   const size_t bytes = qs_summary_smem(f.qs);
-  cudaError_t e = cudaFuncSetAttribute(rf_qs_summary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = set_smem(rf_qs_summary_kernel, (int)bytes);
   if (e != cudaSuccess) return e;
   int64_t blocks = (a.q + kQsThreads - 1) / kQsThreads;
   if (blocks > sm_count) blocks = sm_count;
@@ -455,7 +455,7 @@ cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t*
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (f.coded && f.qs.enabled && qs_smem(f.qs) <= 220 * 1024) {
     const size_t bytes = qs_smem(f.qs);
-    cudaError_t e = cudaFuncSetAttribute(rf_qs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = set_smem(rf_qs_kernel, (int)bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rf_qs_kernel, kQsThreads, bytes);
@@ -470,7 +470,7 @@ cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t*
     const bool in_smem = coded_smem(f.cf, true) <= 220 * 1024;
     const size_t bytes = coded_smem(f.cf, in_smem);
     auto kern = in_smem ? pick_real<true>(f.cf.has_real) : pick_real<false>(f.cf.has_real);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = set_smem(kern, (int)bytes);
     if (e != cudaSuccess) return e;
     int64_t blocks = (q + kRfThreads - 1) / kRfThreads;
     if (blocks > sms) blocks = sms;

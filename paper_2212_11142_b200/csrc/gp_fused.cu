@@ -399,8 +399,7 @@ cudaError_t launch_mt(const FusedArgs& a, int sm_count, cudaStream_t s) {
                                                   kf.n_nodes, kf.n_uvals, kf.n_trees, kf.n_codes)
                                    : fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT);
   if (L.total > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(gp_fused_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       L.total);
+  cudaError_t e = set_smem(gp_fused_kernel<MT>, L.total);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gp_fused_kernel<MT>, nw * 32, L.total);

@@ -385,8 +385,7 @@ cudaError_t launch_lml(const double* sq, int n, int D, const double* z, const do
   const size_t bytes = ((size_t)n * (n + 1) / 2 + n) * sizeof(double);
   const int use_smem = bytes <= 200 * 1024;
   if (use_smem) {
-    cudaError_t e = cudaFuncSetAttribute(lml_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+    cudaError_t e = set_smem(lml_kernel, (int)bytes);
     if (e != cudaSuccess) return e;
   }
   lml_kernel<<<c, kLmlThreads, use_smem ? bytes : 0, s>>>(sq, n, D, z, thetas, out, scratch, use_smem);
@@ -414,7 +413,7 @@ cudaError_t launch_tri_inverse(const double* L, int n, double* A, int lda, cudaS
   const size_t smem = (size_t)warps * n * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;  // n > 25600
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(tri_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem(tri_inverse_kernel, (int)smem);
     if (e != cudaSuccess) return e;
   }
   tri_inverse_kernel<<<(n + warps - 1) / warps, warps * 32, smem, s>>>(L, n, A, lda);

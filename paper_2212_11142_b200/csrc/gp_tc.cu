@@ -769,7 +769,7 @@ cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
 #undef BX_ND
     default: break;
   }
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  cudaError_t e = set_smem(kernel, L.total);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.f.q + kM - 1) / kM;
   int64_t grid = sm_count;

@@ -1,6 +1,6 @@
 // merge.cu — reduce per-block partial summaries into the bx_score_summary of a call.
 //
-// Fast path (n_partials <= 1024, lists <= 96 KB): a two-level warp tournament (merge_fast_kernel).
+// Fast path (n_partials <= 1024, lists <= 200 KB): a two-level warp tournament (merge_fast_kernel).
 // Otherwise
 // 128 threads: each folds a strided subset of the partials into its own top-k list in shared
 // memory, then a log2(128)-level tree merges pairs of sorted lists (two-pointer merge, keep k)
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const Partial* par
 // [w G, (w+1) G) by k rounds of a warp argmax over the list heads (order: value desc, index asc),
 // then warp 0 merges the 32 warp lists the same way.  Trackers: warp argmax by (value desc, key).
 constexpr int kFastThreads = 1024;
-constexpr int kFastBytes = 96 * 1024;  // n_parts * k * sizeof(TopRec) must fit
+constexpr int kFastBytes = 200 * 1024;  // n_parts * k * sizeof(TopRec) must fit
 
 __device__ __forceinline__ bool rec_before(const TopRec& a, const TopRec& b) {
   return a.value > b.value || (a.value == b.value && a.index < b.index);
@@ -321,7 +321,7 @@ cudaError_t launch_partial_merge(const Partial* partials, int n_partials, const 
                                  Partial* acc_out, cudaStream_t s) {
   const size_t bytes = (size_t)n_partials * (k > 0 ? k : 1) * sizeof(TopRec);
   if (n_partials > 1024 || bytes > (size_t)kFastBytes) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(merge_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cudaError_t e = set_smem(merge_fast_kernel, (int)bytes);
   if (e != cudaSuccess) return e;
   merge_fast_kernel<<<1, kFastThreads, bytes, s>>>(partials, n_partials, space, k, nullptr, 0, nullptr, acc_out);
   return cudaGetLastError();
@@ -332,15 +332,14 @@ cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const 
                                  bx_score_summary* out, cudaStream_t s) {
   const size_t fb = (size_t)n_partials * (k > 0 ? k : 1) * sizeof(TopRec);
   if (n_partials <= 1024 && fb <= (size_t)kFastBytes) {
-    cudaError_t e = cudaFuncSetAttribute(merge_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb);
+    cudaError_t e = set_smem(merge_fast_kernel, (int)fb);
     if (e != cudaSuccess) return e;
     merge_fast_kernel<<<1, kFastThreads, fb, s>>>(partials, n_partials, space, k, pool_rows, index_base, out,
                                                    nullptr);
     return cudaGetLastError();
   }
   const size_t bytes = (size_t)kMergeThreads * (k > 0 ? k : 1) * sizeof(TopRec);
-  cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bytes);
+  cudaError_t e = set_smem(merge_kernel, (int)bytes);
   if (e != cudaSuccess) return e;
   merge_kernel<<<1, kMergeThreads, bytes, s>>>(partials, n_partials, space, k, pool_rows,
                                                 index_base, out);

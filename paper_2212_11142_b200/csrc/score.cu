@@ -325,8 +325,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(ScoreArgs a) {
 template <int CPW>
 cudaError_t launch_score_t(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials) {
   const SmemLayout L = smem_layout(CPW, a.gp.ncols_pad, a.space.n_params);
-  cudaError_t e = cudaFuncSetAttribute(score_kernel<CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       L.total);
+  cudaError_t e = set_smem(score_kernel<CPW>, L.total);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<CPW>, kThreads, L.total);

@@ -41,6 +41,7 @@ def run(case="C3", q=1 << 20):
     from paper_2212_11142_b200.device import scorer
     meta, arr, space = load(case)
     gp, feas = model(meta, arr, space)
+    os.environ["BX_TC_TRACE"] = ""  # present at handle creation (enables the per-launch check), empty = off
     sc = scorer()
     sc.set_gp(gp)
     rng = np.random.default_rng(0)
