@@ -124,3 +124,36 @@ def test_space_exhausted_raises():
         A.optimize_acquisition(ctx, sp, cot)
     ctx = Ctx(gp, None, 1.0, 0.0, np.random.default_rng(0), set(allc[:5]))
     assert A.optimize_acquisition(ctx, sp, cot) == allc[5]
+
+
+@pytest.mark.parametrize("n", [64, 200, 300, 500])
+def test_mixed_space_large_n_against_oracle(n):
+    """C5 (d=10 mixed: log-ordinal, integer, real, categorical, Spearman and Kendall permutations)
+    at n up to 500 — the tensor-core kernel (n <= 255) and the generic kernel beyond — against the
+    oracle's FP64 posterior on a sample of a 2^18 pool (BASELINE config 5 uses n = 500)."""
+    import oracle
+    from paper_2212_11142_b200 import scenarios
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    space = scenarios.build_space("C5")
+    rng = np.random.default_rng(n)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    cfgs = lay.decode(scenarios.sample_rows_uniform(lay, n, rng))
+    y = np.array([scenarios.objective("C5", c) for c in cfgs])
+    hyp = Hyper(outputscale=1.7, noise_variance=1e-4,
+                lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
+    gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+    sc.set_gp(gp)
+    assert sc.gp_kernel() == ("tensor" if n <= 255 else "generic")
+    rows = sc.to_device(scenarios.sample_rows_uniform(lay, 1 << 18, rng))
+    mean, var = (x.cpu().numpy() for x in sc.predict(rows))
+    idx = rng.choice(len(mean), 1500, replace=False)
+    sample = lay.decode(rows.cpu().numpy().view(np.uint32)[idx])
+    og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
+                         L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
+    m0, v0 = oracle.gp.predict(og, sample)
+    np.testing.assert_allclose(mean[idx], m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
+    np.testing.assert_allclose(var[idx], v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
+    sc.close()
