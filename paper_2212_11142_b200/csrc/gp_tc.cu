@@ -23,6 +23,7 @@
 //   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*16 x 32 per chunk and slice, b = K* digit)
 //   warp 1  lane 0 : TMA producer: one 3 KB bulk copy per (chunk, slice) block, 8-stage ring
 //   warp 1  lane 1 : row prefetcher: the next tiles' encoded rows, one bulk copy per tile
+//   warps 2-3      : decoders: candidate values / masks / forest offsets of the next tile
 //   warps 4-7      : epilogue, thread = candidate = TMEM lane: tcgen05.ld of the 6 groups,
 //                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction;
 //                    between chunks, the candidate's forest probability from QuickScorer tables
@@ -180,10 +181,10 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += n_params * npad * 8;
   L.kmask = off;   // [n_kendall][npad][2]
   off += n_kendall * npad * 16;
-  L.cval = off;    // [n_params][128] decoded candidate values
-  off += n_params * kM * 8;
-  L.cmask = off;   // [n_kendall][128][2] candidate Kendall masks
-  off += n_kendall * kM * 16;
+  L.cval = off;    // [2][n_params][128] decoded candidate values (tile parity)
+  off += 2 * n_params * kM * 8;
+  L.cmask = off;   // [2][n_kendall][128][2] candidate Kendall masks
+  off += 2 * n_kendall * kM * 16;
   L.exp2 = off;    // 2^(j/256), j < 256
   off += 256 * 8;
   L.rowscale = off;  // [2][256]: row factors, then the same with the alpha / padding rows zeroed
@@ -204,7 +205,7 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   L.mat = off;     // [stage][digit][16 x 32 B]
   off += kStages * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
-  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 2 + 1) * 8;
+  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 2 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
@@ -240,7 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* rows_full = acc_empty + 2;
   uint64_t* rows_empty = rows_full + 2;
   uint64_t* qs_free = rows_empty + 2;  // the epilogue is done with a tile's forest offsets
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qs_free + 2);
+  uint64_t* cval_full = qs_free + 2;   // the decoders filled a tile's candidate values
+  uint64_t* cval_free = cval_full + 2; // every producer is done with them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cval_free + 2);
   uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
   // rows are staged by 16-byte bulk copies when the pool pointer allows it
   const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
@@ -293,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       mb_init(&rows_full[i], 1);
       mb_init(&rows_empty[i], 1);
       mb_init(&qs_free[i], 4);
+      mb_init(&cval_full[i], 1);
+      mb_init(&cval_free[i], kProdWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -315,7 +320,84 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     return (int)(((count * words * 4) & ~(int64_t)15) / 4);
   };
 
-  if (warp == 1 && lane == 1) {
+  if (warp == 2 || warp == 3) {
+    // ---- decoders: the next tile's candidates (coordinate / lengthscale, labels, packed
+    // permutations, Kendall masks, forest table offsets) into the tile-parity buffers ----------
+    const int dt = tid - 64;  // 0..63
+    for (int t = 0; t < my_tiles; ++t) {
+      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+      const int buf = t & 1;
+      if (t >= 2) mb_wait(&cval_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+      mb_wait(&rows_full[buf], (uint32_t)((t >> 1) & 1));
+      const uint32_t* rs = rowsbuf + (size_t)buf * kM * words;
+      const int sw = staged_words(tile);
+      uint64_t* cv = cval + (size_t)buf * n_params * kM;
+      for (int idx = dt; idx < n_params * kM; idx += 64) {
+        const int k = idx / kM, cc = idx % kM;
+        const int64_t gi = tile * kM + cc;
+        const bx_param_desc& p = params[k];
+        auto word = [&](int w) -> uint32_t {
+          const int o = cc * words + w;
+          return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
+        };
+        uint64_t v = 0;
+        if (gi < a.q) {
+          if (p.kind == BX_PERMUTATION) {
+            v = (uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32);
+          } else if (p.kind == BX_CATEGORICAL) {
+            v = word(p.word);
+          } else {
+            double x;
+            if (p.kind == BX_REAL)
+              x = __longlong_as_double((long long)((uint64_t)word(p.word + 2) | ((uint64_t)word(p.word + 3) << 32))) *
+                  a.gp.inv_l[k];
+            else if (use_stab)
+              x = stab[p.coord + (int)word(p.word)];
+            else
+              x = a.space.coord_lut[p.coord + (int)word(p.word)] * a.gp.inv_l[k];
+            v = (uint64_t)__double_as_longlong(x);
+          }
+        }
+        cv[idx] = v;
+      }
+      if (rf) {  // forest table offsets of the tile, read by the epilogue (its thread = candidate)
+        if (t >= 2) mb_wait(&qs_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
+        for (int idx = dt; idx < qf.n_codes * kM; idx += 64) {
+          const int sl = idx / kM, cc = idx % kM;
+          const int64_t gi = tile * kM + cc;
+          int v = 0;
+          if (gi < a.q) {
+            auto word = [&](int w) -> uint32_t {
+              const int o = cc * words + w;
+              return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
+            };
+            const bx_param_desc& p = params[qf.code_param[sl]];
+            if (p.kind == BX_PERMUTATION)
+              v = perm_pos((uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32), p.size, qf.code_sub[sl]);
+            else if (p.kind == BX_CATEGORICAL)
+              v = (int)word(p.word) == qf.code_sub[sl] ? 1 : 0;
+            else
+              v = (int)word(p.word);
+          }
+          qo[idx] = (qf.soff[sl] + v) * qf.tpad;
+        }
+      }
+      asm volatile("bar.sync 3, 64;" ::: "memory");
+      if (dt == 0) mb_arrive(&rows_empty[buf]);
+      uint64_t* cm = cmask + (size_t)buf * a.n_kendall * kM * 2;
+      for (int idx = dt; idx < a.n_kendall * kM; idx += 64) {
+        const int kk = idx / kM, cc = idx % kM;
+        const bx_param_desc& p = params[a.kendall_param[kk]];
+        uint64_t lo = 0, hi = 0;
+        kendall_mask(cv[a.kendall_param[kk] * kM + cc], p.size, lo, hi);
+        cm[2 * idx] = lo;
+        cm[2 * idx + 1] = hi;
+      }
+      asm volatile("bar.sync 3, 64;" ::: "memory");
+      if (dt == 0) mb_arrive(&cval_full[buf]);
+    }
+  } else if (warp == 1 && lane == 1) {
     // ---- row prefetcher: the encoded rows of each tile, one bulk copy ahead ----------------
     {
       for (int t = 0; t < my_tiles; ++t) {
@@ -511,80 +593,17 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     const double kscale = ta.kscale;
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");  // every producer is done with the last tile
       if (pt == 0) TC_TRACE(0, 1, t);
-      const int buf = t & 1;
-      mb_wait(&rows_full[buf], (uint32_t)((t >> 1) & 1));
-      const uint32_t* rs = rowsbuf + (size_t)buf * kM * words;
-      const int sw = staged_words(tile);
-      for (int idx = pt; idx < n_params * kM; idx += kProdThreads) {
-        const int k = idx / kM, cc = idx % kM;
-        const int64_t gi = tile * kM + cc;
-        const bx_param_desc& p = params[k];
-        auto word = [&](int w) -> uint32_t {
-          const int o = cc * words + w;
-          return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
-        };
-        uint64_t v = 0;
-        if (gi < a.q) {
-          if (p.kind == BX_PERMUTATION) {
-            v = (uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32);
-          } else if (p.kind == BX_CATEGORICAL) {
-            v = word(p.word);
-          } else {
-            double x;
-            if (p.kind == BX_REAL)
-              x = __longlong_as_double((long long)((uint64_t)word(p.word + 2) | ((uint64_t)word(p.word + 3) << 32))) *
-                  a.gp.inv_l[k];
-            else if (use_stab)
-              x = stab[p.coord + (int)word(p.word)];
-            else
-              x = a.space.coord_lut[p.coord + (int)word(p.word)] * a.gp.inv_l[k];
-            v = (uint64_t)__double_as_longlong(x);
-          }
-        }
-        cval[idx] = v;
-      }
-      if (rf) {  // forest table offsets of the tile, read by the epilogue (its thread = candidate)
-        if (t >= 2) mb_wait(&qs_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
-        int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
-        for (int idx = pt; idx < qf.n_codes * kM; idx += kProdThreads) {
-          const int sl = idx / kM, cc = idx % kM;
-          const int64_t gi = tile * kM + cc;
-          int v = 0;
-          if (gi < a.q) {
-            auto word = [&](int w) -> uint32_t {
-              const int o = cc * words + w;
-              return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
-            };
-            const bx_param_desc& p = params[qf.code_param[sl]];
-            if (p.kind == BX_PERMUTATION)
-              v = perm_pos((uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32), p.size, qf.code_sub[sl]);
-            else if (p.kind == BX_CATEGORICAL)
-              v = (int)word(p.word) == qf.code_sub[sl] ? 1 : 0;
-            else
-              v = (int)word(p.word);
-          }
-          qo[idx] = (qf.soff[sl] + v) * qf.tpad;
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
-      if (pt == 0) mb_arrive(&rows_empty[buf]);
-      for (int idx = pt; idx < a.n_kendall * kM; idx += kProdThreads) {
-        const int kk = idx / kM, cc = idx % kM;
-        const bx_param_desc& p = params[a.kendall_param[kk]];
-        uint64_t lo = 0, hi = 0;
-        kendall_mask(cval[a.kendall_param[kk] * kM + cc], p.size, lo, hi);
-        cmask[2 * idx] = lo;
-        cmask[2 * idx + 1] = hi;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
+      const int cb = t & 1;
+      mb_wait(&cval_full[cb], (uint32_t)((t >> 1) & 1));
+      const uint64_t* cv = cval + (size_t)cb * n_params * kM;
+      const uint64_t* cmk = cmask + (size_t)cb * a.n_kendall * kM * 2;
       const int64_t gi = tile * kM + c;
       if (pt == 0) TC_TRACE(0, 2, t);
       double xr[ND > 0 ? ND : 1];
       if constexpr (ND > 0) {
 #pragma unroll
-        for (int k = 0; k < ND; ++k) xr[k] = __longlong_as_double((long long)cval[k * kM + c]);
+        for (int k = 0; k < ND; ++k) xr[k] = __longlong_as_double((long long)cv[k * kM + c]);
       }
       for (int ks = nsl - 1; ks >= 0; --ks) {
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
@@ -607,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         }
         for (int i = 0; i < (ND > 0 ? 0 : a.n_num); ++i) {
           const int k = a.num_param[i];
-          const double x = __longlong_as_double((long long)cval[k * kM + c]);
+          const double x = __longlong_as_double((long long)cv[k * kM + c]);
           // 16-byte broadcast loads: half the shared-memory wavefronts of scalar loads
           const double2* pl = reinterpret_cast<const double2*>(planes + (size_t)k * npad + j0);
 #pragma unroll
@@ -620,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         }
         for (int i = 0; i < (ND > 0 ? 0 : a.n_cat); ++i) {
           const int k = a.cat_param[i];
-          const uint64_t x = cval[k * kM + c];
+          const uint64_t x = cv[k * kM + c];
           const double wl = a.gp.inv_l2[k];
           const uint64_t* pl = planes + (size_t)k * npad + j0;
 #pragma unroll
@@ -629,10 +648,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         for (int i = 0, kend = 0; i < (ND > 0 ? 0 : a.n_perm); ++i) {
           const int k = a.perm_param[i];
           const bx_param_desc& p = params[k];
-          const uint64_t x = cval[k * kM + c];
+          const uint64_t x = cv[k * kM + c];
           const bool kd = p.metric == BX_KENDALL;
-          const uint64_t xl = kd ? cmask[2 * (kend * kM + c)] : 0;
-          const uint64_t xh = kd ? cmask[2 * (kend * kM + c) + 1] : 0;
+          const uint64_t xl = kd ? cmk[2 * (kend * kM + c)] : 0;
+          const uint64_t xh = kd ? cmk[2 * (kend * kM + c) + 1] : 0;
           const double* tab = a.gp.disc_tab + a.gp.disc_off[k];
           const uint64_t* pl = planes + (size_t)k * npad + j0;
           const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
@@ -682,7 +701,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mb_arrive(cand_full);  // one arrival per producer warp
+      if (lane == 0) {
+        mb_arrive(cand_full);        // one arrival per producer warp
+        mb_arrive(&cval_free[cb]);   // the decoders may refill this parity's buffers
+      }
       if (pt == 0) TC_TRACE(0, 6, t);
     }
   }
