@@ -305,6 +305,9 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
 // QuickScorer forest fused with the acquisition summary (the work of summary_kernel): runs after the
 // posterior kernel, reads its EI, applies value = -inf if p < eps_f else EI * p (acquisition.py:
 // 77-79) and keeps per-warp partials (stable top-k, both trackers) merged into one per block.
+// NC > 0: exactly NC code slots, the candidate's mask-row addresses held in registers and two slots'
+// loads issued back to back; NC == 0: any slot count (offsets through shared memory)
+template <int NC>
 __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, QsForestDev f, SummaryArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
@@ -338,20 +341,49 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
     double value = -INFINITY, prob = -INFINITY;
     if (valid) {
       const uint32_t* row = a.rows + (size_t)i * words;
-      for (int c = 0; c < f.n_codes; ++c)
-        sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+      uint32_t colr[NC > 0 ? NC : 1];
+      if constexpr (NC > 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          colr[c] = mask_s + 8u * (uint32_t)((f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+      } else {
+        for (int c = 0; c < f.n_codes; ++c)
+          sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+      }
       double sum = 0.0;
       for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {
         uint64_t m[kQsGroup];
 #pragma unroll
         for (int j = 0; j < kQsGroup; ++j) m[j] = ~0ull;
-        for (int c = 0; c < f.n_codes; ++c) {
-          const uint32_t col = mask_s + (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + g0) * 8u;
+        if constexpr (NC > 0) {
 #pragma unroll
-          for (int j = 0; j < kQsGroup / 2; ++j) {
-            const ulonglong2 w = lds_u64x2(col + 16u * j);
-            m[2 * j] &= w.x;
-            m[2 * j + 1] &= w.y;
+          for (int c = 0; c < NC; c += 2) {
+            ulonglong2 w0[kQsGroup / 2], w1[kQsGroup / 2];
+#pragma unroll
+            for (int j = 0; j < kQsGroup / 2; ++j) w0[j] = lds_u64x2(colr[c] + 8u * g0 + 16u * j);
+            if (c + 1 < NC) {
+#pragma unroll
+              for (int j = 0; j < kQsGroup / 2; ++j) w1[j] = lds_u64x2(colr[c + 1] + 8u * g0 + 16u * j);
+            }
+#pragma unroll
+            for (int j = 0; j < kQsGroup / 2; ++j) {
+              m[2 * j] &= w0[j].x;
+              m[2 * j + 1] &= w0[j].y;
+              if (c + 1 < NC) {
+                m[2 * j] &= w1[j].x;
+                m[2 * j + 1] &= w1[j].y;
+              }
+            }
+          }
+        } else {
+          for (int c = 0; c < f.n_codes; ++c) {
+            const uint32_t col = mask_s + (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + g0) * 8u;
+#pragma unroll
+            for (int j = 0; j < kQsGroup / 2; ++j) {
+              const ulonglong2 w = lds_u64x2(col + 16u * j);
+              m[2 * j] &= w.x;
+              m[2 * j + 1] &= w.y;
+            }
           }
         }
 #pragma unroll
@@ -437,13 +469,22 @@ bool qs_summary_available(const ForestDev& f) {
 cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
                               cudaStream_t s, int* n_partials) {
   const size_t bytes = qs_summary_smem(f.qs);
-  cudaError_t e = set_smem(rf_qs_summary_kernel, (int)bytes);
+  auto kern = rf_qs_summary_kernel<0>;
+  switch (f.qs.n_codes) {
+#define BX_NC(c) \
+    case c: kern = rf_qs_summary_kernel<c>; break;
+    BX_NC(1) BX_NC(2) BX_NC(3) BX_NC(4) BX_NC(5) BX_NC(6) BX_NC(7) BX_NC(8)
+    BX_NC(9) BX_NC(10) BX_NC(11) BX_NC(12) BX_NC(13) BX_NC(14) BX_NC(15) BX_NC(16)
+#undef BX_NC
+    default: break;
+  }
+  cudaError_t e = set_smem(kern, (int)bytes);
   if (e != cudaSuccess) return e;
   int64_t blocks = (a.q + kQsThreads - 1) / kQsThreads;
   if (blocks > sm_count) blocks = sm_count;
   if (blocks < 1) blocks = 1;
   *n_partials = (int)blocks;
-  rf_qs_summary_kernel<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, a);
+  kern<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, a);
   return cudaGetLastError();
 }
 
