@@ -41,14 +41,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         obj = PKG / "csrc" / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        cmds.append([nvcc(), *ARCH, *FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)])
+        objs.append(str(obj))
+    # one nvcc per translation unit, in parallel (gp_tc.cu and forest.cu dominate)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        list(pool.map(run, cmds))
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-cudart", "static"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
