@@ -47,7 +47,6 @@ constexpr int kStages = 8;       // matrix block ring
 constexpr int kMaxChunks = 16;   // n <= 255
 constexpr int kMaxSlices = 8;
 constexpr int kProdWarps = 16;   // K* producers: 4 per TMEM lane quarter
-constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // 8 columns of a slice per producer thread
 constexpr int kThreads = (8 + kProdWarps) * 32;
 constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
@@ -594,7 +593,6 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       mb_wait(&cval_full[cb], (uint32_t)((t >> 1) & 1));
       const uint64_t* cv = cval + (size_t)cb * n_params * kM;
       const uint64_t* cmk = cmask + (size_t)cb * a.n_kendall * kM * 2;
-      const int64_t gi = tile * kM + c;
       if (pt == 0) TC_TRACE(0, 2, t);
       double xr[ND > 0 ? ND : 1];
       if constexpr (ND > 0) {
