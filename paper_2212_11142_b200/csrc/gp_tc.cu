@@ -587,7 +587,6 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     const MaternConst mc{sigma * ta.kscale, sigma * kSqrt5 * ta.kscale, sigma * (5.0 / 3.0) * ta.kscale};
     const double kscale = ta.kscale;
     for (int t = 0; t < my_tiles; ++t) {
-      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       if (pt == 0) TC_TRACE(0, 1, t);
       const int cb = t & 1;
       mb_wait(&cval_full[cb], (uint32_t)((t >> 1) & 1));
