@@ -98,6 +98,13 @@ struct bx_handle {
   bool no_qs_forest = false;        // BX_FOREST_WALK=1: node walks instead of QuickScorer tables
   bool rf_after_gp = false;         // last score_impl ran the forest + summary kernel after the posterior
   int tc_debug = 0;                 // BX_TC_DEBUG (timing experiments)
+  // streaming host pools (bx_score_host on the tensor-core path): the pool in device memory, one
+  // ready flag per copied chunk, pinned ones to write the flags with the copy engine
+  DevBuf d_pool, d_ready;
+  uint32_t* h_ones = nullptr;
+  int64_t h_ones_len = 0;
+  const uint32_t* stream_ready = nullptr;  // set while a streaming posterior launch is enqueued
+  int stream_shift = 0;
   bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
@@ -262,6 +269,8 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.n_slices = h->tc_nsl;
     t.n_chunks = h->tc_nch;
     t.kscale = h->tc_kscale;
+    t.ready = h->stream_ready;
+    t.ready_shift = h->stream_shift;
     t.n_coord = (int32_t)h->coord_host.size();
     std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
     t.debug = h->tc_debug;
@@ -367,6 +376,9 @@ void bx_destroy(bx_handle* h) {
   for (int i = 0; i < 5; ++i)
     if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
   h->d_panels.release();
+  h->d_pool.release();
+  h->d_ready.release();
+  if (h->h_ones) cudaFreeHost(h->h_ones);
   h->d_mdig.release();
   h->d_rowscale.release();
   h->d_ei.release();
@@ -1001,7 +1013,7 @@ static SummaryArgs last_summary_args(bx_handle* h, const uint32_t* rows, int64_t
 static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
                       double f_model, double eps_f, int32_t k, int32_t flags, double* values,
                       double* probs_out, Partial* partials, int* n_partials, cudaStream_t s,
-                      bool timing, bool track_prob = false) {
+                      bool timing, bool track_prob = false, cudaEvent_t rows_ready = nullptr) {
   ScoreArgs a{};
   a.space = space_dev(h);
   a.gp = gp_dev(h);
@@ -1042,6 +1054,8 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     const bool rf_summ = forest && !fuse_rf && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
                          h->use_tc && qs_summary_available(h->forest);
     h->rf_after_gp = rf_summ;
+    // a stand-alone forest kernel before the posterior reads the rows: a streaming pool must be in
+    if (rows_ready && forest && !fuse_rf && !rf_summ) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
     if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
     if (forest && !fuse_rf && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
@@ -1060,6 +1074,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
+    if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));  // streaming pool fully copied
     if (rf_summ) {
       if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
       BX_CUDA(h, launch_rf_summary(a.space, h->forest, m, h->sm_count, s, n_partials));
@@ -1152,6 +1167,57 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->row_words;
+  if (h->use_tc && !getenv("BX_HOST_CHUNKED")) {
+    // Streaming: the whole pool is copied in 2^16-row chunks on the copy stream, each followed by a
+    // 4-byte ready flag written by the copy engine; one posterior launch consumes tiles as their
+    // chunk lands (the row prefetcher waits on the flag), so only the first chunk's copy is
+    // exposed and there is no per-chunk launch cost.  The forest + summary kernel runs after the
+    // last copy.
+    const int shift = 16;
+    const int64_t n_chunks = (q + (1 << shift) - 1) >> shift;
+    BX_CUDA(h, h->d_pool.ensure((size_t)q * W * 4));
+    BX_CUDA(h, h->d_ready.ensure((size_t)n_chunks * 4));
+    if (h->h_ones_len < n_chunks) {
+      if (h->h_ones) cudaFreeHost(h->h_ones);
+      h->h_ones = nullptr;
+      BX_CUDA(h, cudaMallocHost(&h->h_ones, (size_t)n_chunks * 4));
+      for (int64_t i = 0; i < n_chunks; ++i) h->h_ones[i] = 1u;
+      h->h_ones_len = n_chunks;
+    }
+    BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
+    BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
+    uint32_t* pool = h->d_pool.as<uint32_t>();
+    uint32_t* ready = h->d_ready.as<uint32_t>();
+    BX_CUDA(h, cudaMemsetAsync(ready, 0, (size_t)n_chunks * 4, s));
+    BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
+    BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[0], 0));
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      const int64_t off = c << shift, len = std::min<int64_t>((int64_t)1 << shift, q - off);
+      BX_CUDA(h, cudaMemcpyAsync(pool + (size_t)off * W, host_rows + (size_t)off * W, (size_t)len * W * 4,
+                                 cudaMemcpyHostToDevice, h->copy_stream));
+      BX_CUDA(h, cudaMemcpyAsync(ready + c, h->h_ones + c, 4, cudaMemcpyHostToDevice, h->copy_stream));
+    }
+    BX_CUDA(h, cudaEventRecord(h->ev_copy[0], h->copy_stream));
+    Partial* parts = h->d_partials.as<Partial>();
+    for (int pass = 0; pass < 2; ++pass) {
+      int np = 0;
+      h->stream_ready = pass == 0 ? ready : nullptr;
+      h->stream_shift = shift;
+      r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_NO_SUMMARY, nullptr,
+                     nullptr, parts, &np, s, false, pass == 1, pass == 0 ? h->ev_copy[0] : nullptr);
+      h->stream_ready = nullptr;
+      if (r) return r;
+      BX_CUDA(h, launch_summary_merge(parts, np, space_dev(h), k, nullptr, 0,
+                                      h->d_summary.as<bx_score_summary>(), s));
+      BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary), cudaMemcpyDeviceToHost, s));
+      BX_CUDA(h, cudaStreamSynchronize(s));
+      if (summary->n_finite != 0) break;
+    }
+    for (int i = 0; i < summary->n_top; ++i)
+      std::memcpy(summary->top[i].row, host_rows + (size_t)(summary->top[i].index - index_base) * W,
+                  (size_t)W * 4);
+    return BX_OK;
+  }
   // chunks of 2^17, 2^18, then 2^19 rows through a 2-buffer ring: the first copy, which nothing
   // overlaps, stays short, and later chunks are large enough that per-launch costs vanish (measured
   // on B200 over PCIe at 26 GB/s; BX_HOST_CHUNK / _RAMP / _BUFS override for tuning)
@@ -1177,6 +1243,14 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
                          np_max * n_chunks * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
   const bool running = !fits_once && np_max + 1 <= 1024 &&
                        (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
+  // BX_HOST_TRACE=1: per-chunk copy / compute timeline on stderr (pipeline tuning aid)
+  const bool trace = getenv("BX_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  if (trace) {
+    tev.resize(4 * n_chunks + 1);
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[4 * n_chunks], s);
+  }
   // pass 1 without the probability tracker; pass 2 (with it) only if every value is -inf
   for (int pass = 0; pass < 2; ++pass) {
   int total = 0;
@@ -1187,10 +1261,13 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     const int64_t len = (q - off) < chunk_len(c) ? (q - off) : chunk_len(c);
     // the copy into buffer b waits until the kernels that last read buffer b are done
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
+    if (trace && pass == 0) cudaEventRecord(tev[4 * c], h->copy_stream);
     BX_CUDA(h, cudaMemcpyAsync(h->d_host_rows[b].p, host_rows + (size_t)off * W, (size_t)len * W * 4,
                                cudaMemcpyHostToDevice, h->copy_stream));
     BX_CUDA(h, cudaEventRecord(h->ev_copy[b], h->copy_stream));
+    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 1], h->copy_stream);
     BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
+    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 2], s);
     int np = 0;
     // running merge: the chunk's partials land at base + 1 and are folded into base[0]
     Partial* dst = running ? base + 1 : base + total;
@@ -1203,6 +1280,7 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
                         : launch_partial_merge(base, np + 1, space_dev(h), k, base, s));
     total = running ? 1 : total + np;
     BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
+    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 3], s);
   }
   BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
                                   h->d_summary.as<bx_score_summary>(), s));
@@ -1210,6 +1288,15 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
                              cudaMemcpyDeviceToHost, s));
   BX_CUDA(h, cudaStreamSynchronize(s));
   if (summary->n_finite != 0 || !fused_path(h)) break;
+  }
+  if (trace) {
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      float t[4];
+      for (int e = 0; e < 4; ++e) cudaEventElapsedTime(&t[e], tev[4 * n_chunks], tev[4 * c + e]);
+      fprintf(stderr, "chunk %lld len %lld: copy %.3f-%.3f ms, compute %.3f-%.3f ms\n", (long long)c,
+              (long long)chunk_len(c), t[0], t[1], t[2], t[3]);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
   }
   // the pool is host-resident: the top-k rows come straight from the caller's buffer
   for (int i = 0; i < summary->n_top; ++i)

@@ -387,6 +387,10 @@ struct TcArgs {
   int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
                               // 4 epilogue TMEM reads without the arithmetic
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
+  // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
+  // is in device memory (written by the copy stream after the chunk), null = all rows present
+  const uint32_t* ready;
+  int32_t ready_shift;
 };
 
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).

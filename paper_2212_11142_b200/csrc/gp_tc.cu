@@ -399,6 +399,18 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
         const int buf = t & 1;
         if (t >= 2) mb_wait(&rows_empty[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        if (ta.ready) {  // streaming pool: wait until the copy stream has landed this tile's chunk
+          const int64_t last = min(a.q, (tile + 1) * kM) - 1;
+          const uint32_t* flag = ta.ready + (last >> ta.ready_shift);
+          uint32_t ok = 0;
+          for (long long spins = 0;; ++spins) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ok) : "l"(flag) : "memory");
+            if (ok) break;
+            if (spins > (1ll << 26)) asm volatile("trap;");  // ~20 s without the chunk: fail loudly
+            __nanosleep(256);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // make the data visible to TMA
+        }
         const int sw = staged_words(tile);
         if (sw > 0) {
           mb_expect(&rows_full[buf], (uint32_t)sw * 4);

@@ -157,3 +157,40 @@ def test_mixed_space_large_n_against_oracle(n):
     np.testing.assert_allclose(mean[idx], m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
     np.testing.assert_allclose(var[idx], v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
     sc.close()
+
+
+@pytest.mark.parametrize("case,q,eps", [("C3", 3 * 65536 + 777, None), ("C3", 70001, 1.01),
+                                        ("C2", 200003, None), ("mixed_fit", 65536, None)])
+def test_streaming_host_pool_matches_device_pool(case, q, eps, monkeypatch):
+    """bx_score_host streams the pool (chunked copies + ready flags consumed by one posterior
+    launch); its summary equals bx_score's on the same rows — ragged sizes, a forest-less case and
+    the all -inf fallback (eps_f > 1: probability tracker) included — and equals the chunked
+    pipeline (BX_HOST_CHUNKED=1)."""
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    gp, feas = model(meta, arr, space)
+    f = gp.objective_to_model(meta["f_best"])
+    eps_f = meta["eps_f"] if eps is None else eps
+    out = []
+    for chunked in (False, True):
+        if chunked:
+            monkeypatch.setenv("BX_HOST_CHUNKED", "1")
+        sc = Scorer()
+        sc.set_gp(gp)
+        if feas is not None:
+            sc.set_forest(feas)
+        rows_h = scenarios.sample_rows_uniform(sc.layout, q, np.random.default_rng(q))
+        pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
+        a, _, _ = sc.score(sc.to_device(rows_h), f, eps_f, k=10)
+        b = sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10)
+        for x, y in ((a, b),):
+            assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
+            assert [c.index for c in x.top] == [c.index for c in y.top]
+            assert [c.value for c in x.top] == [c.value for c in y.top]
+            idx = lambda c: None if c is None else (c.index, tuple(c.row))
+            assert idx(x.best) == idx(y.best) and idx(x.best_prob) == idx(y.best_prob)
+        out.append(b)
+        sc.close()
+    assert [c.index for c in out[0].top] == [c.index for c in out[1].top]
+    if eps is not None:
+        assert out[0].n_finite == 0 and out[0].best_prob is not None
