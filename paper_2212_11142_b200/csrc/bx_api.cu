@@ -105,6 +105,8 @@ struct bx_handle {
   int64_t h_ones_len = 0;
   const uint32_t* stream_ready = nullptr;  // set while a streaming posterior launch is enqueued
   int stream_shift = 0;
+  const SummaryArgs* tc_summ = nullptr;    // set while a full-step posterior launch is enqueued
+  bool tc_no_full = true;                  // BX_TC_FULL=1: forest + summary inside the posterior kernel
   bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
@@ -271,6 +273,10 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.kscale = h->tc_kscale;
     t.ready = h->stream_ready;
     t.ready_shift = h->stream_shift;
+    if (h->tc_summ) {
+      t.summ = *h->tc_summ;
+      t.summ_on = 1;
+    }
     t.n_coord = (int32_t)h->coord_host.size();
     std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
     t.debug = h->tc_debug;
@@ -334,6 +340,11 @@ bx_handle* bx_create(int device) {
   // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
   // drains) is exact but measured slower than the stand-alone QuickScorer kernel run after it:
   // opt-in with BX_TC_FOREST_FUSED=1.
+  // The full step inside the tensor-core kernel (QuickScorer on the decoder warps, summaries in the
+  // epilogue) is exact but measured ~4 % slower than posterior + forest/summary kernels back to
+  // back: the forest's shared-memory work competes with the producers for issue slots.  Opt-in.
+  const char* tfull = getenv("BX_TC_FULL");
+  h->tc_no_full = !(tfull && tfull[0] == '1');
   const char* tff = getenv("BX_TC_FOREST_FUSED");
   h->tc_separate_forest = !(tff && tff[0] == '1');
   const char* dm = getenv("BX_GP_DMMA");
@@ -1049,6 +1060,34 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // The stand-alone forest kernel and the GP kernel each fill every SM's shared memory, so
     // they cannot co-reside: run them back to back on the caller's stream (which also makes the
     // per-kernel CUDA-event timing exact).
+    // The whole step in the tensor-core kernel: decoder warps evaluate the QuickScorer forest and
+    // the epilogue keeps the summaries (no forest / summary kernels, no EI round trip through HBM).
+    const bool tc_full =
+        h->use_tc && !h->tc_no_full && partials != nullptr && !(flags & BX_SCORE_RF_PAIRWISE) && !fuse_rf &&
+        (forest ? qf.enabled && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true) <=
+                                    227 * 1024
+                : !h->has_forest &&
+                      tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, nullptr, true) <= 227 * 1024);
+    if (tc_full) {
+      h->rf_after_gp = false;
+      if (timing) {
+        BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+        BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+        BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
+      }
+      FusedArgs f = fused_args(h, rows, q, f_model);
+      if (forest) f.qs = qf;
+      SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
+      m.track_prob = track_prob ? 1 : 0;
+      h->tc_summ = &m;
+      const cudaError_t e = launch_posterior(h, f, s);
+      h->tc_summ = nullptr;
+      BX_CUDA(h, e);
+      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
+      const int64_t tiles = (q + 127) / 128;
+      *n_partials = (int)(tiles < h->sm_count ? tiles : h->sm_count);
+      return BX_OK;
+    }
     // QuickScorer forest + summary in one kernel after the posterior (it reads the EI): used
     // whenever a summary is wanted and the tables fit.
     const bool rf_summ = forest && !fuse_rf && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
@@ -1130,10 +1169,10 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
   if (want && summary->n_finite == 0 && fused_path(h)) {
     // every value is -inf: only now is the probability tracker needed (acquisition.py:179-184)
-    SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs, partials);
-    m.track_prob = 1;
-    if (h->rf_after_gp) BX_CUDA(h, launch_rf_summary(space_dev(h), h->forest, m, h->sm_count, s, &np));
-    else BX_CUDA(h, launch_summary(m, h->sm_count, s, &np));
+    // rerun the step with the tracker on (it is the only rare path, so no state is kept for it)
+    r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_TIMING, values, probs, partials,
+                   &np, s, false, true);
+    if (r) return r;
     BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),

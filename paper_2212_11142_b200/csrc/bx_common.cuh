@@ -374,25 +374,6 @@ struct FusedArgs {
   double* probs_out;
 };
 
-// Tensor-core posterior (gp_tc.cu): FusedArgs plus the digit-sliced [L^-1; alpha^T].
-struct TcArgs {
-  FusedArgs f;
-  const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 16 rows x 32 columns
-  const double* rowscale;     // [32 * n_chunks] 2^(e_i - 56) * sc (0 beyond row n)
-  int32_t n_slices;           // ceil(n / 32) column slices of K*
-  int32_t n_chunks;           // floor(n / 16) + 1 row chunks of [L^-1; alpha^T]
-  double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
-  int32_t n_coord;            // coord_lut entries
-  double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
-  int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
-                              // 4 epilogue TMEM reads without the arithmetic
-  long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
-  // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
-  // is in device memory (written by the copy stream after the chunk), null = all rows present
-  const uint32_t* ready;
-  int32_t ready_shift;
-};
-
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).
 struct SummaryArgs {
   SpaceDev space;
@@ -413,6 +394,31 @@ struct SummaryArgs {
   Partial* partials;
 };
 
+// Tensor-core posterior (gp_tc.cu): FusedArgs plus the digit-sliced [L^-1; alpha^T].
+struct TcArgs {
+  FusedArgs f;
+  const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 16 rows x 32 columns
+  const double* rowscale;     // [32 * n_chunks] 2^(e_i - 56) * sc (0 beyond row n)
+  int32_t n_slices;           // ceil(n / 32) column slices of K*
+  int32_t n_chunks;           // floor(n / 16) + 1 row chunks of [L^-1; alpha^T]
+  double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
+  int32_t n_coord;            // coord_lut entries
+  double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
+  int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
+                              // 4 epilogue TMEM reads without the arithmetic
+  long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
+  // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
+  // is in device memory (written by the copy stream after the chunk), null = all rows present
+  const uint32_t* ready;
+  int32_t ready_shift;
+  // summ_on: the whole acquisition step in this kernel — the decoder warps evaluate the QuickScorer
+  // forest (f.qs), the epilogue forms value = -inf if p < eps_f else EI * p and keeps per-warp
+  // partials (stable top-k, trackers) merged into summ.partials[blockIdx.x]
+  SummaryArgs summ;
+  int32_t summ_on;
+};
+
+
 int fused_max_rows();
 size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8);
 size_t fused_smem_bytes_forest(int n, int n_params, int n_kendall, int rows8,
@@ -421,7 +427,8 @@ size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs = nullptr);
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs = nullptr,
+                     bool summ = false);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, cudaStream_t s);

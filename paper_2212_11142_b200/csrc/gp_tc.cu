@@ -33,6 +33,7 @@
 // overlaps the MMAs of the next, then 40 columns (5 digits x 32 bytes) per column slice.
 #include "bx_common.cuh"
 #include "matern.cuh"
+#include "summary.cuh"
 
 namespace bx {
 
@@ -158,13 +159,13 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, mat, bars,
-      total;
+  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
+      mat, bars, total;
 };
 
 // qs: the QuickScorer forest evaluated by warps 2-3 (qs->enabled == 0 -> no forest tables)
 __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words,
-                                              const QsForestDev* qs = nullptr) {
+                                              const QsForestDev* qs = nullptr, bool summ = false) {
   const bool rf = qs && qs->enabled;
   const int nsl = (n + 31) / 32, npad = 32 * nsl;
   TcLayout L;
@@ -196,11 +197,17 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += rf ? ((qs->n_trees * 64 * 2 + 15) & ~15) : 0;
   L.qs_off = off;    // [2][n_codes][128] table offsets (soff + code) of the tiles' candidates
   off += rf ? 2 * qs->n_codes * kM * 4 : 0;
+  off = (off + 15) & ~15;
+  L.prob = off;      // [2][128] forest probabilities of the tiles' candidates
+  off += rf ? 2 * kM * 8 : 0;
+  off = (off + 15) & ~15;
+  L.parts = off;     // [4] epilogue-warp partial summaries (summ_on)
+  off += summ ? 4 * (int)sizeof(Partial) : 0;
   off = (off + 1023) & ~1023;
   L.mat = off;     // [stage][digit][16 x 32 B]
   off += kStages * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
-  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 2 + 4 + 1) * 8;
+  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 4 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
   const QsForestDev& qf = a.qs;
   const bool rf = qf.enabled != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -235,10 +242,13 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* rows_full = acc_empty + 2;
   uint64_t* rows_empty = rows_full + 2;
-  uint64_t* qs_free = rows_empty + 2;  // the epilogue is done with a tile's forest offsets
-  uint64_t* cval_full = qs_free + 2;   // the decoders filled a tile's candidate values
+  uint64_t* cval_full = rows_empty + 2;  // the decoders filled a tile's candidate values
   uint64_t* cval_free = cval_full + 2; // every producer is done with them
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cval_free + 2);
+  uint64_t* prob_full = cval_free + 2; // the decoders evaluated a tile's forest
+  uint64_t* prob_free = prob_full + 2; // the epilogue consumed it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(prob_free + 2);
+  double* s_prob = reinterpret_cast<double*>(smem + L.prob);
+  Partial* s_parts = reinterpret_cast<Partial*>(smem + L.parts);
   uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
   // rows are staged by 16-byte bulk copies when the pool pointer allows it
   const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
@@ -290,9 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       mb_init(&acc_empty[i], 4);
       mb_init(&rows_full[i], 1);
       mb_init(&rows_empty[i], 1);
-      mb_init(&qs_free[i], 4);
       mb_init(&cval_full[i], 1);
       mb_init(&cval_free[i], kProdWarps);
+      mb_init(&prob_full[i], 1);
+      mb_init(&prob_free[i], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -355,8 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         }
         cv[idx] = v;
       }
-      if (rf) {  // forest table offsets of the tile, read by the epilogue (its thread = candidate)
-        if (t >= 2) mb_wait(&qs_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+      if (rf) {  // forest table offsets of the tile (read below by these warps)
         int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
         for (int idx = dt; idx < qf.n_codes * kM; idx += 64) {
           const int sl = idx / kM, cc = idx % kM;
@@ -391,6 +401,56 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       }
       asm volatile("bar.sync 3, 64;" ::: "memory");
       if (dt == 0) mb_arrive(&cval_full[buf]);
+      if (rf) {
+        // QuickScorer forest for the tile's candidates (two per thread), leaves summed strictly in
+        // tree order (the q >= 2 numpy order, feasibility.py:89); the epilogue reads s_prob
+        if (t >= 2) mb_wait(&prob_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        const int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
+        const uint32_t mask_s = su32(qs_mask);
+        constexpr int G = 8;
+        // both candidates of the thread in flight together: 16 independent mask chains per slot
+        const int c0 = dt, c1 = dt + 64;
+        double s0 = 0.0, s1 = 0.0;
+        for (int g0 = 0; g0 < qf.n_trees; g0 += G) {
+          uint64_t m0[G], m1[G];
+#pragma unroll
+          for (int j = 0; j < G; ++j) m0[j] = m1[j] = ~0ull;
+          for (int sl = 0; sl < qf.n_codes; ++sl) {
+            const uint32_t col0 = mask_s + (uint32_t)(qo[sl * kM + c0] + g0) * 8u;
+            const uint32_t col1 = mask_s + (uint32_t)(qo[sl * kM + c1] + g0) * 8u;
+            ulonglong2 w0[G / 2], w1[G / 2];
+#pragma unroll
+            for (int j = 0; j < G / 2; ++j) {
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w0[j].x), "=l"(w0[j].y) : "r"(col0 + 16u * j));
+              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w1[j].x), "=l"(w1[j].y) : "r"(col1 + 16u * j));
+            }
+#pragma unroll
+            for (int j = 0; j < G / 2; ++j) {
+              m0[2 * j] &= w0[j].x;
+              m0[2 * j + 1] &= w0[j].y;
+              m1[2 * j] &= w1[j].x;
+              m1[2 * j + 1] &= w1[j].y;
+            }
+          }
+          double v0[G], v1[G];
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const int tr = g0 + j < qf.n_trees ? g0 + j : 0;
+            v0[j] = qs_uval[qs_vid[tr * 64 + __ffsll((long long)m0[j]) - 1]];
+            v1[j] = qs_uval[qs_vid[tr * 64 + __ffsll((long long)m1[j]) - 1]];
+          }
+#pragma unroll
+          for (int j = 0; j < G; ++j)
+            if (g0 + j < qf.n_trees) {
+              s0 = (g0 + j == 0) ? v0[j] : __dadd_rn(s0, v0[j]);
+              s1 = (g0 + j == 0) ? v1[j] : __dadd_rn(s1, v1[j]);
+            }
+        }
+        s_prob[buf * kM + c0] = __ddiv_rn(s0, (double)qf.n_trees);  // np.mean: sum / count
+        s_prob[buf * kM + c1] = __ddiv_rn(s1, (double)qf.n_trees);
+        asm volatile("bar.sync 3, 64;" ::: "memory");
+        if (dt == 0) mb_arrive(&prob_full[buf]);
+      }
     }
   } else if (warp == 1 && lane == 1) {
     // ---- row prefetcher: the encoded rows of each tile, one bulk copy ahead ----------------
@@ -493,39 +553,13 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     const double sigma = a.gp.outputscale;
     uint32_t ph_f = 0;
     int chunk_no = 0;
-    // forest (QuickScorer tables): groups of G trees evaluated while the next chunk's MMAs run;
-    // leaves summed strictly in tree order (the q >= 2 numpy order, feasibility.py:89)
-    constexpr int G = 8;
-    const int n_groups = rf ? (qf.n_trees + G - 1) / G : 0;
-    const uint32_t qs_mask_s = su32(qs_mask);
+    const SummaryArgs& sa = ta.summ;
+    Partial* summ = s_parts + (warp - 4);
+    if (ta.summ_on && lane == 0) partial_init(summ);
+    __syncwarp();
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       double ss = 0.0, mean_s = 0.0;
-      const int32_t* qo = qs_off + (size_t)(t & 1) * (rf ? qf.n_codes : 0) * kM + r;
-      double fsum = 0.0;
-      int g_next = 0;
-      auto forest_group = [&](int g) {
-        const int g0 = g * G;
-        uint64_t m[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) m[j] = ~0ull;
-        for (int sl = 0; sl < qf.n_codes; ++sl) {
-          const uint32_t col = qs_mask_s + (uint32_t)(qo[sl * kM] + g0) * 8u;
-#pragma unroll
-          for (int j = 0; j < G / 2; ++j) {
-            ulonglong2 w;
-            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w.x), "=l"(w.y) : "r"(col + 16u * j));
-            m[2 * j] &= w.x;
-            m[2 * j + 1] &= w.y;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < G; ++j)
-          if (g0 + j < qf.n_trees) {
-            const double v = qs_uval[qs_vid[(g0 + j) * 64 + __ffsll((long long)m[j]) - 1]];
-            fsum = (g0 + j == 0) ? v : __dadd_rn(fsum, v);
-          }
-      };
       for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);
@@ -558,16 +592,17 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         __syncwarp();
         if (lane == 0) mb_arrive(&acc_empty[buf]);
         if (lane == 0 && warp == 4) TC_TRACE(2, 2, c);
-        const int target = n_groups * (nch - c) / nch;
-        while (g_next < target) forest_group(g_next++);
       }
-      while (g_next < n_groups) forest_group(g_next++);
       const int64_t gi = tile * kM + r;
+      double prob = 1.0;
       if (rf) {
-        if (gi < a.q) a.probs_out[gi] = __ddiv_rn(fsum, (double)qf.n_trees);  // np.mean: sum / count
+        mb_wait(&prob_full[t & 1], (uint32_t)((t >> 1) & 1));
+        prob = s_prob[(t & 1) * kM + r];
         __syncwarp();
-        if (lane == 0) mb_arrive(&qs_free[t & 1]);
+        if (lane == 0) mb_arrive(&prob_free[t & 1]);
+        if (a.probs_out && gi < a.q) a.probs_out[gi] = prob;
       }
+      double ei_c = -INFINITY;
       if (gi < a.q) {
         const double var_s = fmax(sigma - ss, 0.0);                 // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * mean_s;      // :328
@@ -584,7 +619,71 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           }
           a.ei_out[gi] = fmax(ei, 0.0);
         }
+        if (ta.summ_on) {
+          const double sd = sqrt(fmax(var, 0.0));
+          const double delta = a.f_model - mean;
+          double ei = fmax(delta, 0.0);
+          if (sd > 0.0) {
+            const double z = delta / sd;
+            ei = delta * normcdf(z) + sd * (kInvSqrt2Pi * exp(-0.5 * z * z));
+          }
+          ei_c = fmax(ei, 0.0);
+        }
       }
+      if (ta.summ_on) {
+        // acquisition value and the warp's partial summary (the logic of summary_kernel)
+        const bool valid = gi < a.q;
+        double value = -INFINITY, pv = -INFINITY;
+        if (valid) {
+          pv = rf ? prob : 1.0;
+          value = rf ? ((prob < sa.eps_f) ? -INFINITY : ei_c * prob) : ei_c;
+          if (sa.values_out) sa.values_out[gi] = value;
+          if (sa.probs_out) sa.probs_out[gi] = pv;
+        }
+        const int words_s = sa.space.row_words;
+        const bool fin = valid && value != -INFINITY;
+        const bool top_open = sa.k > 0 && summ->n_top < sa.k;
+        const double kth = (sa.k > 0 && !top_open) ? summ->top[sa.k - 1].value : -INFINITY;
+        const bool prob_ok = sa.track_prob && pv >= summ->best_prob.prob;
+        const bool maybe = valid && ((fin && sa.k > 0 && (top_open || value >= kth)) ||
+                                     (fin && value >= summ->best.value) || prob_ok);
+        bool evaluated = false;
+        if (maybe && sa.evald.count > 0) evaluated = is_evaluated(sa.evald, a.rows + (size_t)gi * words_s, words_s);
+        const bool pass = maybe && ((fin && sa.k > 0 && (top_open || value >= kth)) ||
+                                    (!evaluated && ((fin && value >= summ->best.value) || prob_ok)));
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const unsigned fmask = __ballot_sync(0xffffffffu, fin);
+        unsigned pmask = __ballot_sync(0xffffffffu, pass);
+        const unsigned emask = __ballot_sync(0xffffffffu, evaluated);
+        if (lane == 0) {
+          summ->n_scored += __popc(vmask);
+          summ->n_finite += __popc(fmask);
+        }
+        const int64_t wbase = tile * kM + (warp - 4) * 32;
+        while (pmask) {
+          const int cl = __ffs(pmask) - 1;
+          pmask &= pmask - 1;
+          const double vc = __shfl_sync(0xffffffffu, value, cl);
+          const double pc = __shfl_sync(0xffffffffu, pv, cl);
+          if (lane == 0)
+            partial_add(summ, sa.k, params, sa.space.n_params, sa.space.rank_lut, words_s, vc, pc,
+                        sa.index_base + wbase + cl, (emask >> cl) & 1u, a.rows + (size_t)(wbase + cl) * words_s,
+                        sa.track_prob != 0);
+          __syncwarp();
+        }
+      }
+    }
+    if (ta.summ_on) {  // fold the four warp partials into the CTA's
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+      if (warp == 4 && lane == 0) {
+        for (int w = 1; w < 4; ++w)
+          partial_merge(&s_parts[0], &s_parts[w], sa.k, params, sa.space.n_params, sa.space.rank_lut,
+                        sa.space.row_words);
+      }
+      asm volatile("bar.sync 4, 128;" ::: "memory");
+      const int32_t* src = reinterpret_cast<const int32_t*>(&s_parts[0]);
+      int32_t* dst = reinterpret_cast<int32_t*>(sa.partials + blockIdx.x);
+      for (int i = r; i < (int)(sizeof(Partial) / 4); i += 128) dst[i] = src[i];
     }
   } else if (warp >= 8) {
     // ---- K* producers ------------------------------------------------------------------------
@@ -760,8 +859,8 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 }  // namespace
 
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs) {
-  return tc_layout(n, n_params, n_kendall, row_words, qs).total;
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs, bool summ) {
+  return tc_layout(n, n_params, n_kendall, row_words, qs, summ).total;
 }
 
 size_t tc_mdig_bytes(int n) {
@@ -782,7 +881,8 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 }
 
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
-  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs);
+  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
+                               a.summ_on != 0);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   // all-numeric spaces with up to 16 parameters get the unrolled distance loop
   const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;

@@ -159,14 +159,17 @@ def test_mixed_space_large_n_against_oracle(n):
     sc.close()
 
 
+@pytest.mark.parametrize("full", [False, True])
 @pytest.mark.parametrize("case,q,eps", [("C3", 3 * 65536 + 777, None), ("C3", 70001, 1.01),
                                         ("C2", 200003, None), ("mixed_fit", 65536, None)])
-def test_streaming_host_pool_matches_device_pool(case, q, eps, monkeypatch):
+def test_streaming_host_pool_matches_device_pool(case, q, eps, full, monkeypatch):
     """bx_score_host streams the pool (chunked copies + ready flags consumed by one posterior
     launch); its summary equals bx_score's on the same rows — ragged sizes, a forest-less case and
     the all -inf fallback (eps_f > 1: probability tracker) included — and equals the chunked
-    pipeline (BX_HOST_CHUNKED=1)."""
+    pipeline (BX_HOST_CHUNKED=1).  full: the whole step inside the tensor-core kernel (BX_TC_FULL=1)."""
     from paper_2212_11142_b200.device import Scorer
+    if full:
+        monkeypatch.setenv("BX_TC_FULL", "1")
     meta, arr, space = load(case)
     gp, feas = model(meta, arr, space)
     f = gp.objective_to_model(meta["f_best"])
@@ -194,3 +197,25 @@ def test_streaming_host_pool_matches_device_pool(case, q, eps, monkeypatch):
     assert [c.index for c in out[0].top] == [c.index for c in out[1].top]
     if eps is not None:
         assert out[0].n_finite == 0 and out[0].best_prob is not None
+
+
+def test_full_step_kernel_values_match_separate_kernels(c3, monkeypatch):
+    """BX_TC_FULL=1 (forest on the decoder warps, summaries in the epilogue) gives bit-identical
+    values, probabilities and summaries to the separate forest + summary kernels."""
+    from paper_2212_11142_b200.device import Scorer
+    sc0, meta, arr, space, gp, feas, rows_h = c3
+    f = gp.objective_to_model(meta["f_best"])
+    res = []
+    for full in (False, True):
+        if full:
+            monkeypatch.setenv("BX_TC_FULL", "1")
+        sc = Scorer()
+        sc.set_gp(gp)
+        sc.set_forest(feas)
+        s, v, p = sc.score(sc.to_device(rows_h[:300_001]), f, meta["eps_f"], k=10, want_values=True)
+        res.append((s, v.cpu().numpy(), p.cpu().numpy()))
+        sc.close()
+    (a, va, pa), (b, vb, pb) = res
+    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
+    assert [c.index for c in a.top] == [c.index for c in b.top]
+    assert (a.n_scored, a.n_finite, a.best.index) == (b.n_scored, b.n_finite, b.best.index)
