@@ -106,6 +106,9 @@ struct bx_handle {
   const uint32_t* stream_ready = nullptr;  // set while a streaming posterior launch is enqueued
   int stream_shift = 0;
   const SummaryArgs* tc_summ = nullptr;    // set while a full-step posterior launch is enqueued
+  bool tc_dot = false;                     // centred dot-product distances (bx_set_gp decides)
+  bool tc_no_dot = false;                  // BX_TC_NO_DOT=1: always the difference form
+  DevBuf d_mu;
   bool tc_no_full = true;                  // BX_TC_FULL=1: forest + summary inside the posterior kernel
   bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
@@ -277,6 +280,8 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
       t.summ = *h->tc_summ;
       t.summ_on = 1;
     }
+    t.dot = h->tc_dot ? 1 : 0;
+    t.mu = h->d_mu.as<double>();
     t.n_coord = (int32_t)h->coord_host.size();
     std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
     t.debug = h->tc_debug;
@@ -343,6 +348,8 @@ bx_handle* bx_create(int device) {
   // The full step inside the tensor-core kernel (QuickScorer on the decoder warps, summaries in the
   // epilogue) is exact but measured ~4 % slower than posterior + forest/summary kernels back to
   // back: the forest's shared-memory work competes with the producers for issue slots.  Opt-in.
+  const char* tnd = getenv("BX_TC_NO_DOT");
+  h->tc_no_dot = tnd && tnd[0] == '1';
   const char* tfull = getenv("BX_TC_FULL");
   h->tc_no_full = !(tfull && tfull[0] == '1');
   const char* tff = getenv("BX_TC_FOREST_FUSED");
@@ -389,6 +396,7 @@ void bx_destroy(bx_handle* h) {
   h->d_panels.release();
   h->d_pool.release();
   h->d_ready.release();
+  h->d_mu.release();
   if (h->h_ones) cudaFreeHost(h->h_ones);
   h->d_mdig.release();
   h->d_rowscale.release();
@@ -557,6 +565,43 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
     BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
                                  h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), s));
     h->use_tc = true;
+    // dot-product distances: all-numeric spaces whose coordinates, centred on the training mean and
+    // scaled by 1/l, stay small (|x'|^2 <= 64 for every domain point), so |x'|^2 + |y'|^2 - 2 x'.y'
+    // loses at most ~2^-46 of W (well under the 2^-40 fixed point of K*)
+    h->tc_dot = false;
+    bool numeric = true;
+    for (int k = 0; k < D && numeric; ++k)
+      numeric = h->params[k].kind != BX_CATEGORICAL && h->params[k].kind != BX_PERMUTATION;
+    if (numeric && !h->tc_no_dot) {
+      std::vector<double> mu(D, 0.0);
+      double bound = 0.0;
+      for (int k = 0; k < D; ++k) {
+        const bx_param_desc& p = h->params[k];
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) {
+          const uint32_t* row = train_rows + (size_t)j * h->row_words;
+          double x;
+          if (p.kind == BX_REAL) {
+            uint64_t bits = (uint64_t)row[p.word + 2] | ((uint64_t)row[p.word + 3] << 32);
+            std::memcpy(&x, &bits, 8);
+          } else {
+            x = h->coord_host[p.coord + row[p.word]];
+          }
+          acc += x * inv_l[k];
+        }
+        mu[k] = acc / n;
+        double lo = 1e300, hi = -1e300;  // domain extremes (finite domains / the real grid)
+        for (int i = 0; i < p.size; ++i) {
+          lo = std::min(lo, h->coord_host[p.coord + i] * inv_l[k]);
+          hi = std::max(hi, h->coord_host[p.coord + i] * inv_l[k]);
+        }
+        bound += std::max((lo - mu[k]) * (lo - mu[k]), (hi - mu[k]) * (hi - mu[k]));
+      }
+      if (bound <= 64.0) {
+        BX_CUDA(h, upload(h->d_mu, mu.data(), mu.size()));
+        h->tc_dot = true;
+      }
+    }
   }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
   h->outputscale = outputscale;

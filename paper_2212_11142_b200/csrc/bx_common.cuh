@@ -416,6 +416,11 @@ struct TcArgs {
   // partials (stable top-k, trackers) merged into summ.partials[blockIdx.x]
   SummaryArgs summ;
   int32_t summ_on;
+  // dot != 0 (all-numeric spaces whose centred coordinates are small, checked on the host):
+  // W = |x'|^2 + |y'|^2 - 2 x'.y' on coordinates centred by mu (scaled units), 12 FP64 operations
+  // per pair instead of 2 per dimension
+  const double* mu;           // [n_params]
+  int32_t dot;
 };
 
 

@@ -159,7 +159,7 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, rowscale, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
+  int par, planes, kmask, cval, cmask, exp2, rowscale, yy, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
       mat, bars, total;
 };
 
@@ -185,6 +185,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += 256 * 8;
   L.rowscale = off;  // [2][256]: row factors, then the same with the alpha / padding rows zeroed
   off += 2 * kMaxChunks * kN * 8;
+  L.yy = off;        // [npad] |y'_j|^2 of the centred training points (dot mode)
+  off += npad * 8;
   L.rows = off;    // [2][128 x row_words] encoded rows of the next tiles (bulk-copy staging)
   off += 2 * kM * words * 4;
   L.stab = off;    // coord_lut / lengthscale of the finite numeric domains (when it fits)
@@ -257,7 +259,21 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
   for (int i = tid; i < n_params * npad; i += blockDim.x) {
     const int k = i / npad, j = i % npad;
-    planes[i] = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
+    uint64_t v = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
+    if (ta.dot) v = (uint64_t)__double_as_longlong(j < n ? __longlong_as_double((long long)v) - ta.mu[k] : 0.0);
+    planes[i] = v;
+  }
+  double* s_yy = reinterpret_cast<double*>(smem + L.yy);
+  if (ta.dot) {
+    __syncthreads();
+    for (int j = tid; j < npad; j += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < n_params; ++k) {
+        const double y = __longlong_as_double((long long)planes[k * npad + j]);
+        acc = fma(y, y, acc);
+      }
+      s_yy[j] = acc;
+    }
   }
   for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
     const int kk = i / npad, j = i % npad;
@@ -361,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
               x = stab[p.coord + (int)word(p.word)];
             else
               x = a.space.coord_lut[p.coord + (int)word(p.word)] * a.gp.inv_l[k];
+            if (ta.dot) x -= ta.mu[k];
             v = (uint64_t)__double_as_longlong(x);
           }
         }
@@ -705,9 +722,13 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       const uint64_t* cmk = cmask + (size_t)cb * a.n_kendall * kM * 2;
       if (pt == 0) TC_TRACE(0, 2, t);
       double xr[ND > 0 ? ND : 1];
+      double xx = 0.0;
       if constexpr (ND > 0) {
 #pragma unroll
-        for (int k = 0; k < ND; ++k) xr[k] = __longlong_as_double((long long)cv[k * kM + c]);
+        for (int k = 0; k < ND; ++k) {
+          xr[k] = __longlong_as_double((long long)cv[k * kM + c]);
+          xx = fma(xr[k], xr[k], xx);
+        }
       }
       for (int ks = nsl - 1; ks >= 0; --ks) {
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
@@ -716,15 +737,35 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
         if constexpr (ND > 0) {
           const double2* pl0 = reinterpret_cast<const double2*>(planes + j0);
+          if (ta.dot) {  // W = |x'|^2 + |y'|^2 - 2 x'.y' (centred, small: no harmful cancellation)
 #pragma unroll
-          for (int k = 0; k < ND; ++k) {
-            const double2* pl = pl0 + (size_t)k * (npad / 2);
+            for (int k = 0; k < ND; ++k) {
+              const double2* pl = pl0 + (size_t)k * (npad / 2);
+#pragma unroll
+              for (int u = 0; u < kColsPerItem / 2; ++u) {
+                const double2 y = pl[u];
+                W[2 * u] = fma(xr[k], y.x, W[2 * u]);
+                W[2 * u + 1] = fma(xr[k], y.y, W[2 * u + 1]);
+              }
+            }
+            const double2* yy2 = reinterpret_cast<const double2*>(s_yy + j0);
 #pragma unroll
             for (int u = 0; u < kColsPerItem / 2; ++u) {
-              const double2 y = pl[u];
-              const double d0 = xr[k] - y.x, d1 = xr[k] - y.y;
-              W[2 * u] = fma(d0, d0, W[2 * u]);
-              W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
+              const double2 y = yy2[u];
+              W[2 * u] = fmax(fma(-2.0, W[2 * u], xx + y.x), 0.0);
+              W[2 * u + 1] = fmax(fma(-2.0, W[2 * u + 1], xx + y.y), 0.0);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+              const double2* pl = pl0 + (size_t)k * (npad / 2);
+#pragma unroll
+              for (int u = 0; u < kColsPerItem / 2; ++u) {
+                const double2 y = pl[u];
+                const double d0 = xr[k] - y.x, d1 = xr[k] - y.y;
+                W[2 * u] = fma(d0, d0, W[2 * u]);
+                W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
+              }
             }
           }
         }
@@ -886,6 +927,7 @@ cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   // all-numeric spaces with up to 16 parameters get the unrolled distance loop
   const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;
+  if (a.dot && !numeric) return cudaErrorInvalidValue;  // the host enables dot only for these
   const int nd = numeric ? a.f.n_num : 0;
   auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
   switch (nd) {

@@ -262,3 +262,28 @@ def test_forest_paths_bit_exact(case, monkeypatch):
     for name in ("qs", "fused"):
         for a, b in zip(out[name], out["walk"]):
             assert np.array_equal(a, b), name
+
+
+@pytest.mark.parametrize("case", ["C3", "C2", "C1"])
+def test_dot_product_distances_match_difference_form(case, monkeypatch):
+    """Centred dot-product distances (enabled by bx_set_gp for well-scaled all-numeric spaces, C3)
+    agree with the difference form to far inside the parity bar; spaces it does not apply to
+    (C1: small lengthscales, C2: categorical / permutation) are unaffected."""
+    from paper_2212_11142_b200 import scenarios
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    gp, _ = model(meta, arr, space)
+    res = []
+    for no_dot in (True, False):
+        if no_dot:
+            monkeypatch.setenv("BX_TC_NO_DOT", "1")
+        else:
+            monkeypatch.delenv("BX_TC_NO_DOT")
+        sc = Scorer()
+        sc.set_gp(gp)
+        rows = sc.to_device(scenarios.sample_rows_uniform(sc.layout, 200_000, np.random.default_rng(2)))
+        res.append([x.cpu().numpy() for x in sc.predict(rows)])
+        sc.close()
+    (m0, v0), (m1, v1) = res
+    close(m1, m0, rtol=1e-9)
+    close(v1, v0, rtol=1e-7)
