@@ -838,9 +838,9 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     if (ok) {
       if (uval.empty()) uval.push_back(0.0);
       // transpose to [slot value][tree] so a group of 8 trees is one 64-byte run per slot
-      // row stride == 4 words (mod 32): rows of different code values start on different banks
-      int tpad = (T + 7) / 8 * 8;
-      while (tpad % 16 != 2) ++tpad;
+      // odd row length (in 8-byte words): the <= 16 distinct code-value rows a half-warp reads with
+      // 8-byte loads fall in 16 distinct bank pairs (groups of 8 trees read t .. t+7)
+      int tpad = (T + 7) / 8 * 8 + 1;
       std::vector<uint64_t> mt((size_t)stride * tpad, ~0ull);
       for (int t = 0; t < T; ++t)
         for (int r = 0; r < stride; ++r) mt[(size_t)r * tpad + t] = mask[(size_t)t * stride + r];

@@ -124,7 +124,7 @@ struct QsForestDev {
   const int32_t* code_param; // [n_codes] (the coded forest's slots)
   const int32_t* code_sub;
   int32_t n_trees, n_codes, stride, n_uvals;
-  int32_t tpad;              // row length >= n_trees rounded up to 8, == 2 (mod 16) (bank spread)
+  int32_t tpad;              // row length: n_trees rounded up to 8, plus 1 (odd: bank spread)
   int32_t enabled;
 };
 

@@ -200,11 +200,14 @@ __global__ void __launch_bounds__(kRfThreads, 1) rf_coded_kernel(SpaceDev sp, Co
 constexpr int kQsThreads = 1024;
 constexpr int kQsGroup = 8;  // trees evaluated together (8 masks in registers)
 
-// explicit shared-space 16-byte load (the mask table is indexed through computed offsets, which
-// otherwise compile to generic loads)
+// explicit shared-space loads (the mask table is indexed through computed offsets, which otherwise
+// compile to generic loads)
 __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t saddr) {
+  // two 8-byte loads, not one 16-byte load: with an odd mask-row length the <= 16 distinct rows a
+  // half-warp touches fall in distinct banks, so each load is a single wavefront per half-warp
   ulonglong2 v;
-  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(saddr));
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v.x) : "r"(saddr));
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v.y) : "r"(saddr + 8u));
   return v;
 }
 

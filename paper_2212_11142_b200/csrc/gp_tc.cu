@@ -438,8 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             ulonglong2 w0[G / 2], w1[G / 2];
 #pragma unroll
             for (int j = 0; j < G / 2; ++j) {
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w0[j].x), "=l"(w0[j].y) : "r"(col0 + 16u * j));
-              asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w1[j].x), "=l"(w1[j].y) : "r"(col1 + 16u * j));
+              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w0[j].x) : "r"(col0 + 16u * j));
+              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w0[j].y) : "r"(col0 + 16u * j + 8u));
+              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w1[j].x) : "r"(col1 + 16u * j));
+              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w1[j].y) : "r"(col1 + 16u * j + 8u));
             }
 #pragma unroll
             for (int j = 0; j < G / 2; ++j) {
