@@ -129,25 +129,27 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
     }                                                                                      \
   } while (0)
 
-// sigma * matern52(sqrt(W)) * kscale truncated to a 40-bit integer (the producers' hot path), in 18
-// FP64 operations: d = sqrt(W) from rsqrt.approx + one Newton step on d; e^x (x = -sqrt5 d) as
-// 2^(k/256) (256-entry table, k clamped so the exponent stays normal; such K* truncate to 0) times a
-// degree-4 Taylor polynomial in |r| <= ln2/512 (truncation < 4e-17).
+// sigma * matern52(sqrt(W)) * kscale truncated to a 40-bit integer (the producers' hot path), in 16
+// FP64 operations: d = sqrt(W) from rsqrt.approx + one Newton step on d (the 1/2 folded into the
+// exponent of the approximation, an integer op); e^(-sqrt5 d) as 2^(k/256) (256-entry table, k
+// clamped so the exponent stays normal; such K* truncate to 0) times a degree-4 Taylor polynomial.
+// The range reduction runs in units of d (r = d + k ln2 / (256 sqrt5), |sqrt5 r| <= ln2/512,
+// truncation < 4e-17), so -sqrt5 is folded into the polynomial coefficients instead of a multiply.
 __device__ __forceinline__ unsigned long long kstar_fixed(double W, const MaternConst& m, const double* tab256) {
   const double w = W + 1e-300;                      // W = 0 -> d = 1e-150, K* = sigma
   const double y0 = rsqrt_approx(w);
+  const double y0h = __hiloint2double(__double2hiint(y0) - (1 << 20), __double2loint(y0));  // y0 / 2
   const double d0 = w * y0;
-  const double e0 = fma(-d0, y0, 1.0);               // 1 - w y0^2
-  const double d = fma(0.5 * d0, e0, d0);            // d0 (1 + e0 / 2)
-  const double x = -kSqrt5 * d;
-  const double t = fma(x, 369.3299304675746, 6755399441055744.0);  // x * 256 / ln2 + 1.5 * 2^52
+  const double e0h = fma(-d0, y0h, 0.5);            // (1 - w y0^2) / 2
+  const double d = fma(d0, e0h, d0);                // d0 (1 + e0 / 2)
+  const double t = fma(d, -825.8468306507675, 6755399441055744.0);  // -d sqrt5 256 / ln2 + 1.5 * 2^52
   const int k = max(__double2loint(t), -256 * 900);
   const double kf = t - 6755399441055744.0;
-  double r = fma(kf, -0.00270760617331689, x);       // ln2/256 split: hi (32 bits, exact product) ...
-  r = fma(kf, -7.453964567463233e-13, r);            // ... and lo
-  double p = fma(r, 1.0 / 24.0, 1.0 / 6.0);
-  p = fma(r, p, 0.5);
-  p = fma(r, p, 1.0);
+  double r = fma(kf, 0.0012108782921131933, d);      // ln2/(256 sqrt5) split: hi (32 bits, exact product) ...
+  r = fma(kf, 1.8708673154509723e-13, r);            // ... and lo
+  double p = fma(r, 25.0 / 24.0, -1.8633899812498247);  // e^(-sqrt5 r): 25/24, -5 sqrt5/6, 5/2, -sqrt5, 1
+  p = fma(r, p, 2.5);
+  p = fma(r, p, -2.23606797749979);
   p = fma(r, p, 1.0);
   const double tj = tab256[k & 255];
   const double scale = __hiloint2double(__double2hiint(tj) + ((k >> 8) << 20), __double2loint(tj));
@@ -754,8 +756,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
 #pragma unroll
             for (int u = 0; u < kColsPerItem / 2; ++u) {
               const double2 y = yy2[u];
-              W[2 * u] = fmax(fma(-2.0, W[2 * u], xx + y.x), 0.0);
-              W[2 * u + 1] = fmax(fma(-2.0, W[2 * u + 1], xx + y.y), 0.0);
+              W[2 * u] = fma(-2.0, W[2 * u], xx + y.x);  // may round below 0: |W| is taken below
+              W[2 * u + 1] = fma(-2.0, W[2 * u + 1], xx + y.y);
             }
           } else {
 #pragma unroll
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             // columns j >= n meet zero matrix digits and candidates beyond q are never stored, so
             // neither needs masking; sc leaves >= 2^-20 headroom, so X < 2^40 without a clamp
             const unsigned long long X =
-                kPrecise ? __double2ull_rz(kstar(W[u], sigma) * kscale) : kstar_fixed(W[u], mc, s_exp2);
+                kPrecise ? __double2ull_rz(kstar(fabs(W[u]), sigma) * kscale) : kstar_fixed(fabs(W[u]), mc, s_exp2);
             lo[v] = (uint32_t)X;
             hi[v] = (uint32_t)(X >> 32);
           }
