@@ -405,7 +405,7 @@ struct TcArgs {
   int32_t n_coord;            // coord_lut entries
   double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
   int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
-                              // 4 epilogue TMEM reads without the arithmetic
+                              // 4 epilogue TMEM reads without the arithmetic, 8 matrix ring (not resident)
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
   // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
   // is in device memory (written by the copy stream after the chunk), null = all rows present
@@ -421,6 +421,9 @@ struct TcArgs {
   // per pair instead of 2 per dimension
   const double* mu;           // [n_params]
   int32_t dot;
+  // mat_resident != 0: every (chunk, slice) digit block is loaded into shared memory once per CTA
+  // and stays there for all tiles (set by launch_gp_tc when it fits; else the 8-stage ring)
+  int32_t mat_resident;
 };
 
 

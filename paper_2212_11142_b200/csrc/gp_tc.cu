@@ -47,7 +47,10 @@ constexpr int kGroups = 6;       // a + b in 0..5
 constexpr int kStages = 8;       // matrix block ring
 constexpr int kMaxChunks = 16;   // n <= 255
 constexpr int kMaxSlices = 8;
-constexpr int kProdWarps = 16;   // K* producers: 4 per TMEM lane quarter
+#ifndef BX_TC_PROD_WARPS
+#define BX_TC_PROD_WARPS 8
+#endif
+constexpr int kProdWarps = BX_TC_PROD_WARPS;   // K* producers: 4 per TMEM lane quarter
 constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // 8 columns of a slice per producer thread
 constexpr int kThreads = (8 + kProdWarps) * 32;
 constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
@@ -153,9 +156,19 @@ __device__ __forceinline__ unsigned long long kstar_fixed(double W, const Matern
   p = fma(r, p, 1.0);
   const double tj = tab256[k & 255];
   const double scale = __hiloint2double(__double2hiint(tj) + ((k >> 8) << 20), __double2loint(tj));
-  return __double2ull_rz(fma(m.s2, W, fma(m.s1, d, m.s0)) * (p * scale));
+  // + 2^52: the 40-bit fixed-point value (rounded to nearest) lands in the low mantissa bits, so the
+  // last multiply is an FMA and no FP64 -> integer conversion is needed
+  const double X = fma(fma(m.s2, W, fma(m.s1, d, m.s0)), p * scale, 4503599627370496.0);
+  return (unsigned long long)__double_as_longlong(X) & 0xFFFFFFFFFFull;
 }
 
+__device__ __forceinline__ void tmem_st1(uint32_t addr, uint32_t v0) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(addr), "r"(v0) : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]) : "memory");
+}
 __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(addr), "r"(v0), "r"(v1) : "memory");
 }
@@ -166,8 +179,17 @@ struct TcLayout {
 };
 
 // qs: the QuickScorer forest evaluated by warps 2-3 (qs->enabled == 0 -> no forest tables)
+// (chunk c, slice ks <= min(c / 2, nsl - 1)) blocks of the lower triangle, chunk-major: index of
+// chunk c's first block, and the total for nch chunks
+__host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
+  int o = 0;
+  for (int i = 0; i < c; ++i) o += min(i >> 1, nsl - 1) + 1;
+  return o;
+}
+
 __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words,
-                                              const QsForestDev* qs = nullptr, bool summ = false) {
+                                              const QsForestDev* qs = nullptr, bool summ = false,
+                                              bool resident = false) {
   const bool rf = qs && qs->enabled;
   const int nsl = (n + 31) / 32, npad = 32 * nsl;
   TcLayout L;
@@ -208,8 +230,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   L.parts = off;     // [4] epilogue-warp partial summaries (summ_on)
   off += summ ? 4 * (int)sizeof(Partial) : 0;
   off = (off + 1023) & ~1023;
-  L.mat = off;     // [stage][digit][16 x 32 B]
-  off += kStages * kMatBlock;
+  L.mat = off;     // [stage][digit][16 x 32 B], or every block of the triangle when resident
+  off += (resident ? tc_block0(n / 16 + 1, nsl) : kStages) * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
   off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 4 + 4 + 1) * 8;
   L.total = off;
@@ -227,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
   const QsForestDev& qf = a.qs;
   const bool rf = qf.enabled != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0);
+  const bool resident = ta.mat_resident != 0;
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0, resident);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -276,6 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       }
       s_yy[j] = acc;
     }
+    __syncthreads();  // then the planes hold -2 y' (exact), so W = |x'|^2 + |y'|^2 + sum x' (-2 y')
+    for (int i = tid; i < (ND > 0 ? n_params * npad : 0); i += blockDim.x)
+      planes[i] = (uint64_t)__double_as_longlong(-2.0 * __longlong_as_double((long long)planes[i]));
   }
   for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
     const int kk = i / npad, j = i % npad;
@@ -504,7 +530,16 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     }
   } else if (warp == 1 && lane == 0) {
     // ---- TMA producer: matrix digit blocks in MMA consumption order ------------------------
-    {
+    if (resident) {  // the whole triangle once, on one barrier
+      const int nb = tc_block0(nch, nsl);
+      if (my_tiles > 0) {
+        mb_expect(&mat_full[0], (uint32_t)(nb * kMatBlock));
+        for (int c = 0; c < nch; ++c)
+          for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks)
+            bulk_g2s(mat + (size_t)(tc_block0(c, nsl) + ks) * kMatBlock, ta.mdig + ((size_t)c * nsl + ks) * kMatBlock,
+                     kMatBlock, &mat_full[0]);
+      }
+    } else {
       uint32_t ph = 0;  // parity bit per stage
       int s = 0, issued = 0;
       for (int t = 0; t < my_tiles; ++t)
@@ -544,11 +579,14 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           tc_fence_after();
         }
         const uint32_t dbase = tmem + (uint32_t)(buf * kAccCols);
+        const int b0 = resident ? tc_block0(c, nsl) : 0;
         for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks) {
-          mb_wait(&mat_full[s], (ph_m >> s) & 1u);
-          ph_m ^= 1u << s;
-          tc_fence_after();
-          const uint64_t bd = bdesc0 + (uint64_t)((s * kMatBlock) >> 4);
+          if (!resident || chunk_no == 0) {  // resident: the one load, before the first chunk
+            mb_wait(&mat_full[resident ? 0 : s], resident ? 0u : (ph_m >> s) & 1u);
+            if (!resident) ph_m ^= 1u << s;
+            tc_fence_after();
+          }
+          const uint64_t bd = bdesc0 + (uint64_t)(((resident ? b0 + ks : s) * kMatBlock) >> 4);
           const uint32_t at = tmem + (uint32_t)(kDigCol0 + ks * kSliceCols);
           const uint32_t acc = ks > 0 ? 1u : 0u;
           if (!(ta.debug & 2)) {
@@ -558,8 +596,10 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             mma_i8<idesc_i8<3 * kN>()>(dbase + 3 * kN, at + 3 * 8, bd, 1u);
             mma_i8<idesc_i8<2 * kN>()>(dbase + 4 * kN, at + 4 * 8, bd, 1u);
           }
-          tc_commit_warp(&mat_empty[s]);  // the stage is free once these MMAs retire
-          s = (s + 1 == kStages) ? 0 : s + 1;
+          if (!resident) {
+            tc_commit_warp(&mat_empty[s]);  // the stage is free once these MMAs retire
+            s = (s + 1 == kStages) ? 0 : s + 1;
+          }
         }
         tc_commit_warp(&acc_full[buf]);
         // chunk c is the last reader of slice c / 2 when c is even (chunks run downwards)
@@ -736,28 +776,39 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       }
       for (int ks = nsl - 1; ks >= 0; --ks) {
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
+        if constexpr (ND > 0) {
+          // re-read the coordinates per slice (volatile: not hoisted) so they are not live across
+          // the Matérn chains: 2 * ND registers more for interleaving them
+          const uint32_t xa = su32(cv + c);
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            unsigned long long v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(xa + (uint32_t)(k * kM * 8)));
+            xr[k] = __longlong_as_double((long long)v);
+          }
+        }
         double W[kColsPerItem];
 #pragma unroll
         for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
         if constexpr (ND > 0) {
           const double2* pl0 = reinterpret_cast<const double2*>(planes + j0);
           if (ta.dot) {  // W = |x'|^2 + |y'|^2 - 2 x'.y' (centred, small: no harmful cancellation)
-#pragma unroll
-            for (int k = 0; k < ND; ++k) {
-              const double2* pl = pl0 + (size_t)k * (npad / 2);
-#pragma unroll
-              for (int u = 0; u < kColsPerItem / 2; ++u) {
-                const double2 y = pl[u];
-                W[2 * u] = fma(xr[k], y.x, W[2 * u]);
-                W[2 * u + 1] = fma(xr[k], y.y, W[2 * u + 1]);
-              }
-            }
             const double2* yy2 = reinterpret_cast<const double2*>(s_yy + j0);
 #pragma unroll
             for (int u = 0; u < kColsPerItem / 2; ++u) {
               const double2 y = yy2[u];
-              W[2 * u] = fma(-2.0, W[2 * u], xx + y.x);  // may round below 0: |W| is taken below
-              W[2 * u + 1] = fma(-2.0, W[2 * u + 1], xx + y.y);
+              W[2 * u] = xx + y.x;
+              W[2 * u + 1] = xx + y.y;
+            }
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+              const double2* pl = pl0 + (size_t)k * (npad / 2);  // -2 y'
+#pragma unroll
+              for (int u = 0; u < kColsPerItem / 2; ++u) {
+                const double2 y = pl[u];
+                W[2 * u] = fma(xr[k], y.x, W[2 * u]);  // may round below 0: |W| is taken below
+                W[2 * u + 1] = fma(xr[k], y.y, W[2 * u + 1]);
+              }
             }
           } else {
 #pragma unroll
@@ -845,7 +896,12 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         if (pt == 0) TC_TRACE(0, 4, ks);
 #pragma unroll
         for (int b = 0; b < kDB; ++b)
-          tmem_st2(tmem + lane_base + (uint32_t)(kDigCol0 + ks * kSliceCols + b * 8 + part * 2), dw[b][0], dw[b][1]);
+        {
+          const uint32_t col = tmem + lane_base + (uint32_t)(kDigCol0 + ks * kSliceCols + b * 8 + part * (kColsPerItem / 4));
+          if constexpr (kColsPerItem == 8) tmem_st2(col, dw[b][0], dw[b][1]);
+          else if constexpr (kColsPerItem == 16) tmem_st4(col, dw[b]);
+          else tmem_st1(col, dw[b][0]);
+        }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -925,9 +981,15 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
   return cudaGetLastError();
 }
 
-cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s) {
+cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
+  TcArgs a = a0;
+  // matrix digits resident in shared memory when they fit (BX_TC_DEBUG bit 8: always the ring)
+  a.mat_resident = 0;
+  if (!(a.debug & 8) && tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
+                                  a.summ_on != 0, true).total <= 227 * 1024)
+    a.mat_resident = 1;
   const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
-                               a.summ_on != 0);
+                               a.summ_on != 0, a.mat_resident != 0);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   // all-numeric spaces with up to 16 parameters get the unrolled distance loop
   const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;
