@@ -126,7 +126,7 @@ def test_space_exhausted_raises():
     assert A.optimize_acquisition(ctx, sp, cot) == allc[5]
 
 
-@pytest.mark.parametrize("n", [64, 200, 300, 500])
+@pytest.mark.parametrize("n", [64, 200, 250, 300, 500])
 def test_mixed_space_large_n_against_oracle(n):
     """C5 (d=10 mixed: log-ordinal, integer, real, categorical, Spearman and Kendall permutations)
     at n up to 500 — the tensor-core kernel (n <= 255) and the generic kernel beyond — against the
@@ -219,3 +219,22 @@ def test_full_step_kernel_values_match_separate_kernels(c3, monkeypatch):
     assert np.array_equal(pa, pb) and np.array_equal(va, vb)
     assert [c.index for c in a.top] == [c.index for c in b.top]
     assert (a.n_scored, a.n_finite, a.best.index) == (b.n_scored, b.n_finite, b.best.index)
+
+
+def test_matrix_ring_matches_resident_matrix(c3, monkeypatch):
+    """The tensor-core posterior keeps the digit-sliced [L^-1; alpha^T] resident in shared memory
+    when it fits, else streams it through an 8-stage ring; both give bit-identical posteriors
+    (BX_TC_DEBUG=8 forces the ring)."""
+    from paper_2212_11142_b200.device import Scorer
+    sc0, meta, arr, space, gp, feas, rows_h = c3
+    out = []
+    for ring in (False, True):
+        if ring:
+            monkeypatch.setenv("BX_TC_DEBUG", "8")
+        sc = Scorer()
+        sc.set_gp(gp)
+        assert sc.gp_kernel() == "tensor"
+        mean, var = sc.predict(sc.to_device(rows_h[:200_003]))
+        out.append((mean.cpu().numpy(), var.cpu().numpy()))
+        sc.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])

@@ -27,9 +27,7 @@ def ncu_csv(path, page, extra=()):
     return list(csv.reader(io.StringIO(out)))
 
 
-def summarise(path):
-    rows = ncu_csv(path, "raw")
-    head, vals = rows[0], rows[2]
+def summarise_row(path, head, vals, launch):
     out = {"kernel": vals[head.index("Kernel Name")] if "Kernel Name" in head else None}
     for m in METRICS:
         if m in head:
@@ -42,11 +40,13 @@ def summarise(path):
                 stalls[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = v
     out["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
     try:
-        src = ncu_csv(path, "source", ["--print-source=sass"])
+        src = ncu_csv(path, "source", ["--print-source=sass", "--launch-skip", str(launch), "--launch-count", "1"])
         h = src[1]
         si, ii = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
         agg, cnt, tot = collections.Counter(), collections.Counter(), 0
         for x in src[2:]:
+            if len(x) < 2:
+                continue
             t = x[1].split()
             if not t:
                 continue
@@ -66,6 +66,14 @@ def summarise(path):
     except (KeyError, ValueError):
         pass
     return out
+
+
+def summarise(path):
+    """One summary per captured launch (a list when the report holds several kernels)."""
+    rows = ncu_csv(path, "raw")
+    head = rows[0]
+    res = [summarise_row(path, head, vals, i) for i, vals in enumerate(rows[2:]) if len(vals) == len(head)]
+    return res[0] if len(res) == 1 else res
 
 
 if __name__ == "__main__":

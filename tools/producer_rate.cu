@@ -16,7 +16,9 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
 template <int V>
 __device__ __forceinline__ unsigned long long kstar_fixed(double W, double s0, double s1, double s2, const double* tab) {
   const double w = W + 1e-300;
-  const double y0 = rsqrt_approx(w);
+  double y0;
+  if (V == 8) y0 = __hiloint2double(0x5fe6eb50 - (__double2hiint(w) >> 1), 0);  // timing only: integer seed
+  else y0 = rsqrt_approx(w);
   const double y0h = __hiloint2double(__double2hiint(y0) - (1 << 20), __double2loint(y0));
   const double d0 = w * y0;
   const double e0h = fma(-d0, y0h, 0.5);
@@ -54,6 +56,12 @@ __global__ void __launch_bounds__(512, 1) bench(const double* planes, const doub
     xr[k] = xs[(threadIdx.x * 7 + k) & 255] * 0.1;
     xx = fma(xr[k], xr[k], xx);
   }
+  double xr2[10], xx2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    xr2[k] = xs[(threadIdx.x * 5 + k + 3) & 255] * 0.1;
+    xx2 = fma(xr2[k], xr2[k], xx2);
+  }
   const double s0 = 1099511627776.0 * 0.7, s1 = s0 * 2.2360679774997896, s2 = s0 * 5.0 / 3.0;
   uint32_t acc = 0;
   const int part = (threadIdx.x >> 7) & 3;
@@ -83,6 +91,55 @@ __global__ void __launch_bounds__(512, 1) bench(const double* planes, const doub
 #pragma unroll
       for (int u = 0; u < 8; ++u) W[u] = xx + u + (it & 7);
     }
+    if (V == 5) {  // lane pairs: 2 candidates x 4 columns per thread, half the plane loads
+      const int jh = j0 + 4 * (threadIdx.x & 1);
+      double Wb[8];
+      const double2* yyp = reinterpret_cast<const double2*>(sp + 2560 + jh);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double2 y = yyp[u];
+        Wb[2 * u] = xx + y.x; Wb[2 * u + 1] = xx + y.y;
+        Wb[4 + 2 * u] = xx2 + y.x; Wb[4 + 2 * u + 1] = xx2 + y.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const double2* pl = reinterpret_cast<const double2*>(sp + k * 256 + jh);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const double2 y = pl[u];
+          Wb[2 * u] = fma(xr[k], y.x, Wb[2 * u]);
+          Wb[2 * u + 1] = fma(xr[k], y.y, Wb[2 * u + 1]);
+          Wb[4 + 2 * u] = fma(xr2[k], y.x, Wb[4 + 2 * u]);
+          Wb[4 + 2 * u + 1] = fma(xr2[k], y.y, Wb[4 + 2 * u + 1]);
+        }
+      }
+      uint32_t lo[8], hi[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned long long X = kstar_fixed<0>(fabs(Wb[u]), s0, s1, s2, tab);
+        lo[u] = (uint32_t)X;
+        hi[u] = (uint32_t)(X >> 32);
+      }
+      uint32_t dw[2][5];
+#pragma unroll
+      for (int qd = 0; qd < 2; ++qd) {
+        const uint32_t p01 = __byte_perm(lo[4 * qd], lo[4 * qd + 1], 0x5140), p23 = __byte_perm(lo[4 * qd + 2], lo[4 * qd + 3], 0x5140);
+        const uint32_t q01 = __byte_perm(lo[4 * qd], lo[4 * qd + 1], 0x7362), q23 = __byte_perm(lo[4 * qd + 2], lo[4 * qd + 3], 0x7362);
+        const uint32_t h01 = __byte_perm(hi[4 * qd], hi[4 * qd + 1], 0x5140), h23 = __byte_perm(hi[4 * qd + 2], hi[4 * qd + 3], 0x5140);
+        dw[qd][0] = __byte_perm(h01, h23, 0x5410); dw[qd][1] = __byte_perm(q01, q23, 0x7632);
+        dw[qd][2] = __byte_perm(q01, q23, 0x5410); dw[qd][3] = __byte_perm(p01, p23, 0x7632);
+        dw[qd][4] = __byte_perm(p01, p23, 0x5410);
+      }
+      // even lanes keep candidate 0's words and send candidate 1's; odd lanes the reverse
+      const bool odd = threadIdx.x & 1;
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        const uint32_t send = odd ? dw[0][b] : dw[1][b];
+        const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 1);
+        acc += (odd ? dw[1][b] : dw[0][b]) ^ got;
+      }
+      continue;
+    }
     const double2* yy2 = reinterpret_cast<const double2*>(sp + 2560 + j0);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -95,7 +152,7 @@ __global__ void __launch_bounds__(512, 1) bench(const double* planes, const doub
     for (int u = 0; u < 8; ++u) {
       unsigned long long X;
       if (V == 3) X = (unsigned long long)__double_as_longlong(W[u]);
-      else X = kstar_fixed<V == 1 ? 1 : 0>(fabs(W[u]), s0, s1, s2, tab);
+      else X = kstar_fixed<V == 1 ? 1 : (V == 8 ? 8 : 0)>(fabs(W[u]), s0, s1, s2, tab);
       lo[u] = (uint32_t)X;
       hi[u] = (uint32_t)(X >> 32);
     }
@@ -127,9 +184,9 @@ int main() {
   cudaMemcpy(dx, hx, sizeof hx, cudaMemcpyHostToDevice);
   cudaMemcpy(de, he, sizeof he, cudaMemcpyHostToDevice);
   const char* names[] = {"full loop", "no exp-table load", "distances from registers", "distance only",
-                         "Matern only"};
+                         "Matern only", "lane pairs (2 cand x 4 col)", "full loop, 8 warps", "lane pairs, 8 warps", "no MUFU (integer seed)"};
   const int iters = 4000;
-  for (int v = 0; v < 5; ++v) {
+  for (int v = 0; v < 9; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (v) {
         case 0: bench<0><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
@@ -137,6 +194,10 @@ int main() {
         case 2: bench<2><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
         case 3: bench<3><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
         case 4: bench<4><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
+        case 5: bench<5><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
+        case 6: bench<0><<<148, 256>>>(dp, dx, de, iters, dout, dclk); break;
+        case 7: bench<5><<<148, 256>>>(dp, dx, de, iters, dout, dclk); break;
+        case 8: bench<8><<<148, 512>>>(dp, dx, de, iters, dout, dclk); break;
       }
       cudaDeviceSynchronize();
     }
@@ -144,7 +205,7 @@ int main() {
     cudaMemcpy(h, dclk, sizeof h, cudaMemcpyDeviceToHost);
     long long mx = 0;
     for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-    const double per = 512.0 * iters * 8 / mx;
+    const double per = (v >= 6 ? 256.0 : 512.0) * iters * 8 / mx;
     printf("%-26s %.3f K*/clk/SM  (%.1f SMSP clk per 32 K*)\n", names[v], per, 4 * 32 / per);
   }
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
