@@ -19,15 +19,17 @@
 // row chunks of 16: chunk c needs column slices 0..c/2 only (lower triangle + alpha).  Chunks run
 // from the last to the first, so column slice k is dead after chunk 2k and the producers refill
 // it for the next tile while the MMAs finish the smaller chunks.
-// CTA = 24 warps, one per SM, persistent over tiles:
+// CTA = 16 warps (128 registers each), one per SM, persistent over tiles:
 //   warp 0         : MMA issuer (5 UTCIMMA 128 x (6-b)*16 x 32 per chunk and slice, b = K* digit)
-//   warp 1  lane 0 : TMA producer: one 3 KB bulk copy per (chunk, slice) block, 8-stage ring
+//   warp 1  lane 0 : TMA producer: the whole digit-sliced matrix once per CTA when it fits in shared
+//                    memory (resident for every tile), else one 3 KB bulk copy per (chunk, slice)
+//                    block through an 8-stage ring
 //   warp 1  lane 1 : row prefetcher: the next tiles' encoded rows, one bulk copy per tile
 //   warps 2-3      : decoders: candidate values / masks / forest offsets of the next tile
 //   warps 4-7      : epilogue, thread = candidate = TMEM lane: tcgen05.ld of the 6 groups,
 //                    int64 recombination, sum of squares, mean, EI — no cross-thread reduction;
 //                    between chunks, the candidate's forest probability from QuickScorer tables
-//   warps 8-23     : K* producers: 8 Matérn values (FP64) per thread and slice, sliced into
+//   warps 8-15     : K* producers: 16 Matérn values (FP64) per thread and slice, sliced into
 //                    digits and stored into the candidate's TMEM lane (tcgen05.st)
 // TMEM (512 columns): two 96-column accumulators (6 groups x 16 rows) so the epilogue of one chunk
 // overlaps the MMAs of the next, then 40 columns (5 digits x 32 bytes) per column slice.
@@ -50,8 +52,8 @@ constexpr int kMaxSlices = 8;
 #ifndef BX_TC_PROD_WARPS
 #define BX_TC_PROD_WARPS 8
 #endif
-constexpr int kProdWarps = BX_TC_PROD_WARPS;   // K* producers: 4 per TMEM lane quarter
-constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // 8 columns of a slice per producer thread
+constexpr int kProdWarps = BX_TC_PROD_WARPS;   // K* producers: kProdWarps / 4 per TMEM lane quarter
+constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // columns of a slice per producer thread (16)
 constexpr int kThreads = (8 + kProdWarps) * 32;
 constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
 constexpr int kAccCols = kGroups * kN;    // 96 TMEM columns per accumulator
