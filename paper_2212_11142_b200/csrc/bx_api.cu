@@ -113,7 +113,7 @@ struct bx_handle {
   bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
-  DevBuf d_mdig, d_rowscale;
+  DevBuf d_mdig, d_rowscale, d_tc_part;
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
@@ -282,6 +282,7 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     }
     t.dot = h->tc_dot ? 1 : 0;
     t.mu = h->d_mu.as<double>();
+    t.part = h->tc_nsl > 8 ? h->d_tc_part.as<double>() : nullptr;
     t.n_coord = (int32_t)h->coord_host.size();
     std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
     t.debug = h->tc_debug;
@@ -400,6 +401,7 @@ void bx_destroy(bx_handle* h) {
   if (h->h_ones) cudaFreeHost(h->h_ones);
   h->d_mdig.release();
   h->d_rowscale.release();
+  h->d_tc_part.release();
   h->d_ei.release();
   h->d_grad_scratch.release();
   h->d_leaf_count.release();
@@ -551,9 +553,10 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
       h->use_fused = true;
     }
   }
-  // tensor-core path: n <= 255 (8 row chunks) and the shared-memory budget
+  // tensor-core path: n <= 511 (32 row chunks; n > 255 runs two column passes per tile) and the
+  // shared-memory budget
   h->use_tc = false;
-  if (!h->no_tc && n <= 255 && tc_smem_bytes(n, D, h->n_kendall, h->row_words) <= 227 * 1024) {
+  if (!h->no_tc && n <= 511 && tc_smem_bytes(n, D, h->n_kendall, h->row_words) <= 227 * 1024) {
     int E = 0;
     const double m = frexp(outputscale, &E);  // sigma < 2^E = sc
     if (m > 1.0 - ldexp(1.0, -20)) ++E;        // headroom: K* * 2^40 / sc < 2^40 - 2^20
@@ -561,7 +564,9 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
     h->tc_nch = n / 16 + 1;
     h->tc_kscale = ldexp(1.0, 40 - E);
     BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
-    BX_CUDA(h, h->d_rowscale.ensure(2 * 256 * 8));
+    BX_CUDA(h, h->d_rowscale.ensure(2 * 512 * 8));
+    if (h->tc_nsl > 8)  // pass-0 partial sums of rows >= 256: [CTA][256 rows][128 candidates]
+      BX_CUDA(h, h->d_tc_part.ensure((size_t)h->sm_count * 256 * 128 * 8));
     BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
                                  h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), s));
     h->use_tc = true;

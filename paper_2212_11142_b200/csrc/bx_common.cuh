@@ -424,6 +424,9 @@ struct TcArgs {
   // mat_resident != 0: every (chunk, slice) digit block is loaded into shared memory once per CTA
   // and stays there for all tiles (set by launch_gp_tc when it fits; else the 8-stage ring)
   int32_t mat_resident;
+  // n > 255 (two passes per tile): [grid][256 rows][128 candidates] pass-0 partial sums of the
+  // rows >= 256, written and read back by the same epilogue thread; null otherwise
+  double* part;
 };
 
 

@@ -47,8 +47,13 @@ constexpr int kDA = 6;           // matrix digits (signed)
 constexpr int kDB = 5;           // K* digits (unsigned)
 constexpr int kGroups = 6;       // a + b in 0..5
 constexpr int kStages = 8;       // matrix block ring
-constexpr int kMaxChunks = 16;   // n <= 255
-constexpr int kMaxSlices = 8;
+constexpr int kMaxChunks = 32;   // n <= 511
+constexpr int kSlots = 8;        // K* column slices held in tensor memory at a time
+// n > 255 (more than kSlots column slices): each tile runs two passes.  Pass 0 holds slices 0-7
+// (columns 0-255) in the slots and runs every row chunk — rows < 256 complete, rows >= 256 leave
+// their partial sums (exact int64, converted to double) in global scratch; pass 1 refills the slots
+// with slices 8.. and runs the chunks of rows >= 256 again over those columns, adding the partials.
+__host__ __device__ __forceinline__ int tc_passes(int nsl) { return nsl > kSlots ? 2 : 1; }
 #ifndef BX_TC_PROD_WARPS
 #define BX_TC_PROD_WARPS 8
 #endif
@@ -235,7 +240,7 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   L.mat = off;     // [stage][digit][16 x 32 B], or every block of the triangle when resident
   off += (resident ? tc_block0(n / 16 + 1, nsl) : kStages) * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
-  off += (1 + kMaxSlices + 2 * kStages + 4 + 4 + 4 + 4 + 1) * 8;
+  off += (1 + kSlots + 2 * kStages + 4 + 4 + 4 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
@@ -249,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.gp.n, n_params = a.space.n_params, words = a.space.row_words;
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
+  const int npass = tc_passes(nsl);
   const QsForestDev& qf = a.qs;
   const bool rf = qf.enabled != 0;
   const bool resident = ta.mat_resident != 0;
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* cand_full = bars;
   uint64_t* slice_empty = bars + 1;
-  uint64_t* mat_full = slice_empty + kMaxSlices;
+  uint64_t* mat_full = slice_empty + kSlots;
   uint64_t* mat_empty = mat_full + kStages;
   uint64_t* acc_full = mat_empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   }
   if (tid == 0) {
     mb_init(cand_full, kProdWarps);
-    for (int i = 0; i < kMaxSlices; ++i) mb_init(&slice_empty[i], 1);
+    for (int i = 0; i < kSlots; ++i) mb_init(&slice_empty[i], 1);
     for (int i = 0; i < kStages; ++i) {
       mb_init(&mat_full[i], 1);
       mb_init(&mat_empty[i], 1);
@@ -545,8 +551,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       uint32_t ph = 0;  // parity bit per stage
       int s = 0, issued = 0;
       for (int t = 0; t < my_tiles; ++t)
-        for (int c = nch - 1; c >= 0; --c)
-          for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks) {
+        for (int p = 0; p < npass; ++p)
+        for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c)
+          for (int ks = kSlots * p; ks <= min(c >> 1, min(nsl, kSlots * (p + 1)) - 1); ++ks) {
             if (issued >= kStages) {
               mb_wait(&mat_empty[s], (ph >> s) & 1u);
               ph ^= 1u << s;
@@ -567,13 +574,16 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     const uint64_t bdesc0 = sdesc(mat);
     uint32_t ph_m = 0, ph_e = 0, ph_c = 0;  // parity bits per stage / accumulator
     int s = 0, chunk_no = 0;
-    for (int t = 0; t < my_tiles; ++t) {
+    for (int t = 0; t < my_tiles; ++t)
+    for (int p = 0; p < npass; ++p) {
+      const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));  // this pass's column slices
+      const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // pass 1 takes the slots pass 0 frees first
       if (lane == 0) TC_TRACE(1, 1, t);
       mb_wait(cand_full, ph_c);
       ph_c ^= 1u;
       tc_fence_after();
       if (lane == 0) TC_TRACE(1, 2, t);
-      for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
+      for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         if (chunk_no >= 2) {
           mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
@@ -582,15 +592,15 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         }
         const uint32_t dbase = tmem + (uint32_t)(buf * kAccCols);
         const int b0 = resident ? tc_block0(c, nsl) : 0;
-        for (int ks = 0; ks <= min(c >> 1, nsl - 1); ++ks) {
+        for (int ks = lo; ks <= min(c >> 1, hi - 1); ++ks) {
           if (!resident || chunk_no == 0) {  // resident: the one load, before the first chunk
             mb_wait(&mat_full[resident ? 0 : s], resident ? 0u : (ph_m >> s) & 1u);
             if (!resident) ph_m ^= 1u << s;
             tc_fence_after();
           }
           const uint64_t bd = bdesc0 + (uint64_t)(((resident ? b0 + ks : s) * kMatBlock) >> 4);
-          const uint32_t at = tmem + (uint32_t)(kDigCol0 + ks * kSliceCols);
-          const uint32_t acc = ks > 0 ? 1u : 0u;
+          const uint32_t at = tmem + (uint32_t)(kDigCol0 + (ks - lo + soff) * kSliceCols);
+          const uint32_t acc = ks > lo ? 1u : 0u;
           if (!(ta.debug & 2)) {
             mma_i8<idesc_i8<6 * kN>()>(dbase, at, bd, acc);
             mma_i8<idesc_i8<5 * kN>()>(dbase + 1 * kN, at + 1 * 8, bd, 1u);
@@ -604,8 +614,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           }
         }
         tc_commit_warp(&acc_full[buf]);
-        // chunk c is the last reader of slice c / 2 when c is even (chunks run downwards)
-        if (!(c & 1) && (c >> 1) < nsl) tc_commit_warp(&slice_empty[c >> 1]);
+        // chunk c is the last reader of slice c / 2 (slot c / 2 - lo) when c is even (chunks run
+        // downwards)
+        if (!(c & 1) && (c >> 1) >= lo && (c >> 1) < hi) tc_commit_warp(&slice_empty[(c >> 1) - lo + soff]);
         if (lane == 0) TC_TRACE(1, 3, c);
       }
     }
@@ -623,7 +634,12 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       double ss = 0.0, mean_s = 0.0;
-      for (int c = nch - 1; c >= 0; --c, ++chunk_no) {
+      for (int p = 0; p < npass; ++p)
+      for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
+        // two passes (n > 255): rows >= 256 park their pass-0 partial sums in this CTA's scratch
+        // ([256 rows][128 candidates], coalesced per row) and add them back in pass 1
+        const int mode = (npass == 1 || c < 2 * kSlots) ? 0 : (p == 0 ? 1 : 2);
+        double* park = ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
         mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);
         ph_f ^= 1u << buf;
@@ -645,7 +661,12 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             Z += (long long)(int32_t)g[3][j] << 16;
             Z += (long long)(int32_t)g[4][j] << 8;
             Z += (long long)(int32_t)g[5][j];
-            const double zd = (double)Z;
+            double zd = (double)Z;
+            if (mode == 1) {
+              park[(size_t)(row - kSlots * 32) * kM] = zd;
+              continue;
+            }
+            if (mode == 2) zd += park[(size_t)(row - kSlots * 32) * kM];
             const double v = zd * rowscale_ss[row];  // 0 for the alpha row and the padding rows
             ss = fma(v, v, ss);
             if (row == n) mean_s = zd * rowscale[row];  // only in the alpha row's chunk
@@ -760,6 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     // K* * kscale: the fixed-point scale is folded into the Matérn polynomial
     const MaternConst mc{sigma * ta.kscale, sigma * kSqrt5 * ta.kscale, sigma * (5.0 / 3.0) * ta.kscale};
     const double kscale = ta.kscale;
+    uint32_t slot_used = 0, slot_par = 0;  // per TMEM slot: filled before / parity of its next wait
     for (int t = 0; t < my_tiles; ++t) {
       if (pt == 0) TC_TRACE(0, 1, t);
       const int cb = t & 1;
@@ -776,7 +798,11 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           xx = fma(xr[k], xr[k], xx);
         }
       }
-      for (int ks = nsl - 1; ks >= 0; --ks) {
+      for (int p = 0; p < npass; ++p) {
+      const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));  // this pass's column slices
+      const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // pass 1 takes the slots pass 0 frees first
+      for (int ks = hi - 1; ks >= lo; --ks) {
+        const int slot = ks - lo + soff;
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
         if constexpr (ND > 0) {
           // re-read the coordinates per slice (volatile: not hoisted) so they are not live across
@@ -891,15 +917,17 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           dw[4][qd] = __byte_perm(p01, p23, 0x5410);  // bits 0..7
         }
         if (pt == 0) TC_TRACE(0, 3, ks);
-        if (t > 0) {  // every producer waits for the MMAs to release the slice (no CTA barrier)
-          mb_wait(&slice_empty[ks], (uint32_t)((t - 1) & 1));
+        if ((slot_used >> slot) & 1u) {  // every producer waits for the MMAs to release the slot
+          mb_wait(&slice_empty[slot], (slot_par >> slot) & 1u);
+          slot_par ^= 1u << slot;
           tc_fence_after();
         }
+        slot_used |= 1u << slot;
         if (pt == 0) TC_TRACE(0, 4, ks);
 #pragma unroll
         for (int b = 0; b < kDB; ++b)
         {
-          const uint32_t col = tmem + lane_base + (uint32_t)(kDigCol0 + ks * kSliceCols + b * 8 + part * (kColsPerItem / 4));
+          const uint32_t col = tmem + lane_base + (uint32_t)(kDigCol0 + slot * kSliceCols + b * 8 + part * (kColsPerItem / 4));
           if constexpr (kColsPerItem == 8) tmem_st2(col, dw[b][0], dw[b][1]);
           else if constexpr (kColsPerItem == 16) tmem_st4(col, dw[b]);
           else tmem_st1(col, dw[b][0]);
@@ -909,8 +937,9 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mb_arrive(cand_full);        // one arrival per producer warp
-        mb_arrive(&cval_free[cb]);   // the decoders may refill this parity's buffers
+        mb_arrive(cand_full);        // one arrival per producer warp and pass
+        if (p == npass - 1) mb_arrive(&cval_free[cb]);  // the decoders may refill this parity's buffers
+      }
       }
       if (pt == 0) TC_TRACE(0, 6, t);
     }
@@ -971,7 +1000,7 @@ size_t tc_mdig_bytes(int n) {
   return (size_t)nsl * nch * kMatBlock;
 }
 
-// rowscale must hold 2 * 256 doubles (epilogue factors, then digit scales)
+// rowscale must hold 2 * 512 doubles (epilogue factors, then digit scales)
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, cudaStream_t s) {
   const int nsl = (n + 31) / 32, nch = n / kN + 1;

@@ -129,7 +129,7 @@ def test_space_exhausted_raises():
 @pytest.mark.parametrize("n", [64, 200, 250, 300, 500])
 def test_mixed_space_large_n_against_oracle(n):
     """C5 (d=10 mixed: log-ordinal, integer, real, categorical, Spearman and Kendall permutations)
-    at n up to 500 — the tensor-core kernel (n <= 255) and the generic kernel beyond — against the
+    at n up to 500 — the tensor-core kernel (one column pass for n <= 255, two beyond) — against the
     oracle's FP64 posterior on a sample of a 2^18 pool (BASELINE config 5 uses n = 500)."""
     import oracle
     from paper_2212_11142_b200 import scenarios
@@ -146,7 +146,7 @@ def test_mixed_space_large_n_against_oracle(n):
                 lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
     gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
     sc.set_gp(gp)
-    assert sc.gp_kernel() == ("tensor" if n <= 255 else "generic")
+    assert sc.gp_kernel() == "tensor"  # n > 255: two column passes per tile
     rows = sc.to_device(scenarios.sample_rows_uniform(lay, 1 << 18, rng))
     mean, var = (x.cpu().numpy() for x in sc.predict(rows))
     idx = rng.choice(len(mean), 1500, replace=False)

@@ -30,14 +30,16 @@ def main(n=500, q=1 << 20):
     rows = sc.to_device(scenarios.sample_rows_uniform(lay, q, rng))
     sc.predict(rows)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(3):
+    ts = []
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         mean, var = sc.predict(rows)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 3
-    print(f"predict 2^20: {ms:.3f} ms  {q / ms * 1e3:,.0f} cand/s")
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    print(f"predict 2^20: {ms:.3f} ms  {q / ms * 1e3:,.0f} cand/s  (runs: {' '.join(f'{t:.2f}' for t in ts)})")
     sample = lay.decode(rows[:2000].cpu().numpy().view(np.uint32))
     og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
                          L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
