@@ -84,6 +84,17 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t phase) {
                  "selp.u32 %0, 1, 0, p;\n\t}\n"
                  : "=r"(done) : "r"(su32(b)), "r"(phase) : "memory");
 }
+// For the roles that wait on the producers (MMA issuer, epilogue, decoders, copy threads): the
+// suspend-time hint parks the warp until the phase completes instead of re-polling after the
+// short default window — when the producers are the bottleneck (mixed spaces) those polling loops
+// took ~30 % of the issue slots.
+__device__ __forceinline__ void mb_wait_sleep(uint64_t* b, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(done) : "r"(su32(b)), "r"(phase), "n"(1000000) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
@@ -385,8 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       const int buf = t & 1;
-      if (t >= 2) mb_wait(&cval_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
-      mb_wait(&rows_full[buf], (uint32_t)((t >> 1) & 1));
+      if (t >= 2) mb_wait_sleep(&cval_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+      mb_wait_sleep(&rows_full[buf], (uint32_t)((t >> 1) & 1));
       const uint32_t* rs = rowsbuf + (size_t)buf * kM * words;
       const int sw = staged_words(tile);
       uint64_t* cv = cval + (size_t)buf * n_params * kM;
@@ -457,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       if (rf) {
         // QuickScorer forest for the tile's candidates (two per thread), leaves summed strictly in
         // tree order (the q >= 2 numpy order, feasibility.py:89); the epilogue reads s_prob
-        if (t >= 2) mb_wait(&prob_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        if (t >= 2) mb_wait_sleep(&prob_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
         const int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
         const uint32_t mask_s = su32(qs_mask);
         constexpr int G = 8;
@@ -513,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       for (int t = 0; t < my_tiles; ++t) {
         const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
         const int buf = t & 1;
-        if (t >= 2) mb_wait(&rows_empty[buf], (uint32_t)(((t - 2) >> 1) & 1));
+        if (t >= 2) mb_wait_sleep(&rows_empty[buf], (uint32_t)(((t - 2) >> 1) & 1));
         if (ta.ready) {  // streaming pool: wait until the copy stream has landed this tile's chunk
           const int64_t last = min(a.q, (tile + 1) * kM) - 1;
           const uint32_t* flag = ta.ready + (last >> ta.ready_shift);
@@ -555,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c)
           for (int ks = kSlots * p; ks <= min(c >> 1, min(nsl, kSlots * (p + 1)) - 1); ++ks) {
             if (issued >= kStages) {
-              mb_wait(&mat_empty[s], (ph >> s) & 1u);
+              mb_wait_sleep(&mat_empty[s], (ph >> s) & 1u);
               ph ^= 1u << s;
             }
             TC_TRACE(3, 1, c * 16 + ks);
@@ -579,14 +590,14 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));  // this pass's column slices
       const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // pass 1 takes the slots pass 0 frees first
       if (lane == 0) TC_TRACE(1, 1, t);
-      mb_wait(cand_full, ph_c);
+      mb_wait_sleep(cand_full, ph_c);
       ph_c ^= 1u;
       tc_fence_after();
       if (lane == 0) TC_TRACE(1, 2, t);
       for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         if (chunk_no >= 2) {
-          mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
+          mb_wait_sleep(&acc_empty[buf], (ph_e >> buf) & 1u);
           ph_e ^= 1u << buf;
           tc_fence_after();
         }
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         const int b0 = resident ? tc_block0(c, nsl) : 0;
         for (int ks = lo; ks <= min(c >> 1, hi - 1); ++ks) {
           if (!resident || chunk_no == 0) {  // resident: the one load, before the first chunk
-            mb_wait(&mat_full[resident ? 0 : s], resident ? 0u : (ph_m >> s) & 1u);
+            mb_wait_sleep(&mat_full[resident ? 0 : s], resident ? 0u : (ph_m >> s) & 1u);
             if (!resident) ph_m ^= 1u << s;
             tc_fence_after();
           }
@@ -641,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         const int mode = (npass == 1 || c < 2 * kSlots) ? 0 : (p == 0 ? 1 : 2);
         double* park = ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
-        mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);
+        mb_wait_sleep(&acc_full[buf], (ph_f >> buf) & 1u);
         ph_f ^= 1u << buf;
         tc_fence_after();
         if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
@@ -680,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       const int64_t gi = tile * kM + r;
       double prob = 1.0;
       if (rf) {
-        mb_wait(&prob_full[t & 1], (uint32_t)((t >> 1) & 1));
+        mb_wait_sleep(&prob_full[t & 1], (uint32_t)((t >> 1) & 1));
         prob = s_prob[(t & 1) * kM + r];
         __syncwarp();
         if (lane == 0) mb_arrive(&prob_free[t & 1]);
@@ -877,18 +888,42 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           const int k = a.perm_param[i];
           const bx_param_desc& p = params[k];
           const uint64_t x = cv[k * kM + c];
-          const bool kd = p.metric == BX_KENDALL;
-          const uint64_t xl = kd ? cmk[2 * (kend * kM + c)] : 0;
-          const uint64_t xh = kd ? cmk[2 * (kend * kM + c) + 1] : 0;
-          const double* tab = a.gp.disc_tab + a.gp.disc_off[k];
           const uint64_t* pl = planes + (size_t)k * npad + j0;
-          const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
+          // the reference's (raw / raw_mx) / l^2 (surrogate.py:222-223) as raw * (1 / l^2 / raw_mx):
+          // one FMA per pair instead of a table load
+          const double cw = a.gp.inv_l2[k] / p.raw_mx;
+          if (p.metric == BX_KENDALL) {  // discordant pairs: popcount of the pair-order masks
+            const uint64_t xl = cmk[2 * (kend * kM + c)], xh = cmk[2 * (kend * kM + c) + 1];
+            const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
 #pragma unroll
-          for (int u = 0; u < kColsPerItem; ++u) {
-            const uint64_t bl = kd ? km[2 * u] : 0, bh = kd ? km[2 * u + 1] : 0;
-            W[u] += __ldg(tab + perm_raw(p.metric, p.size, x, pl[u], xl, xh, bl, bh));
+            for (int u = 0; u < kColsPerItem; ++u) {
+              const int raw = __popcll(xl ^ km[2 * u]) + __popcll(xh ^ km[2 * u + 1]);
+              W[u] = fma((double)raw, cw, W[u]);
+            }
+            ++kend;
+          } else if (p.metric == BX_SPEARMAN) {
+            // sum (a_i - b_i)^2 = 2 (sum_{v<m} v^2 - sum a_i b_i) for permutations of 0..m-1; the
+            // dot product of the packed nibbles as byte dot products (even / odd nibbles)
+            const int m = p.size;
+            const int c2 = (m - 1) * m * (2 * m - 1) / 3;
+            const uint64_t xe = x & 0x0F0F0F0F0F0F0F0Full, xo = (x >> 4) & 0x0F0F0F0F0F0F0F0Full;
+#pragma unroll
+            for (int u = 0; u < kColsPerItem; ++u) {
+              const uint64_t y = pl[u];
+              const uint64_t ye = y & 0x0F0F0F0F0F0F0F0Full, yo = (y >> 4) & 0x0F0F0F0F0F0F0F0Full;
+              int dot = __dp4a((unsigned)xe, (unsigned)ye, 0u);
+              dot = __dp4a((unsigned)xo, (unsigned)yo, (unsigned)dot);
+              if (m > 8) {
+                dot = __dp4a((unsigned)(xe >> 32), (unsigned)(ye >> 32), (unsigned)dot);
+                dot = __dp4a((unsigned)(xo >> 32), (unsigned)(yo >> 32), (unsigned)dot);
+              }
+              W[u] = fma((double)(c2 - 2 * dot), cw, W[u]);
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < kColsPerItem; ++u)
+              W[u] = fma((double)perm_raw(p.metric, p.size, x, pl[u], 0, 0, 0, 0), cw, W[u]);
           }
-          kend += kd ? 1 : 0;
         }
         // K* -> 40-bit fixed point -> five base-256 digits, 4 columns per 32-bit word.  Straight-line
         // code (padding columns are evaluated on the zero planes and masked afterwards) so the 16
