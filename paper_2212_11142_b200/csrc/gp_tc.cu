@@ -192,7 +192,7 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, rowscale, yy, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
+  int par, planes, kmask, cval, cmask, exp2, cw, rowscale, yy, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
       mat, bars, total;
 };
 
@@ -225,6 +225,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += 2 * n_kendall * kM * 16;
   L.exp2 = off;    // 2^(j/256), j < 256
   off += 256 * 8;
+  L.cw = off;      // [n_params] permutation weight per raw unit: 1 / l^2 / raw_mx
+  off += ((n_params + 1) & ~1) * 8;  // keeps the 16-byte alignment of what follows
   L.rowscale = off;  // [2][256]: row factors, then the same with the alpha / padding rows zeroed
   off += 2 * kMaxChunks * kN * 8;
   L.yy = off;        // [npad] |y'_j|^2 of the centred training points (dot mode)
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   uint64_t* cval = reinterpret_cast<uint64_t*>(smem + L.cval);
   uint64_t* cmask = reinterpret_cast<uint64_t*>(smem + L.cmask);
   double* s_exp2 = reinterpret_cast<double*>(smem + L.exp2);
+  double* s_cw = reinterpret_cast<double*>(smem + L.cw);
   double* rowscale = reinterpret_cast<double*>(smem + L.rowscale);
   double* rowscale_ss = rowscale + kMaxChunks * kN;
   unsigned char* mat = smem + L.mat;
@@ -329,6 +332,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
   }
   for (int i = tid; i < 256; i += blockDim.x) s_exp2[i] = ta.exp2tab256[i];
+  for (int k = tid; k < n_params; k += blockDim.x)
+    s_cw[k] = a.space.params[k].kind == BX_PERMUTATION ? a.gp.inv_l2[k] / a.space.params[k].raw_mx : 0.0;
   // finite numeric coordinates pre-divided by the lengthscale: decode = two shared loads
   double* stab = reinterpret_cast<double*>(smem + L.stab);
   const bool use_stab = ta.n_coord <= kMaxCoord;
@@ -891,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
           const uint64_t* pl = planes + (size_t)k * npad + j0;
           // the reference's (raw / raw_mx) / l^2 (surrogate.py:222-223) as raw * (1 / l^2 / raw_mx):
           // one FMA per pair instead of a table load
-          const double cw = a.gp.inv_l2[k] / p.raw_mx;
+          const double cw = s_cw[k];
           if (p.metric == BX_KENDALL) {  // discordant pairs: popcount of the pair-order masks
             const uint64_t xl = cmk[2 * (kend * kM + c)], xh = cmk[2 * (kend * kM + c) + 1];
             const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
