@@ -110,7 +110,8 @@ struct bx_handle {
   bool tc_no_dot = false;                  // BX_TC_NO_DOT=1: always the difference form
   DevBuf d_mu;
   bool tc_no_full = true;                  // BX_TC_FULL=1: forest + summary inside the posterior kernel
-  bool tc_trace = false;            // BX_TC_TRACE set (role timeline dump)
+  bool tc_trace = false;
+  bool lml_narrow = false;          // BX_LML_NARROW=1: _lml_core always one CTA per setting            // BX_TC_TRACE set (role timeline dump)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale, d_tc_part;
@@ -341,6 +342,7 @@ bx_handle* bx_create(int device) {
   h->no_fused = gpg && gpg[0] == '1';
   if (const char* dbg = getenv("BX_TC_DEBUG")) h->tc_debug = atoi(dbg);
   h->tc_trace = getenv("BX_TC_TRACE") != nullptr;
+  if (const char* ln = getenv("BX_LML_NARROW")) h->lml_narrow = ln[0] == '1';
   const char* fw = getenv("BX_FOREST_WALK");
   h->no_qs_forest = fw && fw[0] == '1';
   // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
@@ -1485,6 +1487,16 @@ int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const d
   if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
     return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
   cudaSetDevice(h->device);
+  if (lml_wide_supported(n) && !h->lml_narrow) {
+    // blocked Cholesky batched over the settings, in groups that keep the factors under 1 GiB
+    const int np = (n + 31) / 32 * 32;
+    const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)c, (1ull << 30) / ((size_t)np * np * 8)));
+    BX_CUDA(h, h->d_lml_scratch.ensure(lml_coarse_wide_scratch_doubles(n, group) * sizeof(double)));
+    for (int c0 = 0; c0 < c; c0 += group)
+      BX_CUDA(h, launch_lml_coarse_wide(sq, n, D, z, thetas + (size_t)c0 * (2 + D), std::min(group, c - c0),
+                                        out + c0, h->d_lml_scratch.as<double>(), (cudaStream_t)stream));
+    return BX_OK;
+  }
   const size_t bytes = ((size_t)n * (n + 1) / 2 + n) * sizeof(double);
   double* scratch = nullptr;
   if (bytes > 200 * 1024) {
@@ -1593,6 +1605,16 @@ int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const doub
     return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
   if (want_grad && !grad) return fail(h, BX_ERR_ARG, "want_grad needs a gradient buffer");
   cudaSetDevice(h->device);
+  // a few settings (the L-BFGS-B objective passes one): each spread over the whole GPU; many
+  // settings: one CTA per setting
+  if (c <= 4 && lml_wide_supported(n) && !h->lml_narrow) {
+    BX_CUDA(h, h->d_grad_scratch.ensure(lml_wide_scratch_doubles(n, D) * sizeof(double)));
+    for (int i = 0; i < c; ++i)
+      BX_CUDA(h, launch_lml_wide(sq, n, D, z, params + (size_t)i * (2 + D), prior_shape, prior_rate, use_prior,
+                                 want_grad, value + i, want_grad ? grad + (size_t)i * (2 + D) : nullptr, ok + i,
+                                 h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
+    return BX_OK;
+  }
   BX_CUDA(h, h->d_grad_scratch.ensure(lml_grad_scratch_doubles(n, c) * sizeof(double)));
   BX_CUDA(h, launch_lml_grad(sq, n, D, z, params, c, prior_shape, prior_rate, use_prior, want_grad,
                              value, grad, ok, h->d_grad_scratch.as<double>(), (cudaStream_t)stream));

@@ -287,3 +287,40 @@ def test_dot_product_distances_match_difference_form(case, monkeypatch):
     (m0, v0), (m1, v1) = res
     close(m1, m0, rtol=1e-9)
     close(v1, v0, rtol=1e-7)
+
+
+@pytest.mark.parametrize("n", [64, 300, 500])
+def test_lml_wide_paths_large_n(n, monkeypatch):
+    """The whole-GPU _lml_core (one setting over every SM) and the batched blocked coarse LML at
+    n up to 500 (BASELINE config 5) against the oracle, and against the one-CTA-per-setting kernels
+    (BX_LML_NARROW=1)."""
+    from paper_2212_11142_b200 import acquisition as A
+    from paper_2212_11142_b200.device import Scorer
+
+    rng = np.random.default_rng(n)
+    D = 10
+    X = rng.uniform(0, 1, (n, D))
+    sq = np.stack([(X[:, k, None] - X[None, :, k]) ** 2 for k in range(D)])
+    z = rng.standard_normal(n)
+    ls = rng.uniform(0.3, 2.0, D)
+    args = (sq, z, 1.3, 1e-3, ls)
+    v, g = A.lml_core(*args, want_grad=True)
+    v0, g0 = oracle.lml_core(*args, want_grad=True, prior=None)
+    assert v == pytest.approx(v0, rel=1e-9, abs=1e-7)
+    np.testing.assert_allclose(g, g0, rtol=1e-7, atol=1e-7 * np.abs(g0).max())
+    th = np.concatenate([np.log([[1.3, 1e-3]]).repeat(16, 0), np.log(rng.uniform(0.3, 2.0, (16, D)))], 1)
+    th[3, 2:] = np.log(50.0)  # long lengthscales: near-singular Gram, may fail like LAPACK
+    out = A.batched_coarse_lml(sq, z, th)
+    ref = oracle.lml.coarse_lml(sq, z, th)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(out), fin)
+    np.testing.assert_allclose(out[fin], ref[fin], rtol=1e-9, atol=1e-7)
+    monkeypatch.setenv("BX_LML_NARROW", "1")
+    sc = Scorer()
+    monkeypatch.setattr(A, "scorer", lambda: sc)
+    v1, g1 = A.lml_core(*args, want_grad=True)
+    out1 = A.batched_coarse_lml(sq, z, th)
+    sc.close()
+    assert v1 == pytest.approx(v, rel=1e-10, abs=1e-8)
+    np.testing.assert_allclose(g1, g, rtol=1e-8, atol=1e-8 * np.abs(g).max())
+    np.testing.assert_allclose(out1[fin], out[fin], rtol=1e-10, atol=1e-8)
