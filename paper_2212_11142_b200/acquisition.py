@@ -227,32 +227,49 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     best_val = best.value if best else -math.inf
     best_cfg = candidates[best.index] if best else None
     if local_search:
-        for start in summ.top[:n_starts]:
-            cur_cfg, cur_v = candidates[start.index], start.value
-            cur_row = rows[start.index:start.index + 1]
-            for _ in range(MAX_CLIMB_STEPS):
-                nb, valid = sc.neighbors(cur_row, use_cot=cot is not None)
-                nb = nb[valid.bool()]
-                if nb.shape[0] == 0:
-                    break
-                s2, vals, _ = sc.score(nb, f_model, ctx.eps_f, k=1, want_values=True)
-                if s2.best is not None:
-                    cfg2 = lay.decode(s2.best.row)[0]
-                    if best_cfg is None or _better(s2.best.value, cfg2, best_val, best_cfg):
-                        best_val, best_cfg = s2.best.value, cfg2
-                v = vals.cpu().numpy()
+        # the starts climb in lockstep: one neighbour launch and one scoring launch per step for all
+        # still-climbing starts.  Each start's trajectory depends only on its own state, and the
+        # running best is the maximum under a total order (value desc, configuration asc), so the
+        # result equals the reference's start-after-start loop (acquisition.py:186-205).
+        starts = summ.top[:n_starts]
+        cur_rows = torch.cat([rows[st.index:st.index + 1] for st in starts]) if starts else rows[:0]
+        cur_v = [st.value for st in starts]
+        active = list(range(len(starts)))
+        n_slots = sc.n_slots
+        for _ in range(MAX_CLIMB_STEPS):
+            if not active:
+                break
+            nb, valid = sc.neighbors(cur_rows[active], use_cot=cot is not None)
+            vmask = valid.bool()
+            counts = vmask.view(len(active), n_slots).sum(1).cpu().numpy()
+            nb = nb[vmask]
+            if nb.shape[0] == 0:
+                break
+            s2, vals, _ = sc.score(nb, f_model, ctx.eps_f, k=1, want_values=True)
+            if s2.best is not None:
+                cfg2 = lay.decode(s2.best.row)[0]
+                if best_cfg is None or _better(s2.best.value, cfg2, best_val, best_cfg):
+                    best_val, best_cfg = s2.best.value, cfg2
+            v_all = vals.cpu().numpy()
+            nb_host = nb.cpu().numpy().view(np.uint32)
+            still, off = [], 0
+            for a, cnt in zip(active, counts):
+                cnt = int(cnt)
+                if cnt == 0:  # no neighbours: this start stops (acquisition.py:193-195)
+                    continue
+                v = v_all[off:off + cnt]
                 i = int(np.argmax(v))
                 ties = np.flatnonzero(v == v[i])
-                nb_host = nb.cpu().numpy().view(np.uint32)
                 if len(ties) > 1:
-                    cfgs = lay.decode(nb_host[ties])
+                    cfgs = lay.decode(nb_host[off + ties])
                     j = min(range(len(ties)), key=lambda t: cfgs[t])
-                    i, nxt = int(ties[j]), cfgs[j]
-                else:
-                    nxt = lay.decode(nb_host[i])[0]
-                if v[i] <= cur_v:  # acquisition.py:200
-                    break
-                cur_cfg, cur_v, cur_row = nxt, float(v[i]), nb[i:i + 1]
+                    i = int(ties[j])
+                if v[i] > cur_v[a]:  # acquisition.py:200
+                    cur_v[a] = float(v[i])
+                    cur_rows[a] = nb[off + i]
+                    still.append(a)
+                off += cnt
+            active = still
     if best_cfg is None:
         return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
     return best_cfg
