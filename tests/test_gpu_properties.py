@@ -238,3 +238,39 @@ def test_matrix_ring_matches_resident_matrix(c3, monkeypatch):
         out.append((mean.cpu().numpy(), var.cpu().numpy()))
         sc.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 255, 256, 257, 511, 512])
+def test_posterior_size_boundaries(n):
+    """Training-set sizes at the tile / pass boundaries of the tensor-core posterior (32-column
+    slices, 16-row chunks, one vs two column passes at 256, the 511 limit) and the generic kernel
+    beyond, against the oracle on a numeric space (C3) and a mixed one (C5)."""
+    import oracle
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    for case in ("C3", "C5"):
+        space = scenarios.build_space(case)
+        rng = np.random.default_rng(n * 7 + len(case))
+        sc = Scorer()
+        lay = sc.set_space(space)
+        cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, n + 40, rng))))[:n]
+        if len(cfgs) < n:
+            sc.close()
+            continue
+        y = np.array([scenarios.objective(case, c) for c in cfgs])
+        hyp = Hyper(outputscale=1.3, noise_variance=1e-3,
+                    lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
+        gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+        sc.set_gp(gp)
+        assert sc.gp_kernel() == ("tensor" if n <= 511 else "generic")
+        q = 3 * 128 + 17
+        rows = sc.to_device(scenarios.sample_rows_uniform(lay, q, rng))
+        mean, var = (x.cpu().numpy() for x in sc.predict(rows))
+        sample = lay.decode(rows.cpu().numpy().view(np.uint32))
+        og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
+                             L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
+        m0, v0 = oracle.gp.predict(og, sample)
+        np.testing.assert_allclose(mean, m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
+        np.testing.assert_allclose(var, v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
+        sc.close()
