@@ -107,6 +107,8 @@ struct bx_handle {
   int stream_shift = 0;
   const SummaryArgs* tc_summ = nullptr;    // set while a full-step posterior launch is enqueued
   bool tc_dot = false;                     // centred dot-product distances (bx_set_gp decides)
+  bool tc_dmma = false;                    // ... computed on FP64 DMMA by the producers
+  bool tc_no_dmma = false;                 // BX_TC_NO_DMMA=1: FMA distances
   bool tc_no_dot = false;                  // BX_TC_NO_DOT=1: always the difference form
   DevBuf d_mu;
   bool tc_no_full = true;                  // BX_TC_FULL=1: forest + summary inside the posterior kernel
@@ -282,6 +284,7 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
       t.summ_on = 1;
     }
     t.dot = h->tc_dot ? 1 : 0;
+    t.dmma = h->tc_dmma ? 1 : 0;
     t.mu = h->d_mu.as<double>();
     t.part = h->tc_nsl > 8 ? h->d_tc_part.as<double>() : nullptr;
     t.n_coord = (int32_t)h->coord_host.size();
@@ -343,6 +346,7 @@ bx_handle* bx_create(int device) {
   if (const char* dbg = getenv("BX_TC_DEBUG")) h->tc_debug = atoi(dbg);
   h->tc_trace = getenv("BX_TC_TRACE") != nullptr;
   if (const char* ln = getenv("BX_LML_NARROW")) h->lml_narrow = ln[0] == '1';
+  if (const char* nd = getenv("BX_TC_NO_DMMA")) h->tc_no_dmma = nd[0] == '1';
   const char* fw = getenv("BX_FOREST_WALK");
   h->no_qs_forest = fw && fw[0] == '1';
   // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
@@ -569,8 +573,6 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
     BX_CUDA(h, h->d_rowscale.ensure(2 * 512 * 8));
     if (h->tc_nsl > 8)  // pass-0 partial sums of rows >= 256: [CTA][256 rows][128 candidates]
       BX_CUDA(h, h->d_tc_part.ensure((size_t)h->sm_count * 256 * 128 * 8));
-    BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
-                                 h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), s));
     h->use_tc = true;
     // dot-product distances: all-numeric spaces whose coordinates, centred on the training mean and
     // scaled by 1/l, stay small (|x'|^2 <= 64 for every domain point), so |x'|^2 + |y'|^2 - 2 x'.y'
@@ -609,6 +611,11 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
         h->tc_dot = true;
       }
     }
+    // distances on the FP64 tensor cores when the centred product form holds (and fits)
+    h->tc_dmma = h->tc_dot && D <= 16 && !h->matern_precise && !h->tc_no_dmma &&
+                 tc_smem_bytes(n, D, h->n_kendall, h->row_words, nullptr, false, true) <= 227 * 1024;
+    BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
+                                 h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), h->tc_dmma ? 1 : 0, s));
   }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
   h->outputscale = outputscale;
@@ -1105,7 +1112,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     const bool fuse_rf =
         forest && !(flags & BX_SCORE_RF_PAIRWISE) &&
         (h->use_tc ? qf.enabled && !h->tc_separate_forest &&
-                         tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf) <= 227 * 1024
+                         tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, false, h->tc_dmma) <= 227 * 1024
                    : kf.enabled && !h->no_fused_forest &&
                          fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
                              220 * 1024);
@@ -1116,10 +1123,10 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // the epilogue keeps the summaries (no forest / summary kernels, no EI round trip through HBM).
     const bool tc_full =
         h->use_tc && !h->tc_no_full && partials != nullptr && !(flags & BX_SCORE_RF_PAIRWISE) && !fuse_rf &&
-        (forest ? qf.enabled && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true) <=
+        (forest ? qf.enabled && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true, h->tc_dmma) <=
                                     227 * 1024
                 : !h->has_forest &&
-                      tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, nullptr, true) <= 227 * 1024);
+                      tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, nullptr, true, h->tc_dmma) <= 227 * 1024);
     if (tc_full) {
       h->rf_after_gp = false;
       if (timing) {
@@ -1152,9 +1159,16 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                            h->d_probs.as<double>(), s));
     if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
-    BX_CUDA(h, h->d_ei.ensure((size_t)q * 8));
+    // the posterior writes mean / var and the summary kernel after it evaluates the EI (only for the
+    // candidates whose probability passes eps_f) — the posterior's epilogue is on its critical path
+    BX_CUDA(h, h->d_ei.ensure((size_t)q * 16));
     FusedArgs f = fused_args(h, rows, q, f_model);
-    f.ei_out = h->d_ei.as<double>();
+    if (fuse_rf) {
+      f.ei_out = h->d_ei.as<double>();
+    } else {
+      f.mean_out = h->d_ei.as<double>();
+      f.var_out = h->d_ei.as<double>() + q;
+    }
     if (fuse_rf) {
       if (h->use_tc) f.qs = qf;
       else f.kf = kf;
@@ -1165,6 +1179,11 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
+    if (!fuse_rf) {
+      m.mean = h->d_ei.as<double>();
+      m.var = h->d_ei.as<double>() + q;
+      m.f_model = f_model;
+    }
     if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));  // streaming pool fully copied
     if (rf_summ) {
       if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));

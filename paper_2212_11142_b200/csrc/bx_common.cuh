@@ -24,6 +24,19 @@ constexpr int kRealGrid = 64;          // space.py:23 REAL_NEIGHBOR_GRID
 constexpr double kSqrt5 = 2.23606797749978969640917366873128;  // surrogate.py:35 math.sqrt(5.0)
 constexpr double kInvSqrt2Pi = 0.398942280401432702863218082712;  // acquisition.py:27
 
+// expected_improvement_vec (acquisition.py:40-51) for one candidate; the one definition every
+// kernel uses, so the value does not depend on which kernel evaluates it
+__device__ __forceinline__ double ei_value(double mean, double var, double f_model) {
+  const double sd = sqrt(fmax(var, 0.0));
+  const double delta = f_model - mean;
+  double ei = fmax(delta, 0.0);
+  if (sd > 0.0) {
+    const double z = delta / sd;
+    ei = delta * normcdf(z) + sd * (kInvSqrt2Pi * exp(-0.5 * z * z));
+  }
+  return fmax(ei, 0.0);
+}
+
 // ---- device-resident state owned by a handle -------------------------------------------------
 
 struct SpaceDev {
@@ -382,6 +395,10 @@ struct SummaryArgs {
   int64_t q;
   int64_t index_base;
   const double* ei;
+  // mean != NULL: the posterior wrote mean / var instead of the EI, computed here with ei_value
+  const double* mean;
+  const double* var;
+  double f_model;
   const double* probs_in;  // NULL -> constant / no forest
   int32_t use_forest;
   int32_t has_trees;
@@ -427,6 +444,9 @@ struct TcArgs {
   // n > 255 (two passes per tile): [grid][256 rows][128 candidates] pass-0 partial sums of the
   // rows >= 256, written and read back by the same epilogue thread; null otherwise
   double* part;
+  // dmma != 0 (centred all-numeric spaces): producers compute the distances on FP64 DMMA and the
+  // matrix digits carry the C-fragment column permutation (launch_build_mdig perm)
+  int32_t dmma;
 };
 
 
@@ -439,10 +459,10 @@ cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncol
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
 size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs = nullptr,
-                     bool summ = false);
+                     bool summ = false, bool dmma = false);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
-                              double* rowscale, cudaStream_t s);
+                              double* rowscale, int perm, cudaStream_t s);
 cudaError_t launch_gp_tc(const TcArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_summary(const SummaryArgs& a, int sm_count, cudaStream_t s, int* n_partials);
 int summary_max_partials(int sm_count);

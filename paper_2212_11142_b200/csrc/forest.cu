@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
           }
       }
       prob = __ddiv_rn(sum, (double)f.n_trees);
-      value = (prob < a.eps_f) ? -INFINITY : a.ei[i] * prob;
+      value = (prob < a.eps_f) ? -INFINITY : (a.mean ? ei_value(a.mean[i], a.var[i], a.f_model) : a.ei[i]) * prob;
       if (a.values_out) a.values_out[i] = value;
       if (a.probs_out) a.probs_out[i] = prob;
     }

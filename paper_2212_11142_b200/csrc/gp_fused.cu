@@ -375,16 +375,7 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
         const double var = (a.gp.y_std * a.gp.y_std) * var_s;
         if (a.mean_out) a.mean_out[gi] = mean;
         if (a.var_out) a.var_out[gi] = var;
-        if (a.ei_out) {
-          const double s = sqrt(fmax(var, 0.0));  // acquisition.py:40-51
-          const double delta = a.f_model - mean;
-          double ei = fmax(delta, 0.0);
-          if (s > 0.0) {
-            const double z = delta / s;
-            ei = delta * normcdf(z) + s * (kInvSqrt2Pi * exp(-0.5 * z * z));
-          }
-          a.ei_out[gi] = fmax(ei, 0.0);
-        }
+        if (a.ei_out) a.ei_out[gi] = ei_value(mean, var, a.f_model);  // acquisition.py:40-51
       }
     }
     __syncwarp();

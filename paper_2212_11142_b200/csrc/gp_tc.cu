@@ -180,6 +180,17 @@ __device__ __forceinline__ unsigned long long kstar_fixed(double W, const Matern
   return (unsigned long long)__double_as_longlong(X) & 0xFFFFFFFFFFull;
 }
 
+// FP64 tensor-core MMA m8n8k4: lane holds A[lane/4][lane%4], B[lane%4][lane/4], C[lane/4][2(lane%4)+{0,1}]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+// 16 TMEM lanes x 8 columns, the mma C-fragment layout: thread t writes lanes t/4 and t/4 + 8,
+// columns 2 (t%4) and 2 (t%4) + 1 (v = {lane t/4: col, col+1; lane t/4+8: col, col+1})
+__device__ __forceinline__ void tmem_st_16x256(uint32_t addr, uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v0), "r"(v1),
+               "r"(v2), "r"(v3) : "memory");
+}
 __device__ __forceinline__ void tmem_st1(uint32_t addr, uint32_t v0) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(addr), "r"(v0) : "memory");
 }
@@ -205,9 +216,13 @@ __host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
   return o;
 }
 
+// dmma (the FP64-tensor distance producers, centred numeric spaces): the planes hold the augmented
+// B operand, 4 * ceil((n_params + 2) / 4) rows (-2 y', |y'|^2, 1, zero padding)
+__host__ __device__ constexpr int tc_dmma_rows(int n_params) { return (n_params + 2 + 3) / 4 * 4; }
+
 __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words,
                                               const QsForestDev* qs = nullptr, bool summ = false,
-                                              bool resident = false) {
+                                              bool resident = false, bool dmma = false) {
   const bool rf = qs && qs->enabled;
   const int nsl = (n + 31) / 32, npad = 32 * nsl;
   TcLayout L;
@@ -215,8 +230,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   L.par = off;
   off += n_params * (int)sizeof(bx_param_desc);
   off = (off + 15) & ~15;
-  L.planes = off;  // [n_params][npad], zero-padded beyond n
-  off += n_params * npad * 8;
+  L.planes = off;  // [n_params (dmma: tc_dmma_rows)][npad], zero-padded beyond n
+  off += (dmma ? tc_dmma_rows(n_params) : n_params) * npad * 8;
   L.kmask = off;   // [n_kendall][npad][2]
   off += n_kendall * npad * 16;
   L.cval = off;    // [2][n_params][128] decoded candidate values (tile parity)
@@ -260,7 +275,7 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
 
 // ND > 0: all-numeric space with exactly ND parameters — the distance loop is unrolled at compile
 // time and the candidate coordinates stay in registers for the whole tile.  ND == 0: any space.
-template <bool kPrecise, int ND>
+template <bool kPrecise, int ND, bool kDmma = false>
 __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const FusedArgs& a = ta.f;
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
   const QsForestDev& qf = a.qs;
   const bool rf = qf.enabled != 0;
   const bool resident = ta.mat_resident != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0, resident);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0, resident, kDmma);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -324,6 +339,13 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
     __syncthreads();  // then the planes hold -2 y' (exact), so W = |x'|^2 + |y'|^2 + sum x' (-2 y')
     for (int i = tid; i < (ND > 0 ? n_params * npad : 0); i += blockDim.x)
       planes[i] = (uint64_t)__double_as_longlong(-2.0 * __longlong_as_double((long long)planes[i]));
+    if constexpr (kDmma) {  // augmented rows: |y'|^2 (times the candidate's 1), 1 (times |x'|^2), zeros
+      for (int i = tid; i < (tc_dmma_rows(ND) - ND) * npad; i += blockDim.x) {
+        const int r = ND + i / npad, j = i % npad;
+        const double v = r == ND ? s_yy[j] : (r == ND + 1 ? 1.0 : 0.0);
+        planes[(size_t)r * npad + j] = (uint64_t)__double_as_longlong(v);
+      }
+    }
   }
   for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
     const int kk = i / npad, j = i % npad;
@@ -709,26 +731,8 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         const double var = (a.gp.y_std * a.gp.y_std) * var_s;
         if (a.mean_out) a.mean_out[gi] = mean;
         if (a.var_out) a.var_out[gi] = var;
-        if (a.ei_out) {
-          const double sd = sqrt(fmax(var, 0.0));  // acquisition.py:40-51
-          const double delta = a.f_model - mean;
-          double ei = fmax(delta, 0.0);
-          if (sd > 0.0) {
-            const double z = delta / sd;
-            ei = delta * normcdf(z) + sd * (kInvSqrt2Pi * exp(-0.5 * z * z));
-          }
-          a.ei_out[gi] = fmax(ei, 0.0);
-        }
-        if (ta.summ_on) {
-          const double sd = sqrt(fmax(var, 0.0));
-          const double delta = a.f_model - mean;
-          double ei = fmax(delta, 0.0);
-          if (sd > 0.0) {
-            const double z = delta / sd;
-            ei = delta * normcdf(z) + sd * (kInvSqrt2Pi * exp(-0.5 * z * z));
-          }
-          ei_c = fmax(ei, 0.0);
-        }
+        if (a.ei_out) a.ei_out[gi] = ei_value(mean, var, a.f_model);  // acquisition.py:40-51
+        if (ta.summ_on) ei_c = ei_value(mean, var, a.f_model);
       }
       if (ta.summ_on) {
         // acquisition value and the warp's partial summary (the logic of summary_kernel)
@@ -784,6 +788,114 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       const int32_t* src = reinterpret_cast<const int32_t*>(&s_parts[0]);
       int32_t* dst = reinterpret_cast<int32_t*>(sa.partials + blockIdx.x);
       for (int i = r; i < (int)(sizeof(Partial) / 4); i += 128) dst[i] = src[i];
+    }
+  } else if (kDmma && warp >= 8) {
+    // ---- K* producers, FP64 tensor-core distances (centred all-numeric spaces) ---------------
+    // Warp (quarter q, half h) owns candidates 32 q + 16 h + 0..15 (TMEM lanes of its quarter) and
+    // every column of a slice.  W = |x'|^2 + |y'|^2 + x'.(-2 y') is one augmented product
+    // [x', 1, |x'|^2] . [-2 y'; |y'|^2; 1] on DMMA m8n8k4 (2 row blocks x 4 column blocks x KS
+    // k-steps per slice), so the distance costs 24 MMA instructions instead of 176 FMAs + 88 shared
+    // loads per thread; the Matérn runs on the C fragments and the digits go to TMEM with the
+    // matching 16x256b store.  Within a slice the K order is permuted so that each thread's C
+    // columns are 8 consecutive K bytes: K byte 8 t0 + 4 hh + 2 jj + e <- column 8 (2 hh + jj) + 2 t0 + e
+    // (mdig_kernel builds the matrix digits with the same permutation).
+    constexpr int KS = tc_dmma_rows(ND > 0 ? ND : 1) / 4;
+    const int pt = tid - 8 * 32;
+    const int quarter = warp & 3, half = (warp - 8) >> 2;
+    const int t0 = lane & 3, t1 = lane >> 2;
+    const uint32_t lane_base = (uint32_t)(quarter * 32 + half * 16) << 16;
+    const double sigma = a.gp.outputscale;
+    const MaternConst mc{sigma * ta.kscale, sigma * kSqrt5 * ta.kscale, sigma * (5.0 / 3.0) * ta.kscale};
+    uint32_t slot_used = 0, slot_par = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      if (pt == 0) TC_TRACE(0, 1, t);
+      const int cb = t & 1;
+      mb_wait(&cval_full[cb], (uint32_t)((t >> 1) & 1));
+      const uint64_t* cv = cval + (size_t)cb * n_params * kM;
+      if (pt == 0) TC_TRACE(0, 2, t);
+      // A fragments: row = candidate 32 q + 16 h + 8 rb + t1, k = t0 + 4 kk of [x', 1, |x'|^2, 0..]
+      double afr[2][KS];
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        const int c = quarter * 32 + half * 16 + 8 * rb + t1;
+        double xx = 0.0;
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+          const double x = __longlong_as_double((long long)cv[k * kM + c]);
+          xx = fma(x, x, xx);
+        }
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = t0 + 4 * kk;
+          afr[rb][kk] = k < ND ? __longlong_as_double((long long)cv[(k < ND ? k : 0) * kM + c])
+                               : (k == ND ? 1.0 : (k == ND + 1 ? xx : 0.0));
+        }
+      }
+      for (int p = 0; p < npass; ++p) {
+      const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));
+      const int soff = p == 0 ? 0 : kSlots - (hi - lo);
+      for (int ks = hi - 1; ks >= lo; --ks) {
+        const int slot = ks - lo + soff;
+        const int j0 = 32 * ks;
+        double acc[2][4][2];
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[rb][j][0] = acc[rb][j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const double* brow = reinterpret_cast<const double*>(planes) + (size_t)(t0 + 4 * kk) * npad + j0 + t1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double b = brow[8 * j];  // B[k = t0 + 4 kk][column 8 j + t1]
+            dmma884(acc[0][j][0], acc[0][j][1], afr[0][kk], b);
+            dmma884(acc[1][j][0], acc[1][j][1], afr[1][kk], b);
+          }
+        }
+        // acc[rb][j][e] = W(candidate row rb, column 8 j + 2 t0 + e) -> K byte 8 t0 + 4 (j / 2) + 2 (j % 2) + e
+        uint32_t dw[kDB][4];  // [digit][rb * 2 + hh]
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t lo4[4], hi4[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const unsigned long long X = kstar_fixed(fabs(acc[rb][2 * hh + (v >> 1)][v & 1]), mc, s_exp2);
+              lo4[v] = (uint32_t)X;
+              hi4[v] = (uint32_t)(X >> 32);
+            }
+            const uint32_t p01 = __byte_perm(lo4[0], lo4[1], 0x5140), p23 = __byte_perm(lo4[2], lo4[3], 0x5140);
+            const uint32_t q01 = __byte_perm(lo4[0], lo4[1], 0x7362), q23 = __byte_perm(lo4[2], lo4[3], 0x7362);
+            const uint32_t h01 = __byte_perm(hi4[0], hi4[1], 0x5140), h23 = __byte_perm(hi4[2], hi4[3], 0x5140);
+            dw[0][rb * 2 + hh] = __byte_perm(h01, h23, 0x5410);
+            dw[1][rb * 2 + hh] = __byte_perm(q01, q23, 0x7632);
+            dw[2][rb * 2 + hh] = __byte_perm(q01, q23, 0x5410);
+            dw[3][rb * 2 + hh] = __byte_perm(p01, p23, 0x7632);
+            dw[4][rb * 2 + hh] = __byte_perm(p01, p23, 0x5410);
+          }
+        if (pt == 0) TC_TRACE(0, 3, ks);
+        if ((slot_used >> slot) & 1u) {
+          mb_wait(&slice_empty[slot], (slot_par >> slot) & 1u);
+          slot_par ^= 1u << slot;
+          tc_fence_after();
+        }
+        slot_used |= 1u << slot;
+        if (pt == 0) TC_TRACE(0, 4, ks);
+#pragma unroll
+        for (int b = 0; b < kDB; ++b)
+          tmem_st_16x256(tmem + lane_base + (uint32_t)(kDigCol0 + slot * kSliceCols + b * 8), dw[b][0], dw[b][1],
+                         dw[b][2], dw[b][3]);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mb_arrive(cand_full);
+        if (p == npass - 1) mb_arrive(&cval_free[cb]);
+      }
+      }
+      if (pt == 0) TC_TRACE(0, 6, t);
     }
   } else if (warp >= 8) {
     // ---- K* producers ------------------------------------------------------------------------
@@ -1007,15 +1119,18 @@ __global__ void row_scale_kernel(const double* A, int lda, int n, double sc, dou
 }
 
 // [chunk][slice][digit][32 rows x 32 columns, K-major] balanced base-256 digits of A
+// perm: K byte kb of a slice holds column 8 (2 hh + jj) + 2 t0 + e, kb = 8 t0 + 4 hh + 2 jj + e (the
+// C-fragment order of the DMMA producers)
 __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, const double* rowscale,
-                            unsigned char* mdig) {
+                            unsigned char* mdig, int perm) {
   const int64_t total = (int64_t)nch * nsl * kN * 32;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int kb = (int)(t & 31), r = (int)((t >> 5) & (kN - 1));
     const int blk = (int)(t / (kN * 32));
     const int ks = blk % nsl, c = blk / nsl;
-    const int row = c * kN + r, col = ks * 32 + kb;
+    const int kc = perm ? 8 * (2 * ((kb >> 2) & 1) + ((kb >> 1) & 1)) + 2 * (kb >> 3) + (kb & 1) : kb;
+    const int row = c * kN + r, col = ks * 32 + kc;
     const double x = (row <= n && col < n) ? A[(size_t)row * lda + col] : 0.0;
     long long X = __double2ll_rn(x * rowscale[kMaxChunks * kN + row]);
     unsigned char* out = mdig + (size_t)blk * kMatBlock + kmaj(r, kb);
@@ -1031,8 +1146,9 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 }  // namespace
 
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs, bool summ) {
-  return tc_layout(n, n_params, n_kendall, row_words, qs, summ).total;
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs, bool summ,
+                     bool dmma) {
+  return tc_layout(n, n_params, n_kendall, row_words, qs, summ, false, dmma).total;
 }
 
 size_t tc_mdig_bytes(int n) {
@@ -1042,34 +1158,36 @@ size_t tc_mdig_bytes(int n) {
 
 // rowscale must hold 2 * 512 doubles (epilogue factors, then digit scales)
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
-                              double* rowscale, cudaStream_t s) {
+                              double* rowscale, int perm, cudaStream_t s) {
   const int nsl = (n + 31) / 32, nch = n / kN + 1;
   if (nch > kMaxChunks) return cudaErrorInvalidValue;
   row_scale_kernel<<<kMaxChunks * kN, 32, 0, s>>>(A, lda, n, sc, rowscale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  mdig_kernel<<<148, 256, 0, s>>>(A, lda, n, nsl, nch, rowscale, mdig);
+  mdig_kernel<<<148, 256, 0, s>>>(A, lda, n, nsl, nch, rowscale, mdig, perm);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   TcArgs a = a0;
+  const bool dmma = a.dmma != 0;
   // matrix digits resident in shared memory when they fit (BX_TC_DEBUG bit 8: always the ring)
   a.mat_resident = 0;
   if (!(a.debug & 8) && tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
-                                  a.summ_on != 0, true).total <= 227 * 1024)
+                                  a.summ_on != 0, true, dmma).total <= 227 * 1024)
     a.mat_resident = 1;
   const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
-                               a.summ_on != 0, a.mat_resident != 0);
+                               a.summ_on != 0, a.mat_resident != 0, dmma);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
   // all-numeric spaces with up to 16 parameters get the unrolled distance loop
   const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;
   if (a.dot && !numeric) return cudaErrorInvalidValue;  // the host enables dot only for these
+  if (dmma && !(a.dot && numeric && a.f.n_num <= 16)) return cudaErrorInvalidValue;
   const int nd = numeric ? a.f.n_num : 0;
   auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
   switch (nd) {
 #define BX_ND(d) \
-    case d: kernel = gp_tc_kernel<false, d>; break;
+    case d: kernel = dmma ? gp_tc_kernel<false, d, true> : gp_tc_kernel<false, d>; break;
     BX_ND(1) BX_ND(2) BX_ND(3) BX_ND(4) BX_ND(5) BX_ND(6) BX_ND(7) BX_ND(8)
     BX_ND(9) BX_ND(10) BX_ND(11) BX_ND(12) BX_ND(13) BX_ND(14) BX_ND(15) BX_ND(16)
 #undef BX_ND

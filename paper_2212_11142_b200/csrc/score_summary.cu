@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kSumThreads) summary_kernel(SummaryArgs a) {
     const bool valid = gi < a.q;
     double value = -INFINITY, prob = -INFINITY;
     if (valid) {
-      const double ei = a.ei[gi];
+      const double ei = a.mean ? ei_value(a.mean[gi], a.var[gi], a.f_model) : a.ei[gi];
       if (a.use_forest) {
         prob = a.has_trees ? a.probs_in[gi] : a.constant;
         value = (prob < a.eps_f) ? -INFINITY : ei * prob;
