@@ -274,3 +274,22 @@ def test_posterior_size_boundaries(n):
         np.testing.assert_allclose(mean, m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
         np.testing.assert_allclose(var, v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
         sc.close()
+
+
+def test_dmma_distances_match_fma_distances(c3, monkeypatch):
+    """The posterior's DMMA distance producers (augmented [x',1,|x'|^2].[-2y';|y'|^2;1] product,
+    permuted matrix K order) against the FMA producers (BX_TC_NO_DMMA=1) on 2^18 C3 candidates:
+    the two differ only in the rounding of W, far inside the 1e-5 parity bar."""
+    from paper_2212_11142_b200.device import Scorer
+    sc0, meta, arr, space, gp, feas, rows_h = c3
+    out = []
+    for no_dmma in (False, True):
+        if no_dmma:
+            monkeypatch.setenv("BX_TC_NO_DMMA", "1")
+        sc = Scorer()
+        sc.set_gp(gp)
+        mean, var = sc.predict(sc.to_device(rows_h[: 1 << 18]))
+        out.append((mean.cpu().numpy(), var.cpu().numpy()))
+        sc.close()
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-9, atol=1e-12 * np.abs(out[1][0]).max())
+    np.testing.assert_allclose(out[0][1], out[1][1], rtol=1e-7, atol=1e-12 * np.abs(out[1][1]).max())
