@@ -65,7 +65,7 @@ struct bx_handle {
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
   DevBuf d_knodes, d_kvid, d_kuval;
-  DevBuf d_qmask, d_qvid, d_quval, d_qsoff;
+  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub;
   bool no_fused_forest = true;   // DMMA kernel: BX_FOREST_FUSED=1 walks the forest inside it
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
@@ -391,7 +391,7 @@ void bx_destroy(bx_handle* h) {
                     &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
                     &h->d_knodes, &h->d_kvid, &h->d_kuval, &h->d_qmask, &h->d_qvid,
-                    &h->d_quval, &h->d_qsoff};
+                    &h->d_quval, &h->d_qsoff, &h->d_qcode_param, &h->d_qcode_sub};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < bx_handle::kHostBufs; ++i) {
@@ -849,6 +849,54 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
         }
       }
     }
+    // one code per categorical parameter instead of one per one-hot feature: the mask of label L
+    // is the AND over the parameter's one-hot codes of their masks at [L == sub] (fewer table
+    // loads per candidate: one per parameter and tree)
+    std::vector<int32_t> qparam, qsub, qsoff, qrange;
+    if (ok) {
+      std::vector<int> merged(h->n_params, -1);
+      for (int c = 0; c < S; ++c) {
+        const bx_param_desc& p = h->params[code_param[c]];
+        if (p.kind == BX_CATEGORICAL) {
+          if (merged[code_param[c]] >= 0) continue;
+          merged[code_param[c]] = (int)qparam.size();
+          qparam.push_back(code_param[c]);
+          qsub.push_back(-1);
+          qrange.push_back(p.size);
+        } else {
+          qparam.push_back(code_param[c]);
+          qsub.push_back(code_sub[c]);
+          qrange.push_back(range[c]);
+        }
+      }
+      int stride2 = 0;
+      for (size_t c = 0; c < qparam.size(); ++c) {
+        qsoff.push_back(stride2);
+        stride2 += qrange[c];
+      }
+      ok = (size_t)T * stride2 * 8 <= 160 * 1024;
+      if (ok) {
+        std::vector<uint64_t> m2((size_t)T * stride2, ~0ull);
+        for (int t = 0; t < T; ++t) {
+          size_t c2 = 0;
+          for (int c = 0; c < S; ++c) {
+            const bx_param_desc& p = h->params[code_param[c]];
+            if (p.kind == BX_CATEGORICAL) {
+              const int mc = merged[code_param[c]];
+              for (int L = 0; L < p.size; ++L)
+                m2[(size_t)t * stride2 + qsoff[mc] + L] &=
+                    mask[(size_t)t * stride + soff[c] + (L == code_sub[c] ? 1 : 0)];
+            } else {
+              while (qparam[c2] != code_param[c] || qsub[c2] != code_sub[c]) ++c2;
+              for (int v = 0; v < range[c]; ++v)
+                m2[(size_t)t * stride2 + qsoff[c2] + v] = mask[(size_t)t * stride + soff[c] + v];
+            }
+          }
+        }
+        mask.swap(m2);
+        stride = stride2;
+      }
+    }
     if (ok) {
       if (uval.empty()) uval.push_back(0.0);
       // transpose to [slot value][tree] so a group of 8 trees is one 64-byte run per slot
@@ -863,15 +911,17 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       BX_CUDA(h, upload(h->d_qmask, mask.data(), mask.size()));
       BX_CUDA(h, upload(h->d_qvid, vid.data(), vid.size()));
       BX_CUDA(h, upload(h->d_quval, uval.data(), uval.size()));
-      BX_CUDA(h, upload(h->d_qsoff, soff.data(), soff.size()));
+      BX_CUDA(h, upload(h->d_qsoff, qsoff.data(), qsoff.size()));
+      BX_CUDA(h, upload(h->d_qcode_param, qparam.data(), qparam.size()));
+      BX_CUDA(h, upload(h->d_qcode_sub, qsub.data(), qsub.size()));
       qs.mask = h->d_qmask.as<uint64_t>();
       qs.vid = h->d_qvid.as<uint16_t>();
       qs.uval = h->d_quval.as<double>();
       qs.soff = h->d_qsoff.as<int32_t>();
-      qs.code_param = cf.code_param;
-      qs.code_sub = cf.code_sub;
+      qs.code_param = h->d_qcode_param.as<int32_t>();
+      qs.code_sub = h->d_qcode_sub.as<int32_t>();
       qs.n_trees = T;
-      qs.n_codes = S;
+      qs.n_codes = (int)qparam.size();
       qs.stride = stride;
       qs.n_uvals = (int)uval.size();
       qs.enabled = h->no_qs_forest ? 0 : 1;

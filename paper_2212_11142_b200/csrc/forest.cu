@@ -213,7 +213,9 @@ __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t saddr) {
 
 __device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* row, int sub) {
   if (p.kind == BX_PERMUTATION) return perm_pos(row_u64(row, p.word), p.size, sub);
-  if (p.kind == BX_CATEGORICAL) return (int)row[p.word] == sub ? 1 : 0;
+  // sub < 0: one code for the whole categorical parameter (its label index; the per-label masks
+  // are the ANDs of the one-hot features' masks), else the one-hot feature [label == sub]
+  if (p.kind == BX_CATEGORICAL) return sub < 0 ? (int)row[p.word] : ((int)row[p.word] == sub ? 1 : 0);
   return (int)row[p.word];
 }
 

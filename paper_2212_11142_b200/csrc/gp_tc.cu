@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
             if (p.kind == BX_PERMUTATION)
               v = perm_pos((uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32), p.size, qf.code_sub[sl]);
             else if (p.kind == BX_CATEGORICAL)
-              v = (int)word(p.word) == qf.code_sub[sl] ? 1 : 0;
+              v = qf.code_sub[sl] < 0 ? (int)word(p.word) : ((int)word(p.word) == qf.code_sub[sl] ? 1 : 0);
             else
               v = (int)word(p.word);
           }
