@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         // two passes (n > 255): rows >= 256 park their pass-0 partial sums in this CTA's scratch
         // ([256 rows][128 candidates], coalesced per row) and add them back in pass 1
         const int mode = (npass == 1 || c < 2 * kSlots) ? 0 : (p == 0 ? 1 : 2);
-        double* park = ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r;  // + (row - 256) * kM
+        double* park = mode ? ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r : nullptr;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
         mb_wait_sleep(&acc_full[buf], (ph_f >> buf) & 1u);
         ph_f ^= 1u << buf;
