@@ -180,7 +180,8 @@ int bx_set_constraints(bx_handle* h, int32_t n_constraints, const int32_t* host_
 enum bx_score_flags {
   BX_SCORE_RF_PAIRWISE = 1,   /* numpy pairwise-8 tree sum (what predict_proba does at q == 1) */
   BX_SCORE_NO_SUMMARY = 2,    /* skip the top-k / tracker reduction                             */
-  BX_SCORE_TIMING = 4         /* record per-kernel CUDA-event durations (bx_last_timing)        */
+  BX_SCORE_TIMING = 4,        /* record per-kernel CUDA-event durations (bx_last_timing)        */
+  BX_SCORE_TIMING_POSTERIOR = 8  /* time the posterior kernel only (two events; rf / merge = -1) */
 };
 
 /* Durations (ms, CUDA events on the call's stream) of the forest, fused-score and merge kernels

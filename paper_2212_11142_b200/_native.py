@@ -33,6 +33,7 @@ EXPORTED = (
     "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel",
 )
 BX_SCORE_TIMING = 4
+BX_SCORE_TIMING_POSTERIOR = 8
 
 
 class ParamDesc(C.Structure):

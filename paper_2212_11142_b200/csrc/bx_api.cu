@@ -1133,7 +1133,7 @@ static SummaryArgs last_summary_args(bx_handle* h, const uint32_t* rows, int64_t
 static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
                       double f_model, double eps_f, int32_t k, int32_t flags, double* values,
                       double* probs_out, Partial* partials, int* n_partials, cudaStream_t s,
-                      bool timing, bool track_prob = false, cudaEvent_t rows_ready = nullptr) {
+                      int timing, bool track_prob = false, cudaEvent_t rows_ready = nullptr) {
   ScoreArgs a{};
   a.space = space_dev(h);
   a.gp = gp_dev(h);
@@ -1204,11 +1204,11 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     h->rf_after_gp = rf_summ;
     // a stand-alone forest kernel before the posterior reads the rows: a streaming pool must be in
     if (rows_ready && forest && !fuse_rf && !rf_summ) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
-    if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+    if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
     if (forest && !fuse_rf && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                            h->d_probs.as<double>(), s));
-    if (timing && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+    if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
     // the posterior writes mean / var and the summary kernel after it evaluates the EI (only for the
     // candidates whose probability passes eps_f) — the posterior's epilogue is on its critical path
     BX_CUDA(h, h->d_ei.ensure((size_t)q * 16));
@@ -1236,21 +1236,21 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     }
     if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));  // streaming pool fully copied
     if (rf_summ) {
-      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+      if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
       BX_CUDA(h, launch_rf_summary(a.space, h->forest, m, h->sm_count, s, n_partials));
-      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+      if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
       return BX_OK;
     }
     BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));
     return BX_OK;
   }
-  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
+  if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
   if (forest) {
     BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                          h->d_probs.as<double>(), s));
     a.probs_in = h->d_probs.as<double>();
   }
-  if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
+  if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
   if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
   BX_CUDA(h, launch_score(a, h->sm_count, s, n_partials));
   if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
@@ -1267,7 +1267,7 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool want = !(flags & BX_SCORE_NO_SUMMARY) && summary != nullptr;
-  const bool timing = (flags & BX_SCORE_TIMING) != 0;
+  const int timing = (flags & BX_SCORE_TIMING) ? 1 : ((flags & BX_SCORE_TIMING_POSTERIOR) ? 2 : 0);
   Partial* partials = nullptr;
   if (want) {
     BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
@@ -1281,18 +1281,18 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
   if (want) {
     BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
-    if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
+    if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
     BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
                                cudaMemcpyDeviceToHost, s));
-  } else if (timing) {
+  } else if (timing == 1) {
     BX_CUDA(h, cudaEventRecord(h->ev_t[4], s));
   }
   if (want || timing) BX_CUDA(h, cudaStreamSynchronize(s));
   if (want && summary->n_finite == 0 && fused_path(h)) {
     // every value is -inf: only now is the probability tracker needed (acquisition.py:179-184)
     // rerun the step with the tracker on (it is the only rare path, so no state is kept for it)
-    r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_TIMING, values, probs, partials,
-                   &np, s, false, true);
+    r = score_impl(h, rows, q, index_base, f_model, eps_f, k, flags & ~(BX_SCORE_TIMING | BX_SCORE_TIMING_POSTERIOR),
+                   values, probs, partials, &np, s, 0, true);
     if (r) return r;
     BX_CUDA(h, launch_summary_merge(partials, np, space_dev(h), k, rows, index_base,
                                     h->d_summary.as<bx_score_summary>(), s));
@@ -1300,10 +1300,13 @@ int bx_score(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, 
                                cudaMemcpyDeviceToHost, s));
     BX_CUDA(h, cudaStreamSynchronize(s));
   }
-  if (timing) {
+  if (timing == 1) {
     cudaEventElapsedTime(&h->t_ms[0], h->ev_t[0], h->ev_t[1]);
     cudaEventElapsedTime(&h->t_ms[1], h->ev_t[2], h->ev_t[3]);
     cudaEventElapsedTime(&h->t_ms[2], h->rf_after_gp ? h->ev_t[1] : h->ev_t[3], h->ev_t[4]);
+  } else if (timing == 2) {  // the posterior only: the other kernels run back to back, unobserved
+    cudaEventElapsedTime(&h->t_ms[1], h->ev_t[2], h->ev_t[3]);
+    h->t_ms[0] = h->t_ms[2] = -1.0f;
   }
   return BX_OK;
 }

@@ -203,10 +203,11 @@ class Scorer:
 
     def score(self, rows: torch.Tensor, f_model: float, eps_f: float = 0.0, k: int = 10,
               want_values: bool = False, summary: bool = True, rf_pairwise: bool | None = None,
-              index_base: int = 0, timing: bool = False):
-        """bx_score over device rows.  Returns (Summary | None, values | None, probs | None)."""
+              index_base: int = 0, timing: bool | str = False):
+        """bx_score over device rows.  Returns (Summary | None, values | None, probs | None).
+        timing=True records every kernel's duration, timing="posterior" only the posterior's."""
         q = rows.shape[0]
-        flags = N.BX_SCORE_TIMING if timing else 0
+        flags = N.BX_SCORE_TIMING_POSTERIOR if timing == "posterior" else (N.BX_SCORE_TIMING if timing else 0)
         if rf_pairwise if rf_pairwise is not None else q == 1:
             flags |= N.BX_SCORE_RF_PAIRWISE
         if not summary:
