@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
       for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         if (chunk_no >= 2) {
-          mb_wait_sleep(&acc_empty[buf], (ph_e >> buf) & 1u);
+          mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
           ph_e ^= 1u << buf;
           tc_fence_after();
         }
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
         const int mode = (npass == 1 || c < 2 * kSlots) ? 0 : (p == 0 ? 1 : 2);
         double* park = mode ? ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r : nullptr;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
-        mb_wait_sleep(&acc_full[buf], (ph_f >> buf) & 1u);
+        mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);  // the MMA / epilogue chain paces the kernel: spin
         ph_f ^= 1u << buf;
         tc_fence_after();
         if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
