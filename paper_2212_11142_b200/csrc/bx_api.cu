@@ -925,6 +925,10 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       qs.stride = stride;
       qs.n_uvals = (int)uval.size();
       qs.enabled = h->no_qs_forest ? 0 : 1;
+      if (getenv("BX_QS_INFO"))  // development aid: table geometry
+        fprintf(stderr, "qs: trees %d codes %d stride %d tpad %d uvals %d masks %zu B summary smem %zu B\n", T,
+                qs.n_codes, stride, tpad, qs.n_uvals, (size_t)stride * tpad * 8,
+                (size_t)qs_summary_smem_bytes(qs));
     }
   }
 

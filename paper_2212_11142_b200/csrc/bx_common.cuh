@@ -476,6 +476,7 @@ cudaError_t launch_partial_merge(const Partial* partials, int n_partials, const 
 cudaError_t launch_summary_merge(const Partial* partials, int n_partials, const SpaceDev& space,
                                  int k, const uint32_t* pool_rows, int64_t index_base,
                                  bx_score_summary* out, cudaStream_t s);
+size_t qs_summary_smem_bytes(const QsForestDev& q);
 bool qs_summary_available(const ForestDev& f);
 cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
                               cudaStream_t s, int* n_partials);

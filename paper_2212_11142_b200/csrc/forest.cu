@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
   uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + off);
   off += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + off);
-  off += (size_t)f.n_codes * kQsThreads * 4;
+  if constexpr (NC == 0) off += (size_t)f.n_codes * kQsThreads * 4;
   Partial* parts = reinterpret_cast<Partial*>(smem + ((off + 15) & ~(size_t)15));  // [warps]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
@@ -459,11 +459,18 @@ auto pick_real(bool real) {
   return real ? rf_coded_kernel<SMEM, true> : rf_coded_kernel<SMEM, false>;
 }
 
+// code counts up to kQsMaxNC keep each thread's table offsets in registers (no offset array)
+constexpr int kQsMaxNC = 24;
+
 size_t qs_summary_smem(const QsForestDev& f) {
-  return ((qs_smem(f) + 15) & ~(size_t)15) + (size_t)(kQsThreads / 32) * sizeof(Partial);
+  const size_t offs = f.n_codes > kQsMaxNC ? (size_t)f.n_codes * kQsThreads * 4 : 0;
+  return ((qs_smem(f) - (size_t)f.n_codes * kQsThreads * 4 + offs + 15) & ~(size_t)15) +
+         (size_t)(kQsThreads / 32) * sizeof(Partial);
 }
 
 }  // namespace
+
+size_t qs_summary_smem_bytes(const QsForestDev& q) { return qs_summary_smem(q); }
 
 bool qs_summary_available(const ForestDev& f) {
   return f.coded && f.has_trees && f.qs.enabled && qs_summary_smem(f.qs) <= 227 * 1024;
@@ -480,9 +487,11 @@ cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const S
     case c: kern = rf_qs_summary_kernel<c>; break;
     BX_NC(1) BX_NC(2) BX_NC(3) BX_NC(4) BX_NC(5) BX_NC(6) BX_NC(7) BX_NC(8)
     BX_NC(9) BX_NC(10) BX_NC(11) BX_NC(12) BX_NC(13) BX_NC(14) BX_NC(15) BX_NC(16)
+    BX_NC(17) BX_NC(18) BX_NC(19) BX_NC(20) BX_NC(21) BX_NC(22) BX_NC(23) BX_NC(24)
 #undef BX_NC
     default: break;
   }
+  static_assert(kQsMaxNC == 24, "instantiate rf_qs_summary_kernel<1..kQsMaxNC>");
   cudaError_t e = set_smem(kern, (int)bytes);
   if (e != cudaSuccess) return e;
   int64_t blocks = (a.q + kQsThreads - 1) / kQsThreads;
