@@ -65,7 +65,7 @@ struct bx_handle {
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
   DevBuf d_knodes, d_kvid, d_kuval;
-  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub;
+  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub, d_qrthr;
   bool no_fused_forest = true;   // DMMA kernel: BX_FOREST_FUSED=1 walks the forest inside it
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
@@ -391,7 +391,7 @@ void bx_destroy(bx_handle* h) {
                     &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
                     &h->d_knodes, &h->d_kvid, &h->d_kuval, &h->d_qmask, &h->d_qvid,
-                    &h->d_quval, &h->d_qsoff, &h->d_qcode_param, &h->d_qcode_sub};
+                    &h->d_quval, &h->d_qsoff, &h->d_qcode_param, &h->d_qcode_sub, &h->d_qrthr};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int i = 0; i < bx_handle::kHostBufs; ++i) {
@@ -795,13 +795,42 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
   // QuickScorer tables (QsForestDev): integer splits only, <= 64 leaves per tree
   QsForestDev& qs = h->forest.qs;
   qs = QsForestDev{};
-  if (!has_real) {
+  // real features: the code of a real parameter is the number of its distinct split thresholds
+  // below the candidate's coordinate, so `x <= thr_j` (go left) is `code < j + 1` like every other
+  // split (thresholds sorted per parameter; the device finds the code by binary search)
+  std::vector<std::vector<double>> rthr(D);
+  std::vector<int32_t> qcut(nodes.size(), 0);
+  bool rthr_ok = true;
+  if (has_real) {
+    for (size_t u = 0; u < nodes.size(); ++u)
+      if (nodes[u].feat >= 0 && h->params[h->feat_param_host[nodes[u].feat]].kind == BX_REAL)
+        rthr[h->feat_param_host[nodes[u].feat]].push_back(nodes[u].thr);
+    for (int k = 0; k < D; ++k) {
+      std::sort(rthr[k].begin(), rthr[k].end());
+      rthr[k].erase(std::unique(rthr[k].begin(), rthr[k].end()), rthr[k].end());
+      if (rthr[k].size() >= 32768) rthr_ok = false;
+    }
+    for (size_t u = 0; u < nodes.size(); ++u)
+      if (nodes[u].feat >= 0 && h->params[h->feat_param_host[nodes[u].feat]].kind == BX_REAL) {
+        const std::vector<double>& tv = rthr[h->feat_param_host[nodes[u].feat]];
+        qcut[u] = (int32_t)(std::lower_bound(tv.begin(), tv.end(), nodes[u].thr) - tv.begin()) + 1;
+      }
+  }
+  std::vector<int32_t> roff(D, 0);
+  std::vector<double> rflat;
+  for (int k = 0; k < D; ++k) {
+    roff[k] = (int32_t)rflat.size();
+    rflat.insert(rflat.end(), rthr[k].begin(), rthr[k].end());
+  }
+  if (rflat.size() >= 65536) rthr_ok = false;
+  if (rflat.empty()) rflat.push_back(0.0);
+  if (rthr_ok) {
     const int S = (int)code_param.size();
     std::vector<int32_t> soff(S), range(S);
     int stride = 0;
     for (int c = 0; c < S; ++c) {
       const bx_param_desc& p = h->params[code_param[c]];
-      range[c] = p.kind == BX_CATEGORICAL ? 2 : p.size;  // one-hot {0,1}; position < m; index < size
+      range[c] = p.kind == BX_CATEGORICAL ? 2 : (p.kind == BX_REAL ? (int)rthr[code_param[c]].size() + 1 : p.size);
       soff[c] = stride;
       stride += range[c];
     }
@@ -842,7 +871,8 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
           hi[u] = leaves;
           // going right (code >= cut) rules out the left subtree's leaves [lo, mid)
           const uint32_t lo32 = (uint32_t)coded[u];
-          const int slot = (int)((lo32 >> 24) & 63u), cut = (int)(lo32 & 0xFFFFFFu);
+          const bool real_split = ((coded[u] >> 30) & 3u) == 1u;
+          const int slot = (int)((lo32 >> 24) & 63u), cut = real_split ? qcut[u] : (int)(lo32 & 0xFFFFFFu);
           const uint64_t left = ((mid[u] - lo[u]) >= 64 ? ~0ull : ((1ull << (mid[u] - lo[u])) - 1)) << lo[u];
           for (int v = cut; v < range[slot]; ++v) mask[(size_t)t * stride + soff[slot] + v] &= ~left;
           stack.pop_back();
@@ -854,7 +884,7 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     // loads per candidate: one per parameter and tree)
     std::vector<int32_t> qparam, qsub, qsoff, qrange;
     if (ok) {
-      std::vector<int> merged(h->n_params, -1);
+      std::vector<int> merged(h->n_params, -1), newidx(S, -1);
       for (int c = 0; c < S; ++c) {
         const bx_param_desc& p = h->params[code_param[c]];
         if (p.kind == BX_CATEGORICAL) {
@@ -864,8 +894,11 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
           qsub.push_back(-1);
           qrange.push_back(p.size);
         } else {
+          newidx[c] = (int)qparam.size();
           qparam.push_back(code_param[c]);
-          qsub.push_back(code_sub[c]);
+          // a real code carries its threshold run: offset | count << 16 into qs.rthr
+          qsub.push_back(p.kind == BX_REAL ? (int32_t)(roff[code_param[c]] | (rthr[code_param[c]].size() << 16))
+                                           : code_sub[c]);
           qrange.push_back(range[c]);
         }
       }
@@ -878,7 +911,6 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       if (ok) {
         std::vector<uint64_t> m2((size_t)T * stride2, ~0ull);
         for (int t = 0; t < T; ++t) {
-          size_t c2 = 0;
           for (int c = 0; c < S; ++c) {
             const bx_param_desc& p = h->params[code_param[c]];
             if (p.kind == BX_CATEGORICAL) {
@@ -887,7 +919,7 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
                 m2[(size_t)t * stride2 + qsoff[mc] + L] &=
                     mask[(size_t)t * stride + soff[c] + (L == code_sub[c] ? 1 : 0)];
             } else {
-              while (qparam[c2] != code_param[c] || qsub[c2] != code_sub[c]) ++c2;
+              const int c2 = newidx[c];
               for (int v = 0; v < range[c]; ++v)
                 m2[(size_t)t * stride2 + qsoff[c2] + v] = mask[(size_t)t * stride + soff[c] + v];
             }
@@ -914,6 +946,9 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       BX_CUDA(h, upload(h->d_qsoff, qsoff.data(), qsoff.size()));
       BX_CUDA(h, upload(h->d_qcode_param, qparam.data(), qparam.size()));
       BX_CUDA(h, upload(h->d_qcode_sub, qsub.data(), qsub.size()));
+      BX_CUDA(h, upload(h->d_qrthr, rflat.data(), rflat.size()));
+      qs.rthr = h->d_qrthr.as<double>();
+      qs.has_real = has_real ? 1 : 0;
       qs.mask = h->d_qmask.as<uint64_t>();
       qs.vid = h->d_qvid.as<uint16_t>();
       qs.uval = h->d_quval.as<double>();
@@ -1165,7 +1200,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     const QsForestDev& qf = h->forest.qs;
     const bool fuse_rf =
         forest && !(flags & BX_SCORE_RF_PAIRWISE) &&
-        (h->use_tc ? qf.enabled && !h->tc_separate_forest &&
+        (h->use_tc ? qf.enabled && !qf.has_real && !h->tc_separate_forest &&
                          tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, false, h->tc_dmma) <= 227 * 1024
                    : kf.enabled && !h->no_fused_forest &&
                          fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
@@ -1177,7 +1212,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // the epilogue keeps the summaries (no forest / summary kernels, no EI round trip through HBM).
     const bool tc_full =
         h->use_tc && !h->tc_no_full && partials != nullptr && !(flags & BX_SCORE_RF_PAIRWISE) && !fuse_rf &&
-        (forest ? qf.enabled && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true, h->tc_dmma) <=
+        (forest ? qf.enabled && !qf.has_real && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true, h->tc_dmma) <=
                                     227 * 1024
                 : !h->has_forest &&
                       tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, nullptr, true, h->tc_dmma) <= 227 * 1024);

@@ -139,6 +139,10 @@ struct QsForestDev {
   int32_t n_trees, n_codes, stride, n_uvals;
   int32_t tpad;              // row length: n_trees rounded up to 8, plus 1 (odd: bank spread)
   int32_t enabled;
+  // real features: sorted distinct split thresholds per real parameter; a real code's code_sub is
+  // offset | count << 16 into rthr and its value is the number of thresholds below the coordinate
+  const double* rthr;
+  int32_t has_real;
 };
 
 struct ForestDev {

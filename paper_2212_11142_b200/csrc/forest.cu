@@ -211,7 +211,19 @@ __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t saddr) {
   return v;
 }
 
-__device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* row, int sub) {
+__device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* row, int sub,
+                                       const double* rthr) {
+  if (p.kind == BX_REAL) {  // thresholds strictly below the coordinate (binary search, L1-resident)
+    const double x = row_f64(row, p.word + 2);
+    const double* t = rthr + (sub & 0xFFFF);
+    int lo = 0, hi = sub >> 16;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(t + mid) < x) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  }
   if (p.kind == BX_PERMUTATION) return perm_pos(row_u64(row, p.word), p.size, sub);
   // sub < 0: one code for the whole categorical parameter (its label index; the per-label masks
   // are the ANDs of the one-hot features' masks), else the one-hot feature [label == sub]
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
     const uint32_t* row = rows + (size_t)i * sp.row_words;
     for (int c = 0; c < f.n_codes; ++c)
       sts_s32(off_s + 4u * kQsThreads * c,
-              (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+              (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
     double sum = 0.0;
     if (use_pairwise) {
       sum = pairwise(
@@ -350,10 +362,10 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
       if constexpr (NC > 0) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-          colr[c] = mask_s + 8u * (uint32_t)((f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+          colr[c] = mask_s + 8u * (uint32_t)((f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
       } else {
         for (int c = 0; c < f.n_codes; ++c)
-          sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c])) * f.tpad);
+          sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
       }
       double sum = 0.0;
       for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {
