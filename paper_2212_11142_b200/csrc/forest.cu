@@ -1,8 +1,14 @@
 // forest.cu — random-forest feasibility probability (FeasibilityModel.predict_proba_batch,
 // feasibility.py:72-89) over encoded rows, bit-exact.
 //
-// Two kernels:
-//  * rf_coded_kernel (fast path): the forest is integer-coded on the host (CodedForestDev): each
+// Kernels:
+//  * rf_qs_kernel / rf_qs_summary_kernel (fast path): QuickScorer tables (QsForestDev) — per tree
+//    and code value the AND of the leaf-elimination masks of the right-going splits on that code;
+//    a candidate's exit leaf is the lowest set bit of the AND of its codes' masks.  Codes: an
+//    integer / ordinal index, a permutation element's position, a categorical label index (its
+//    one-hot masks pre-ANDed), a real coordinate's rank among the parameter's split thresholds.
+//    The summary variant also forms p * EI, the eps_f filter and per-warp top-k / trackers.
+//  * rf_coded_kernel: the forest is integer-coded on the host (CodedForestDev): each
 //    split is `code < cut` on a per-candidate integer code, the node table and leaf values sit in
 //    shared memory, leaves point at themselves so two trees can be walked in lockstep with no
 //    per-tree exit branch.  One 512-thread CTA per SM.
