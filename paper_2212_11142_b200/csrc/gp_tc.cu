@@ -54,12 +54,13 @@ constexpr int kSlots = 8;        // K* column slices held in tensor memory at a 
 // their partial sums (exact int64, converted to double) in global scratch; pass 1 refills the slots
 // with slices 8.. and runs the chunks of rows >= 256 again over those columns, adding the partials.
 __host__ __device__ __forceinline__ int tc_passes(int nsl) { return nsl > kSlots ? 2 : 1; }
-#ifndef BX_TC_PROD_WARPS
-#define BX_TC_PROD_WARPS 8
-#endif
-constexpr int kProdWarps = BX_TC_PROD_WARPS;   // K* producers: kProdWarps / 4 per TMEM lane quarter
-constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // columns of a slice per producer thread (16)
-constexpr int kThreads = (8 + kProdWarps) * 32;
+// K* producer warps (a multiple of 4: kProdWarps / 4 per TMEM lane quarter).  The DMMA producers
+// are written for two per quarter; mixed spaces (ND == 0: integer-heavy distance code, latency
+// bound) run four per quarter at 80 registers, the rest two per quarter at 128.
+template <int ND, bool kDmma>
+constexpr int tc_prod_warps() { return (ND == 0 && !kDmma) ? 16 : 8; }
+template <int ND, bool kDmma>
+constexpr int tc_threads() { return (8 + tc_prod_warps<ND, kDmma>()) * 32; }
 constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
 constexpr int kAccCols = kGroups * kN;    // 96 TMEM columns per accumulator
 constexpr int kDigCol0 = 2 * kAccCols;    // first TMEM column of the candidate digits
@@ -276,7 +277,9 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
 // ND > 0: all-numeric space with exactly ND parameters — the distance loop is unrolled at compile
 // time and the candidate coordinates stay in registers for the whole tile.  ND == 0: any space.
 template <bool kPrecise, int ND, bool kDmma = false>
-__global__ void __launch_bounds__(kThreads, 1) gp_tc_kernel(TcArgs ta) {
+__global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcArgs ta) {
+  constexpr int kProdWarps = tc_prod_warps<ND, kDmma>();
+  constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // columns of a slice per producer thread
   extern __shared__ __align__(1024) unsigned char smem[];
   const FusedArgs& a = ta.f;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1185,9 +1188,13 @@ cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   if (dmma && !(a.dot && numeric && a.f.n_num <= 16)) return cudaErrorInvalidValue;
   const int nd = numeric ? a.f.n_num : 0;
   auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
+  int threads = tc_threads<0, false>();
   switch (nd) {
 #define BX_ND(d) \
-    case d: kernel = dmma ? gp_tc_kernel<false, d, true> : gp_tc_kernel<false, d>; break;
+    case d:                                                                            \
+      kernel = dmma ? gp_tc_kernel<false, d, true> : gp_tc_kernel<false, d>;           \
+      threads = dmma ? tc_threads<d, true>() : tc_threads<d, false>();                 \
+      break;
     BX_ND(1) BX_ND(2) BX_ND(3) BX_ND(4) BX_ND(5) BX_ND(6) BX_ND(7) BX_ND(8)
     BX_ND(9) BX_ND(10) BX_ND(11) BX_ND(12) BX_ND(13) BX_ND(14) BX_ND(15) BX_ND(16)
 #undef BX_ND
@@ -1199,7 +1206,7 @@ cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   int64_t grid = sm_count;
   if (tiles < grid) grid = tiles;
   if (grid < 1) grid = 1;
-  kernel<<<(int)grid, kThreads, L.total, s>>>(a);
+  kernel<<<(int)grid, threads, L.total, s>>>(a);
   return cudaGetLastError();
 }
 
