@@ -293,3 +293,44 @@ def test_dmma_distances_match_fma_distances(c3, monkeypatch):
         sc.close()
     np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-9, atol=1e-12 * np.abs(out[1][0]).max())
     np.testing.assert_allclose(out[0][1], out[1][1], rtol=1e-7, atol=1e-12 * np.abs(out[1][1]).max())
+
+
+@pytest.mark.parametrize("D", [1, 3, 6, 12, 16])
+def test_numeric_dimensions_dmma_producers(D):
+    """Random all-numeric spaces of D = 1..16 dimensions (ordinal / integer / real mixes): every
+    gp_tc_kernel<0, D, 1> instance (DMMA distance producers, 1..5 augmented k-steps) against the
+    oracle's FP64 posterior."""
+    import oracle
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    rng = np.random.default_rng(100 + D)
+    params = []
+    for i in range(D):
+        kind = ("ordinal", "integer", "real")[i % 3]
+        if kind == "ordinal":
+            params.append({"name": f"o{i}", "kind": "ordinal", "values": [1, 2, 4, 8, 16, 32, 64][: 3 + i % 5],
+                           "transform": "log" if i % 2 else "none"})
+        elif kind == "integer":
+            params.append({"name": f"i{i}", "kind": "integer", "lo": 0, "hi": 5 + 7 * (i % 4)})
+        else:
+            params.append({"name": f"r{i}", "kind": "real", "lo": -1.0 - i, "hi": 2.0 + i})
+    space = scenarios.build_space({"params": params, "constraints": []})
+    sc = Scorer()
+    lay = sc.set_space(space)
+    n = 90
+    cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, n + 50, rng))))[:n]
+    y = rng.standard_normal(len(cfgs))
+    hyp = Hyper(outputscale=1.1, noise_variance=1e-3, lengthscales=tuple(rng.uniform(0.5, 2.5, D)))
+    gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+    sc.set_gp(gp)
+    assert sc.gp_kernel() == "tensor"
+    rows = sc.to_device(scenarios.sample_rows_uniform(lay, 5 * 128 + 3, rng))
+    mean, var = (x.cpu().numpy() for x in sc.predict(rows))
+    sample = lay.decode(rows.cpu().numpy().view(np.uint32))
+    og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
+                         L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
+    m0, v0 = oracle.gp.predict(og, sample)
+    np.testing.assert_allclose(mean, m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
+    np.testing.assert_allclose(var, v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
+    sc.close()
