@@ -127,7 +127,9 @@ int bx_gp_kernel(bx_handle* h);
 
 /* ---- model state (once per BO iteration) ------------------------------------------------ */
 /* Space tables.  coord_lut / rank_lut are host arrays indexed by bx_param_desc offsets;
-   n_features = encode_configs width (feasibility.py:33-51). */
+   n_features = encode_configs width (feasibility.py:33-51).  Setting a space clears every other
+   piece of model state (GP, forest, evaluated set, chain of trees, constraints): each must be set
+   again for the new space before the calls that need it (they return BX_ERR_STATE until then). */
 int bx_set_space(bx_handle* h, const bx_param_desc* host_params, int32_t n_params, int32_t row_words,
                  const double* host_coord_lut, int32_t coord_len,
                  const int32_t* host_rank_lut, int32_t rank_len, int32_t n_features);

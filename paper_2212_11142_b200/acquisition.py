@@ -13,6 +13,7 @@ import math
 import numpy as np
 import torch
 
+from . import _native as N
 from .device import Candidate, Scorer, scorer
 
 N_CANDIDATES = 5000   # acquisition.py:23
@@ -115,7 +116,6 @@ def predict_proba_batch(feas, configs):
     if feas.constant is not None:
         return np.full(len(configs), feas.constant)
     if feas.roots is None or len(feas.roots) == 0:
-        from .device import N
         raise N.NativeError(N.BX_ERR_NO_TREES, "feasibility model has no trees")
     sc = scorer()
     if sc.layout is None or sc.layout.space is not feas.space or \
@@ -184,14 +184,10 @@ def _default_sampler(space, cot):
 
 
 def _sample_uniform_for(space):
-    mod = type(space).__module__
-    try:
-        import importlib
+    """The caller's own `sample_uniform` (space.py:312-332): the module that defines the space."""
+    import importlib
 
-        return importlib.import_module(mod).sample_uniform
-    except Exception:
-        from .space import sample_uniform
-        return sample_uniform
+    return importlib.import_module(type(space).__module__).sample_uniform
 
 
 def _better(a_val, a_cfg, b_val, b_cfg) -> bool:
@@ -216,8 +212,9 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
         sc.set_cot(cot)
     f_model = ctx.gp.objective_to_model(ctx.best_feasible_value)
     rows = sc.to_device(lay.encode(candidates))
-    summ, _, _ = sc.score(rows, f_model, ctx.eps_f, k=min(n_starts, 32),
-                          rf_pairwise=len(candidates) == 1)
+    many = local_search and n_starts > N.BX_MAX_K  # the fused top-k holds BX_MAX_K records
+    summ, pool_vals, _ = sc.score(rows, f_model, ctx.eps_f, k=min(n_starts, N.BX_MAX_K),
+                                  want_values=many, rf_pairwise=len(candidates) == 1)
     if summ.n_finite == 0:  # acquisition.py:179-184
         if summ.best_prob is None:
             return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
@@ -231,9 +228,14 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
         # still-climbing starts.  Each start's trajectory depends only on its own state, and the
         # running best is the maximum under a total order (value desc, configuration asc), so the
         # result equals the reference's start-after-start loop (acquisition.py:186-205).
-        starts = summ.top[:n_starts]
-        cur_rows = torch.cat([rows[st.index:st.index + 1] for st in starts]) if starts else rows[:0]
-        cur_v = [st.value for st in starts]
+        if many:  # np.argsort(-values, kind="stable")[:n_starts] on the host (acquisition.py:188)
+            v = pool_vals.cpu().numpy()
+            order = [int(i) for i in np.argsort(-v, kind="stable")[:n_starts] if v[i] != -np.inf]
+            starts = [(i, float(v[i])) for i in order]
+        else:
+            starts = [(st.index, st.value) for st in summ.top[:n_starts]]
+        cur_rows = torch.cat([rows[i:i + 1] for i, _ in starts]) if starts else rows[:0]
+        cur_v = [v for _, v in starts]
         active = list(range(len(starts)))
         n_slots = sc.n_slots
         for _ in range(MAX_CLIMB_STEPS):
@@ -245,12 +247,9 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
             nb = nb[vmask]
             if nb.shape[0] == 0:
                 break
-            s2, vals, _ = sc.score(nb, f_model, ctx.eps_f, k=1, want_values=True)
-            if s2.best is not None:
-                cfg2 = lay.decode(s2.best.row)[0]
-                if best_cfg is None or _better(s2.best.value, cfg2, best_val, best_cfg):
-                    best_val, best_cfg = s2.best.value, cfg2
-            v_all = vals.cpu().numpy()
+            v_all, s_val, s_cfg = _score_neighbours(sc, lay, nb, counts, f_model, ctx.eps_f)
+            if s_cfg is not None and (best_cfg is None or _better(s_val, s_cfg, best_val, best_cfg)):
+                best_val, best_cfg = s_val, s_cfg
             nb_host = nb.cpu().numpy().view(np.uint32)
             still, off = [], 0
             for a, cnt in zip(active, counts):
@@ -273,6 +272,33 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     if best_cfg is None:
         return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
     return best_cfg
+
+
+def _score_neighbours(sc, lay, nb, counts, f_model, eps_f):
+    """Score the neighbour lists of every climbing start at once: (values, best value, best config).
+
+    The reference scores each start's list with its own `_scores` call (acquisition.py:196), so a
+    list of exactly one configuration gets the forest's q == 1 summation order (numpy's pairwise
+    sum, feasibility.py:89) and every longer list the sequential one.  Single-neighbour lists are
+    therefore scored in a second call with the pairwise order; the running best is the maximum of
+    the two calls' trackers under (value desc, configuration asc)."""
+    single = counts[counts > 0] == 1
+    if not single.any() or single.all():
+        s2, vals, _ = sc.score(nb, f_model, eps_f, k=1, want_values=True, rf_pairwise=bool(single.all()))
+        cfg = lay.decode(s2.best.row)[0] if s2.best is not None else None
+        return vals.cpu().numpy(), (s2.best.value if s2.best is not None else -math.inf), cfg
+    row_single = np.repeat(counts[counts > 0] == 1, counts[counts > 0])
+    v_all = np.empty(nb.shape[0])
+    b_val, b_cfg = -math.inf, None
+    for idx, pairwise in ((np.flatnonzero(~row_single), False), (np.flatnonzero(row_single), True)):
+        s2, vals, _ = sc.score(nb[torch.as_tensor(idx, device=nb.device)], f_model, eps_f, k=1,
+                               want_values=True, rf_pairwise=pairwise)
+        v_all[idx] = vals.cpu().numpy()
+        if s2.best is not None:
+            cfg = lay.decode(s2.best.row)[0]
+            if b_cfg is None or _better(s2.best.value, cfg, b_val, b_cfg):
+                b_val, b_cfg = s2.best.value, cfg
+    return v_all, b_val, b_cfg
 
 
 def _enumerate_feasible(space, cot, Exhausted):

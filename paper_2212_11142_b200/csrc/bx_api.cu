@@ -480,7 +480,14 @@ int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, in
   h->n_features = n_features;
   h->n_slots = (int)sparam.size();
   h->has_space = true;
-  h->has_gp = false;  // planes depend on the space
+  // every other piece of model state is expressed in the old space's rows / features / domain
+  // indices: drop it, so a caller that forgets to re-set it gets BX_ERR_STATE, not stale reads
+  h->has_gp = false;
+  h->has_forest = false;
+  h->has_cot = false;
+  h->has_leaf_count = false;
+  h->has_constraints = false;
+  h->ev_count = 0;
   return BX_OK;
 }
 

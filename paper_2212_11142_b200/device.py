@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .constraints import Program, flatten_cot
+from .constraints import CotTables, Program, flatten_cot
 from .layout import SpaceLayout
 
 
@@ -120,8 +120,9 @@ class Scorer:
         self._space_key = key
         self.space_gen += 1
         self.n_slots = self._lib.bx_neighbor_slots(self.h)
-        self._cot_key = None
+        self._cot_key = None  # bx_set_space cleared every other piece of model state
         self._cons_key = None
+        self.has_forest = False
         return lay
 
     def set_gp(self, gp):
@@ -172,10 +173,12 @@ class Scorer:
         self._check(self._lib.bx_set_evaluated(self.h, _ptr(rows), len(rows)))
 
     def set_cot(self, cot):
+        """Upload the reference's ChainOfTrees (constraints.py:398-410), or pre-flattened
+        `CotTables` (workloads loaded without the reference)."""
         key = id(cot)
         if getattr(self, "_cot_key", None) == key:
             return
-        t = flatten_cot(cot, self.layout)
+        t = cot if isinstance(cot, CotTables) else flatten_cot(cot, self.layout)
         self._check(self._lib.bx_set_cot(self.h, t.n_groups, _ptr(t.group_kind),
                                          _ptr(t.group_param_begin), _ptr(t.group_params),
                                          _ptr(t.group_root), t.n_nodes, _ptr(t.child_begin),

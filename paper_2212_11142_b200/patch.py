@@ -16,6 +16,11 @@ TARGETS = (
     ("engine", "optimize_acquisition", gpu.optimize_acquisition),
     ("acquisition", "_scores", gpu.scores),
     ("acquisition", "neighbors", gpu.neighbors),
+)
+# hyperparameter-fit objectives: opt-in, because their values are FP64 but not bit-identical to
+# LAPACK's, and they feed argsort / L-BFGS-B (surrogate.py:505-530), so the fitted hyperparameters
+# - and with them the BO history - may drift from the reference's in the last bits
+LML_TARGETS = (
     ("surrogate", "_batched_coarse_lml", gpu.batched_coarse_lml),
     ("surrogate", "_lml_core", gpu.lml_core),
 )
@@ -25,12 +30,13 @@ METHODS = (
 )
 
 
-def install(boxtune, whole_path: bool = True):
+def install(boxtune, whole_path: bool = True, lml: bool = False):
     """Replace the reference's hot-path functions; returns a callable that undoes it.
     With whole_path=False the engine keeps the reference optimize_acquisition (which then calls
-    the GPU _scores / neighbors): the per-call parity mode."""
+    the GPU _scores / neighbors): the per-call parity mode.  lml=True also moves the
+    hyperparameter-fit objectives (_batched_coarse_lml, _lml_core) to the GPU."""
     saved = []
-    for mod_name, attr, fn in TARGETS:
+    for mod_name, attr, fn in TARGETS + (LML_TARGETS if lml else ()):
         if not whole_path and attr == "optimize_acquisition":
             continue
         mod = getattr(boxtune, mod_name)

