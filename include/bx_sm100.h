@@ -124,6 +124,9 @@ int bx_device_sm_count(bx_handle* h);
    BX_GP_GENERIC (shared-memory FP64 kernel for n + 1 > 256). */
 enum { BX_GP_GENERIC = 0, BX_GP_DMMA = 1, BX_GP_TENSOR = 2 };
 int bx_gp_kernel(bx_handle* h);
+/* Tensor-core posterior only: the DMMA k-steps of its distance product over the Euclidean
+   embedding of W (0: FMA distances per parameter kind, or not the tensor-core kernel). */
+int bx_gp_distance_ksteps(bx_handle* h);
 
 /* ---- model state (once per BO iteration) ------------------------------------------------ */
 /* Space tables.  coord_lut / rank_lut are host arrays indexed by bx_param_desc offsets;
@@ -193,6 +196,10 @@ int bx_last_timing(bx_handle* h, float* rf_ms, float* score_ms, float* merge_ms)
 /* Diagnostic (no reference counterpart): measured FP64 peaks of the DFMA pipe and of the DMMA
    m8n8k4 tensor path on `device`, in TFLOP/s - the roofline denominator of the contraction. */
 int bx_probe_fp64(int device, double* dfma_tflops, double* dmma_tflops);
+/* Live int8 tcgen05.mma rates: dense_mac_s = MACs/s of the peak shape (M128 N256 K32, operands in
+   shared memory) over every SM; block_ns = one (chunk, slice) block of the posterior's split
+   product (five MMAs, A from TMEM, N = 96..32) on one SM.  The roofline denominators of bench.py. */
+int bx_probe_int8(int device, double* dense_mac_s, double* block_ns);
 
 /* Score dev_rows[0..q) (encoded, device).  f_model = objective_to_model(best feasible value);
    eps_f = feasibility limit.  Writes values/probs when non-NULL (device, q doubles each) and,

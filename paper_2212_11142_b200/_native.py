@@ -29,8 +29,8 @@ EXPORTED = (
     "bx_set_space", "bx_set_gp", "bx_set_forest", "bx_clear_forest", "bx_set_evaluated",
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_cot_contains",
-    "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64",
-    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel",
+    "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64", "bx_probe_int8",
+    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps",
 )
 BX_SCORE_TIMING = 4
 BX_SCORE_TIMING_POSTERIOR = 8
@@ -72,6 +72,7 @@ _SIGS = {
     "bx_abi_version": (C.c_int, []),
     "bx_device_sm_count": (C.c_int, [_p]),
     "bx_gp_kernel": (C.c_int, [_p]),
+    "bx_gp_distance_ksteps": (C.c_int, [_p]),
     "bx_set_space": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _p, _i32, _i32]),
     "bx_set_gp": (C.c_int, [_p, _p, _i32, _p, _p, _f64, _p, _f64, _f64, _p]),
     "bx_set_forest": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _f64]),
@@ -92,6 +93,7 @@ _SIGS = {
     "bx_pairwise_sq": (C.c_int, [_p, _p, _i32, _p, _i32, _p, _p]),
     "bx_last_timing": (C.c_int, [_p, _p, _p, _p]),
     "bx_probe_fp64": (C.c_int, [C.c_int, _p, _p]),
+    "bx_probe_int8": (C.c_int, [C.c_int, _p, _p]),
     "bx_lml_core": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _f64, _f64, _i32, _i32, _p, _p, _p, _p]),
     "bx_generate": (C.c_int, [_p, C.c_uint64, _i64, _i64, _i32, _p, _p]),
     "bx_score_generated": (C.c_int, [_p, C.c_uint64, _i64, _i64, _i32, _f64, _f64, _i32, _p, _p]),

@@ -64,9 +64,7 @@ struct bx_handle {
   bool has_forest = false;
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
-  DevBuf d_knodes, d_kvid, d_kuval;
-  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub, d_qrthr;
-  bool no_fused_forest = true;   // DMMA kernel: BX_FOREST_FUSED=1 walks the forest inside it
+  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub, d_qrthr, d_qiidx, d_qimask;
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
   std::vector<double> coord_host;
@@ -82,10 +80,9 @@ struct bx_handle {
   ConstraintDev cons{};
   DevBuf d_prog_begin, d_code, d_consts, d_vtag, d_vint, d_vflt, d_voff, d_str_id, d_fault;
   // scratch
-  static constexpr int kHostBufs = 4;  // bx_score_host ring: copies run up to 3 chunks ahead
-  DevBuf d_probs, d_partials, d_summary, d_lml_scratch, d_host_rows[kHostBufs];
+  DevBuf d_probs, d_partials, d_summary, d_lml_scratch;
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_copy[kHostBufs] = {}, ev_done[kHostBufs] = {};
+  cudaEvent_t ev_copy = nullptr, ev_done = nullptr;
   cudaEvent_t ev_t[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // rf / gp / merge timing
   float t_ms[3] = {0, 0, 0};
   // register-resident fused GP path (gp_fused.cu)
@@ -94,7 +91,6 @@ struct bx_handle {
   // tensor-core posterior (gp_tc.cu): digit-sliced [L^-1; alpha^T] + row scales
   bool use_tc = false;
   bool no_tc = false;     // BX_GP_DMMA=1 forces the FP64 DMMA kernel
-  bool tc_separate_forest = true;   // gp_tc + stand-alone forest kernel (BX_TC_FOREST_FUSED=1: fused)
   bool no_qs_forest = false;        // BX_FOREST_WALK=1: node walks instead of QuickScorer tables
   bool rf_after_gp = false;         // last score_impl ran the forest + summary kernel after the posterior
   int tc_debug = 0;                 // BX_TC_DEBUG (timing experiments)
@@ -105,15 +101,16 @@ struct bx_handle {
   int64_t h_ones_len = 0;
   const uint32_t* stream_ready = nullptr;  // set while a streaming posterior launch is enqueued
   int stream_shift = 0;
-  const SummaryArgs* tc_summ = nullptr;    // set while a full-step posterior launch is enqueued
-  bool tc_dot = false;                     // centred dot-product distances (bx_set_gp decides)
-  bool tc_dmma = false;                    // ... computed on FP64 DMMA by the producers
+  // distances on the FP64 tensor cores over the embedding of W (bx_set_gp decides): tc_ks k-steps,
+  // 0 -> FMA distances
+  int tc_ks = 0;
+  bool tc_aug = false;
+  std::vector<EmbDim> tc_emb;
+  std::vector<double> tc_tab;
+  DevBuf d_emb, d_emb_tab, d_emb_planes, d_emb_yy;
   bool tc_no_dmma = false;                 // BX_TC_NO_DMMA=1: FMA distances
-  bool tc_no_dot = false;                  // BX_TC_NO_DOT=1: always the difference form
-  DevBuf d_mu;
-  bool tc_no_full = true;                  // BX_TC_FULL=1: forest + summary inside the posterior kernel
-  bool tc_trace = false;
-  bool lml_narrow = false;          // BX_LML_NARROW=1: _lml_core always one CTA per setting            // BX_TC_TRACE set (role timeline dump)
+  bool tc_trace = false;                   // BX_TC_TRACE set (role timeline dump)
+  bool lml_narrow = false;                 // BX_LML_NARROW=1: _lml_core always one CTA per setting
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale, d_tc_part;
@@ -279,13 +276,14 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.kscale = h->tc_kscale;
     t.ready = h->stream_ready;
     t.ready_shift = h->stream_shift;
-    if (h->tc_summ) {
-      t.summ = *h->tc_summ;
-      t.summ_on = 1;
-    }
-    t.dot = h->tc_dot ? 1 : 0;
-    t.dmma = h->tc_dmma ? 1 : 0;
-    t.mu = h->d_mu.as<double>();
+    t.ks = h->tc_ks;
+    t.n_emb = (int32_t)h->tc_emb.size();
+    t.aug = h->tc_aug ? 1 : 0;
+    t.emb = h->d_emb.as<EmbDim>();
+    t.emb_tab = h->d_emb_tab.as<double>();
+    t.emb_tab_len = (int32_t)h->tc_tab.size();
+    t.emb_planes = h->d_emb_planes.as<double>();
+    t.emb_yy = h->d_emb_yy.as<double>();
     t.part = h->tc_nsl > 8 ? h->d_tc_part.as<double>() : nullptr;
     t.n_coord = (int32_t)h->coord_host.size();
     std::memcpy(t.exp2tab256, exp2_tables().t256, sizeof(t.exp2tab256));
@@ -323,6 +321,136 @@ int check_gp(bx_handle* h) {
 static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
                               const std::vector<int32_t>& roots, int max_depth);
 
+
+// Helmert basis: (L - 1) x L orthonormal rows spanning the sum-zero subspace of R^L
+static std::vector<double> helmert(int L) {
+  std::vector<double> Q((size_t)(L - 1) * L, 0.0);
+  for (int j = 1; j < L; ++j) {
+    const double nrm = std::sqrt((double)j * (j + 1));
+    for (int i = 0; i < j; ++i) Q[(size_t)(j - 1) * L + i] = 1.0 / nrm;
+    Q[(size_t)(j - 1) * L + j] = -(double)j / nrm;
+  }
+  return Q;
+}
+
+// The Euclidean embedding of W = sum_k sq_k / l_k^2 (surrogate.py:173-223; EmbDim in bx_common.cuh),
+// centred on the training mean; planes = the DMMA B operand [4 ks][npad] (-2 y', then |y'|^2 and 1
+// when they fit the padding: *aug), yy[npad] = |y'|^2.  False when a metric does not embed (naive
+// permutation indicator) or the centred coordinates are too large for the |x|^2 + |y|^2 - 2 x.y
+// form (bound 256: the cancellation error stays near the 2^-40 fixed point of K*).
+static bool build_embedding(const bx_handle* h, const uint32_t* train_rows, int n, const double* inv_l,
+                            const double* inv_l2, int npad, std::vector<EmbDim>& emb, std::vector<double>& tab,
+                            std::vector<double>& planes, std::vector<double>& yy, bool* aug) {
+  std::vector<int> seg;  // table entries per coordinate that carry the centring
+  for (int k = 0; k < h->n_params; ++k) {
+    const bx_param_desc& p = h->params[k];
+    if (p.kind == BX_INTEGER || p.kind == BX_ORDINAL) {
+      emb.push_back(EmbDim{BX_EMB_CODE, p.word, 0, 0, 0, (int)tab.size()});
+      for (int i = 0; i < p.size; ++i) tab.push_back(h->coord_host[p.coord + i] * inv_l[k]);
+      seg.push_back(p.size);
+    } else if (p.kind == BX_REAL) {
+      emb.push_back(EmbDim{BX_EMB_REAL, p.word, 0, 0, 0, (int)tab.size()});
+      tab.push_back(inv_l[k]);
+      tab.push_back(0.0);
+      seg.push_back(0);
+    } else if (p.kind == BX_CATEGORICAL) {
+      const int L = p.size;
+      const std::vector<double> Q = helmert(L);
+      const double sw = std::sqrt(inv_l2[k] / 2.0);  // unit-edge simplex: |V_a - V_b|^2 = 1
+      for (int j = 0; j + 1 < L; ++j) {
+        emb.push_back(EmbDim{BX_EMB_CODE, p.word, 0, 0, 0, (int)tab.size()});
+        for (int a = 0; a < L; ++a) tab.push_back(Q[(size_t)j * L + a] * sw);
+        seg.push_back(L);
+      }
+    } else {  // permutation
+      const int m = p.size;
+      const double wm = inv_l2[k] / p.raw_mx;
+      if (p.metric == BX_SPEARMAN) {
+        const std::vector<double> Q = helmert(m);
+        for (int j = 0; j + 1 < m; ++j) {
+          emb.push_back(EmbDim{BX_EMB_PERM_LIN, p.word, 0, 0, m, (int)tab.size()});
+          for (int i = 0; i < m; ++i) tab.push_back(Q[(size_t)j * m + i] * std::sqrt(wm));
+          tab.push_back(0.0);
+          seg.push_back(-1);
+        }
+      } else if (p.metric == BX_KENDALL) {
+        for (int a = 0; a < m; ++a)
+          for (int b = a + 1; b < m; ++b) {
+            emb.push_back(EmbDim{BX_EMB_KENDALL, p.word, a, b, m, (int)tab.size()});
+            tab.push_back(0.0);
+            tab.push_back(std::sqrt(wm));
+            seg.push_back(2);
+          }
+      } else if (p.metric == BX_HAMMING) {
+        const std::vector<double> Q = helmert(m);
+        for (int pos = 0; pos < m; ++pos)
+          for (int j = 0; j + 1 < m; ++j) {
+            emb.push_back(EmbDim{BX_EMB_PERM_HOT, p.word, pos, 0, m, (int)tab.size()});
+            for (int v = 0; v < m; ++v) tab.push_back(Q[(size_t)j * m + v] * std::sqrt(wm / 2.0));
+            seg.push_back(m);
+          }
+      } else {
+        return false;  // the naive indicator 1{a != b} over m! permutations does not embed cheaply
+      }
+    }
+    if (emb.size() > 32) return false;
+  }
+  const int E = (int)emb.size();
+  if (E == 0) return false;
+  // centre on the training mean (translation leaves every distance unchanged)
+  for (int e = 0; e < E; ++e) {
+    double mu = 0.0;
+    for (int j = 0; j < n; ++j) mu += emb_value(emb[e], train_rows + (size_t)j * h->row_words, tab.data());
+    mu /= n;
+    const EmbDim& d = emb[e];
+    if (seg[e] > 0) {
+      for (int i = 0; i < seg[e]; ++i) tab[d.off + i] -= mu;
+    } else if (d.kind == BX_EMB_REAL) {
+      tab[d.off + 1] = -mu;
+    } else {
+      tab[d.off + d.m] = -mu;
+    }
+  }
+  // magnitude bound over the whole domain
+  double bound = 0.0;
+  for (int e = 0; e < E; ++e) {
+    const EmbDim& d = emb[e];
+    double mx = 0.0;
+    if (seg[e] > 0) {
+      for (int i = 0; i < seg[e]; ++i) mx = std::max(mx, std::fabs(tab[d.off + i]));
+    } else if (d.kind == BX_EMB_REAL) {
+      int kp = 0;
+      while (kp + 1 < h->n_params && h->params[kp].word != d.word) ++kp;
+      const bx_param_desc& p = h->params[kp];
+      for (int i : {0, p.size - 1}) mx = std::max(mx, std::fabs(h->coord_host[p.coord + i] * tab[d.off] + tab[d.off + 1]));
+    } else {
+      mx = std::fabs(tab[d.off + d.m]);
+      for (int i = 0; i < d.m; ++i) mx += std::fabs(tab[d.off + i]) * (d.m - 1);
+    }
+    bound += mx * mx;
+  }
+  if (!(bound <= 256.0)) return false;
+  const int ks = (E + 3) / 4;
+  *aug = E + 2 <= 4 * ks;
+  planes.assign((size_t)4 * ks * npad, 0.0);
+  yy.assign((size_t)npad, 0.0);
+  for (int j = 0; j < n; ++j) {
+    const uint32_t* row = train_rows + (size_t)j * h->row_words;
+    double s2 = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double y = emb_value(emb[e], row, tab.data());
+      planes[(size_t)e * npad + j] = -2.0 * y;
+      s2 = std::fma(y, y, s2);
+    }
+    yy[j] = s2;
+    if (*aug) {
+      planes[(size_t)E * npad + j] = s2;
+      planes[(size_t)(E + 1) * npad + j] = 1.0;
+    }
+  }
+  return true;
+}
+
 extern "C" {
 
 int bx_abi_version(void) { return BX_ABI_VERSION; }
@@ -336,10 +464,8 @@ bx_handle* bx_create(int device) {
   h->no_coded_forest = generic && generic[0] == '1';
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
-  for (int i = 0; i < bx_handle::kHostBufs; ++i) {
-    cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
-  }
+  cudaEventCreateWithFlags(&h->ev_copy, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming);
   for (int i = 0; i < 5; ++i) cudaEventCreate(&h->ev_t[i]);
   const char* gpg = getenv("BX_GP_GENERIC");
   h->no_fused = gpg && gpg[0] == '1';
@@ -349,27 +475,10 @@ bx_handle* bx_create(int device) {
   if (const char* nd = getenv("BX_TC_NO_DMMA")) h->tc_no_dmma = nd[0] == '1';
   const char* fw = getenv("BX_FOREST_WALK");
   h->no_qs_forest = fw && fw[0] == '1';
-  // The QuickScorer forest evaluated inside the tensor-core kernel (epilogue warps, between chunk
-  // drains) is exact but measured slower than the stand-alone QuickScorer kernel run after it:
-  // opt-in with BX_TC_FOREST_FUSED=1.
-  // The full step inside the tensor-core kernel (QuickScorer on the decoder warps, summaries in the
-  // epilogue) is exact but measured ~4 % slower than posterior + forest/summary kernels back to
-  // back: the forest's shared-memory work competes with the producers for issue slots.  Opt-in.
-  const char* tnd = getenv("BX_TC_NO_DOT");
-  h->tc_no_dot = tnd && tnd[0] == '1';
-  const char* tfull = getenv("BX_TC_FULL");
-  h->tc_no_full = !(tfull && tfull[0] == '1');
-  const char* tff = getenv("BX_TC_FOREST_FUSED");
-  h->tc_separate_forest = !(tff && tff[0] == '1');
   const char* dm = getenv("BX_GP_DMMA");
   h->no_tc = h->no_fused || (dm && dm[0] == '1');
   const char* mp = getenv("BX_MATERN_PRECISE");
   h->matern_precise = mp && mp[0] == '1';
-  // The forest walk fused into the GP kernel is correct but measured slower than the concurrent
-  // stand-alone kernel (the per-panel CTA barrier aligns every warp's integer phase), so it is
-  // opt-in: BX_FOREST_FUSED=1.
-  const char* fs = getenv("BX_FOREST_FUSED");
-  h->no_fused_forest = !(fs && fs[0] == '1');
   cudaStreamCreateWithFlags(&h->rf_stream, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_rf, cudaEventDisableTiming);
@@ -387,23 +496,23 @@ void bx_destroy(bx_handle* h) {
                     &h->d_child_begin, &h->d_child_count, &h->d_child_value, &h->d_prog_begin, &h->d_code,
                     &h->d_consts, &h->d_vtag, &h->d_vint, &h->d_vflt, &h->d_voff, &h->d_str_id,
                     &h->d_fault, &h->d_probs, &h->d_partials, &h->d_summary, &h->d_lml_scratch,
-                    &h->d_host_rows[0], &h->d_host_rows[1], &h->d_host_rows[2], &h->d_host_rows[3],
                     &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
-                    &h->d_knodes, &h->d_kvid, &h->d_kuval, &h->d_qmask, &h->d_qvid,
-                    &h->d_quval, &h->d_qsoff, &h->d_qcode_param, &h->d_qcode_sub, &h->d_qrthr};
+                    &h->d_qmask, &h->d_qvid, &h->d_quval, &h->d_qsoff, &h->d_qcode_param,
+                    &h->d_qcode_sub, &h->d_qrthr, &h->d_qiidx, &h->d_qimask};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  for (int i = 0; i < bx_handle::kHostBufs; ++i) {
-    if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
-    if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
-  }
+  if (h->ev_copy) cudaEventDestroy(h->ev_copy);
+  if (h->ev_done) cudaEventDestroy(h->ev_done);
   for (int i = 0; i < 5; ++i)
     if (h->ev_t[i]) cudaEventDestroy(h->ev_t[i]);
   h->d_panels.release();
   h->d_pool.release();
   h->d_ready.release();
-  h->d_mu.release();
+  h->d_emb.release();
+  h->d_emb_tab.release();
+  h->d_emb_planes.release();
+  h->d_emb_yy.release();
   if (h->h_ones) cudaFreeHost(h->h_ones);
   h->d_mdig.release();
   h->d_rowscale.release();
@@ -426,6 +535,8 @@ int bx_gp_kernel(bx_handle* h) {
   if (!h) return BX_GP_GENERIC;
   return h->use_tc ? BX_GP_TENSOR : h->use_fused ? BX_GP_DMMA : BX_GP_GENERIC;
 }
+
+int bx_gp_distance_ksteps(bx_handle* h) { return h && h->use_tc ? h->tc_ks : 0; }
 
 int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, int32_t row_words,
                  const double* coord_lut, int32_t coord_len, const int32_t* rank_lut,
@@ -567,62 +678,45 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
     }
   }
   // tensor-core path: n <= 511 (32 row chunks; n > 255 runs two column passes per tile) and the
-  // shared-memory budget
+  // shared-memory budget.  Distances on the FP64 tensor cores over the Euclidean embedding of W
+  // (EmbDim) when every metric embeds and the centred coordinates stay small, else FMA distances.
   h->use_tc = false;
-  if (!h->no_tc && n <= 511 && tc_smem_bytes(n, D, h->n_kendall, h->row_words) <= 227 * 1024) {
-    int E = 0;
-    const double m = frexp(outputscale, &E);  // sigma < 2^E = sc
-    if (m > 1.0 - ldexp(1.0, -20)) ++E;        // headroom: K* * 2^40 / sc < 2^40 - 2^20
-    h->tc_nsl = (n + 31) / 32;
-    h->tc_nch = n / 16 + 1;
-    h->tc_kscale = ldexp(1.0, 40 - E);
-    BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
-    BX_CUDA(h, h->d_rowscale.ensure(2 * 512 * 8));
-    if (h->tc_nsl > 8)  // pass-0 partial sums of rows >= 256: [CTA][256 rows][128 candidates]
-      BX_CUDA(h, h->d_tc_part.ensure((size_t)h->sm_count * 256 * 128 * 8));
-    h->use_tc = true;
-    // dot-product distances: all-numeric spaces whose coordinates, centred on the training mean and
-    // scaled by 1/l, stay small (|x'|^2 <= 64 for every domain point), so |x'|^2 + |y'|^2 - 2 x'.y'
-    // loses at most ~2^-46 of W (well under the 2^-40 fixed point of K*)
-    h->tc_dot = false;
-    bool numeric = true;
-    for (int k = 0; k < D && numeric; ++k)
-      numeric = h->params[k].kind != BX_CATEGORICAL && h->params[k].kind != BX_PERMUTATION;
-    if (numeric && !h->tc_no_dot) {
-      std::vector<double> mu(D, 0.0);
-      double bound = 0.0;
-      for (int k = 0; k < D; ++k) {
-        const bx_param_desc& p = h->params[k];
-        double acc = 0.0;
-        for (int j = 0; j < n; ++j) {
-          const uint32_t* row = train_rows + (size_t)j * h->row_words;
-          double x;
-          if (p.kind == BX_REAL) {
-            uint64_t bits = (uint64_t)row[p.word + 2] | ((uint64_t)row[p.word + 3] << 32);
-            std::memcpy(&x, &bits, 8);
-          } else {
-            x = h->coord_host[p.coord + row[p.word]];
-          }
-          acc += x * inv_l[k];
-        }
-        mu[k] = acc / n;
-        double lo = 1e300, hi = -1e300;  // domain extremes (finite domains / the real grid)
-        for (int i = 0; i < p.size; ++i) {
-          lo = std::min(lo, h->coord_host[p.coord + i] * inv_l[k]);
-          hi = std::max(hi, h->coord_host[p.coord + i] * inv_l[k]);
-        }
-        bound += std::max((lo - mu[k]) * (lo - mu[k]), (hi - mu[k]) * (hi - mu[k]));
+  h->tc_ks = 0;
+  if (!h->no_tc && n <= 511) {
+    h->tc_emb.clear();
+    h->tc_tab.clear();
+    std::vector<double> planes, yy;
+    const int nsl = (n + 31) / 32;
+    bool dmma = !h->tc_no_dmma && !h->matern_precise &&
+                build_embedding(h, train_rows, n, inv_l.data(), inv_l2.data(), 32 * nsl, h->tc_emb, h->tc_tab,
+                                planes, yy, &h->tc_aug);
+    const int E = (int)h->tc_emb.size();
+    const int ks = dmma ? (E + 3) / 4 : 0;
+    dmma = dmma && ks >= 1 && ks <= 8 &&
+           tc_smem_bytes(n, D, h->n_kendall, h->row_words, ks, E, (int)h->tc_tab.size(), h->tc_aug, false) <= 227 * 1024;
+    if (dmma || tc_smem_bytes(n, D, h->n_kendall, h->row_words, 0, 0, 0, false, false) <= 227 * 1024) {
+      int Ex = 0;
+      const double m = frexp(outputscale, &Ex);  // sigma < 2^Ex = sc
+      if (m > 1.0 - ldexp(1.0, -20)) ++Ex;        // headroom: K* * 2^40 / sc < 2^40 - 2^20
+      h->tc_nsl = nsl;
+      h->tc_nch = n / 16 + 1;
+      h->tc_kscale = ldexp(1.0, 40 - Ex);
+      BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
+      BX_CUDA(h, h->d_rowscale.ensure(2 * 512 * 8));
+      if (h->tc_nsl > 8)  // pass-0 partial sums of rows >= 256: [CTA][256 rows][128 candidates]
+        BX_CUDA(h, h->d_tc_part.ensure((size_t)h->sm_count * 256 * 128 * 8));
+      if (dmma) {
+        h->tc_ks = ks;
+        BX_CUDA(h, upload(h->d_emb, h->tc_emb.data(), h->tc_emb.size()));
+        BX_CUDA(h, upload(h->d_emb_tab, h->tc_tab.data(), h->tc_tab.size()));
+        planes.resize((size_t)4 * ks * 32 * nsl, 0.0);  // k-rows beyond E (+2) are zero
+        BX_CUDA(h, upload(h->d_emb_planes, planes.data(), planes.size()));
+        BX_CUDA(h, upload(h->d_emb_yy, yy.data(), yy.size()));
       }
-      if (bound <= 64.0) {
-        BX_CUDA(h, upload(h->d_mu, mu.data(), mu.size()));
-        h->tc_dot = true;
-      }
+      h->use_tc = true;
+      BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, Ex),
+                                   h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), dmma ? 1 : 0, s));
     }
-    // distances on the FP64 tensor cores when the centred product form holds (and fits)
-    h->tc_dmma = h->tc_dot && D <= 16 && !h->matern_precise && !h->tc_no_dmma &&
-                 tc_smem_bytes(n, D, h->n_kendall, h->row_words, nullptr, false, true) <= 227 * 1024;
-    BX_CUDA(h, launch_build_mdig(h->d_A.as<double>(), h->gp_lda, n, ldexp(1.0, E),
-                                 h->d_mdig.as<unsigned char>(), h->d_rowscale.as<double>(), h->tc_dmma ? 1 : 0, s));
   }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
   h->outputscale = outputscale;
@@ -845,7 +939,7 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     std::vector<uint64_t> mask((size_t)T * stride, ~0ull);
     std::vector<uint16_t> vid((size_t)T * 64, 0);
     std::vector<double> uval;
-    bool ok = (size_t)T * stride * 8 <= 160 * 1024;
+    bool ok = (size_t)T * stride <= ((size_t)1 << 24);  // host tables; the shared-memory budget is checked below
     std::vector<int32_t> lo(nodes.size()), mid(nodes.size()), hi(nodes.size());
     for (int t = 0; ok && t < T; ++t) {
       // left-to-right leaf numbering and subtree leaf ranges by an explicit post-order walk
@@ -914,8 +1008,7 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
         qsoff.push_back(stride2);
         stride2 += qrange[c];
       }
-      ok = (size_t)T * stride2 * 8 <= 160 * 1024;
-      if (ok) {
+      {
         std::vector<uint64_t> m2((size_t)T * stride2, ~0ull);
         for (int t = 0; t < T; ++t) {
           for (int c = 0; c < S; ++c) {
@@ -936,89 +1029,102 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
         stride = stride2;
       }
     }
+    // indirect slots: real parameters whose codes span many thresholds keep, per tree, only the few
+    // distinct masks its own splits produce (runs of equal masks along the code) and a [code][tree]
+    // u16 index into them
+    std::vector<int> ind;
+    std::vector<int32_t> dparam, dsub, dsoff;
+    int dstride = 0;
+    if (ok) {
+      for (size_t c = 0; c < qparam.size(); ++c)
+        if (h->params[qparam[c]].kind == BX_REAL && qrange[c] > 32 && ind.size() < 2) ind.push_back((int)c);
+      for (size_t c = 0; c < qparam.size(); ++c) {
+        if (std::find(ind.begin(), ind.end(), (int)c) != ind.end()) continue;
+        dparam.push_back(qparam[c]);
+        dsub.push_back(qsub[c]);
+        dsoff.push_back(dstride);
+        dstride += qrange[c];
+      }
+      ok = (size_t)T * dstride * 8 <= 160 * 1024;
+    }
     if (ok) {
       if (uval.empty()) uval.push_back(0.0);
-      // transpose to [slot value][tree] so a group of 8 trees is one 64-byte run per slot
-      // odd row length (in 8-byte words): the <= 16 distinct code-value rows a half-warp reads with
-      // 8-byte loads fall in 16 distinct bank pairs (groups of 8 trees read t .. t+7)
+      // direct slots transposed to [slot value][tree] so a group of 8 trees is one 64-byte run per
+      // slot; odd row length (in 8-byte words): the <= 16 distinct code-value rows a half-warp reads
+      // with 8-byte loads fall in 16 distinct bank pairs (groups of 8 trees read t .. t+7)
       int tpad = (T + 7) / 8 * 8 + 1;
-      std::vector<uint64_t> mt((size_t)stride * tpad, ~0ull);
-      for (int t = 0; t < T; ++t)
-        for (int r = 0; r < stride; ++r) mt[(size_t)r * tpad + t] = mask[(size_t)t * stride + r];
-      mask.swap(mt);
-      qs.tpad = tpad;
-      BX_CUDA(h, upload(h->d_qmask, mask.data(), mask.size()));
-      BX_CUDA(h, upload(h->d_qvid, vid.data(), vid.size()));
-      BX_CUDA(h, upload(h->d_quval, uval.data(), uval.size()));
-      BX_CUDA(h, upload(h->d_qsoff, qsoff.data(), qsoff.size()));
-      BX_CUDA(h, upload(h->d_qcode_param, qparam.data(), qparam.size()));
-      BX_CUDA(h, upload(h->d_qcode_sub, qsub.data(), qsub.size()));
-      BX_CUDA(h, upload(h->d_qrthr, rflat.data(), rflat.size()));
-      qs.rthr = h->d_qrthr.as<double>();
-      qs.has_real = has_real ? 1 : 0;
-      qs.mask = h->d_qmask.as<uint64_t>();
-      qs.vid = h->d_qvid.as<uint16_t>();
-      qs.uval = h->d_quval.as<double>();
-      qs.soff = h->d_qsoff.as<int32_t>();
-      qs.code_param = h->d_qcode_param.as<int32_t>();
-      qs.code_sub = h->d_qcode_sub.as<int32_t>();
-      qs.n_trees = T;
-      qs.n_codes = (int)qparam.size();
-      qs.stride = stride;
-      qs.n_uvals = (int)uval.size();
-      qs.enabled = h->no_qs_forest ? 0 : 1;
-      if (getenv("BX_QS_INFO"))  // development aid: table geometry
-        fprintf(stderr, "qs: trees %d codes %d stride %d tpad %d uvals %d masks %zu B summary smem %zu B\n", T,
-                qs.n_codes, stride, tpad, qs.n_uvals, (size_t)stride * tpad * 8,
-                (size_t)qs_summary_smem_bytes(qs));
+      std::vector<uint64_t> mt((size_t)std::max(dstride, 1) * tpad, ~0ull);
+      for (size_t c = 0, d = 0; c < qparam.size(); ++c) {
+        if (std::find(ind.begin(), ind.end(), (int)c) != ind.end()) continue;
+        for (int v = 0; v < qrange[c]; ++v)
+          for (int t = 0; t < T; ++t) mt[(size_t)(dsoff[d] + v) * tpad + t] = mask[(size_t)t * stride + qsoff[c] + v];
+        ++d;
+      }
+      // indirect tables: rows (slot, code) x itpad u16 indices (itpad = 8 * odd: 16-byte rows)
+      int itpad = (T + 7) / 8 * 8;
+      if ((itpad / 8) % 2 == 0) itpad += 8;
+      int irows = 0;
+      for (int c : ind) irows += qrange[c];
+      std::vector<uint16_t> iidx((size_t)std::max(irows, 1) * itpad, 0);
+      std::vector<uint64_t> imask;
+      qs.n_ind = (int)ind.size();
+      int ioff = 0;
+      for (size_t i = 0; i < ind.size() && ok; ++i) {
+        const int c = ind[i];
+        qs.ind_param[i] = qparam[c];
+        qs.ind_sub[i] = qsub[c];
+        qs.ind_off[i] = ioff;
+        for (int t = 0; t < T && ok; ++t) {
+          int cur = -1;
+          for (int v = 0; v < qrange[c]; ++v) {
+            const uint64_t mv = mask[(size_t)t * stride + qsoff[c] + v];
+            if (cur < 0 || imask[cur] != mv) {
+              cur = (int)imask.size();
+              imask.push_back(mv);
+            }
+            if (cur > 65535) { ok = false; break; }
+            iidx[(size_t)(ioff + v) * itpad + t] = (uint16_t)cur;
+          }
+        }
+        ioff += qrange[c];
+      }
+      if (imask.empty()) imask.push_back(~0ull);
+      if (ok) {
+        qs.tpad = tpad;
+        BX_CUDA(h, upload(h->d_qmask, mt.data(), mt.size()));
+        BX_CUDA(h, upload(h->d_qvid, vid.data(), vid.size()));
+        BX_CUDA(h, upload(h->d_quval, uval.data(), uval.size()));
+        if (dsoff.empty()) { dsoff.push_back(0); dparam.push_back(0); dsub.push_back(0); }
+        BX_CUDA(h, upload(h->d_qsoff, dsoff.data(), dsoff.size()));
+        BX_CUDA(h, upload(h->d_qcode_param, dparam.data(), dparam.size()));
+        BX_CUDA(h, upload(h->d_qcode_sub, dsub.data(), dsub.size()));
+        BX_CUDA(h, upload(h->d_qrthr, rflat.data(), rflat.size()));
+        BX_CUDA(h, upload(h->d_qiidx, iidx.data(), iidx.size()));
+        BX_CUDA(h, upload(h->d_qimask, imask.data(), imask.size()));
+        qs.rthr = h->d_qrthr.as<double>();
+        qs.has_real = has_real ? 1 : 0;
+        qs.mask = h->d_qmask.as<uint64_t>();
+        qs.vid = h->d_qvid.as<uint16_t>();
+        qs.uval = h->d_quval.as<double>();
+        qs.soff = h->d_qsoff.as<int32_t>();
+        qs.code_param = h->d_qcode_param.as<int32_t>();
+        qs.code_sub = h->d_qcode_sub.as<int32_t>();
+        qs.iidx = h->d_qiidx.as<uint16_t>();
+        qs.imask = h->d_qimask.as<uint64_t>();
+        qs.itpad = itpad;
+        qs.n_iidx_rows = irows;
+        qs.n_imask = (int)imask.size();
+        qs.n_trees = T;
+        qs.n_codes = dstride > 0 ? (int)dparam.size() : 0;
+        qs.stride = dstride;
+        qs.n_uvals = (int)uval.size();
+        qs.enabled = h->no_qs_forest ? 0 : 1;
+        if (getenv("BX_QS_INFO"))  // development aid: table geometry
+          fprintf(stderr, "qs: trees %d codes %d (+%d indirect: %d rows, %d masks) stride %d tpad %d uvals %d masks %zu B summary smem %zu B\n",
+                  T, qs.n_codes, qs.n_ind, irows, qs.n_imask, dstride, tpad, qs.n_uvals, (size_t)dstride * tpad * 8,
+                  (size_t)qs_summary_smem_bytes(qs));
+      }
     }
-  }
-
-  // compact 32-bit form for the walk fused into the GP kernel (CompactForestDev)
-  CompactForestDev& kf = h->forest.kf;
-  kf = CompactForestDev{};
-  bool ok = !has_real;
-  for (size_t c = 0; ok && c < code_param.size(); ++c) {
-    const bx_param_desc& p = h->params[code_param[c]];
-    if ((p.kind == BX_INTEGER || p.kind == BX_ORDINAL) && p.size > 511) ok = false;
-  }
-  std::vector<uint32_t> knodes(nodes.size());
-  std::vector<uint16_t> vid(nodes.size(), 0);
-  std::vector<double> uval;
-  for (size_t u = 0; ok && u < nodes.size(); ++u) {
-    const uint32_t lo = (uint32_t)coded[u];
-    const uint32_t type = lo >> 30;
-    if (type == 2) {
-      const double v = leaf_val[leaf_idx[u]];
-      size_t id = 0;
-      while (id < uval.size() && std::memcmp(&uval[id], &v, 8) != 0) ++id;
-      if (id == uval.size()) uval.push_back(v);
-      if (id > 65535) { ok = false; break; }
-      vid[u] = (uint16_t)id;
-      knodes[u] = 0x80000000u | (511u << 16);  // stays: code < 511 always
-      continue;
-    }
-    const uint32_t slot = (lo >> 24) & 63u, cut = lo & 0xFFFFFFu;
-    const uint64_t off = (uint64_t)(coded[u] >> 32) - u;
-    if (cut > 511 || off == 0 || off > 65535) { ok = false; break; }
-    knodes[u] = (slot << 25) | (cut << 16) | (uint32_t)off;
-  }
-  if (ok) {
-    BX_CUDA(h, upload(h->d_knodes, knodes.data(), knodes.size()));
-    BX_CUDA(h, upload(h->d_kvid, vid.data(), vid.size()));
-    BX_CUDA(h, upload(h->d_kuval, uval.data(), uval.size()));
-    kf.nodes = h->d_knodes.as<uint32_t>();
-    kf.vid = h->d_kvid.as<uint16_t>();
-    kf.uval = h->d_kuval.as<double>();
-    kf.roots = h->forest.roots;
-    kf.code_param = cf.code_param;
-    kf.code_sub = cf.code_sub;
-    kf.n_nodes = (int)knodes.size();
-    kf.n_uvals = (int)uval.size();
-    kf.n_trees = cf.n_trees;
-    kf.max_depth = max_depth;
-    kf.n_codes = cf.n_codes;
-    kf.enabled = 1;
   }
   return BX_OK;
 }
@@ -1199,87 +1305,34 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   const bool forest = h->has_forest && h->forest.has_trees;
   if (forest) BX_CUDA(h, h->d_probs.ensure((size_t)q * 8));
   if (fused_path(h)) {
-    // The forest walk runs inside the GP kernel (FP64 and integer/LSU work interleave in the same
-    // warps) unless the numpy pairwise order (q == 1) or the table budget rules it out; then it
-    // runs on the side stream and is joined before the summary.
-    const CompactForestDev& kf = h->forest.kf;
-    // Tensor-core kernel: optionally the QuickScorer forest inside the kernel (BX_TC_FOREST_FUSED=1).
-    const QsForestDev& qf = h->forest.qs;
-    const bool fuse_rf =
-        forest && !(flags & BX_SCORE_RF_PAIRWISE) &&
-        (h->use_tc ? qf.enabled && !qf.has_real && !h->tc_separate_forest &&
-                         tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, false, h->tc_dmma) <= 227 * 1024
-                   : kf.enabled && !h->no_fused_forest &&
-                         fused_smem_bytes_forest(h->gp_n, h->n_params, h->n_kendall, h->rows8, kf) <=
-                             220 * 1024);
-    // The stand-alone forest kernel and the GP kernel each fill every SM's shared memory, so
-    // they cannot co-reside: run them back to back on the caller's stream (which also makes the
-    // per-kernel CUDA-event timing exact).
-    // The whole step in the tensor-core kernel: decoder warps evaluate the QuickScorer forest and
-    // the epilogue keeps the summaries (no forest / summary kernels, no EI round trip through HBM).
-    const bool tc_full =
-        h->use_tc && !h->tc_no_full && partials != nullptr && !(flags & BX_SCORE_RF_PAIRWISE) && !fuse_rf &&
-        (forest ? qf.enabled && !qf.has_real && tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, &qf, true, h->tc_dmma) <=
-                                    227 * 1024
-                : !h->has_forest &&
-                      tc_smem_bytes(h->gp_n, h->n_params, h->n_kendall, h->row_words, nullptr, true, h->tc_dmma) <= 227 * 1024);
-    if (tc_full) {
-      h->rf_after_gp = false;
-      if (timing) {
-        BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
-        BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
-        BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
-      }
-      FusedArgs f = fused_args(h, rows, q, f_model);
-      if (forest) f.qs = qf;
-      SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
-      m.track_prob = track_prob ? 1 : 0;
-      h->tc_summ = &m;
-      const cudaError_t e = launch_posterior(h, f, s);
-      h->tc_summ = nullptr;
-      BX_CUDA(h, e);
-      if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
-      const int64_t tiles = (q + 127) / 128;
-      *n_partials = (int)(tiles < h->sm_count ? tiles : h->sm_count);
-      return BX_OK;
-    }
-    // QuickScorer forest + summary in one kernel after the posterior (it reads the EI): used
-    // whenever a summary is wanted and the tables fit.
-    const bool rf_summ = forest && !fuse_rf && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
-                         h->use_tc && qs_summary_available(h->forest);
+    // posterior (mean / var) -> forest -> summary.  With a summary wanted and QuickScorer tables
+    // that fit, the forest and the summary are one kernel after the posterior (it evaluates the EI
+    // only for the candidates whose probability passes eps_f); otherwise the stand-alone forest
+    // kernel runs before the posterior and the summary kernel after it.  The forest and posterior
+    // kernels each fill every SM's shared memory, so they run back to back on the caller's stream
+    // (which also makes the per-kernel CUDA-event timing exact).
+    const bool rf_summ = forest && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
+                         qs_summary_available(h->forest);
     h->rf_after_gp = rf_summ;
     // a stand-alone forest kernel before the posterior reads the rows: a streaming pool must be in
-    if (rows_ready && forest && !fuse_rf && !rf_summ) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
+    if (rows_ready && forest && !rf_summ) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
     if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
-    if (forest && !fuse_rf && !rf_summ)
+    if (forest && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
                            h->d_probs.as<double>(), s));
     if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
-    // the posterior writes mean / var and the summary kernel after it evaluates the EI (only for the
-    // candidates whose probability passes eps_f) — the posterior's epilogue is on its critical path
     BX_CUDA(h, h->d_ei.ensure((size_t)q * 16));
     FusedArgs f = fused_args(h, rows, q, f_model);
-    if (fuse_rf) {
-      f.ei_out = h->d_ei.as<double>();
-    } else {
-      f.mean_out = h->d_ei.as<double>();
-      f.var_out = h->d_ei.as<double>() + q;
-    }
-    if (fuse_rf) {
-      if (h->use_tc) f.qs = qf;
-      else f.kf = kf;
-      f.probs_out = h->d_probs.as<double>();
-    }
+    f.mean_out = h->d_ei.as<double>();
+    f.var_out = h->d_ei.as<double>() + q;
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
     BX_CUDA(h, launch_posterior(h, f, s));
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
-    if (!fuse_rf) {
-      m.mean = h->d_ei.as<double>();
-      m.var = h->d_ei.as<double>() + q;
-      m.f_model = f_model;
-    }
+    m.mean = h->d_ei.as<double>();
+    m.var = h->d_ei.as<double>() + q;
+    m.f_model = f_model;
     if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));  // streaming pool fully copied
     if (rf_summ) {
       if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
@@ -1376,7 +1429,12 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->row_words;
-  if (h->use_tc && !getenv("BX_HOST_CHUNKED")) {
+  BX_CUDA(h, h->d_pool.ensure((size_t)q * W * 4));
+  BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
+  BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
+  uint32_t* pool = h->d_pool.as<uint32_t>();
+  Partial* parts = h->d_partials.as<Partial>();
+  if (h->use_tc) {
     // Streaming: the whole pool is copied in 2^16-row chunks on the copy stream, each followed by a
     // 4-byte ready flag written by the copy engine; one posterior launch consumes tiles as their
     // chunk lands (the row prefetcher waits on the flag), so only the first chunk's copy is
@@ -1384,7 +1442,6 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     // last copy.
     const int shift = 16;
     const int64_t n_chunks = (q + (1 << shift) - 1) >> shift;
-    BX_CUDA(h, h->d_pool.ensure((size_t)q * W * 4));
     BX_CUDA(h, h->d_ready.ensure((size_t)n_chunks * 4));
     if (h->h_ones_len < n_chunks) {
       if (h->h_ones) cudaFreeHost(h->h_ones);
@@ -1393,27 +1450,23 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
       for (int64_t i = 0; i < n_chunks; ++i) h->h_ones[i] = 1u;
       h->h_ones_len = n_chunks;
     }
-    BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
-    BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
-    uint32_t* pool = h->d_pool.as<uint32_t>();
     uint32_t* ready = h->d_ready.as<uint32_t>();
     BX_CUDA(h, cudaMemsetAsync(ready, 0, (size_t)n_chunks * 4, s));
-    BX_CUDA(h, cudaEventRecord(h->ev_done[0], s));
-    BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[0], 0));
+    BX_CUDA(h, cudaEventRecord(h->ev_done, s));
+    BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done, 0));
     for (int64_t c = 0; c < n_chunks; ++c) {
       const int64_t off = c << shift, len = std::min<int64_t>((int64_t)1 << shift, q - off);
       BX_CUDA(h, cudaMemcpyAsync(pool + (size_t)off * W, host_rows + (size_t)off * W, (size_t)len * W * 4,
                                  cudaMemcpyHostToDevice, h->copy_stream));
       BX_CUDA(h, cudaMemcpyAsync(ready + c, h->h_ones + c, 4, cudaMemcpyHostToDevice, h->copy_stream));
     }
-    BX_CUDA(h, cudaEventRecord(h->ev_copy[0], h->copy_stream));
-    Partial* parts = h->d_partials.as<Partial>();
-    for (int pass = 0; pass < 2; ++pass) {
+    BX_CUDA(h, cudaEventRecord(h->ev_copy, h->copy_stream));
+    for (int pass = 0; pass < 2; ++pass) {  // pass 2 (probability tracker) only if every value is -inf
       int np = 0;
       h->stream_ready = pass == 0 ? ready : nullptr;
       h->stream_shift = shift;
       r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_NO_SUMMARY, nullptr,
-                     nullptr, parts, &np, s, false, pass == 1, pass == 0 ? h->ev_copy[0] : nullptr);
+                     nullptr, parts, &np, s, false, pass == 1, pass == 0 ? h->ev_copy : nullptr);
       h->stream_ready = nullptr;
       if (r) return r;
       BX_CUDA(h, launch_summary_merge(parts, np, space_dev(h), k, nullptr, 0,
@@ -1422,90 +1475,12 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
       BX_CUDA(h, cudaStreamSynchronize(s));
       if (summary->n_finite != 0) break;
     }
-    for (int i = 0; i < summary->n_top; ++i)
-      std::memcpy(summary->top[i].row, host_rows + (size_t)(summary->top[i].index - index_base) * W,
-                  (size_t)W * 4);
-    return BX_OK;
-  }
-  // chunks of 2^17, 2^18, then 2^19 rows through a 2-buffer ring: the first copy, which nothing
-  // overlaps, stays short, and later chunks are large enough that per-launch costs vanish (measured
-  // on B200 over PCIe at 26 GB/s; BX_HOST_CHUNK / _RAMP / _BUFS override for tuning)
-  int64_t chunk = 1 << 19;
-  int ramp = 2, nbuf = 2;
-  if (const char* e = getenv("BX_HOST_CHUNK")) chunk = (int64_t)1 << atoi(e);   // tuning aids
-  if (const char* e = getenv("BX_HOST_RAMP")) ramp = atoi(e);
-  if (const char* e = getenv("BX_HOST_BUFS")) nbuf = std::max(1, std::min(bx_handle::kHostBufs, atoi(e)));
-  auto chunk_len = [&](int64_t c) -> int64_t { return c >= ramp ? chunk : (chunk >> (ramp - c)); };
-  int64_t n_chunks = 0;
-  for (int64_t off = 0; off < q; off += chunk_len(n_chunks), ++n_chunks) {}
-  const size_t per_chunk = (size_t)max_partials(h->sm_count);
-  BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * per_chunk * (size_t)n_chunks));
-  BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
-  for (int b = 0; b < bx_handle::kHostBufs; ++b) BX_CUDA(h, h->d_host_rows[b].ensure((size_t)chunk * W * 4));
-  Partial* base = h->d_partials.as<Partial>();
-  // Partials per chunk: one per SM (forest + summary kernel) or two (summary kernel).  They are
-  // merged once at the end when all of them fit the fast merge, else folded into a running
-  // partial after every chunk.
-  const bool rf_summ = h->use_tc && h->has_forest && h->forest.has_trees && qs_summary_available(h->forest);
-  const int64_t np_max = fused_path(h) ? (rf_summ ? 1 : 2) * (int64_t)h->sm_count : (int64_t)per_chunk;
-  const bool fits_once = np_max * n_chunks <= 1024 &&
-                         np_max * n_chunks * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
-  const bool running = !fits_once && np_max + 1 <= 1024 &&
-                       (np_max + 1) * (k > 0 ? k : 1) * (int64_t)sizeof(TopRec) <= 200 * 1024;
-  // BX_HOST_TRACE=1: per-chunk copy / compute timeline on stderr (pipeline tuning aid)
-  const bool trace = getenv("BX_HOST_TRACE") != nullptr;
-  std::vector<cudaEvent_t> tev;
-  if (trace) {
-    tev.resize(4 * n_chunks + 1);
-    for (auto& e : tev) cudaEventCreate(&e);
-    cudaEventRecord(tev[4 * n_chunks], s);
-  }
-  // pass 1 without the probability tracker; pass 2 (with it) only if every value is -inf
-  for (int pass = 0; pass < 2; ++pass) {
-  int total = 0;
-  for (int b = 0; b < bx_handle::kHostBufs; ++b) BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
-  int64_t off = 0;
-  for (int64_t c = 0; c < n_chunks; off += chunk_len(c), ++c) {
-    const int b = (int)(c % nbuf);
-    const int64_t len = (q - off) < chunk_len(c) ? (q - off) : chunk_len(c);
-    // the copy into buffer b waits until the kernels that last read buffer b are done
-    BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done[b], 0));
-    if (trace && pass == 0) cudaEventRecord(tev[4 * c], h->copy_stream);
-    BX_CUDA(h, cudaMemcpyAsync(h->d_host_rows[b].p, host_rows + (size_t)off * W, (size_t)len * W * 4,
-                               cudaMemcpyHostToDevice, h->copy_stream));
-    BX_CUDA(h, cudaEventRecord(h->ev_copy[b], h->copy_stream));
-    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 1], h->copy_stream);
-    BX_CUDA(h, cudaStreamWaitEvent(s, h->ev_copy[b], 0));
-    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 2], s);
-    int np = 0;
-    // running merge: the chunk's partials land at base + 1 and are folded into base[0]
-    Partial* dst = running ? base + 1 : base + total;
-    r = score_impl(h, h->d_host_rows[b].as<uint32_t>(), len, index_base + off, f_model, eps_f, k,
-                   flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr, dst, &np, s, false,
-                   pass == 1);
+  } else {
+    // the other posterior kernels: one copy, then the device-resident path
+    BX_CUDA(h, cudaMemcpyAsync(pool, host_rows, (size_t)q * W * 4, cudaMemcpyHostToDevice, s));
+    r = bx_score(h, pool, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr,
+                 summary, stream);
     if (r) return r;
-    if (running)
-      BX_CUDA(h, c == 0 ? launch_partial_merge(base + 1, np, space_dev(h), k, base, s)
-                        : launch_partial_merge(base, np + 1, space_dev(h), k, base, s));
-    total = running ? 1 : total + np;
-    BX_CUDA(h, cudaEventRecord(h->ev_done[b], s));
-    if (trace && pass == 0) cudaEventRecord(tev[4 * c + 3], s);
-  }
-  BX_CUDA(h, launch_summary_merge(base, total, space_dev(h), k, nullptr, 0,
-                                  h->d_summary.as<bx_score_summary>(), s));
-  BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary),
-                             cudaMemcpyDeviceToHost, s));
-  BX_CUDA(h, cudaStreamSynchronize(s));
-  if (summary->n_finite != 0 || !fused_path(h)) break;
-  }
-  if (trace) {
-    for (int64_t c = 0; c < n_chunks; ++c) {
-      float t[4];
-      for (int e = 0; e < 4; ++e) cudaEventElapsedTime(&t[e], tev[4 * n_chunks], tev[4 * c + e]);
-      fprintf(stderr, "chunk %lld len %lld: copy %.3f-%.3f ms, compute %.3f-%.3f ms\n", (long long)c,
-              (long long)chunk_len(c), t[0], t[1], t[2], t[3]);
-    }
-    for (auto& e : tev) cudaEventDestroy(e);
   }
   // the pool is host-resident: the top-k rows come straight from the caller's buffer
   for (int i = 0; i < summary->n_top; ++i)

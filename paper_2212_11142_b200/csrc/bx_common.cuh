@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "../../include/bx_sm100.h"
@@ -107,22 +108,6 @@ struct CodedForestDev {
   int32_t nodes_in_smem;     // node table + leaf values copied to shared memory
 };
 
-// Compact forest for the GP kernel's fused walk (gp_fused.cu): 32-bit nodes
-//   internal: [31] 0, [30:25] code slot, [24:16] cut, [15:0] left-child offset (right = left + 1)
-//   leaf:     [31] 1, [30:0] 0 (offset 0 -> the walk stays); value = uval[vid[node]]
-// Available when there are no real splits, every cut and code fits 9 bits and every tree has
-// fewer than 65536 nodes.
-struct CompactForestDev {
-  const uint32_t* nodes;
-  const uint16_t* vid;       // [n_nodes] unique-value id of leaves
-  const double* uval;        // [n_uvals] distinct leaf values
-  const int32_t* roots;
-  const int32_t* code_param;
-  const int32_t* code_sub;
-  int32_t n_nodes, n_uvals, n_trees, max_depth, n_codes;
-  int32_t enabled;
-};
-
 // QuickScorer-style tables (Lucchese et al., SIGIR 2015) over the integer codes: leaves of every
 // tree are numbered left to right; a node whose test goes right (code >= cut) rules out its left
 // subtree's leaves, and the exit leaf is the leftmost leaf no such node rules out.  mask[t][s][v]
@@ -143,6 +128,15 @@ struct QsForestDev {
   // offset | count << 16 into rthr and its value is the number of thresholds below the coordinate
   const double* rthr;
   int32_t has_real;
+  // indirect slots (real parameters with many distinct thresholds across the forest): per tree only
+  // the few masks its own splits produce are stored (imask), and a [code][tree] table of u16
+  // indices into imask replaces the [code][tree] u64 mask rows (4x smaller), so the forest's
+  // tables fit in shared memory; the slots' codes are computed like a real code (code_sub)
+  int32_t n_ind;
+  int32_t ind_param[2], ind_sub[2], ind_off[2];  // ind_off: first row of the slot in iidx
+  const uint16_t* iidx;      // [rows][itpad] index into imask
+  const uint64_t* imask;     // [n_imask]
+  int32_t itpad, n_iidx_rows, n_imask;
 };
 
 struct ForestDev {
@@ -154,7 +148,6 @@ struct ForestDev {
   int32_t coded;         // 1 -> use `cf` (integer-coded fast path)
   double constant;       // single-class shortcut (feasibility.py:73-74)
   CodedForestDev cf;
-  CompactForestDev kf;
   QsForestDev qs;
 };
 
@@ -386,9 +379,6 @@ struct FusedArgs {
   int32_t perm_param[BX_MAX_PARAMS];
   double exp2tab[64];     // 2^(j/64), correctly rounded (host long double)
   int32_t precise;        // 1 -> libm sqrt/exp in the Matérn (BX_MATERN_PRECISE=1)
-  CompactForestDev kf;    // kf.enabled -> walk the forest inside the kernel, write probs_out
-  QsForestDev qs;         // gp_tc.cu: qs.enabled -> evaluate the forest inside the kernel
-  double* probs_out;
 };
 
 // Feasibility weight, eps_f filter and per-warp summaries over precomputed EI (score_summary.cu).
@@ -416,10 +406,49 @@ struct SummaryArgs {
 };
 
 // Tensor-core posterior (gp_tc.cu): FusedArgs plus the digit-sliced [L^-1; alpha^T].
+// One coordinate of the Euclidean embedding of the weighted distance W (surrogate.py:173-223):
+// W(x, y) = sum_k sq_k(x, y) / l_k^2 = |e(x) - e(y)|^2 for every metric except the naive
+// permutation indicator.  Numeric: coord / l; categorical (1{a != b}): the L labels as the vertices
+// of a unit-edge simplex in L - 1 dimensions (Helmert basis); Spearman: the position vector in the
+// m - 1 dimensional sum-zero subspace; Kendall: the m(m-1)/2 pair-order indicators; Hamming: per
+// position the simplex of the m values.  Each coordinate is scaled by sqrt(weight) and centred on
+// the training mean, and its values come from a table, so host (training points) and device
+// (candidates) evaluate the identical expression.
+enum { BX_EMB_CODE = 0, BX_EMB_REAL = 1, BX_EMB_PERM_LIN = 2, BX_EMB_KENDALL = 3, BX_EMB_PERM_HOT = 4 };
+struct EmbDim {
+  int32_t kind;
+  int32_t word;   // row word of the parameter
+  int32_t a, b;   // KENDALL: positions a < b; PERM_HOT: position a
+  int32_t m;      // permutation size
+  int32_t off;    // first table entry
+};
+
+__host__ __device__ __forceinline__ int emb_elem(uint64_t x, int m, int i) {
+  return (int)((x >> (4 * (m - 1 - i))) & 15u);  // element at position i (0-based value)
+}
+// CODE: tab[off + domain index]; REAL: coord * tab[off] + tab[off + 1]; PERM_LIN: tab[off + m] +
+// sum_i elem_i * tab[off + i]; KENDALL: tab[off + (elem_a < elem_b)]; PERM_HOT: tab[off + elem_a]
+__host__ __device__ __forceinline__ double emb_value(const EmbDim& e, const uint32_t* row, const double* tab) {
+  if (e.kind == BX_EMB_CODE) return tab[e.off + (int)row[e.word]];
+  if (e.kind == BX_EMB_REAL) {
+    const uint64_t bits = (uint64_t)row[e.word + 2] | ((uint64_t)row[e.word + 3] << 32);
+    double x;
+    memcpy(&x, &bits, 8);
+    return fma(x, tab[e.off], tab[e.off + 1]);
+  }
+  const uint64_t x = (uint64_t)row[e.word] | ((uint64_t)row[e.word + 1] << 32);
+  if (e.kind == BX_EMB_KENDALL) return tab[e.off + (emb_elem(x, e.m, e.a) < emb_elem(x, e.m, e.b) ? 1 : 0)];
+  if (e.kind == BX_EMB_PERM_HOT) return tab[e.off + emb_elem(x, e.m, e.a)];
+  double acc = tab[e.off + e.m];
+  for (int i = 0; i < e.m; ++i) acc = fma((double)emb_elem(x, e.m, i), tab[e.off + i], acc);
+  return acc;
+}
+
 struct TcArgs {
   FusedArgs f;
   const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 16 rows x 32 columns
-  const double* rowscale;     // [32 * n_chunks] 2^(e_i - 56) * sc (0 beyond row n)
+  const double* rowscale;     // [16 * n_chunks] 2^(e_i - 56) * sc (0 beyond row n), then the same
+                              // with the alpha / padding rows zeroed, then (tc_row_scale) digit scales
   int32_t n_slices;           // ceil(n / 32) column slices of K*
   int32_t n_chunks;           // floor(n / 16) + 1 row chunks of [L^-1; alpha^T]
   double kscale;              // 2^40 / sc: K* -> 40-bit fixed point
@@ -432,38 +461,34 @@ struct TcArgs {
   // is in device memory (written by the copy stream after the chunk), null = all rows present
   const uint32_t* ready;
   int32_t ready_shift;
-  // summ_on: the whole acquisition step in this kernel — the decoder warps evaluate the QuickScorer
-  // forest (f.qs), the epilogue forms value = -inf if p < eps_f else EI * p and keeps per-warp
-  // partials (stable top-k, trackers) merged into summ.partials[blockIdx.x]
-  SummaryArgs summ;
-  int32_t summ_on;
-  // dot != 0 (all-numeric spaces whose centred coordinates are small, checked on the host):
-  // W = |x'|^2 + |y'|^2 - 2 x'.y' on coordinates centred by mu (scaled units), 12 FP64 operations
-  // per pair instead of 2 per dimension
-  const double* mu;           // [n_params]
-  int32_t dot;
   // mat_resident != 0: every (chunk, slice) digit block is loaded into shared memory once per CTA
   // and stays there for all tiles (set by launch_gp_tc when it fits; else the 8-stage ring)
   int32_t mat_resident;
   // n > 255 (two passes per tile): [grid][256 rows][128 candidates] pass-0 partial sums of the
   // rows >= 256, written and read back by the same epilogue thread; null otherwise
   double* part;
-  // dmma != 0 (centred all-numeric spaces): producers compute the distances on FP64 DMMA and the
-  // matrix digits carry the C-fragment column permutation (launch_build_mdig perm)
-  int32_t dmma;
+  // ks > 0: distances on the FP64 tensor cores, W = |x'|^2 + |y'|^2 - 2 x'.y' over the embedding
+  // (EmbDim) as one product of ks k-steps of DMMA m8n8k4; the matrix digits carry the C-fragment
+  // column permutation (launch_build_mdig perm).  ks == 0: FMA distances per parameter kind.
+  int32_t ks;
+  int32_t n_emb;              // E embedding coordinates (4 ks >= E)
+  int32_t aug;                // E + 2 <= 4 ks: k-rows E, E + 1 carry |y'|^2 . 1 and 1 . |x'|^2
+  const EmbDim* emb;          // [E]
+  const double* emb_tab;
+  int32_t emb_tab_len;
+  const double* emb_planes;   // [4 ks][32 n_slices] the B operand: -2 y', (aug: |y'|^2, 1), zeros
+  const double* emb_yy;       // [32 n_slices] |y'|^2 (added explicitly when !aug)
 };
 
 
 int fused_max_rows();
 size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8);
-size_t fused_smem_bytes_forest(int n, int n_params, int n_kendall, int rows8,
-                               const CompactForestDev& kf);
 size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs = nullptr,
-                     bool summ = false, bool dmma = false);
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, int ks, int n_emb, int emb_tab_len,
+                     bool aug, bool resident);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, int perm, cudaStream_t s);

@@ -256,29 +256,85 @@ __device__ __forceinline__ void sts_s32(uint32_t a, int32_t v) {
   asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Tables: masks [stride][tpad] u64, distinct leaf values, leaf value ids [n_trees][64] u16, and the
-// per-thread mask-row offsets [n_codes][kQsThreads]; every access is an explicit shared load.
+// Shared-memory image of the QuickScorer tables: masks [stride][tpad] u64, distinct leaf values,
+// leaf value ids [n_trees][64] u16, indirect-slot indices [rows][itpad] u16 and masks, then (when
+// `offs`) the per-thread mask-row offsets [n_codes][kQsThreads]
+struct QsSmem {
+  size_t mask, uval, vid, iidx, imask, offs, end;
+};
+__host__ __device__ inline QsSmem qs_smem_layout(const QsForestDev& f, bool offs) {
+  QsSmem L;
+  size_t o = 0;
+  L.mask = o;
+  o += (size_t)f.stride * f.tpad * 8;
+  L.uval = o;
+  o += (size_t)f.n_uvals * 8;
+  L.vid = o;
+  o += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
+  L.iidx = o;
+  o += f.n_ind ? (((size_t)f.n_iidx_rows * f.itpad * 2 + 15) & ~(size_t)15) : 0;
+  L.imask = o;
+  o += f.n_ind ? (size_t)f.n_imask * 8 : 0;
+  L.offs = o;
+  o += offs ? (size_t)f.n_codes * kQsThreads * 4 : 0;
+  L.end = (o + 15) & ~(size_t)15;
+  return L;
+}
+
+__device__ void qs_load_tables(const QsForestDev& f, unsigned char* smem, const QsSmem& L) {
+  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem + L.mask);
+  double* s_uval = reinterpret_cast<double*>(smem + L.uval);
+  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + L.vid);
+  for (int i = threadIdx.x; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
+  for (int i = threadIdx.x; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
+  for (int i = threadIdx.x; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
+  if (f.n_ind) {
+    uint16_t* s_iidx = reinterpret_cast<uint16_t*>(smem + L.iidx);
+    uint64_t* s_imask = reinterpret_cast<uint64_t*>(smem + L.imask);
+    for (int i = threadIdx.x; i < f.n_iidx_rows * f.itpad; i += blockDim.x) s_iidx[i] = f.iidx[i];
+    for (int i = threadIdx.x; i < f.n_imask; i += blockDim.x) s_imask[i] = f.imask[i];
+  }
+}
+
+// indirect slots of one candidate: the shared address of its index row (tree 0)
+__device__ __forceinline__ void qs_ind_rows(const QsForestDev& f, const bx_param_desc* params, const uint32_t* row,
+                                            uint32_t iidx_s, uint32_t (&irow)[2]) {
+  for (int i = 0; i < 2; ++i)
+    irow[i] = i < f.n_ind
+                  ? iidx_s + 2u * (uint32_t)((f.ind_off[i] + qs_code(params[f.ind_param[i]], row, f.ind_sub[i], f.rthr)) * f.itpad)
+                  : 0u;
+}
+
+// the indirect slots' masks of trees g0 .. g0 + 7 ANDed into m
+__device__ __forceinline__ void qs_ind_and(const QsForestDev& f, const uint32_t (&irow)[2], uint32_t imask_s, int g0,
+                                           uint64_t (&m)[kQsGroup]) {
+  for (int i = 0; i < f.n_ind; ++i) {
+    const uint32_t ir = irow[i] + 2u * (uint32_t)g0;
+    const uint64_t w0 = lds_u64(ir), w1 = lds_u64(ir + 8u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m[j] &= lds_u64(imask_s + 8u * (uint32_t)((w0 >> (16 * j)) & 0xFFFFu));
+      m[4 + j] &= lds_u64(imask_s + 8u * (uint32_t)((w1 >> (16 * j)) & 0xFFFFu));
+    }
+  }
+}
+
+// Stand-alone probabilities (predict_proba_batch) in either numpy summation order.
 __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForestDev f, const uint32_t* rows,
                                                            int64_t q, int use_pairwise, double* probs) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
-  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem);
-  size_t off = (size_t)f.stride * f.tpad * 8;
-  double* s_uval = reinterpret_cast<double*>(smem + off);
-  off += (size_t)f.n_uvals * 8;
-  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + off);
-  off += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
-  int32_t* s_off = reinterpret_cast<int32_t*>(smem + off);
+  const QsSmem L = qs_smem_layout(f, true);
   for (int i = threadIdx.x; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(sp.params)[i];
-  for (int i = threadIdx.x; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
-  for (int i = threadIdx.x; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
-  for (int i = threadIdx.x; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
+  qs_load_tables(f, smem, L);
   __syncthreads();
-  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(s_mask);
-  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(s_uval);
-  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(s_vid);
-  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(s_off) + 4u * threadIdx.x;
+  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(smem + L.mask);
+  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(smem + L.uval);
+  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(smem + L.vid);
+  const uint32_t iidx_s = (uint32_t)__cvta_generic_to_shared(smem + L.iidx);
+  const uint32_t imask_s = (uint32_t)__cvta_generic_to_shared(smem + L.imask);
+  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(smem + L.offs) + 4u * threadIdx.x;
   auto leaf = [=](int t, uint64_t m) {
     const uint32_t id = lds_u16(vid_s + 2u * (uint32_t)(t * 64 + __ffsll((long long)m) - 1));
     return __longlong_as_double((long long)lds_u64(uval_s + 8u * id));
@@ -289,6 +345,8 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
     for (int c = 0; c < f.n_codes; ++c)
       sts_s32(off_s + 4u * kQsThreads * c,
               (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
+    uint32_t irow[2];
+    qs_ind_rows(f, params, row, iidx_s, irow);
     double sum = 0.0;
     if (use_pairwise) {
       sum = pairwise(
@@ -296,6 +354,8 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
             uint64_t m = ~0ull;
             for (int c = 0; c < f.n_codes; ++c)
               m &= lds_u64(mask_s + 8u * (uint32_t)(lds_s32(off_s + 4u * kQsThreads * c) + t));
+            for (int k = 0; k < f.n_ind; ++k)
+              m &= lds_u64(imask_s + 8u * lds_u16(irow[k] + 2u * (uint32_t)t));
             return leaf(t, m);
           },
           0, f.n_trees);
@@ -313,6 +373,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
             m[2 * j + 1] &= w.y;
           }
         }
+        qs_ind_and(f, irow, imask_s, g0, m);
 #pragma unroll
         for (int j = 0; j < kQsGroup; ++j)
           if (g0 + j < f.n_trees) {
@@ -326,36 +387,30 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
 }
 
 // QuickScorer forest fused with the acquisition summary (the work of summary_kernel): runs after the
-// posterior kernel, reads its EI, applies value = -inf if p < eps_f else EI * p (acquisition.py:
-// 77-79) and keeps per-warp partials (stable top-k, both trackers) merged into one per block.
-// NC > 0: exactly NC code slots, the candidate's mask-row addresses held in registers and two slots'
-// loads issued back to back; NC == 0: any slot count (offsets through shared memory)
+// posterior kernel, reads its mean / variance, applies value = -inf if p < eps_f else EI * p
+// (acquisition.py:77-79; the EI only for the candidates that pass) and keeps per-warp partials
+// (stable top-k, trackers) merged into one per block.  NC > 0: exactly NC direct code slots, the
+// candidate's mask-row addresses held in registers and two slots' loads issued back to back;
+// NC == 0: any slot count (offsets through shared memory).
 template <int NC>
 __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, QsForestDev f, SummaryArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
-  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem);
-  size_t off = (size_t)f.stride * f.tpad * 8;
-  double* s_uval = reinterpret_cast<double*>(smem + off);
-  off += (size_t)f.n_uvals * 8;
-  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + off);
-  off += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
-  int32_t* s_off = reinterpret_cast<int32_t*>(smem + off);
-  if constexpr (NC == 0) off += (size_t)f.n_codes * kQsThreads * 4;
-  Partial* parts = reinterpret_cast<Partial*>(smem + ((off + 15) & ~(size_t)15));  // [warps]
+  const QsSmem L = qs_smem_layout(f, NC == 0);
+  Partial* parts = reinterpret_cast<Partial*>(smem + L.end);  // [warps]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(sp.params)[i];
-  for (int i = tid; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
-  for (int i = tid; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
-  for (int i = tid; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
+  qs_load_tables(f, smem, L);
   Partial* summ = &parts[warp];
   if (lane == 0) partial_init(summ);
   __syncthreads();
-  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(s_mask);
-  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(s_uval);
-  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(s_vid);
-  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(s_off) + 4u * tid;
+  const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(smem + L.mask);
+  const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(smem + L.uval);
+  const uint32_t vid_s = (uint32_t)__cvta_generic_to_shared(smem + L.vid);
+  const uint32_t iidx_s = (uint32_t)__cvta_generic_to_shared(smem + L.iidx);
+  const uint32_t imask_s = (uint32_t)__cvta_generic_to_shared(smem + L.imask);
+  const uint32_t off_s = (uint32_t)__cvta_generic_to_shared(smem + L.offs) + 4u * tid;
   const int words = sp.row_words;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + warp * 32; base < a.q; base += stride) {
@@ -373,6 +428,8 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
         for (int c = 0; c < f.n_codes; ++c)
           sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
       }
+      uint32_t irow[2];
+      qs_ind_rows(f, params, row, iidx_s, irow);
       double sum = 0.0;
       for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {
         uint64_t m[kQsGroup];
@@ -409,6 +466,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
             }
           }
         }
+        qs_ind_and(f, irow, imask_s, g0, m);
 #pragma unroll
         for (int j = 0; j < kQsGroup; ++j)
           if (g0 + j < f.n_trees) {
@@ -461,10 +519,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
   for (int i = tid; i < (int)(sizeof(Partial) / 4); i += kQsThreads) dst[i] = src[i];
 }
 
-size_t qs_smem(const QsForestDev& f) {
-  return (size_t)f.stride * f.tpad * 8 + (size_t)f.n_uvals * 8 + (((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15) +
-         (size_t)f.n_codes * kQsThreads * 4;
-}
+size_t qs_smem(const QsForestDev& f) { return qs_smem_layout(f, true).end; }
 
 size_t coded_smem(const CodedForestDev& cf, bool in_smem) {
   return (in_smem ? ((size_t)cf.n_nodes + cf.n_leaves) * 8 + (((size_t)cf.n_nodes * 4 + 15) & ~(size_t)15) : 0) +
@@ -481,9 +536,7 @@ auto pick_real(bool real) {
 constexpr int kQsMaxNC = 24;
 
 size_t qs_summary_smem(const QsForestDev& f) {
-  const size_t offs = f.n_codes > kQsMaxNC ? (size_t)f.n_codes * kQsThreads * 4 : 0;
-  return ((qs_smem(f) - (size_t)f.n_codes * kQsThreads * 4 + offs + 15) & ~(size_t)15) +
-         (size_t)(kQsThreads / 32) * sizeof(Partial);
+  return qs_smem_layout(f, f.n_codes > kQsMaxNC).end + (size_t)(kQsThreads / 32) * sizeof(Partial);
 }
 
 }  // namespace

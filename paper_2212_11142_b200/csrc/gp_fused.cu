@@ -11,8 +11,7 @@
 // rows above the diagonal block of a panel are never copied.  The epilogue de-standardises, takes
 // max(σ - Σv², 0) and the expected improvement (acquisition.py:40-51) and writes EI (or mean /
 // variance for predict_batch).  The feasibility weight, eps_f filter and summaries are applied by
-// summary_kernel (score_summary.cu), concurrently with nothing: the forest runs on a second stream
-// while this kernel occupies the FP64 pipe.
+// the forest / summary kernels after it (score_summary.cu, forest.cu).
 #include "bx_common.cuh"
 #include "matern.cuh"
 
@@ -65,13 +64,10 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 struct FusedLayout {
-  int par, planes, kmask, abuf, cand, tile, bar, exp2, rf_nodes, rf_vid, rf_uval, rf_roots, rf_codes,
-      total;
+  int par, planes, kmask, abuf, cand, tile, bar, exp2, total;
 };
 
-__host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params, int n_kendall,
-                                                    int rows8, int kf_nodes = 0, int kf_uvals = 0,
-                                                    int kf_trees = 0, int kf_codes = 0) {
+__host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params, int n_kendall, int rows8) {
   FusedLayout L;
   int off = 0;
   L.par = off;
@@ -92,17 +88,6 @@ __host__ __device__ inline FusedLayout fused_layout(int nw, int n, int n_params,
   off += 2 * 8;
   L.exp2 = off;
   off += 64 * 8;
-  // fused forest walk (CompactForestDev): nodes, leaf value ids, distinct values, roots, codes
-  L.rf_nodes = off;
-  off += kf_nodes * 4;
-  L.rf_vid = off;
-  off += (kf_nodes * 2 + 15) & ~15;
-  L.rf_uval = off;
-  off += kf_uvals * 8;
-  L.rf_roots = off;
-  off += (kf_trees * 4 + 15) & ~15;
-  L.rf_codes = off;  // per warp: [8 candidates][n_codes] int32
-  off += nw * 8 * kf_codes * 4;
   L.total = off;
   return L;
 }
@@ -120,24 +105,7 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
   const int n_params = a.space.n_params, words = a.space.row_words;
   const int n = a.gp.n;
   const int rows8 = 8 * MT;
-  const CompactForestDev& kf = a.kf;
-  const bool rf = kf.enabled != 0;
-  const FusedLayout L = rf ? fused_layout(nw, n, n_params, a.n_kendall, rows8, kf.n_nodes, kf.n_uvals,
-                                          kf.n_trees, kf.n_codes)
-                           : fused_layout(nw, n, n_params, a.n_kendall, rows8);
-  uint32_t* rf_nodes = reinterpret_cast<uint32_t*>(smem + L.rf_nodes);
-  uint16_t* rf_vid = reinterpret_cast<uint16_t*>(smem + L.rf_vid);
-  double* rf_uval = reinterpret_cast<double*>(smem + L.rf_uval);
-  int32_t* rf_roots = reinterpret_cast<int32_t*>(smem + L.rf_roots);
-  int32_t* rf_codes = reinterpret_cast<int32_t*>(smem + L.rf_codes) + warp * 8 * kf.n_codes;
-  if (rf) {
-    for (int i = tid; i < kf.n_nodes; i += blockDim.x) {
-      rf_nodes[i] = kf.nodes[i];
-      rf_vid[i] = kf.vid[i];
-    }
-    for (int i = tid; i < kf.n_uvals; i += blockDim.x) rf_uval[i] = kf.uval[i];
-    for (int i = tid; i < kf.n_trees; i += blockDim.x) rf_roots[i] = kf.roots[i];
-  }
+  const FusedLayout L = fused_layout(nw, n, n_params, a.n_kendall, rows8);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -207,57 +175,13 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       cmask[(k * 8 + cc) * 2] = lo;
       cmask[(k * 8 + cc) * 2 + 1] = hi;
     }
-    if (rf) {  // forest codes of the 8 candidates (one per encode_configs column)
-      for (int idx = lane; idx < 8 * kf.n_codes; idx += 32) {
-        const int cc = idx / kf.n_codes, s = idx % kf.n_codes;
-        const int64_t gi = cbase + cc;
-        int v = 0;
-        if (gi < a.q) {
-          const uint32_t* row = a.rows + (size_t)gi * words;
-          const bx_param_desc& p = params[kf.code_param[s]];
-          if (p.kind == BX_PERMUTATION) v = perm_pos(row_u64(row, p.word), p.size, kf.code_sub[s]);
-          else if (p.kind == BX_CATEGORICAL) v = (int)row[p.word] == kf.code_sub[s] ? 1 : 0;
-          else v = (int)row[p.word];
-        }
-        rf_codes[idx] = v;
-      }
-    }
     __syncwarp();
 
     double acc[MT][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-    // forest walk interleaved with the chunks: lane (c, fk) walks trees 4r + fk; lane (c, 0)
-    // keeps the running sum of candidate c in tree order (feasibility.py:89, q >= 2 order)
-    const int rounds = rf ? (kf.n_trees + 3) / 4 : 0;
-    const int rounds_per_chunk = (rounds + n_chunks - 1) / n_chunks;
-    int round = 0;
-    double psum = 0.0;
-    const int32_t* my_codes = rf_codes + c * kf.n_codes;
-
     for (int chunk = 0; chunk < n_chunks; ++chunk) {
       const int buf = chunk & 1;
-      for (int rr = 0; rr < rounds_per_chunk && round < rounds; ++rr, ++round) {
-        const int t = 4 * round + fk;
-        int cur = rf_roots[t < kf.n_trees ? t : 0];
-        for (int it = 0; it <= kf.max_depth; ++it) {
-          const uint32_t nd = rf_nodes[cur];
-          const uint32_t off = nd & 0xFFFFu;
-          if (__all_sync(0xffffffffu, off == 0u)) break;  // every lane sits on a leaf
-          cur += (int)off + (my_codes[(nd >> 25) & 63u] >= (int)((nd >> 16) & 511u) ? 1 : 0);
-        }
-        const double v = rf_uval[rf_vid[cur]];
-        const double v1 = __shfl_down_sync(0xffffffffu, v, 1);
-        const double v2 = __shfl_down_sync(0xffffffffu, v, 2);
-        const double v3 = __shfl_down_sync(0xffffffffu, v, 3);
-        if (fk == 0) {
-          const int t0 = 4 * round;
-          psum = (round == 0) ? v : __dadd_rn(psum, v);
-          if (t0 + 1 < kf.n_trees) psum = __dadd_rn(psum, v1);
-          if (t0 + 2 < kf.n_trees) psum = __dadd_rn(psum, v2);
-          if (t0 + 3 < kf.n_trees) psum = __dadd_rn(psum, v3);
-        }
-      }
       for (int half = 0; half < kKC / 16; ++half) {
       const int jb = chunk * kKC + 16 * half;
       // K* for this lane's four columns of the half panel: j = jb + 4 ks + fk (B fragments)
@@ -365,10 +289,8 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
       t_mean[2 * fk + 1] = mn1;
     }
     __syncwarp();
-    const double prob = __shfl_sync(0xffffffffu, psum, (lane & 7) * 4);  // lane c <- lane 4c
     if (lane < 8) {
       const int64_t gi = cbase + lane;
-      if (rf && gi < a.q) a.probs_out[gi] = __ddiv_rn(prob, (double)kf.n_trees);
       if (gi < a.q) {
         const double var_s = fmax(sigma - t_ss[lane], 0.0);          // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * t_mean[lane];  // :328
@@ -385,10 +307,7 @@ __global__ void __launch_bounds__(warps_for<MT>() * 32, 1) gp_fused_kernel(Fused
 template <int MT>
 cudaError_t launch_mt(const FusedArgs& a, int sm_count, cudaStream_t s) {
   constexpr int nw = warps_for<MT>();
-  const CompactForestDev& kf = a.kf;
-  const FusedLayout L = kf.enabled ? fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT,
-                                                  kf.n_nodes, kf.n_uvals, kf.n_trees, kf.n_codes)
-                                   : fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT);
+  const FusedLayout L = fused_layout(nw, a.gp.n, a.space.n_params, a.n_kendall, 8 * MT);
   if (L.total > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = set_smem(gp_fused_kernel<MT>, L.total);
   if (e != cudaSuccess) return e;
@@ -410,13 +329,6 @@ int fused_max_rows() { return 8 * 32; }
 
 size_t fused_smem_bytes(int n, int n_params, int n_kendall, int rows8) {
   return fused_layout(16, n, n_params, n_kendall, rows8).total;  // upper bound over warp counts
-}
-
-size_t fused_smem_bytes_forest(int n, int n_params, int n_kendall, int rows8,
-                               const CompactForestDev& kf) {
-  return fused_layout(16, n, n_params, n_kendall, rows8, kf.n_nodes, kf.n_uvals, kf.n_trees,
-                      kf.n_codes)
-      .total;
 }
 
 // Panel-major padded copy of A for the TMA stream: panel c holds columns [16c, 16c+16) of rows

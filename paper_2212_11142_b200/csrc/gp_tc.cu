@@ -55,12 +55,12 @@ constexpr int kSlots = 8;        // K* column slices held in tensor memory at a 
 // with slices 8.. and runs the chunks of rows >= 256 again over those columns, adding the partials.
 __host__ __device__ __forceinline__ int tc_passes(int nsl) { return nsl > kSlots ? 2 : 1; }
 // K* producer warps (a multiple of 4: kProdWarps / 4 per TMEM lane quarter).  The DMMA producers
-// are written for two per quarter; mixed spaces (ND == 0: integer-heavy distance code, latency
-// bound) run four per quarter at 80 registers, the rest two per quarter at 128.
-template <int ND, bool kDmma>
-constexpr int tc_prod_warps() { return (ND == 0 && !kDmma) ? 16 : 8; }
-template <int ND, bool kDmma>
-constexpr int tc_threads() { return (8 + tc_prod_warps<ND, kDmma>()) * 32; }
+// (KS > 0) are written for two per quarter at 128 registers; the FMA producers (integer-heavy
+// distance code, latency bound) run four per quarter at 80 registers.
+template <int KS>
+constexpr int tc_prod_warps() { return KS == 0 ? 16 : 8; }
+template <int KS>
+constexpr int tc_threads() { return (8 + tc_prod_warps<KS>()) * 32; }
 constexpr int kMatBlock = kDA * kN * 32;  // 3 KB per (chunk, slice)
 constexpr int kAccCols = kGroups * kN;    // 96 TMEM columns per accumulator
 constexpr int kDigCol0 = 2 * kAccCols;    // first TMEM column of the candidate digits
@@ -204,11 +204,9 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, cw, rowscale, yy, rows, stab, qs_mask, qs_uval, qs_vid, qs_off, prob, parts,
-      mat, bars, total;
+  int par, planes, kmask, cval, cmask, exp2, cw, rowscale, yy, rows, stab, emb, emb_tab, mat, bars, total;
 };
 
-// qs: the QuickScorer forest evaluated by warps 2-3 (qs->enabled == 0 -> no forest tables)
 // (chunk c, slice ks <= min(c / 2, nsl - 1)) blocks of the lower triangle, chunk-major: index of
 // chunk c's first block, and the total for nch chunks
 __host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
@@ -217,79 +215,66 @@ __host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
   return o;
 }
 
-// dmma (the FP64-tensor distance producers, centred numeric spaces): the planes hold the augmented
-// B operand, 4 * ceil((n_params + 2) / 4) rows (-2 y', |y'|^2, 1, zero padding)
-__host__ __device__ constexpr int tc_dmma_rows(int n_params) { return (n_params + 2 + 3) / 4 * 4; }
-
-__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words,
-                                              const QsForestDev* qs = nullptr, bool summ = false,
-                                              bool resident = false, bool dmma = false) {
-  const bool rf = qs && qs->enabled;
-  const int nsl = (n + 31) / 32, npad = 32 * nsl;
+// ks > 0 (tensor-core distances): the planes hold the B operand (4 ks rows), the candidate buffer
+// the tile's E embedding coordinates plus |x'|^2 (one buffer: the producers copy their A fragments
+// into registers at the start of a tile and release it).  ks == 0: per-parameter planes and
+// candidate values, double-buffered (the FMA producers read them for every slice).
+__host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words, int ks, int n_emb,
+                                              int emb_tab_len, bool aug, bool resident) {
+  const int nsl = (n + 31) / 32, npad = 32 * nsl, nch = n / kN + 1;
   TcLayout L;
   int off = 0;
   L.par = off;
   off += n_params * (int)sizeof(bx_param_desc);
   off = (off + 15) & ~15;
-  L.planes = off;  // [n_params (dmma: tc_dmma_rows)][npad], zero-padded beyond n
-  off += (dmma ? tc_dmma_rows(n_params) : n_params) * npad * 8;
+  L.planes = off;
+  off += (ks > 0 ? 4 * ks : n_params) * npad * 8;
   L.kmask = off;   // [n_kendall][npad][2]
-  off += n_kendall * npad * 16;
-  L.cval = off;    // [2][n_params][128] decoded candidate values (tile parity)
-  off += 2 * n_params * kM * 8;
+  off += ks > 0 ? 0 : n_kendall * npad * 16;
+  L.cval = off;
+  off += ks > 0 ? (n_emb + 1) * kM * 8 : 2 * n_params * kM * 8;
   L.cmask = off;   // [2][n_kendall][128][2] candidate Kendall masks
-  off += 2 * n_kendall * kM * 16;
+  off += ks > 0 ? 0 : 2 * n_kendall * kM * 16;
   L.exp2 = off;    // 2^(j/256), j < 256
   off += 256 * 8;
   L.cw = off;      // [n_params] permutation weight per raw unit: 1 / l^2 / raw_mx
-  off += ((n_params + 1) & ~1) * 8;  // keeps the 16-byte alignment of what follows
-  L.rowscale = off;  // [2][256]: row factors, then the same with the alpha / padding rows zeroed
-  off += 2 * kMaxChunks * kN * 8;
-  L.yy = off;        // [npad] |y'_j|^2 of the centred training points (dot mode)
-  off += npad * 8;
-  L.rows = off;    // [2][128 x row_words] encoded rows of the next tiles (bulk-copy staging)
-  off += 2 * kM * words * 4;
-  L.stab = off;    // coord_lut / lengthscale of the finite numeric domains (when it fits)
-  off += kMaxCoord * 8;
-  L.qs_mask = off;   // QuickScorer tables: masks, distinct leaf values, leaf value ids
-  off += rf ? qs->stride * qs->tpad * 8 : 0;
-  L.qs_uval = off;
-  off += rf ? qs->n_uvals * 8 : 0;
-  L.qs_vid = off;
-  off += rf ? ((qs->n_trees * 64 * 2 + 15) & ~15) : 0;
-  L.qs_off = off;    // [2][n_codes][128] table offsets (soff + code) of the tiles' candidates
-  off += rf ? 2 * qs->n_codes * kM * 4 : 0;
-  off = (off + 15) & ~15;
-  L.prob = off;      // [2][128] forest probabilities of the tiles' candidates
-  off += rf ? 2 * kM * 8 : 0;
-  off = (off + 15) & ~15;
-  L.parts = off;     // [4] epilogue-warp partial summaries (summ_on)
-  off += summ ? 4 * (int)sizeof(Partial) : 0;
+  off += ks > 0 ? 0 : ((n_params + 1) & ~1) * 8;
+  L.rowscale = off;  // [2][16 nch]: row factors, then the same with the alpha / padding rows zeroed
+  off += 2 * nch * kN * 8;
+  L.yy = off;        // [npad] |y'|^2 (ks > 0 without the augmented rows)
+  off += (ks > 0 && !aug) ? npad * 8 : 0;
+  L.rows = off;      // [128 x row_words] encoded rows of the next tile (bulk-copy staging)
+  off += ((kM * words * 4) + 15) & ~15;
+  L.stab = off;      // coord_lut / lengthscale of the finite numeric domains (FMA producers)
+  off += ks > 0 ? 0 : kMaxCoord * 8;
+  L.emb = off;
+  off += ks > 0 ? ((n_emb * (int)sizeof(EmbDim) + 15) & ~15) : 0;
+  L.emb_tab = off;
+  off += ks > 0 ? emb_tab_len * 8 : 0;
   off = (off + 1023) & ~1023;
   L.mat = off;     // [stage][digit][16 x 32 B], or every block of the triangle when resident
-  off += (resident ? tc_block0(n / 16 + 1, nsl) : kStages) * kMatBlock;
-  L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty[2], tmem
-  off += (1 + kSlots + 2 * kStages + 4 + 4 + 4 + 4 + 1) * 8;
+  off += (resident ? tc_block0(nch, nsl) : kStages) * kMatBlock;
+  L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty, cval_full/free[2], tmem
+  off += (1 + kSlots + 2 * kStages + 4 + 2 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
 
-// ND > 0: all-numeric space with exactly ND parameters — the distance loop is unrolled at compile
-// time and the candidate coordinates stay in registers for the whole tile.  ND == 0: any space.
-template <bool kPrecise, int ND, bool kDmma = false>
-__global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcArgs ta) {
-  constexpr int kProdWarps = tc_prod_warps<ND, kDmma>();
-  constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // columns of a slice per producer thread
+// KS > 0: tensor-core (DMMA) distances over the embedding with KS k-steps; KS == 0: FMA distances.
+template <bool kPrecise, int KS>
+__global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta) {
+  constexpr bool kDmma = KS > 0;
+  constexpr int kProdWarps = tc_prod_warps<KS>();
+  constexpr int kColsPerItem = 32 / (kProdWarps / 4);  // columns of a slice per FMA producer thread
   extern __shared__ __align__(1024) unsigned char smem[];
   const FusedArgs& a = ta.f;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.gp.n, n_params = a.space.n_params, words = a.space.row_words;
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
   const int npass = tc_passes(nsl);
-  const QsForestDev& qf = a.qs;
-  const bool rf = qf.enabled != 0;
+  const int E = ta.n_emb;
   const bool resident = ta.mat_resident != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, &qf, ta.summ_on != 0, resident, kDmma);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -298,7 +283,10 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
   double* s_exp2 = reinterpret_cast<double*>(smem + L.exp2);
   double* s_cw = reinterpret_cast<double*>(smem + L.cw);
   double* rowscale = reinterpret_cast<double*>(smem + L.rowscale);
-  double* rowscale_ss = rowscale + kMaxChunks * kN;
+  double* rowscale_ss = rowscale + nch * kN;
+  double* s_yy = reinterpret_cast<double*>(smem + L.yy);
+  EmbDim* s_emb = reinterpret_cast<EmbDim*>(smem + L.emb);
+  double* s_etab = reinterpret_cast<double*>(smem + L.emb_tab);
   unsigned char* mat = smem + L.mat;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* cand_full = bars;
@@ -307,79 +295,51 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
   uint64_t* mat_empty = mat_full + kStages;
   uint64_t* acc_full = mat_empty + kStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* rows_full = acc_empty + 2;
-  uint64_t* rows_empty = rows_full + 2;
-  uint64_t* cval_full = rows_empty + 2;  // the decoders filled a tile's candidate values
-  uint64_t* cval_free = cval_full + 2; // every producer is done with them
-  uint64_t* prob_full = cval_free + 2; // the decoders evaluated a tile's forest
-  uint64_t* prob_free = prob_full + 2; // the epilogue consumed it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(prob_free + 2);
-  double* s_prob = reinterpret_cast<double*>(smem + L.prob);
-  Partial* s_parts = reinterpret_cast<Partial*>(smem + L.parts);
+  uint64_t* rows_full = acc_empty + 2;   // the staging buffer holds the next tile's rows
+  uint64_t* rows_empty = rows_full + 1;  // the decoders are done with them
+  uint64_t* cval_full = rows_empty + 1;  // [2] the decoders filled a tile's candidate values
+  uint64_t* cval_free = cval_full + 2;   // [2] every producer is done with them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cval_free + 2);
   uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
   // rows are staged by 16-byte bulk copies when the pool pointer allows it
   const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
 
   for (int i = tid; i < n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
-  for (int i = tid; i < n_params * npad; i += blockDim.x) {
-    const int k = i / npad, j = i % npad;
-    uint64_t v = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
-    if (ta.dot) v = (uint64_t)__double_as_longlong(j < n ? __longlong_as_double((long long)v) - ta.mu[k] : 0.0);
-    planes[i] = v;
-  }
-  double* s_yy = reinterpret_cast<double*>(smem + L.yy);
-  if (ta.dot) {
-    __syncthreads();
-    for (int j = tid; j < npad; j += blockDim.x) {
-      double acc = 0.0;
-      for (int k = 0; k < n_params; ++k) {
-        const double y = __longlong_as_double((long long)planes[k * npad + j]);
-        acc = fma(y, y, acc);
-      }
-      s_yy[j] = acc;
+  if constexpr (kDmma) {
+    for (int i = tid; i < 4 * KS * npad; i += blockDim.x) planes[i] = (uint64_t)__double_as_longlong(ta.emb_planes[i]);
+    if (!ta.aug)
+      for (int j = tid; j < npad; j += blockDim.x) s_yy[j] = ta.emb_yy[j];
+    for (int i = tid; i < E * (int)sizeof(EmbDim) / 4; i += blockDim.x)
+      reinterpret_cast<int32_t*>(s_emb)[i] = reinterpret_cast<const int32_t*>(ta.emb)[i];
+    for (int i = tid; i < ta.emb_tab_len; i += blockDim.x) s_etab[i] = ta.emb_tab[i];
+  } else {
+    for (int i = tid; i < n_params * npad; i += blockDim.x) {
+      const int k = i / npad, j = i % npad;
+      planes[i] = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
     }
-    __syncthreads();  // then the planes hold -2 y' (exact), so W = |x'|^2 + |y'|^2 + sum x' (-2 y')
-    for (int i = tid; i < (ND > 0 ? n_params * npad : 0); i += blockDim.x)
-      planes[i] = (uint64_t)__double_as_longlong(-2.0 * __longlong_as_double((long long)planes[i]));
-    if constexpr (kDmma) {  // augmented rows: |y'|^2 (times the candidate's 1), 1 (times |x'|^2), zeros
-      for (int i = tid; i < (tc_dmma_rows(ND) - ND) * npad; i += blockDim.x) {
-        const int r = ND + i / npad, j = i % npad;
-        const double v = r == ND ? s_yy[j] : (r == ND + 1 ? 1.0 : 0.0);
-        planes[(size_t)r * npad + j] = (uint64_t)__double_as_longlong(v);
-      }
+    for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
+      const int kk = i / npad, j = i % npad;
+      const size_t src = ((size_t)a.kendall_param[kk] * n + j) * 2;
+      kmask[2 * i] = j < n ? a.gp.kmask[src] : 0;
+      kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
     }
-  }
-  for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
-    const int kk = i / npad, j = i % npad;
-    const size_t src = ((size_t)a.kendall_param[kk] * n + j) * 2;
-    kmask[2 * i] = j < n ? a.gp.kmask[src] : 0;
-    kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
+    for (int k = tid; k < n_params; k += blockDim.x)
+      s_cw[k] = a.space.params[k].kind == BX_PERMUTATION ? a.gp.inv_l2[k] / a.space.params[k].raw_mx : 0.0;
   }
   for (int i = tid; i < 256; i += blockDim.x) s_exp2[i] = ta.exp2tab256[i];
-  for (int k = tid; k < n_params; k += blockDim.x)
-    s_cw[k] = a.space.params[k].kind == BX_PERMUTATION ? a.gp.inv_l2[k] / a.space.params[k].raw_mx : 0.0;
   // finite numeric coordinates pre-divided by the lengthscale: decode = two shared loads
   double* stab = reinterpret_cast<double*>(smem + L.stab);
-  const bool use_stab = ta.n_coord <= kMaxCoord;
+  const bool use_stab = !kDmma && ta.n_coord <= kMaxCoord;
   if (use_stab)
     for (int k = 0; k < n_params; ++k) {
       const bx_param_desc& p = a.space.params[k];
       if (p.kind == BX_REAL || p.kind == BX_CATEGORICAL || p.kind == BX_PERMUTATION) continue;
       for (int d = tid; d < p.size; d += blockDim.x) stab[p.coord + d] = a.space.coord_lut[p.coord + d] * a.gp.inv_l[k];
     }
-  for (int i = tid; i < kMaxChunks * kN; i += blockDim.x) {
-    rowscale[i] = i < nch * kN ? ta.rowscale[i] : 0.0;
+  for (int i = tid; i < nch * kN; i += blockDim.x) {
+    rowscale[i] = ta.rowscale[i];
     rowscale_ss[i] = i < n ? ta.rowscale[i] : 0.0;  // sum-of-squares rows: L^-1 only
-  }
-  uint64_t* qs_mask = reinterpret_cast<uint64_t*>(smem + L.qs_mask);
-  double* qs_uval = reinterpret_cast<double*>(smem + L.qs_uval);
-  uint16_t* qs_vid = reinterpret_cast<uint16_t*>(smem + L.qs_vid);
-  int32_t* qs_off = reinterpret_cast<int32_t*>(smem + L.qs_off);
-  if (rf) {
-    for (int i = tid; i < qf.stride * qf.tpad; i += blockDim.x) qs_mask[i] = qf.mask[i];
-    for (int i = tid; i < qf.n_uvals; i += blockDim.x) qs_uval[i] = qf.uval[i];
-    for (int i = tid; i < qf.n_trees * 64; i += blockDim.x) qs_vid[i] = qf.vid[i];
   }
   if (tid == 0) {
     mb_init(cand_full, kProdWarps);
@@ -391,13 +351,11 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
     for (int i = 0; i < 2; ++i) {
       mb_init(&acc_full[i], 1);
       mb_init(&acc_empty[i], 4);
-      mb_init(&rows_full[i], 1);
-      mb_init(&rows_empty[i], 1);
       mb_init(&cval_full[i], 1);
       mb_init(&cval_free[i], kProdWarps);
-      mb_init(&prob_full[i], 1);
-      mb_init(&prob_free[i], 4);
     }
+    mb_init(rows_full, 1);
+    mb_init(rows_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -412,7 +370,7 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
   const int64_t n_tiles = (a.q + kM - 1) / kM;
   const int my_tiles = (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
-  // words of tile t's rows held in its staging buffer (the rest, if any, is read from global)
+  // words of tile t's rows held in the staging buffer (the rest, if any, is read from global)
   auto staged_words = [&](int64_t tile) -> int {
     if (!stage_rows) return 0;
     const int64_t count = min((int64_t)kM, a.q - tile * kM);
@@ -420,16 +378,37 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
   };
 
   if (warp == 2 || warp == 3) {
-    // ---- decoders: the next tile's candidates (coordinate / lengthscale, labels, packed
-    // permutations, Kendall masks, forest table offsets) into the tile-parity buffers ----------
+    // ---- decoders: the next tile's candidates into the candidate buffer --------------------------
     const int dt = tid - 64;  // 0..63
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
-      const int buf = t & 1;
-      if (t >= 2) mb_wait_sleep(&cval_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
-      mb_wait_sleep(&rows_full[buf], (uint32_t)((t >> 1) & 1));
-      const uint32_t* rs = rowsbuf + (size_t)buf * kM * words;
+      const int buf = kDmma ? 0 : (t & 1);
+      // the buffer's previous contents are released by every producer warp: at the start of tile
+      // t - 1 (ks > 0: A fragments copied to registers), or at the end of tile t - 2 (FMA)
+      if (kDmma ? t >= 1 : t >= 2)
+        mb_wait_sleep(&cval_free[buf], (uint32_t)((kDmma ? (t - 1) : ((t - 2) >> 1)) & 1));
+      mb_wait_sleep(rows_full, (uint32_t)(t & 1));
       const int sw = staged_words(tile);
+      if constexpr (kDmma) {
+        // thread = candidate (two per thread): E coordinates and |x'|^2
+        for (int cc = dt; cc < kM; cc += 64) {
+          const int64_t gi = tile * kM + cc;
+          const uint32_t* rw = (cc + 1) * words <= sw ? rowsbuf + cc * words : a.rows + (size_t)gi * words;
+          double xx = 0.0;
+          for (int e = 0; e < E; ++e) {
+            const double v = gi < a.q ? emb_value(s_emb[e], rw, s_etab) : 0.0;
+            cval[e * kM + cc] = (uint64_t)__double_as_longlong(v);
+            xx = fma(v, v, xx);
+          }
+          cval[E * kM + cc] = (uint64_t)__double_as_longlong(xx);
+        }
+        asm volatile("bar.sync 3, 64;" ::: "memory");
+        if (dt == 0) {
+          mb_arrive(rows_empty);
+          mb_arrive(&cval_full[0]);
+        }
+        continue;
+      }
       uint64_t* cv = cval + (size_t)buf * n_params * kM;
       for (int idx = dt; idx < n_params * kM; idx += 64) {
         const int k = idx / kM, cc = idx % kM;
@@ -437,7 +416,7 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
         const bx_param_desc& p = params[k];
         auto word = [&](int w) -> uint32_t {
           const int o = cc * words + w;
-          return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
+          return o < sw ? rowsbuf[o] : a.rows[(size_t)gi * words + w];
         };
         uint64_t v = 0;
         if (gi < a.q) {
@@ -454,36 +433,13 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
               x = stab[p.coord + (int)word(p.word)];
             else
               x = a.space.coord_lut[p.coord + (int)word(p.word)] * a.gp.inv_l[k];
-            if (ta.dot) x -= ta.mu[k];
             v = (uint64_t)__double_as_longlong(x);
           }
         }
         cv[idx] = v;
       }
-      if (rf) {  // forest table offsets of the tile (read below by these warps)
-        int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
-        for (int idx = dt; idx < qf.n_codes * kM; idx += 64) {
-          const int sl = idx / kM, cc = idx % kM;
-          const int64_t gi = tile * kM + cc;
-          int v = 0;
-          if (gi < a.q) {
-            auto word = [&](int w) -> uint32_t {
-              const int o = cc * words + w;
-              return o < sw ? rs[o] : a.rows[(size_t)gi * words + w];
-            };
-            const bx_param_desc& p = params[qf.code_param[sl]];
-            if (p.kind == BX_PERMUTATION)
-              v = perm_pos((uint64_t)word(p.word) | ((uint64_t)word(p.word + 1) << 32), p.size, qf.code_sub[sl]);
-            else if (p.kind == BX_CATEGORICAL)
-              v = qf.code_sub[sl] < 0 ? (int)word(p.word) : ((int)word(p.word) == qf.code_sub[sl] ? 1 : 0);
-            else
-              v = (int)word(p.word);
-          }
-          qo[idx] = (qf.soff[sl] + v) * qf.tpad;
-        }
-      }
       asm volatile("bar.sync 3, 64;" ::: "memory");
-      if (dt == 0) mb_arrive(&rows_empty[buf]);
+      if (dt == 0) mb_arrive(rows_empty);
       uint64_t* cm = cmask + (size_t)buf * a.n_kendall * kM * 2;
       for (int idx = dt; idx < a.n_kendall * kM; idx += 64) {
         const int kk = idx / kM, cc = idx % kM;
@@ -495,86 +451,30 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
       }
       asm volatile("bar.sync 3, 64;" ::: "memory");
       if (dt == 0) mb_arrive(&cval_full[buf]);
-      if (rf) {
-        // QuickScorer forest for the tile's candidates (two per thread), leaves summed strictly in
-        // tree order (the q >= 2 numpy order, feasibility.py:89); the epilogue reads s_prob
-        if (t >= 2) mb_wait_sleep(&prob_free[buf], (uint32_t)(((t - 2) >> 1) & 1));
-        const int32_t* qo = qs_off + (size_t)buf * qf.n_codes * kM;
-        const uint32_t mask_s = su32(qs_mask);
-        constexpr int G = 8;
-        // both candidates of the thread in flight together: 16 independent mask chains per slot
-        const int c0 = dt, c1 = dt + 64;
-        double s0 = 0.0, s1 = 0.0;
-        for (int g0 = 0; g0 < qf.n_trees; g0 += G) {
-          uint64_t m0[G], m1[G];
-#pragma unroll
-          for (int j = 0; j < G; ++j) m0[j] = m1[j] = ~0ull;
-          for (int sl = 0; sl < qf.n_codes; ++sl) {
-            const uint32_t col0 = mask_s + (uint32_t)(qo[sl * kM + c0] + g0) * 8u;
-            const uint32_t col1 = mask_s + (uint32_t)(qo[sl * kM + c1] + g0) * 8u;
-            ulonglong2 w0[G / 2], w1[G / 2];
-#pragma unroll
-            for (int j = 0; j < G / 2; ++j) {
-              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w0[j].x) : "r"(col0 + 16u * j));
-              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w0[j].y) : "r"(col0 + 16u * j + 8u));
-              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w1[j].x) : "r"(col1 + 16u * j));
-              asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w1[j].y) : "r"(col1 + 16u * j + 8u));
-            }
-#pragma unroll
-            for (int j = 0; j < G / 2; ++j) {
-              m0[2 * j] &= w0[j].x;
-              m0[2 * j + 1] &= w0[j].y;
-              m1[2 * j] &= w1[j].x;
-              m1[2 * j + 1] &= w1[j].y;
-            }
-          }
-          double v0[G], v1[G];
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const int tr = g0 + j < qf.n_trees ? g0 + j : 0;
-            v0[j] = qs_uval[qs_vid[tr * 64 + __ffsll((long long)m0[j]) - 1]];
-            v1[j] = qs_uval[qs_vid[tr * 64 + __ffsll((long long)m1[j]) - 1]];
-          }
-#pragma unroll
-          for (int j = 0; j < G; ++j)
-            if (g0 + j < qf.n_trees) {
-              s0 = (g0 + j == 0) ? v0[j] : __dadd_rn(s0, v0[j]);
-              s1 = (g0 + j == 0) ? v1[j] : __dadd_rn(s1, v1[j]);
-            }
-        }
-        s_prob[buf * kM + c0] = __ddiv_rn(s0, (double)qf.n_trees);  // np.mean: sum / count
-        s_prob[buf * kM + c1] = __ddiv_rn(s1, (double)qf.n_trees);
-        asm volatile("bar.sync 3, 64;" ::: "memory");
-        if (dt == 0) mb_arrive(&prob_full[buf]);
-      }
     }
   } else if (warp == 1 && lane == 1) {
     // ---- row prefetcher: the encoded rows of each tile, one bulk copy ahead ----------------
-    {
-      for (int t = 0; t < my_tiles; ++t) {
-        const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
-        const int buf = t & 1;
-        if (t >= 2) mb_wait_sleep(&rows_empty[buf], (uint32_t)(((t - 2) >> 1) & 1));
-        if (ta.ready) {  // streaming pool: wait until the copy stream has landed this tile's chunk
-          const int64_t last = min(a.q, (tile + 1) * kM) - 1;
-          const uint32_t* flag = ta.ready + (last >> ta.ready_shift);
-          uint32_t ok = 0;
-          for (long long spins = 0;; ++spins) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ok) : "l"(flag) : "memory");
-            if (ok) break;
-            if (spins > (1ll << 26)) asm volatile("trap;");  // ~20 s without the chunk: fail loudly
-            __nanosleep(256);
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // make the data visible to TMA
+    for (int t = 0; t < my_tiles; ++t) {
+      const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
+      if (t >= 1) mb_wait_sleep(rows_empty, (uint32_t)((t - 1) & 1));
+      if (ta.ready) {  // streaming pool: wait until the copy stream has landed this tile's chunk
+        const int64_t last = min(a.q, (tile + 1) * kM) - 1;
+        const uint32_t* flag = ta.ready + (last >> ta.ready_shift);
+        uint32_t ok = 0;
+        for (long long spins = 0;; ++spins) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ok) : "l"(flag) : "memory");
+          if (ok) break;
+          if (spins > (1ll << 26)) asm volatile("trap;");  // ~20 s without the chunk: fail loudly
+          __nanosleep(256);
         }
-        const int sw = staged_words(tile);
-        if (sw > 0) {
-          mb_expect(&rows_full[buf], (uint32_t)sw * 4);
-          bulk_g2s(rowsbuf + (size_t)buf * kM * words, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4,
-                   &rows_full[buf]);
-        } else {
-          mb_arrive(&rows_full[buf]);
-        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // make the data visible to TMA
+      }
+      const int sw = staged_words(tile);
+      if (sw > 0) {
+        mb_expect(rows_full, (uint32_t)sw * 4);
+        bulk_g2s(rowsbuf, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4, rows_full);
+      } else {
+        mb_arrive(rows_full);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -668,10 +568,6 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
     const double sigma = a.gp.outputscale;
     uint32_t ph_f = 0;
     int chunk_no = 0;
-    const SummaryArgs& sa = ta.summ;
-    Partial* summ = s_parts + (warp - 4);
-    if (ta.summ_on && lane == 0) partial_init(summ);
-    __syncwarp();
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
       double ss = 0.0, mean_s = 0.0;
@@ -719,15 +615,6 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
         if (lane == 0 && warp == 4) TC_TRACE(2, 2, c);
       }
       const int64_t gi = tile * kM + r;
-      double prob = 1.0;
-      if (rf) {
-        mb_wait_sleep(&prob_full[t & 1], (uint32_t)((t >> 1) & 1));
-        prob = s_prob[(t & 1) * kM + r];
-        __syncwarp();
-        if (lane == 0) mb_arrive(&prob_free[t & 1]);
-        if (a.probs_out && gi < a.q) a.probs_out[gi] = prob;
-      }
-      double ei_c = -INFINITY;
       if (gi < a.q) {
         const double var_s = fmax(sigma - ss, 0.0);                 // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * mean_s;      // :328
@@ -735,105 +622,45 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
         if (a.mean_out) a.mean_out[gi] = mean;
         if (a.var_out) a.var_out[gi] = var;
         if (a.ei_out) a.ei_out[gi] = ei_value(mean, var, a.f_model);  // acquisition.py:40-51
-        if (ta.summ_on) ei_c = ei_value(mean, var, a.f_model);
       }
-      if (ta.summ_on) {
-        // acquisition value and the warp's partial summary (the logic of summary_kernel)
-        const bool valid = gi < a.q;
-        double value = -INFINITY, pv = -INFINITY;
-        if (valid) {
-          pv = rf ? prob : 1.0;
-          value = rf ? ((prob < sa.eps_f) ? -INFINITY : ei_c * prob) : ei_c;
-          if (sa.values_out) sa.values_out[gi] = value;
-          if (sa.probs_out) sa.probs_out[gi] = pv;
-        }
-        const int words_s = sa.space.row_words;
-        const bool fin = valid && value != -INFINITY;
-        const bool top_open = sa.k > 0 && summ->n_top < sa.k;
-        const double kth = (sa.k > 0 && !top_open) ? summ->top[sa.k - 1].value : -INFINITY;
-        const bool prob_ok = sa.track_prob && pv >= summ->best_prob.prob;
-        const bool maybe = valid && ((fin && sa.k > 0 && (top_open || value >= kth)) ||
-                                     (fin && value >= summ->best.value) || prob_ok);
-        bool evaluated = false;
-        if (maybe && sa.evald.count > 0) evaluated = is_evaluated(sa.evald, a.rows + (size_t)gi * words_s, words_s);
-        const bool pass = maybe && ((fin && sa.k > 0 && (top_open || value >= kth)) ||
-                                    (!evaluated && ((fin && value >= summ->best.value) || prob_ok)));
-        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-        const unsigned fmask = __ballot_sync(0xffffffffu, fin);
-        unsigned pmask = __ballot_sync(0xffffffffu, pass);
-        const unsigned emask = __ballot_sync(0xffffffffu, evaluated);
-        if (lane == 0) {
-          summ->n_scored += __popc(vmask);
-          summ->n_finite += __popc(fmask);
-        }
-        const int64_t wbase = tile * kM + (warp - 4) * 32;
-        while (pmask) {
-          const int cl = __ffs(pmask) - 1;
-          pmask &= pmask - 1;
-          const double vc = __shfl_sync(0xffffffffu, value, cl);
-          const double pc = __shfl_sync(0xffffffffu, pv, cl);
-          if (lane == 0)
-            partial_add(summ, sa.k, params, sa.space.n_params, sa.space.rank_lut, words_s, vc, pc,
-                        sa.index_base + wbase + cl, (emask >> cl) & 1u, a.rows + (size_t)(wbase + cl) * words_s,
-                        sa.track_prob != 0);
-          __syncwarp();
-        }
-      }
-    }
-    if (ta.summ_on) {  // fold the four warp partials into the CTA's
-      asm volatile("bar.sync 4, 128;" ::: "memory");
-      if (warp == 4 && lane == 0) {
-        for (int w = 1; w < 4; ++w)
-          partial_merge(&s_parts[0], &s_parts[w], sa.k, params, sa.space.n_params, sa.space.rank_lut,
-                        sa.space.row_words);
-      }
-      asm volatile("bar.sync 4, 128;" ::: "memory");
-      const int32_t* src = reinterpret_cast<const int32_t*>(&s_parts[0]);
-      int32_t* dst = reinterpret_cast<int32_t*>(sa.partials + blockIdx.x);
-      for (int i = r; i < (int)(sizeof(Partial) / 4); i += 128) dst[i] = src[i];
     }
   } else if (kDmma && warp >= 8) {
-    // ---- K* producers, FP64 tensor-core distances (centred all-numeric spaces) ---------------
+    // ---- K* producers, FP64 tensor-core distances over the embedding -----------------------------
     // Warp (quarter q, half h) owns candidates 32 q + 16 h + 0..15 (TMEM lanes of its quarter) and
-    // every column of a slice.  W = |x'|^2 + |y'|^2 + x'.(-2 y') is one augmented product
-    // [x', 1, |x'|^2] . [-2 y'; |y'|^2; 1] on DMMA m8n8k4 (2 row blocks x 4 column blocks x KS
-    // k-steps per slice), so the distance costs 24 MMA instructions instead of 176 FMAs + 88 shared
-    // loads per thread; the Matérn runs on the C fragments and the digits go to TMEM with the
-    // matching 16x256b store.  Within a slice the K order is permuted so that each thread's C
-    // columns are 8 consecutive K bytes: K byte 8 t0 + 4 hh + 2 jj + e <- column 8 (2 hh + jj) + 2 t0 + e
-    // (mdig_kernel builds the matrix digits with the same permutation).
-    constexpr int KS = tc_dmma_rows(ND > 0 ? ND : 1) / 4;
+    // every column of a slice.  W = |x'|^2 + |y'|^2 + x'.(-2 y') is one product of the candidate
+    // embedding [x', 1, |x'|^2] and the training operand [-2 y'; |y'|^2; 1] on DMMA m8n8k4 (2 row
+    // blocks x 4 column blocks x KS k-steps per slice; without room for the two augmented k-rows
+    // |x'|^2 + |y'|^2 is added to the fragments); the Matérn runs on the C fragments and the digits
+    // go to TMEM with the matching 16x256b store.  Within a slice the K order is permuted so that
+    // each thread's C columns are 8 consecutive K bytes: K byte 8 t0 + 4 hh + 2 jj + e <- column
+    // 8 (2 hh + jj) + 2 t0 + e (mdig_kernel builds the matrix digits with the same permutation).
     const int pt = tid - 8 * 32;
     const int quarter = warp & 3, half = (warp - 8) >> 2;
     const int t0 = lane & 3, t1 = lane >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32 + half * 16) << 16;
     const double sigma = a.gp.outputscale;
     const MaternConst mc{sigma * ta.kscale, sigma * kSqrt5 * ta.kscale, sigma * (5.0 / 3.0) * ta.kscale};
+    const bool aug = ta.aug != 0;
     uint32_t slot_used = 0, slot_par = 0;
     for (int t = 0; t < my_tiles; ++t) {
       if (pt == 0) TC_TRACE(0, 1, t);
-      const int cb = t & 1;
-      mb_wait(&cval_full[cb], (uint32_t)((t >> 1) & 1));
-      const uint64_t* cv = cval + (size_t)cb * n_params * kM;
+      mb_wait(&cval_full[0], (uint32_t)(t & 1));
       if (pt == 0) TC_TRACE(0, 2, t);
       // A fragments: row = candidate 32 q + 16 h + 8 rb + t1, k = t0 + 4 kk of [x', 1, |x'|^2, 0..]
-      double afr[2][KS];
+      double afr[2][KS > 0 ? KS : 1], xx[2];
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb) {
         const int c = quarter * 32 + half * 16 + 8 * rb + t1;
-        double xx = 0.0;
-#pragma unroll
-        for (int k = 0; k < ND; ++k) {
-          const double x = __longlong_as_double((long long)cv[k * kM + c]);
-          xx = fma(x, x, xx);
-        }
+        xx[rb] = __longlong_as_double((long long)cval[E * kM + c]);
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = t0 + 4 * kk;
-          afr[rb][kk] = k < ND ? __longlong_as_double((long long)cv[(k < ND ? k : 0) * kM + c])
-                               : (k == ND ? 1.0 : (k == ND + 1 ? xx : 0.0));
+          afr[rb][kk] = k < E ? __longlong_as_double((long long)cval[k * kM + c])
+                              : (aug && k == E ? 1.0 : (aug && k == E + 1 ? xx[rb] : 0.0));
         }
       }
+      __syncwarp();
+      if (lane == 0) mb_arrive(&cval_free[0]);  // the decoders may write the next tile
       for (int p = 0; p < npass; ++p) {
       const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));
       const int soff = p == 0 ? 0 : kSlots - (hi - lo);
@@ -853,6 +680,17 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
             const double b = brow[8 * j];  // B[k = t0 + 4 kk][column 8 j + t1]
             dmma884(acc[0][j][0], acc[0][j][1], afr[0][kk], b);
             dmma884(acc[1][j][0], acc[1][j][1], afr[1][kk], b);
+          }
+        }
+        if (!aug) {  // uniform branch: |x'|^2 + |y'|^2 added to the C fragments
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double2 y = *reinterpret_cast<const double2*>(s_yy + j0 + 8 * j + 2 * t0);
+#pragma unroll
+            for (int rb = 0; rb < 2; ++rb) {
+              acc[rb][j][0] += xx[rb] + y.x;
+              acc[rb][j][1] += xx[rb] + y.y;
+            }
           }
         }
         // acc[rb][j][e] = W(candidate row rb, column 8 j + 2 t0 + e) -> K byte 8 t0 + 4 (j / 2) + 2 (j % 2) + e
@@ -893,15 +731,12 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mb_arrive(cand_full);
-        if (p == npass - 1) mb_arrive(&cval_free[cb]);
-      }
+      if (lane == 0) mb_arrive(cand_full);
       }
       if (pt == 0) TC_TRACE(0, 6, t);
     }
   } else if (warp >= 8) {
-    // ---- K* producers ------------------------------------------------------------------------
+    // ---- K* producers, FMA distances per parameter kind -----------------------------------------
     const int pt = tid - 8 * 32;  // 0..kProdThreads-1
     // warp w may only access TMEM lanes 32 (w % 4) .. +31: candidate = that lane, and the four
     // warps sharing a lane quarter split each 32-column slice into 8-column parts
@@ -920,70 +755,16 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
       const uint64_t* cv = cval + (size_t)cb * n_params * kM;
       const uint64_t* cmk = cmask + (size_t)cb * a.n_kendall * kM * 2;
       if (pt == 0) TC_TRACE(0, 2, t);
-      double xr[ND > 0 ? ND : 1];
-      double xx = 0.0;
-      if constexpr (ND > 0) {
-#pragma unroll
-        for (int k = 0; k < ND; ++k) {
-          xr[k] = __longlong_as_double((long long)cv[k * kM + c]);
-          xx = fma(xr[k], xr[k], xx);
-        }
-      }
       for (int p = 0; p < npass; ++p) {
       const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));  // this pass's column slices
       const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // pass 1 takes the slots pass 0 frees first
       for (int ks = hi - 1; ks >= lo; --ks) {
         const int slot = ks - lo + soff;
         const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
-        if constexpr (ND > 0) {
-          // re-read the coordinates per slice (volatile: not hoisted) so they are not live across
-          // the Matérn chains: 2 * ND registers more for interleaving them
-          const uint32_t xa = su32(cv + c);
-#pragma unroll
-          for (int k = 0; k < ND; ++k) {
-            unsigned long long v;
-            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(xa + (uint32_t)(k * kM * 8)));
-            xr[k] = __longlong_as_double((long long)v);
-          }
-        }
         double W[kColsPerItem];
 #pragma unroll
         for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
-        if constexpr (ND > 0) {
-          const double2* pl0 = reinterpret_cast<const double2*>(planes + j0);
-          if (ta.dot) {  // W = |x'|^2 + |y'|^2 - 2 x'.y' (centred, small: no harmful cancellation)
-            const double2* yy2 = reinterpret_cast<const double2*>(s_yy + j0);
-#pragma unroll
-            for (int u = 0; u < kColsPerItem / 2; ++u) {
-              const double2 y = yy2[u];
-              W[2 * u] = xx + y.x;
-              W[2 * u + 1] = xx + y.y;
-            }
-#pragma unroll
-            for (int k = 0; k < ND; ++k) {
-              const double2* pl = pl0 + (size_t)k * (npad / 2);  // -2 y'
-#pragma unroll
-              for (int u = 0; u < kColsPerItem / 2; ++u) {
-                const double2 y = pl[u];
-                W[2 * u] = fma(xr[k], y.x, W[2 * u]);  // may round below 0: |W| is taken below
-                W[2 * u + 1] = fma(xr[k], y.y, W[2 * u + 1]);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < ND; ++k) {
-              const double2* pl = pl0 + (size_t)k * (npad / 2);
-#pragma unroll
-              for (int u = 0; u < kColsPerItem / 2; ++u) {
-                const double2 y = pl[u];
-                const double d0 = xr[k] - y.x, d1 = xr[k] - y.y;
-                W[2 * u] = fma(d0, d0, W[2 * u]);
-                W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
-              }
-            }
-          }
-        }
-        for (int i = 0; i < (ND > 0 ? 0 : a.n_num); ++i) {
+        for (int i = 0; i < a.n_num; ++i) {
           const int k = a.num_param[i];
           const double x = __longlong_as_double((long long)cv[k * kM + c]);
           // 16-byte broadcast loads: half the shared-memory wavefronts of scalar loads
@@ -996,7 +777,7 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
             W[2 * u + 1] = fma(d1, d1, W[2 * u + 1]);
           }
         }
-        for (int i = 0; i < (ND > 0 ? 0 : a.n_cat); ++i) {
+        for (int i = 0; i < a.n_cat; ++i) {
           const int k = a.cat_param[i];
           const uint64_t x = cv[k * kM + c];
           const double wl = a.gp.inv_l2[k];
@@ -1004,7 +785,7 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
 #pragma unroll
           for (int u = 0; u < kColsPerItem; ++u) W[u] += (x != pl[u]) ? wl : 0.0;
         }
-        for (int i = 0, kend = 0; i < (ND > 0 ? 0 : a.n_perm); ++i) {
+        for (int i = 0, kend = 0; i < a.n_perm; ++i) {
           const int k = a.perm_param[i];
           const bx_param_desc& p = params[k];
           const uint64_t x = cv[k * kM + c];
@@ -1046,7 +827,7 @@ __global__ void __launch_bounds__((tc_threads<ND, kDmma>()), 1) gp_tc_kernel(TcA
           }
         }
         // K* -> 40-bit fixed point -> five base-256 digits, 4 columns per 32-bit word.  Straight-line
-        // code (padding columns are evaluated on the zero planes and masked afterwards) so the 16
+        // code (padding columns are evaluated on the zero planes and masked afterwards) so the
         // independent Matérn chains interleave.
         uint32_t dw[kDB][kColsPerItem / 4];
 #pragma unroll
@@ -1149,9 +930,9 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 }  // namespace
 
-size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, const QsForestDev* qs, bool summ,
-                     bool dmma) {
-  return tc_layout(n, n_params, n_kendall, row_words, qs, summ, false, dmma).total;
+size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, int ks, int n_emb, int emb_tab_len,
+                     bool aug, bool resident) {
+  return tc_layout(n, n_params, n_kendall, row_words, ks, n_emb, emb_tab_len, aug, resident).total;
 }
 
 size_t tc_mdig_bytes(int n) {
@@ -1173,31 +954,23 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 
 cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   TcArgs a = a0;
-  const bool dmma = a.dmma != 0;
+  const int n = a.f.gp.n, P = a.f.space.n_params, K = a.f.n_kendall, W = a.f.space.row_words;
   // matrix digits resident in shared memory when they fit (BX_TC_DEBUG bit 8: always the ring)
-  a.mat_resident = 0;
-  if (!(a.debug & 8) && tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
-                                  a.summ_on != 0, true, dmma).total <= 227 * 1024)
-    a.mat_resident = 1;
-  const TcLayout L = tc_layout(a.f.gp.n, a.f.space.n_params, a.f.n_kendall, a.f.space.row_words, &a.f.qs,
-                               a.summ_on != 0, a.mat_resident != 0, dmma);
-  if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks) return cudaErrorInvalidValue;
-  // all-numeric spaces with up to 16 parameters get the unrolled distance loop
-  const bool numeric = a.f.n_cat == 0 && a.f.n_perm == 0 && a.f.n_num == a.f.space.n_params && !a.f.precise;
-  if (a.dot && !numeric) return cudaErrorInvalidValue;  // the host enables dot only for these
-  if (dmma && !(a.dot && numeric && a.f.n_num <= 16)) return cudaErrorInvalidValue;
-  const int nd = numeric ? a.f.n_num : 0;
+  a.mat_resident = !(a.debug & 8) &&
+                   tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, true).total <= 227 * 1024;
+  const TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0);
+  if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks || a.ks > 8 || (a.ks > 0 && a.f.precise))
+    return cudaErrorInvalidValue;
   auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
-  int threads = tc_threads<0, false>();
-  switch (nd) {
-#define BX_ND(d) \
-    case d:                                                                            \
-      kernel = dmma ? gp_tc_kernel<false, d, true> : gp_tc_kernel<false, d>;           \
-      threads = dmma ? tc_threads<d, true>() : tc_threads<d, false>();                 \
+  int threads = tc_threads<0>();
+  switch (a.ks) {
+#define BX_KS(k)                             \
+    case k:                                  \
+      kernel = gp_tc_kernel<false, k>;       \
+      threads = tc_threads<k>();             \
       break;
-    BX_ND(1) BX_ND(2) BX_ND(3) BX_ND(4) BX_ND(5) BX_ND(6) BX_ND(7) BX_ND(8)
-    BX_ND(9) BX_ND(10) BX_ND(11) BX_ND(12) BX_ND(13) BX_ND(14) BX_ND(15) BX_ND(16)
-#undef BX_ND
+    BX_KS(1) BX_KS(2) BX_KS(3) BX_KS(4) BX_KS(5) BX_KS(6) BX_KS(7) BX_KS(8)
+#undef BX_KS
     default: break;
   }
   cudaError_t e = set_smem(kernel, L.total);

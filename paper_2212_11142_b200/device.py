@@ -229,6 +229,10 @@ class Scorer:
         """Posterior kernel the current model state runs: "tensor", "dmma" or "generic"."""
         return {0: "generic", 1: "dmma", 2: "tensor"}[self._lib.bx_gp_kernel(self.h)]
 
+    def distance_ksteps(self) -> int:
+        """DMMA k-steps of the tensor-core posterior's embedding distance product (0: FMA)."""
+        return int(self._lib.bx_gp_distance_ksteps(self.h))
+
     def last_timing(self) -> dict:
         """CUDA-event durations (ms) of the forest / fused-score / merge kernels of the last
         score(..., timing=True) call."""

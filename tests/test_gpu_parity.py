@@ -238,16 +238,17 @@ def test_posterior_kernels_agree(case, monkeypatch):
     tc.close()
 
 
-@pytest.mark.parametrize("case", ["C3", "C4", "mixed_fit"])
+@pytest.mark.parametrize("case", ["C3", "C4", "mixed_fit", "mixed_metrics", "M200"])
 def test_forest_paths_bit_exact(case, monkeypatch):
-    """QuickScorer tables (stand-alone and fused into the tensor-core kernel) and the node walk
-    give bit-identical probabilities and scores."""
+    """QuickScorer tables (with indirect slots for real parameters with many thresholds: M200,
+    mixed_fit), the integer-coded node walk and the generic f64 walk give bit-identical
+    probabilities and scores, in both summation orders."""
     from paper_2212_11142_b200.device import Scorer
     meta, arr, space = load(case)
     gp, feas = model(meta, arr, space)
     f = gp.objective_to_model(meta["f_best"])
     out = {}
-    for name, env in [("walk", {"BX_FOREST_WALK": "1"}), ("qs", {}), ("fused", {"BX_TC_FOREST_FUSED": "1"})]:
+    for name, env in [("generic", {"BX_FOREST_GENERIC": "1"}), ("walk", {"BX_FOREST_WALK": "1"}), ("qs", {})]:
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         sc = Scorer()
@@ -255,37 +256,41 @@ def test_forest_paths_bit_exact(case, monkeypatch):
         sc.set_forest(feas)
         rows = sc.generate(200_003, seed=3)
         _, values, probs = sc.score(rows, f, meta["eps_f"], k=10, want_values=True)
-        out[name] = (values.cpu().numpy(), probs.cpu().numpy(), sc.rf_predict(rows, pairwise=False).cpu().numpy())
+        out[name] = (values.cpu().numpy(), probs.cpu().numpy(), sc.rf_predict(rows, pairwise=False).cpu().numpy(),
+                     sc.rf_predict(rows[:4099], pairwise=True).cpu().numpy())
         sc.close()
         for k in env:
             monkeypatch.delenv(k)
-    for name in ("qs", "fused"):
-        for a, b in zip(out[name], out["walk"]):
+    for name in ("qs", "walk"):
+        for a, b in zip(out[name], out["generic"]):
             assert np.array_equal(a, b), name
 
 
-@pytest.mark.parametrize("case", ["C3", "C2", "C1"])
-def test_dot_product_distances_match_difference_form(case, monkeypatch):
-    """Centred dot-product distances (enabled by bx_set_gp for well-scaled all-numeric spaces, C3)
-    agree with the difference form to far inside the parity bar; spaces it does not apply to
-    (C1: small lengthscales, C2: categorical / permutation) are unaffected."""
+@pytest.mark.parametrize("case", CASES)
+def test_embedding_distances_match_fma_distances(case, monkeypatch):
+    """The tensor-core distance producers (W = |x'|^2 + |y'|^2 - 2 x'.y' over the Euclidean
+    embedding of every metric, on DMMA) against the FMA producers (BX_TC_NO_DMMA=1): they differ
+    only in the rounding of W, far inside the 1e-5 parity bar.  Every golden space embeds except
+    mixed_metrics (naive permutation indicator), which falls back to the FMA producers."""
     from paper_2212_11142_b200 import scenarios
     from paper_2212_11142_b200.device import Scorer
     meta, arr, space = load(case)
     gp, _ = model(meta, arr, space)
-    res = []
-    for no_dot in (True, False):
-        if no_dot:
-            monkeypatch.setenv("BX_TC_NO_DOT", "1")
+    res, ks = [], []
+    for no_dmma in (True, False):
+        if no_dmma:
+            monkeypatch.setenv("BX_TC_NO_DMMA", "1")
         else:
-            monkeypatch.delenv("BX_TC_NO_DOT")
+            monkeypatch.delenv("BX_TC_NO_DMMA")
         sc = Scorer()
         sc.set_gp(gp)
+        ks.append(sc.distance_ksteps())
         rows = sc.to_device(scenarios.sample_rows_uniform(sc.layout, 200_000, np.random.default_rng(2)))
         res.append([x.cpu().numpy() for x in sc.predict(rows)])
         sc.close()
+    assert ks[0] == 0 and (ks[1] == 0) == (case == "mixed_metrics"), ks
     (m0, v0), (m1, v1) = res
-    close(m1, m0, rtol=1e-9)
+    close(m1, m0, rtol=1e-8)
     close(v1, v0, rtol=1e-7)
 
 

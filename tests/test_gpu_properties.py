@@ -121,7 +121,7 @@ def test_space_exhausted_raises():
     allc = list(cot.enumerate())
     gp = GPState.fit(sp, allc[:3], [1.0, 2.0, 3.0], Hyper(1.0, 1e-3, (0.5, 0.5)))
     ctx = Ctx(gp, None, 1.0, 0.0, np.random.default_rng(0), set(allc))
-    with pytest.raises(A.SpaceExhausted):
+    with pytest.raises(_bt.SpaceExhausted):
         A.optimize_acquisition(ctx, sp, cot)
     ctx = Ctx(gp, None, 1.0, 0.0, np.random.default_rng(0), set(allc[:5]))
     assert A.optimize_acquisition(ctx, sp, cot) == allc[5]
@@ -160,66 +160,33 @@ def test_mixed_space_large_n_against_oracle(n):
     sc.close()
 
 
-@pytest.mark.parametrize("full", [False, True])
 @pytest.mark.parametrize("case,q,eps", [("C3", 3 * 65536 + 777, None), ("C3", 70001, 1.01),
-                                        ("C2", 200003, None), ("mixed_fit", 65536, None)])
-def test_streaming_host_pool_matches_device_pool(case, q, eps, full, monkeypatch):
+                                        ("C2", 200003, None), ("mixed_fit", 65536, None), ("M200", 131075, None)])
+def test_streaming_host_pool_matches_device_pool(case, q, eps):
     """bx_score_host streams the pool (chunked copies + ready flags consumed by one posterior
     launch); its summary equals bx_score's on the same rows — ragged sizes, a forest-less case and
-    the all -inf fallback (eps_f > 1: probability tracker) included — and equals the chunked
-    pipeline (BX_HOST_CHUNKED=1).  full: the whole step inside the tensor-core kernel (BX_TC_FULL=1)."""
+    the all -inf fallback (eps_f > 1: probability tracker) included."""
     from paper_2212_11142_b200.device import Scorer
-    if full:
-        monkeypatch.setenv("BX_TC_FULL", "1")
     meta, arr, space = load(case)
     gp, feas = model(meta, arr, space)
     f = gp.objective_to_model(meta["f_best"])
     eps_f = meta["eps_f"] if eps is None else eps
-    out = []
-    for chunked in (False, True):
-        if chunked:
-            monkeypatch.setenv("BX_HOST_CHUNKED", "1")
-        sc = Scorer()
-        sc.set_gp(gp)
-        if feas is not None:
-            sc.set_forest(feas)
-        rows_h = scenarios.sample_rows_uniform(sc.layout, q, np.random.default_rng(q))
-        pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
-        a, _, _ = sc.score(sc.to_device(rows_h), f, eps_f, k=10)
-        b = sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10)
-        for x, y in ((a, b),):
-            assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
-            assert [c.index for c in x.top] == [c.index for c in y.top]
-            assert [c.value for c in x.top] == [c.value for c in y.top]
-            idx = lambda c: None if c is None else (c.index, tuple(c.row))
-            assert idx(x.best) == idx(y.best) and idx(x.best_prob) == idx(y.best_prob)
-        out.append(b)
-        sc.close()
-    assert [c.index for c in out[0].top] == [c.index for c in out[1].top]
-    if eps is not None:
-        assert out[0].n_finite == 0 and out[0].best_prob is not None
-
-
-def test_full_step_kernel_values_match_separate_kernels(c3, monkeypatch):
-    """BX_TC_FULL=1 (forest on the decoder warps, summaries in the epilogue) gives bit-identical
-    values, probabilities and summaries to the separate forest + summary kernels."""
-    from paper_2212_11142_b200.device import Scorer
-    sc0, meta, arr, space, gp, feas, rows_h = c3
-    f = gp.objective_to_model(meta["f_best"])
-    res = []
-    for full in (False, True):
-        if full:
-            monkeypatch.setenv("BX_TC_FULL", "1")
-        sc = Scorer()
-        sc.set_gp(gp)
+    sc = Scorer()
+    sc.set_gp(gp)
+    if feas is not None:
         sc.set_forest(feas)
-        s, v, p = sc.score(sc.to_device(rows_h[:300_001]), f, meta["eps_f"], k=10, want_values=True)
-        res.append((s, v.cpu().numpy(), p.cpu().numpy()))
-        sc.close()
-    (a, va, pa), (b, vb, pb) = res
-    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
-    assert [c.index for c in a.top] == [c.index for c in b.top]
-    assert (a.n_scored, a.n_finite, a.best.index) == (b.n_scored, b.n_finite, b.best.index)
+    rows_h = scenarios.sample_rows_uniform(sc.layout, q, np.random.default_rng(q))
+    pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
+    x, _, _ = sc.score(sc.to_device(rows_h), f, eps_f, k=10)
+    y = sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10)
+    assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
+    assert [c.index for c in x.top] == [c.index for c in y.top]
+    assert [c.value for c in x.top] == [c.value for c in y.top]
+    idx = lambda c: None if c is None else (c.index, tuple(c.row))
+    assert idx(x.best) == idx(y.best) and idx(x.best_prob) == idx(y.best_prob)
+    if eps is not None:
+        assert y.n_finite == 0 and y.best_prob is not None
+    sc.close()
 
 
 def test_matrix_ring_matches_resident_matrix(c3, monkeypatch):
@@ -277,30 +244,10 @@ def test_posterior_size_boundaries(n):
         sc.close()
 
 
-def test_dmma_distances_match_fma_distances(c3, monkeypatch):
-    """The posterior's DMMA distance producers (augmented [x',1,|x'|^2].[-2y';|y'|^2;1] product,
-    permuted matrix K order) against the FMA producers (BX_TC_NO_DMMA=1) on 2^18 C3 candidates:
-    the two differ only in the rounding of W, far inside the 1e-5 parity bar."""
-    from paper_2212_11142_b200.device import Scorer
-    sc0, meta, arr, space, gp, feas, rows_h = c3
-    out = []
-    for no_dmma in (False, True):
-        if no_dmma:
-            monkeypatch.setenv("BX_TC_NO_DMMA", "1")
-        sc = Scorer()
-        sc.set_gp(gp)
-        mean, var = sc.predict(sc.to_device(rows_h[: 1 << 18]))
-        out.append((mean.cpu().numpy(), var.cpu().numpy()))
-        sc.close()
-    np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-9, atol=1e-12 * np.abs(out[1][0]).max())
-    np.testing.assert_allclose(out[0][1], out[1][1], rtol=1e-7, atol=1e-12 * np.abs(out[1][1]).max())
-
-
 @pytest.mark.parametrize("D", [1, 3, 6, 12, 16])
 def test_numeric_dimensions_dmma_producers(D):
-    """Random all-numeric spaces of D = 1..16 dimensions (ordinal / integer / real mixes): every
-    gp_tc_kernel<0, D, 1> instance (DMMA distance producers, 1..5 augmented k-steps) against the
-    oracle's FP64 posterior."""
+    """Random all-numeric spaces of D = 1..16 dimensions (ordinal / integer / real mixes): the DMMA
+    embedding producers with 1..4 k-steps against the oracle's FP64 posterior."""
     import oracle
     from paper_2212_11142_b200.device import Scorer
     from paper_2212_11142_b200.models import GPState, Hyper
@@ -325,8 +272,65 @@ def test_numeric_dimensions_dmma_producers(D):
     hyp = Hyper(outputscale=1.1, noise_variance=1e-3, lengthscales=tuple(rng.uniform(0.5, 2.5, D)))
     gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
     sc.set_gp(gp)
-    assert sc.gp_kernel() == "tensor"
+    assert sc.gp_kernel() == "tensor" and sc.distance_ksteps() == (D + 3) // 4
     rows = sc.to_device(scenarios.sample_rows_uniform(lay, 5 * 128 + 3, rng))
+    mean, var = (x.cpu().numpy() for x in sc.predict(rows))
+    sample = lay.decode(rows.cpu().numpy().view(np.uint32))
+    og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
+                         L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
+    m0, v0 = oracle.gp.predict(og, sample)
+    np.testing.assert_allclose(mean, m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
+    np.testing.assert_allclose(var, v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
+    sc.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_mixed_space_embedding_against_oracle(seed):
+    """Random mixed spaces (numeric, categorical of 2..5 labels, Spearman / Kendall / Hamming
+    permutations of 3..6 elements): the embedding covers every metric but the naive indicator, with
+    1..8 DMMA k-steps (with and without the augmented k-rows); posterior against the oracle."""
+    import oracle
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    rng = np.random.default_rng(700 + seed)
+    params, E = [], 0
+    while len(params) < 12:
+        kind = ("ordinal", "integer", "real", "categorical", "permutation")[int(rng.integers(5))]
+        i = len(params)
+        if kind == "ordinal":
+            d, e = {"name": f"o{i}", "kind": "ordinal", "values": [1, 2, 4, 8, 16, 32][: int(rng.integers(2, 7))],
+                    "transform": "log"}, 1
+        elif kind == "integer":
+            d, e = {"name": f"i{i}", "kind": "integer", "lo": 0, "hi": int(rng.integers(1, 12))}, 1
+        elif kind == "real":
+            d, e = {"name": f"r{i}", "kind": "real", "lo": 0.0, "hi": 3.0}, 1
+        elif kind == "categorical":
+            L = int(rng.integers(2, 6))
+            d, e = {"name": f"c{i}", "kind": "categorical", "values": [f"v{j}" for j in range(L)]}, L - 1
+        else:
+            m = int(rng.integers(3, 7))
+            metric = ("spearman", "kendall", "hamming")[int(rng.integers(3))]
+            d = {"name": f"p{i}", "kind": "permutation", "size": m, "metric": metric}
+            e = {"spearman": m - 1, "kendall": m * (m - 1) // 2, "hamming": m * (m - 1)}[metric]
+        if E + e > 4 * (1 + seed % 8):
+            if params:
+                break
+            continue
+        params.append(d)
+        E += e
+    space = scenarios.build_space({"params": params, "constraints": []}, _bt.space)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    n = 70
+    cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, n + 60, rng))))[:n]
+    y = rng.standard_normal(len(cfgs))
+    hyp = Hyper(outputscale=0.9, noise_variance=1e-4,
+                lengthscales=tuple(rng.uniform(0.9, 3.0, len(params))))
+    gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+    sc.set_gp(gp)
+    assert sc.gp_kernel() == "tensor" and sc.distance_ksteps() == (E + 3) // 4, (E, sc.distance_ksteps())
+    rows = sc.to_device(scenarios.sample_rows_uniform(lay, 7 * 128 + 5, rng))
     mean, var = (x.cpu().numpy() for x in sc.predict(rows))
     sample = lay.decode(rows.cpu().numpy().view(np.uint32))
     og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
