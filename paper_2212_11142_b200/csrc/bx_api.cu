@@ -1032,14 +1032,36 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     // indirect slots: real parameters whose codes span many thresholds keep, per tree, only the few
     // distinct masks its own splits produce (runs of equal masks along the code) and a [code][tree]
     // u16 index into them
-    std::vector<int> ind;
+    // indirect slots (QsForestDev): a real parameter whose codes span many thresholds, and a
+    // permutation of <= 5 elements as ONE slot coded by its rank (m! codes, the AND of its element
+    // positions' masks) instead of m position slots
+    struct Ind {
+      int param, sub, range;
+      std::vector<int> slots;  // the q-slots it replaces
+    };
+    std::vector<Ind> ind;
+    std::vector<char> taken(qparam.size(), 0);
     std::vector<int32_t> dparam, dsub, dsoff;
     int dstride = 0;
     if (ok) {
-      for (size_t c = 0; c < qparam.size(); ++c)
-        if (h->params[qparam[c]].kind == BX_REAL && qrange[c] > 32 && ind.size() < 2) ind.push_back((int)c);
+      for (size_t c = 0; c < qparam.size() && ind.size() < 4; ++c)
+        if (h->params[qparam[c]].kind == BX_REAL && qrange[c] > 32) {
+          ind.push_back(Ind{qparam[c], qsub[c], qrange[c], {(int)c}});
+          taken[c] = 1;
+        }
+      for (int k = 0; k < h->n_params && ind.size() < 4; ++k) {
+        const bx_param_desc& p = h->params[k];
+        if (p.kind != BX_PERMUTATION || p.size > 5) continue;
+        Ind d{k, -1, 1, std::vector<int>(p.size, -1)};
+        for (int i = 2; i <= p.size; ++i) d.range *= i;
+        for (size_t c = 0; c < qparam.size(); ++c)
+          if (qparam[c] == k) d.slots[qsub[c]] = (int)c;  // slot of element e (code = its position)
+        if (std::find(d.slots.begin(), d.slots.end(), -1) != d.slots.end()) continue;
+        for (int c : d.slots) taken[c] = 1;
+        ind.push_back(d);
+      }
       for (size_t c = 0; c < qparam.size(); ++c) {
-        if (std::find(ind.begin(), ind.end(), (int)c) != ind.end()) continue;
+        if (taken[c]) continue;
         dparam.push_back(qparam[c]);
         dsub.push_back(qsub[c]);
         dsoff.push_back(dstride);
@@ -1055,7 +1077,7 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       int tpad = (T + 7) / 8 * 8 + 1;
       std::vector<uint64_t> mt((size_t)std::max(dstride, 1) * tpad, ~0ull);
       for (size_t c = 0, d = 0; c < qparam.size(); ++c) {
-        if (std::find(ind.begin(), ind.end(), (int)c) != ind.end()) continue;
+        if (taken[c]) continue;
         for (int v = 0; v < qrange[c]; ++v)
           for (int t = 0; t < T; ++t) mt[(size_t)(dsoff[d] + v) * tpad + t] = mask[(size_t)t * stride + qsoff[c] + v];
         ++d;
@@ -1064,29 +1086,55 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
       int itpad = (T + 7) / 8 * 8;
       if ((itpad / 8) % 2 == 0) itpad += 8;
       int irows = 0;
-      for (int c : ind) irows += qrange[c];
+      for (const Ind& d : ind) irows += d.range;
+      ok = (size_t)irows * itpad * 2 <= 96 * 1024;
       std::vector<uint16_t> iidx((size_t)std::max(irows, 1) * itpad, 0);
       std::vector<uint64_t> imask;
       qs.n_ind = (int)ind.size();
       int ioff = 0;
       for (size_t i = 0; i < ind.size() && ok; ++i) {
-        const int c = ind[i];
-        qs.ind_param[i] = qparam[c];
-        qs.ind_sub[i] = qsub[c];
+        const Ind& d = ind[i];
+        qs.ind_param[i] = d.param;
+        qs.ind_sub[i] = d.sub;
         qs.ind_off[i] = ioff;
+        const bx_param_desc& p = h->params[d.param];
         for (int t = 0; t < T && ok; ++t) {
           int cur = -1;
-          for (int v = 0; v < qrange[c]; ++v) {
-            const uint64_t mv = mask[(size_t)t * stride + qsoff[c] + v];
+          for (int v = 0; v < d.range; ++v) {
+            uint64_t mv;
+            if (p.kind == BX_REAL) {
+              mv = mask[(size_t)t * stride + qsoff[d.slots[0]] + v];
+            } else {  // permutation of rank v (Lehmer code): AND of the element-position masks
+              int a[16], used = 0, r = v;
+              for (int i = 0; i < p.size; ++i) {
+                int f = 1;
+                for (int j = 2; j <= p.size - 1 - i; ++j) f *= j;
+                int c = r / f;
+                r %= f;
+                for (int e = 0; e < p.size; ++e)
+                  if (!((used >> e) & 1) && c-- == 0) {
+                    a[i] = e;
+                    used |= 1 << e;
+                    break;
+                  }
+              }
+              mv = ~0ull;
+              for (int i = 0; i < p.size; ++i) mv &= mask[(size_t)t * stride + qsoff[d.slots[a[i]]] + i];
+            }
             if (cur < 0 || imask[cur] != mv) {
-              cur = (int)imask.size();
-              imask.push_back(mv);
+              cur = -1;
+              for (size_t u = imask.size() > 64 ? imask.size() - 64 : 0; u < imask.size(); ++u)
+                if (imask[u] == mv) cur = (int)u;  // reuse a recent equal mask (same tree)
+              if (cur < 0) {
+                cur = (int)imask.size();
+                imask.push_back(mv);
+              }
             }
             if (cur > 65535) { ok = false; break; }
             iidx[(size_t)(ioff + v) * itpad + t] = (uint16_t)cur;
           }
         }
-        ioff += qrange[c];
+        ioff += d.range;
       }
       if (imask.empty()) imask.push_back(~0ull);
       if (ok) {

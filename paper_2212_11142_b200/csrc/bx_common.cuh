@@ -128,12 +128,13 @@ struct QsForestDev {
   // offset | count << 16 into rthr and its value is the number of thresholds below the coordinate
   const double* rthr;
   int32_t has_real;
-  // indirect slots (real parameters with many distinct thresholds across the forest): per tree only
-  // the few masks its own splits produce are stored (imask), and a [code][tree] table of u16
-  // indices into imask replaces the [code][tree] u64 mask rows (4x smaller), so the forest's
-  // tables fit in shared memory; the slots' codes are computed like a real code (code_sub)
+  // indirect slots: per tree only the few distinct masks are stored (imask) and a [code][tree] table
+  // of u16 indices into imask replaces the [code][tree] u64 mask rows (4x smaller).  Real parameters
+  // with many distinct thresholds across the forest (code as a real code, ind_sub = its threshold
+  // run), and permutations of <= 5 elements as one slot coded by the permutation's rank (ind_sub =
+  // -1; m! codes, each the AND of the element-position masks: one table walk instead of m)
   int32_t n_ind;
-  int32_t ind_param[2], ind_sub[2], ind_off[2];  // ind_off: first row of the slot in iidx
+  int32_t ind_param[4], ind_sub[4], ind_off[4];  // ind_off: first row of the slot in iidx
   const uint16_t* iidx;      // [rows][itpad] index into imask
   const uint64_t* imask;     // [n_imask]
   int32_t itpad, n_iidx_rows, n_imask;

@@ -230,7 +230,18 @@ __device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* r
     }
     return lo;
   }
-  if (p.kind == BX_PERMUTATION) return perm_pos(row_u64(row, p.word), p.size, sub);
+  if (p.kind == BX_PERMUTATION) {
+    const uint64_t x = row_u64(row, p.word);
+    if (sub >= 0) return perm_pos(x, p.size, sub);
+    int r = 0;  // rank (Lehmer code) of the permutation, elements in position order
+    for (int i = 0; i < p.size; ++i) {
+      const int ai = (int)((x >> (4 * (p.size - 1 - i))) & 15u);
+      int c = 0;
+      for (int j = i + 1; j < p.size; ++j) c += (int)((x >> (4 * (p.size - 1 - j))) & 15u) < ai ? 1 : 0;
+      r = r * (p.size - i) + c;
+    }
+    return r;
+  }
   // sub < 0: one code for the whole categorical parameter (its label index; the per-label masks
   // are the ANDs of the one-hot features' masks), else the one-hot feature [label == sub]
   if (p.kind == BX_CATEGORICAL) return sub < 0 ? (int)row[p.word] : ((int)row[p.word] == sub ? 1 : 0);
@@ -298,15 +309,15 @@ __device__ void qs_load_tables(const QsForestDev& f, unsigned char* smem, const 
 
 // indirect slots of one candidate: the shared address of its index row (tree 0)
 __device__ __forceinline__ void qs_ind_rows(const QsForestDev& f, const bx_param_desc* params, const uint32_t* row,
-                                            uint32_t iidx_s, uint32_t (&irow)[2]) {
-  for (int i = 0; i < 2; ++i)
+                                            uint32_t iidx_s, uint32_t (&irow)[4]) {
+  for (int i = 0; i < 4; ++i)
     irow[i] = i < f.n_ind
                   ? iidx_s + 2u * (uint32_t)((f.ind_off[i] + qs_code(params[f.ind_param[i]], row, f.ind_sub[i], f.rthr)) * f.itpad)
                   : 0u;
 }
 
 // the indirect slots' masks of trees g0 .. g0 + 7 ANDed into m
-__device__ __forceinline__ void qs_ind_and(const QsForestDev& f, const uint32_t (&irow)[2], uint32_t imask_s, int g0,
+__device__ __forceinline__ void qs_ind_and(const QsForestDev& f, const uint32_t (&irow)[4], uint32_t imask_s, int g0,
                                            uint64_t (&m)[kQsGroup]) {
   for (int i = 0; i < f.n_ind; ++i) {
     const uint32_t ir = irow[i] + 2u * (uint32_t)g0;
@@ -345,7 +356,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
     for (int c = 0; c < f.n_codes; ++c)
       sts_s32(off_s + 4u * kQsThreads * c,
               (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
-    uint32_t irow[2];
+    uint32_t irow[4];
     qs_ind_rows(f, params, row, iidx_s, irow);
     double sum = 0.0;
     if (use_pairwise) {
@@ -428,7 +439,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
         for (int c = 0; c < f.n_codes; ++c)
           sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
       }
-      uint32_t irow[2];
+      uint32_t irow[4];
       qs_ind_rows(f, params, row, iidx_s, irow);
       double sum = 0.0;
       for (int g0 = 0; g0 < f.n_trees; g0 += kQsGroup) {

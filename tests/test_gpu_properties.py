@@ -325,7 +325,7 @@ def test_mixed_space_embedding_against_oracle(seed):
     n = 70
     cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, n + 60, rng))))[:n]
     y = rng.standard_normal(len(cfgs))
-    hyp = Hyper(outputscale=0.9, noise_variance=1e-4,
+    hyp = Hyper(outputscale=0.9, noise_variance=1e-3,
                 lengthscales=tuple(rng.uniform(0.9, 3.0, len(params))))
     gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
     sc.set_gp(gp)
