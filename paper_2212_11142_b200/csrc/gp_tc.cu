@@ -33,6 +33,9 @@
 //                    digits and stored into the candidate's TMEM lane (tcgen05.st)
 // TMEM (512 columns): two 96-column accumulators (6 groups x 16 rows) so the epilogue of one chunk
 // overlaps the MMAs of the next, then 40 columns (5 digits x 32 bytes) per column slice.
+#include <cstdio>
+#include <cstdlib>
+
 #include "bx_common.cuh"
 #include "matern.cuh"
 #include "summary.cuh"
@@ -227,12 +230,14 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   L.par = off;
   off += n_params * (int)sizeof(bx_param_desc);
   off = (off + 15) & ~15;
-  L.planes = off;
-  off += (ks > 0 ? 4 * ks : n_params) * npad * 8;
+  L.planes = off;  // ks > 0: row stride npad + 4 doubles (the B-fragment loads are conflict-free)
+  off += (ks > 0 ? 4 * ks * (npad + 4) : n_params * npad) * 8;
+  off = (off + 15) & ~15;
   L.kmask = off;   // [n_kendall][npad][2]
   off += ks > 0 ? 0 : n_kendall * npad * 16;
-  L.cval = off;
-  off += ks > 0 ? (n_emb + 1) * kM * 8 : 2 * n_params * kM * 8;
+  L.cval = off;    // ks > 0: [E][kM + 1] (odd row stride: conflict-free decoder stores)
+  off += ks > 0 ? n_emb * (kM + 1) * 8 : 2 * n_params * kM * 8;
+  off = (off + 15) & ~15;
   L.cmask = off;   // [2][n_kendall][128][2] candidate Kendall masks
   off += ks > 0 ? 0 : 2 * n_kendall * kM * 16;
   L.exp2 = off;    // 2^(j/256), j < 256
@@ -273,6 +278,8 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
   const int npass = tc_passes(nsl);
   const int E = ta.n_emb;
+  constexpr int kCvs = kM + 1;        // DMMA mode: candidate-buffer row stride (doubles)
+  const int pls = npad + 4;           // DMMA mode: planes row stride (doubles)
   const bool resident = ta.mat_resident != 0;
   const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
@@ -307,7 +314,8 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   for (int i = tid; i < n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
   if constexpr (kDmma) {
-    for (int i = tid; i < 4 * KS * npad; i += blockDim.x) planes[i] = (uint64_t)__double_as_longlong(ta.emb_planes[i]);
+    for (int i = tid; i < 4 * KS * npad; i += blockDim.x)
+      planes[(i / npad) * pls + i % npad] = (uint64_t)__double_as_longlong(ta.emb_planes[i]);
     if (!ta.aug)
       for (int j = tid; j < npad; j += blockDim.x) s_yy[j] = ta.emb_yy[j];
     for (int i = tid; i < E * (int)sizeof(EmbDim) / 4; i += blockDim.x)
@@ -390,17 +398,13 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       mb_wait_sleep(rows_full, (uint32_t)(t & 1));
       const int sw = staged_words(tile);
       if constexpr (kDmma) {
-        // thread = candidate (two per thread): E coordinates and |x'|^2
+        // thread = candidate (two per thread, every lane doing the same coordinate at a time: the
+        // FP64 work of the permutation coordinates stays dense); the producers form |x'|^2
         for (int cc = dt; cc < kM; cc += 64) {
           const int64_t gi = tile * kM + cc;
           const uint32_t* rw = (cc + 1) * words <= sw ? rowsbuf + cc * words : a.rows + (size_t)gi * words;
-          double xx = 0.0;
-          for (int e = 0; e < E; ++e) {
-            const double v = gi < a.q ? emb_value(s_emb[e], rw, s_etab) : 0.0;
-            cval[e * kM + cc] = (uint64_t)__double_as_longlong(v);
-            xx = fma(v, v, xx);
-          }
-          cval[E * kM + cc] = (uint64_t)__double_as_longlong(xx);
+          for (int e = 0; e < E; ++e)
+            cval[e * kCvs + cc] = (uint64_t)__double_as_longlong(gi < a.q ? emb_value(s_emb[e], rw, s_etab) : 0.0);
         }
         asm volatile("bar.sync 3, 64;" ::: "memory");
         if (dt == 0) {
@@ -644,20 +648,30 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
     uint32_t slot_used = 0, slot_par = 0;
     for (int t = 0; t < my_tiles; ++t) {
       if (pt == 0) TC_TRACE(0, 1, t);
-      mb_wait(&cval_full[0], (uint32_t)(t & 1));
+      mb_wait_sleep(&cval_full[0], (uint32_t)(t & 1));  // parked: the decoders need the issue slots
       if (pt == 0) TC_TRACE(0, 2, t);
-      // A fragments: row = candidate 32 q + 16 h + 8 rb + t1, k = t0 + 4 kk of [x', 1, |x'|^2, 0..]
+      // A fragments: row = candidate 32 q + 16 h + 8 rb + t1, k = t0 + 4 kk of [x', 1, |x'|^2, 0..];
+      // |x'|^2 summed over the four lanes t0 that hold the candidate's coordinates
       double afr[2][KS > 0 ? KS : 1], xx[2];
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb) {
         const int c = quarter * 32 + half * 16 + 8 * rb + t1;
-        xx[rb] = __longlong_as_double((long long)cval[E * kM + c]);
+        xx[rb] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
           const int k = t0 + 4 * kk;
-          afr[rb][kk] = k < E ? __longlong_as_double((long long)cval[k * kM + c])
-                              : (aug && k == E ? 1.0 : (aug && k == E + 1 ? xx[rb] : 0.0));
+          afr[rb][kk] = k < E ? __longlong_as_double((long long)cval[k * kCvs + c]) : 0.0;
+          xx[rb] = fma(afr[rb][kk], afr[rb][kk], xx[rb]);
         }
+        xx[rb] += __shfl_xor_sync(0xffffffffu, xx[rb], 1);
+        xx[rb] += __shfl_xor_sync(0xffffffffu, xx[rb], 2);
+        if (aug)
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) {
+            const int k = t0 + 4 * kk;
+            if (k == E) afr[rb][kk] = 1.0;
+            if (k == E + 1) afr[rb][kk] = xx[rb];
+          }
       }
       __syncwarp();
       if (lane == 0) mb_arrive(&cval_free[0]);  // the decoders may write the next tile
@@ -674,7 +688,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
           for (int j = 0; j < 4; ++j) acc[rb][j][0] = acc[rb][j][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
-          const double* brow = reinterpret_cast<const double*>(planes) + (size_t)(t0 + 4 * kk) * npad + j0 + t1;
+          const double* brow = reinterpret_cast<const double*>(planes) + (size_t)(t0 + 4 * kk) * pls + j0 + t1;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const double b = brow[8 * j];  // B[k = t0 + 4 kk][column 8 j + t1]
@@ -961,6 +975,9 @@ cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   const TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0);
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks || a.ks > 8 || (a.ks > 0 && a.f.precise))
     return cudaErrorInvalidValue;
+  if (getenv("BX_TC_INFO"))  // development aid: kernel geometry
+    fprintf(stderr, "gp_tc: n %d ks %d E %d aug %d smem %d resident %d words %d\n", n, a.ks, a.n_emb, a.aug, L.total,
+            a.mat_resident, W);
   auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
   int threads = tc_threads<0>();
   switch (a.ks) {
