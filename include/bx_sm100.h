@@ -186,7 +186,8 @@ enum bx_score_flags {
   BX_SCORE_RF_PAIRWISE = 1,   /* numpy pairwise-8 tree sum (what predict_proba does at q == 1) */
   BX_SCORE_NO_SUMMARY = 2,    /* skip the top-k / tracker reduction                             */
   BX_SCORE_TIMING = 4,        /* record per-kernel CUDA-event durations (bx_last_timing)        */
-  BX_SCORE_TIMING_POSTERIOR = 8  /* time the posterior kernel only (two events; rf / merge = -1) */
+  BX_SCORE_TIMING_POSTERIOR = 8, /* time the posterior kernel only (two events; rf / merge = -1) */
+  BX_SCORE_PACKED = 16           /* bx_score_host: the host pool is in the packed wire format      */
 };
 
 /* Durations (ms, CUDA events on the call's stream) of the forest, fused-score and merge kernels
@@ -209,10 +210,21 @@ int bx_score(bx_handle* h, const uint32_t* dev_rows, int64_t q, int64_t index_ba
              bx_score_summary* host_summary, void* stream);
 
 /* Same as bx_score but the pool is a HOST buffer (pinned or pageable): the call copies it to
-   the device in chunks overlapped with scoring.  This is the end-to-end entry point. */
+   the device in chunks overlapped with scoring.  This is the end-to-end entry point.  With
+   BX_SCORE_PACKED the host rows are in the packed wire format (bx_pack_rows), which the
+   tensor-core posterior unpacks on the fly: 2-4x fewer bytes over PCIe for typical spaces. */
 int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t index_base,
                   double f_model, double eps_f, int32_t k, int32_t flags,
                   bx_score_summary* host_summary, void* stream);
+
+/* Packed wire format of the current space: each parameter at its bit width (finite kinds: domain
+   index; permutation: 4 bits per element; real: the f64 value, plus the f64 coordinate only when a
+   log transform makes it host-dependent - otherwise the device recomputes (v - lo) / (hi - lo)
+   bit-exactly, surrogate.py:163-170), rows padded to whole 32-bit words.  Host-side conversions
+   (CPU loops, no device work). */
+int bx_packed_row_words(bx_handle* h);
+int bx_pack_rows(bx_handle* h, const uint32_t* host_rows, int64_t q, uint32_t* host_packed);
+int bx_unpack_rows(bx_handle* h, const uint32_t* host_packed, int64_t q, uint32_t* host_rows);
 
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the

@@ -30,10 +30,11 @@ EXPORTED = (
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_cot_contains",
     "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64", "bx_probe_int8",
-    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps",
+    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps", "bx_packed_row_words", "bx_pack_rows", "bx_unpack_rows",
 )
 BX_SCORE_TIMING = 4
 BX_SCORE_TIMING_POSTERIOR = 8
+BX_SCORE_PACKED = 16
 
 
 class ParamDesc(C.Structure):
@@ -73,6 +74,9 @@ _SIGS = {
     "bx_device_sm_count": (C.c_int, [_p]),
     "bx_gp_kernel": (C.c_int, [_p]),
     "bx_gp_distance_ksteps": (C.c_int, [_p]),
+    "bx_packed_row_words": (C.c_int, [_p]),
+    "bx_pack_rows": (C.c_int, [_p, _p, _i64, _p]),
+    "bx_unpack_rows": (C.c_int, [_p, _p, _i64, _p]),
     "bx_set_space": (C.c_int, [_p, _p, _i32, _i32, _p, _i32, _p, _i32, _i32]),
     "bx_set_gp": (C.c_int, [_p, _p, _i32, _p, _p, _f64, _p, _f64, _f64, _p]),
     "bx_set_forest": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _p, _i32, _i32, _f64]),

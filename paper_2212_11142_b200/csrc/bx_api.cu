@@ -100,6 +100,7 @@ struct bx_handle {
   uint32_t* h_ones = nullptr;
   int64_t h_ones_len = 0;
   const uint32_t* stream_ready = nullptr;  // set while a streaming posterior launch is enqueued
+  const uint32_t* stream_packed = nullptr; // ... whose pool arrives packed (unpacked into d_pool)
   int stream_shift = 0;
   // distances on the FP64 tensor cores over the embedding of W (bx_set_gp decides): tc_ks k-steps,
   // 0 -> FMA distances
@@ -117,6 +118,8 @@ struct bx_handle {
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
+  PackSpec pack{};                  // packed wire format of the space (bx_set_space)
+  DevBuf d_packed;                  // streamed packed pool
   DevBuf d_panels, d_ei, d_grad_scratch, d_leaf_count, d_gen_rows;
   bool has_leaf_count = false;
   cudaStream_t rf_stream = nullptr;
@@ -276,6 +279,8 @@ cudaError_t launch_posterior(const bx_handle* h, const FusedArgs& f, cudaStream_
     t.kscale = h->tc_kscale;
     t.ready = h->stream_ready;
     t.ready_shift = h->stream_shift;
+    t.packed = h->stream_packed;
+    t.pack = h->pack;
     t.ks = h->tc_ks;
     t.n_emb = (int32_t)h->tc_emb.size();
     t.aug = h->tc_aug ? 1 : 0;
@@ -451,6 +456,21 @@ static bool build_embedding(const bx_handle* h, const uint32_t* train_rows, int 
   return true;
 }
 
+
+namespace bx {
+__global__ void unpack_kernel(PackSpec spec, const uint32_t* packed, int64_t q, int words, uint32_t* rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
+    unpack_row(spec, packed + (size_t)i * spec.pw, rows + (size_t)i * words, words);
+}
+cudaError_t launch_unpack(const PackSpec& spec, const uint32_t* packed, int64_t q, int words, uint32_t* rows,
+                          cudaStream_t s) {
+  int64_t blocks = (q + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  unpack_kernel<<<(int)blocks, 256, 0, s>>>(spec, packed, q, words, rows);
+  return cudaGetLastError();
+}
+}  // namespace bx
+
 extern "C" {
 
 int bx_abi_version(void) { return BX_ABI_VERSION; }
@@ -510,6 +530,7 @@ void bx_destroy(bx_handle* h) {
   h->d_pool.release();
   h->d_ready.release();
   h->d_emb.release();
+  h->d_packed.release();
   h->d_emb_tab.release();
   h->d_emb_planes.release();
   h->d_emb_yy.release();
@@ -537,6 +558,25 @@ int bx_gp_kernel(bx_handle* h) {
 }
 
 int bx_gp_distance_ksteps(bx_handle* h) { return h && h->use_tc ? h->tc_ks : 0; }
+
+int bx_packed_row_words(bx_handle* h) { return h && h->has_space ? h->pack.pw : 0; }
+
+int bx_pack_rows(bx_handle* h, const uint32_t* rows, int64_t q, uint32_t* packed) {
+  int r = check_space(h);
+  if (r) return r;
+  if (q < 0 || (q > 0 && (!rows || !packed))) return fail(h, BX_ERR_ARG, "bad buffers");
+  for (int64_t i = 0; i < q; ++i) pack_row(h->pack, rows + (size_t)i * h->row_words, packed + (size_t)i * h->pack.pw);
+  return BX_OK;
+}
+
+int bx_unpack_rows(bx_handle* h, const uint32_t* packed, int64_t q, uint32_t* rows) {
+  int r = check_space(h);
+  if (r) return r;
+  if (q < 0 || (q > 0 && (!rows || !packed))) return fail(h, BX_ERR_ARG, "bad buffers");
+  for (int64_t i = 0; i < q; ++i)
+    unpack_row(h->pack, packed + (size_t)i * h->pack.pw, rows + (size_t)i * h->row_words, h->row_words);
+  return BX_OK;
+}
 
 int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, int32_t row_words,
                  const double* coord_lut, int32_t coord_len, const int32_t* rank_lut,
@@ -590,6 +630,34 @@ int bx_set_space(bx_handle* h, const bx_param_desc* params, int32_t n_params, in
   h->row_words = row_words;
   h->n_features = n_features;
   h->n_slots = (int)sparam.size();
+  // packed wire format: parameters in order at their bit widths
+  {
+    PackSpec& ps = h->pack;
+    ps = PackSpec{};
+    ps.n = n_params;
+    int bit = 0;
+    for (int k = 0; k < n_params; ++k) {
+      const bx_param_desc& p = params[k];
+      PackParam& q = ps.p[k];
+      q.kind = p.kind;
+      q.word = p.word;
+      q.bit = bit;
+      q.lo = p.lo;
+      q.hi = p.hi;
+      if (p.kind == BX_REAL) {
+        q.carry_coord = p.is_log ? 1 : 0;
+        q.bits = q.carry_coord ? 128 : 64;
+      } else if (p.kind == BX_PERMUTATION) {
+        q.bits = 4 * p.size;
+      } else {
+        int b = 1;
+        while ((1 << b) < p.size) ++b;
+        q.bits = b;
+      }
+      bit += q.bits;
+    }
+    ps.pw = (bit + 31) / 32;
+  }
   h->has_space = true;
   // every other piece of model state is expressed in the old space's rows / features / domain
   // indices: drop it, so a caller that forgets to re-set it gets BX_ERR_STATE, not stale reads
@@ -1477,15 +1545,23 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   cudaSetDevice(h->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int W = h->row_words;
+  const bool packed = (flags & BX_SCORE_PACKED) != 0;
+  const int HW = packed ? h->pack.pw : W;  // words per host row
+  flags &= ~(BX_SCORE_PACKED | BX_SCORE_NO_SUMMARY);
   BX_CUDA(h, h->d_pool.ensure((size_t)q * W * 4));
+  if (packed) BX_CUDA(h, h->d_packed.ensure((size_t)q * HW * 4));
   BX_CUDA(h, h->d_partials.ensure(sizeof(Partial) * (size_t)max_partials(h->sm_count)));
   BX_CUDA(h, h->d_summary.ensure(sizeof(bx_score_summary)));
   uint32_t* pool = h->d_pool.as<uint32_t>();
+  uint32_t* dst = packed ? h->d_packed.as<uint32_t>() : pool;  // where the host rows land
   Partial* parts = h->d_partials.as<Partial>();
-  if (h->use_tc) {
+  const bool forest = h->has_forest && h->forest.has_trees;
+  if (h->use_tc && (!forest || qs_summary_available(h->forest)) && !(flags & BX_SCORE_RF_PAIRWISE) &&
+      (!packed || h->pack.pw <= 16)) {
     // Streaming: the whole pool is copied in 2^16-row chunks on the copy stream, each followed by a
     // 4-byte ready flag written by the copy engine; one posterior launch consumes tiles as their
-    // chunk lands (the row prefetcher waits on the flag), so only the first chunk's copy is
+    // chunk lands (the row prefetcher waits on the flag; packed rows are unpacked by its decoders,
+    // which write the full rows for the kernels after it), so only the first chunk's copy is
     // exposed and there is no per-chunk launch cost.  The forest + summary kernel runs after the
     // last copy.
     const int shift = 16;
@@ -1504,7 +1580,7 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done, 0));
     for (int64_t c = 0; c < n_chunks; ++c) {
       const int64_t off = c << shift, len = std::min<int64_t>((int64_t)1 << shift, q - off);
-      BX_CUDA(h, cudaMemcpyAsync(pool + (size_t)off * W, host_rows + (size_t)off * W, (size_t)len * W * 4,
+      BX_CUDA(h, cudaMemcpyAsync(dst + (size_t)off * HW, host_rows + (size_t)off * HW, (size_t)len * HW * 4,
                                  cudaMemcpyHostToDevice, h->copy_stream));
       BX_CUDA(h, cudaMemcpyAsync(ready + c, h->h_ones + c, 4, cudaMemcpyHostToDevice, h->copy_stream));
     }
@@ -1513,9 +1589,11 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
       int np = 0;
       h->stream_ready = pass == 0 ? ready : nullptr;
       h->stream_shift = shift;
-      r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_NO_SUMMARY, nullptr,
-                     nullptr, parts, &np, s, false, pass == 1, pass == 0 ? h->ev_copy : nullptr);
+      h->stream_packed = (pass == 0 && packed) ? dst : nullptr;  // pass 2 reads the unpacked pool
+      r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags, nullptr, nullptr, parts, &np, s, false,
+                     pass == 1, pass == 0 ? h->ev_copy : nullptr);
       h->stream_ready = nullptr;
+      h->stream_packed = nullptr;
       if (r) return r;
       BX_CUDA(h, launch_summary_merge(parts, np, space_dev(h), k, nullptr, 0,
                                       h->d_summary.as<bx_score_summary>(), s));
@@ -1524,16 +1602,18 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
       if (summary->n_finite != 0) break;
     }
   } else {
-    // the other posterior kernels: one copy, then the device-resident path
-    BX_CUDA(h, cudaMemcpyAsync(pool, host_rows, (size_t)q * W * 4, cudaMemcpyHostToDevice, s));
-    r = bx_score(h, pool, q, index_base, f_model, eps_f, k, flags & ~BX_SCORE_NO_SUMMARY, nullptr, nullptr,
-                 summary, stream);
+    // the other kernel paths: one copy (and a device unpack), then the device-resident path
+    BX_CUDA(h, cudaMemcpyAsync(dst, host_rows, (size_t)q * HW * 4, cudaMemcpyHostToDevice, s));
+    if (packed) BX_CUDA(h, launch_unpack(h->pack, dst, q, W, pool, s));
+    r = bx_score(h, pool, q, index_base, f_model, eps_f, k, flags, nullptr, nullptr, summary, stream);
     if (r) return r;
   }
   // the pool is host-resident: the top-k rows come straight from the caller's buffer
-  for (int i = 0; i < summary->n_top; ++i)
-    std::memcpy(summary->top[i].row, host_rows + (size_t)(summary->top[i].index - index_base) * W,
-                (size_t)W * 4);
+  for (int i = 0; i < summary->n_top; ++i) {
+    const uint32_t* src = host_rows + (size_t)(summary->top[i].index - index_base) * HW;
+    if (packed) unpack_row(h->pack, src, summary->top[i].row, W);
+    else std::memcpy(summary->top[i].row, src, (size_t)W * 4);
+  }
   return BX_OK;
 }
 

@@ -445,6 +445,79 @@ __host__ __device__ __forceinline__ double emb_value(const EmbDim& e, const uint
   return acc;
 }
 
+// Packed wire format (bx_pack_rows): parameter k at bit `bit` of the packed row, `bits` wide;
+// reals carry the f64 value (64 bits) and, when the coordinate is host-dependent (log transform),
+// the f64 coordinate (64 more bits), else the coordinate is (v - lo) / (hi - lo) (surrogate.py:
+// 163-170: IEEE subtract and divide, bit-identical to numpy's).
+struct PackParam {
+  int32_t kind, word, bit, bits, carry_coord, pad;
+  double lo, hi;
+};
+struct PackSpec {
+  int32_t n, pw;  // parameters, packed words per row
+  PackParam p[BX_MAX_PARAMS];
+};
+__host__ __device__ __forceinline__ uint64_t pk_get(const uint32_t* pk, int bit, int bits) {
+  uint64_t v = 0;
+  for (int got = 0; got < bits;) {  // at most 32 bits per word step
+    const int w = (bit + got) >> 5, o = (bit + got) & 31, take = (32 - o < bits - got) ? 32 - o : bits - got;
+    v |= (uint64_t)((pk[w] >> o) & (take == 32 ? 0xFFFFFFFFu : ((1u << take) - 1u))) << got;
+    got += take;
+  }
+  return v;
+}
+__host__ __device__ __forceinline__ void pk_put(uint32_t* pk, int bit, int bits, uint64_t v) {
+  for (int put = 0; put < bits;) {
+    const int w = (bit + put) >> 5, o = (bit + put) & 31, take = (32 - o < bits - put) ? 32 - o : bits - put;
+    const uint32_t m = (take == 32 ? 0xFFFFFFFFu : ((1u << take) - 1u));
+    pk[w] = (pk[w] & ~(m << o)) | ((uint32_t)(v >> put) & m) << o;
+    put += take;
+  }
+}
+__host__ __device__ inline void pack_row(const PackSpec& s, const uint32_t* row, uint32_t* pk) {
+  for (int w = 0; w < s.pw; ++w) pk[w] = 0;
+  for (int k = 0; k < s.n; ++k) {
+    const PackParam& p = s.p[k];
+    if (p.kind == BX_REAL) {
+      pk_put(pk, p.bit, 64, (uint64_t)row[p.word] | ((uint64_t)row[p.word + 1] << 32));
+      if (p.carry_coord) pk_put(pk, p.bit + 64, 64, (uint64_t)row[p.word + 2] | ((uint64_t)row[p.word + 3] << 32));
+    } else if (p.kind == BX_PERMUTATION) {
+      pk_put(pk, p.bit, p.bits, (uint64_t)row[p.word] | ((uint64_t)row[p.word + 1] << 32));
+    } else {
+      pk_put(pk, p.bit, p.bits, row[p.word]);
+    }
+  }
+}
+// words of the full row not covered by a parameter are zero (as SpaceLayout.encode leaves them)
+__host__ __device__ inline void unpack_row(const PackSpec& s, const uint32_t* pk, uint32_t* row, int words) {
+  for (int w = 0; w < words; ++w) row[w] = 0;
+  for (int k = 0; k < s.n; ++k) {
+    const PackParam& p = s.p[k];
+    if (p.kind == BX_REAL) {
+      const uint64_t v = pk_get(pk, p.bit, 64);
+      uint64_t c;
+      if (p.carry_coord) {
+        c = pk_get(pk, p.bit + 64, 64);
+      } else {
+        double x;
+        memcpy(&x, &v, 8);
+        const double cx = (p.hi == p.lo) ? 0.0 : (x - p.lo) / (p.hi - p.lo);
+        memcpy(&c, &cx, 8);
+      }
+      row[p.word] = (uint32_t)v;
+      row[p.word + 1] = (uint32_t)(v >> 32);
+      row[p.word + 2] = (uint32_t)c;
+      row[p.word + 3] = (uint32_t)(c >> 32);
+    } else if (p.kind == BX_PERMUTATION) {
+      const uint64_t v = pk_get(pk, p.bit, p.bits);
+      row[p.word] = (uint32_t)v;
+      row[p.word + 1] = (uint32_t)(v >> 32);
+    } else {
+      row[p.word] = (uint32_t)pk_get(pk, p.bit, p.bits);
+    }
+  }
+}
+
 struct TcArgs {
   FusedArgs f;
   const unsigned char* mdig;  // [chunk][slice] blocks of 6 digit planes x 16 rows x 32 columns
@@ -479,6 +552,11 @@ struct TcArgs {
   int32_t emb_tab_len;
   const double* emb_planes;   // [4 ks][32 n_slices] the B operand: -2 y', (aug: |y'|^2, 1), zeros
   const double* emb_yy;       // [32 n_slices] |y'|^2 (added explicitly when !aug)
+  // packed != null: the pool arrives in the packed wire format (streamed host pools); the
+  // prefetcher stages packed rows, the decoders unpack them into the staging buffer and write the
+  // full rows to f.rows (read by the forest / summary kernels after this one)
+  const uint32_t* packed;
+  PackSpec pack;
 };
 
 

@@ -384,6 +384,15 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
     const int64_t count = min((int64_t)kM, a.q - tile * kM);
     return (int)(((count * words * 4) & ~(int64_t)15) / 4);
   };
+  // packed pools: the tile's packed rows are bulk-copied to the END of the staging buffer and the
+  // decoders unpack them in place (every thread reads its packed rows before any full row is
+  // written; full row c never overlaps a packed row c' > c)
+  const int pw = ta.pack.pw;
+  const int pk_off = (words - pw) * kM;  // words; a multiple of 4 (16-byte aligned)
+  auto staged_packed = [&](int64_t tile) -> int {
+    const int64_t count = min((int64_t)kM, a.q - tile * kM);
+    return (int)(((count * pw * 4) & ~(int64_t)15) / 4);
+  };
 
   if (warp == 2 || warp == 3) {
     // ---- decoders: the next tile's candidates into the candidate buffer --------------------------
@@ -396,7 +405,37 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       if (kDmma ? t >= 1 : t >= 2)
         mb_wait_sleep(&cval_free[buf], (uint32_t)((kDmma ? (t - 1) : ((t - 2) >> 1)) & 1));
       mb_wait_sleep(rows_full, (uint32_t)(t & 1));
-      const int sw = staged_words(tile);
+      int sw = staged_words(tile);
+      if (ta.packed) {
+        // unpack: packed rows (staged or, for a ragged tail, global) into registers, then the full
+        // rows into the staging buffer and to HBM (the forest / summary kernels read them)
+        const int spw = staged_packed(tile);
+        uint32_t pk[2][16];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int cc = dt + 64 * h2;
+          const int64_t gi = tile * kM + cc;
+#pragma unroll
+          for (int w = 0; w < 16; ++w) {
+            const int o = cc * pw + w;
+            pk[h2][w] = (w < pw && gi < a.q) ? (o < spw ? rowsbuf[pk_off + o] : ta.packed[(size_t)gi * pw + w]) : 0u;
+          }
+        }
+        asm volatile("bar.sync 3, 64;" ::: "memory");
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int cc = dt + 64 * h2;
+          const int64_t gi = tile * kM + cc;
+          if (gi < a.q) {
+            uint32_t* dstr = rowsbuf + cc * words;
+            unpack_row(ta.pack, pk[h2], dstr, words);
+            uint32_t* g = const_cast<uint32_t*>(a.rows) + (size_t)gi * words;
+            for (int w = 0; w < words; ++w) g[w] = dstr[w];
+          }
+        }
+        asm volatile("bar.sync 3, 64;" ::: "memory");
+        sw = (int)(min((int64_t)kM, a.q - tile * kM) * words);  // every row is now staged
+      }
       if constexpr (kDmma) {
         // thread = candidate (two per thread, every lane doing the same coordinate at a time: the
         // FP64 work of the permutation coordinates stays dense); the producers form |x'|^2
@@ -473,10 +512,13 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");  // make the data visible to TMA
       }
-      const int sw = staged_words(tile);
+      const int sw = ta.packed ? staged_packed(tile) : staged_words(tile);
       if (sw > 0) {
         mb_expect(rows_full, (uint32_t)sw * 4);
-        bulk_g2s(rowsbuf, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4, rows_full);
+        if (ta.packed)
+          bulk_g2s(rowsbuf + pk_off, ta.packed + (size_t)tile * kM * pw, (uint32_t)sw * 4, rows_full);
+        else
+          bulk_g2s(rowsbuf, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4, rows_full);
       } else {
         mb_arrive(rows_full);
       }

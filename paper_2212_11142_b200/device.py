@@ -241,13 +241,34 @@ class Scorer:
         return {"rf_ms": t[0].value, "score_ms": t[1].value, "merge_ms": t[2].value}
 
     def score_host(self, rows: np.ndarray | torch.Tensor, f_model: float, eps_f: float = 0.0,
-                   k: int = 10, index_base: int = 0) -> Summary:
-        """bx_score_host: the pool stays in (pinned) host memory; copies overlap the scoring."""
+                   k: int = 10, index_base: int = 0, packed: bool = False) -> Summary:
+        """bx_score_host: the pool stays in (pinned) host memory; copies overlap the scoring.
+        packed=True: the rows are in the packed wire format (pack())."""
         q = rows.shape[0]
         s = N.ScoreSummary()
         self._check(self._lib.bx_score_host(self.h, _ptr(rows), q, index_base, float(f_model),
-                                            float(eps_f), int(k), 0, C.byref(s), self.stream))
+                                            float(eps_f), int(k), N.BX_SCORE_PACKED if packed else 0,
+                                            C.byref(s), self.stream))
         return self._summary(s)
+
+    def packed_words(self) -> int:
+        return int(self._lib.bx_packed_row_words(self.h))
+
+    def pack(self, rows: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Encoded rows -> the packed wire format of the current space (host, bx_pack_rows)."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        q = rows.shape[0]
+        if out is None:
+            out = np.empty((q, self.packed_words()), dtype=np.uint32)
+        self._check(self._lib.bx_pack_rows(self.h, _ptr(rows), q, _ptr(out)))
+        return out
+
+    def unpack(self, packed: np.ndarray) -> np.ndarray:
+        packed = np.ascontiguousarray(packed, dtype=np.uint32)
+        q = packed.shape[0]
+        out = np.empty((q, self.layout.row_words), dtype=np.uint32)
+        self._check(self._lib.bx_unpack_rows(self.h, _ptr(packed), q, _ptr(out)))
+        return out
 
     def generate(self, q: int, seed: int, mode: int = 0, index_base: int = 0) -> torch.Tensor:
         """bx_generate: q device-generated rows (mode 0 uniform, 1 chain-of-trees leaf-uniform)."""

@@ -160,13 +160,19 @@ def test_mixed_space_large_n_against_oracle(n):
     sc.close()
 
 
-@pytest.mark.parametrize("case,q,eps", [("C3", 3 * 65536 + 777, None), ("C3", 70001, 1.01),
-                                        ("C2", 200003, None), ("mixed_fit", 65536, None), ("M200", 131075, None)])
-def test_streaming_host_pool_matches_device_pool(case, q, eps):
+@pytest.mark.parametrize("case,q,eps,walk", [("C3", 3 * 65536 + 777, None, False), ("C3", 70001, 1.01, False),
+                                             ("C2", 200003, None, False), ("mixed_fit", 65536, None, False),
+                                             ("M200", 131075, None, False), ("mixed_metrics", 70003, None, False),
+                                             ("M200", 70001, None, True)])
+def test_streaming_host_pool_matches_device_pool(case, q, eps, walk, monkeypatch):
     """bx_score_host streams the pool (chunked copies + ready flags consumed by one posterior
-    launch); its summary equals bx_score's on the same rows — ragged sizes, a forest-less case and
-    the all -inf fallback (eps_f > 1: probability tracker) included."""
+    launch), encoded or in the packed wire format (unpacked by the posterior's decoders); its
+    summary equals bx_score's on the same rows — ragged sizes, a forest-less case, the FMA
+    producers (mixed_metrics), the all -inf fallback (eps_f > 1: probability tracker) and the
+    non-streaming path (node-walk forest before the posterior: one copy + a device unpack kernel)."""
     from paper_2212_11142_b200.device import Scorer
+    if walk:
+        monkeypatch.setenv("BX_FOREST_WALK", "1")
     meta, arr, space = load(case)
     gp, feas = model(meta, arr, space)
     f = gp.objective_to_model(meta["f_best"])
@@ -178,14 +184,33 @@ def test_streaming_host_pool_matches_device_pool(case, q, eps):
     rows_h = scenarios.sample_rows_uniform(sc.layout, q, np.random.default_rng(q))
     pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
     x, _, _ = sc.score(sc.to_device(rows_h), f, eps_f, k=10)
-    y = sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10)
-    assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
-    assert [c.index for c in x.top] == [c.index for c in y.top]
-    assert [c.value for c in x.top] == [c.value for c in y.top]
-    idx = lambda c: None if c is None else (c.index, tuple(c.row))
-    assert idx(x.best) == idx(y.best) and idx(x.best_prob) == idx(y.best_prob)
-    if eps is not None:
-        assert y.n_finite == 0 and y.best_prob is not None
+    packed = torch.from_numpy(sc.pack(rows_h).view(np.int32)).pin_memory()
+    for y in (sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10),
+              sc.score_host(packed.numpy().view(np.uint32), f, eps_f, k=10, packed=True)):
+        assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
+        assert [c.index for c in x.top] == [c.index for c in y.top]
+        assert [c.value for c in x.top] == [c.value for c in y.top]
+        assert [tuple(c.row) for c in x.top] == [tuple(c.row) for c in y.top]
+        idx = lambda c: None if c is None else (c.index, tuple(c.row))
+        assert idx(x.best) == idx(y.best) and idx(x.best_prob) == idx(y.best_prob)
+        if eps is not None:
+            assert y.n_finite == 0 and y.best_prob is not None
+    sc.close()
+
+
+@pytest.mark.parametrize("case", ["mixed_fit", "mixed_metrics", "C1", "C2", "C3", "C4", "M200"])
+def test_packed_wire_format_round_trip(case):
+    """bx_pack_rows / bx_unpack_rows: every parameter at its bit width, real coordinates recomputed
+    bit-exactly unless a log transform makes them host-dependent (then carried); the round trip
+    returns the encoded rows bit for bit (the device unpack is checked by the streaming test)."""
+    from paper_2212_11142_b200.device import Scorer
+    meta, arr, space = load(case)
+    sc = Scorer()
+    lay = sc.set_space(space, meta["use_transforms"])
+    rows = scenarios.sample_rows_uniform(lay, 50_001, np.random.default_rng(11))
+    pk = sc.pack(rows)
+    assert pk.shape[1] == sc.packed_words() <= lay.row_words
+    assert np.array_equal(sc.unpack(pk), rows)
     sc.close()
 
 
