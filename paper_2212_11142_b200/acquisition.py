@@ -221,84 +221,27 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
         return candidates[summ.best_prob.index]
 
     best = summ.best
-    best_val = best.value if best else -math.inf
-    best_cfg = candidates[best.index] if best else None
     if local_search:
-        # the starts climb in lockstep: one neighbour launch and one scoring launch per step for all
-        # still-climbing starts.  Each start's trajectory depends only on its own state, and the
-        # running best is the maximum under a total order (value desc, configuration asc), so the
-        # result equals the reference's start-after-start loop (acquisition.py:186-205).
+        # the climb of every start runs on the device (bx_climb): per step one neighbour launch, the
+        # scoring launches and one bookkeeping launch, and a single 4-byte read of the active count.
+        # Each start's trajectory depends only on its own state and the tracker is a maximum under a
+        # total order (value desc, configuration asc), so the lockstep result equals the reference's
+        # start-after-start loop (acquisition.py:186-205).
         if many:  # np.argsort(-values, kind="stable")[:n_starts] on the host (acquisition.py:188)
             v = pool_vals.cpu().numpy()
             order = [int(i) for i in np.argsort(-v, kind="stable")[:n_starts] if v[i] != -np.inf]
             starts = [(i, float(v[i])) for i in order]
         else:
             starts = [(st.index, st.value) for st in summ.top[:n_starts]]
-        cur_rows = torch.cat([rows[i:i + 1] for i, _ in starts]) if starts else rows[:0]
-        cur_v = [v for _, v in starts]
-        active = list(range(len(starts)))
-        n_slots = sc.n_slots
-        for _ in range(MAX_CLIMB_STEPS):
-            if not active:
-                break
-            nb, valid = sc.neighbors(cur_rows[active], use_cot=cot is not None)
-            vmask = valid.bool()
-            counts = vmask.view(len(active), n_slots).sum(1).cpu().numpy()
-            nb = nb[vmask]
-            if nb.shape[0] == 0:
-                break
-            v_all, s_val, s_cfg = _score_neighbours(sc, lay, nb, counts, f_model, ctx.eps_f)
-            if s_cfg is not None and (best_cfg is None or _better(s_val, s_cfg, best_val, best_cfg)):
-                best_val, best_cfg = s_val, s_cfg
-            nb_host = nb.cpu().numpy().view(np.uint32)
-            still, off = [], 0
-            for a, cnt in zip(active, counts):
-                cnt = int(cnt)
-                if cnt == 0:  # no neighbours: this start stops (acquisition.py:193-195)
-                    continue
-                v = v_all[off:off + cnt]
-                i = int(np.argmax(v))
-                ties = np.flatnonzero(v == v[i])
-                if len(ties) > 1:
-                    cfgs = lay.decode(nb_host[off + ties])
-                    j = min(range(len(ties)), key=lambda t: cfgs[t])
-                    i = int(ties[j])
-                if v[i] > cur_v[a]:  # acquisition.py:200
-                    cur_v[a] = float(v[i])
-                    cur_rows[a] = nb[off + i]
-                    still.append(a)
-                off += cnt
-            active = still
+        for c0 in range(0, len(starts), N.BX_MAX_K):
+            chunk = starts[c0:c0 + N.BX_MAX_K]
+            idx = torch.as_tensor([i for i, _ in chunk], device=rows.device, dtype=torch.long)
+            best, _ = sc.climb(rows.index_select(0, idx), [v for _, v in chunk], cot is not None, f_model,
+                               ctx.eps_f, best, MAX_CLIMB_STEPS)
+    best_cfg = lay.decode(best.row)[0] if best is not None else None
     if best_cfg is None:
         return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
     return best_cfg
-
-
-def _score_neighbours(sc, lay, nb, counts, f_model, eps_f):
-    """Score the neighbour lists of every climbing start at once: (values, best value, best config).
-
-    The reference scores each start's list with its own `_scores` call (acquisition.py:196), so a
-    list of exactly one configuration gets the forest's q == 1 summation order (numpy's pairwise
-    sum, feasibility.py:89) and every longer list the sequential one.  Single-neighbour lists are
-    therefore scored in a second call with the pairwise order; the running best is the maximum of
-    the two calls' trackers under (value desc, configuration asc)."""
-    single = counts[counts > 0] == 1
-    if not single.any() or single.all():
-        s2, vals, _ = sc.score(nb, f_model, eps_f, k=1, want_values=True, rf_pairwise=bool(single.all()))
-        cfg = lay.decode(s2.best.row)[0] if s2.best is not None else None
-        return vals.cpu().numpy(), (s2.best.value if s2.best is not None else -math.inf), cfg
-    row_single = np.repeat(counts[counts > 0] == 1, counts[counts > 0])
-    v_all = np.empty(nb.shape[0])
-    b_val, b_cfg = -math.inf, None
-    for idx, pairwise in ((np.flatnonzero(~row_single), False), (np.flatnonzero(row_single), True)):
-        s2, vals, _ = sc.score(nb[torch.as_tensor(idx, device=nb.device)], f_model, eps_f, k=1,
-                               want_values=True, rf_pairwise=pairwise)
-        v_all[idx] = vals.cpu().numpy()
-        if s2.best is not None:
-            cfg = lay.decode(s2.best.row)[0]
-            if b_cfg is None or _better(s2.best.value, cfg, b_val, b_cfg):
-                b_val, b_cfg = s2.best.value, cfg
-    return v_all, b_val, b_cfg
 
 
 def _enumerate_feasible(space, cot, Exhausted):

@@ -119,6 +119,8 @@ struct bx_handle {
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};
   PackSpec pack{};                  // packed wire format of the space (bx_set_space)
+  const uint8_t* pw_rows = nullptr;  // per-row forest summation order for the next score_impl (bx_climb)
+  DevBuf d_climb;                    // bx_climb scratch
   DevBuf d_packed;                  // streamed packed pool
   DevBuf d_panels, d_ei, d_grad_scratch, d_leaf_count, d_gen_rows;
   bool has_leaf_count = false;
@@ -471,6 +473,67 @@ cudaError_t launch_unpack(const PackSpec& spec, const uint32_t* packed, int64_t 
 }
 }  // namespace bx
 
+
+namespace bx {
+// bx_climb state on the device: per start the current row, value and an active flag; the tracker
+struct ClimbState {
+  int32_t n_active;
+  int32_t pad;
+  TopRec best;                       // index >= 0 once set
+  uint32_t best_row[BX_MAX_ROW_WORDS];
+};
+
+// per-row forest order: a start whose CoT-filtered list has exactly one neighbour is scored like
+// the reference's _scores on one configuration (q == 1: numpy's pairwise tree sum)
+__global__ void climb_flags_kernel(int A, int S, const int32_t* active, const uint8_t* valid, uint8_t* pw) {
+  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+    int cnt = 0;
+    for (int s = 0; s < S; ++s) cnt += valid[a * S + s] ? 1 : 0;
+    for (int s = 0; s < S; ++s) pw[a * S + s] = (active[a] && cnt == 1) ? 1 : 0;
+  }
+}
+
+// one step's bookkeeping (acquisition.py:193-201): per active start the argbest neighbour under
+// (value desc, configuration asc) (_argbest, :87-94), moved to iff strictly better; every scored
+// neighbour folded into the tracker (_Tracker.update, :105-111)
+__global__ void climb_update_kernel(SpaceDev sp, EvalSetDev ev, int A, int S, int32_t* active, uint32_t* cur,
+                                    double* curv, const uint32_t* nb, const uint8_t* valid, const double* vals,
+                                    ClimbState* st) {
+  if (threadIdx.x != 0) return;
+  const int W = sp.row_words;
+  int n_active = 0;
+  for (int a = 0; a < A; ++a) {
+    if (!active[a]) continue;
+    int bs = -1;
+    for (int s = 0; s < S; ++s) {
+      const int r = a * S + s;
+      if (!valid[r]) continue;
+      const double v = vals[r];
+      const uint32_t* row = nb + (size_t)r * W;
+      if (bs < 0 || v > vals[a * S + bs] ||
+          (v == vals[a * S + bs] && key_cmp(sp.params, sp.n_params, sp.rank_lut, row, nb + (size_t)(a * S + bs) * W) < 0))
+        bs = s;
+      if (v != -INFINITY && !(ev.count > 0 && is_evaluated(ev, row, W))) {
+        bool take = st->best.index < 0 || v > st->best.value;
+        if (!take && v == st->best.value) take = key_cmp(sp.params, sp.n_params, sp.rank_lut, row, st->best_row) < 0;
+        if (take) {
+          st->best = TopRec{v, 0.0, 0};
+          for (int w = 0; w < W; ++w) st->best_row[w] = row[w];
+        }
+      }
+    }
+    if (bs >= 0 && vals[a * S + bs] > curv[a]) {  // acquisition.py:200
+      curv[a] = vals[a * S + bs];
+      for (int w = 0; w < W; ++w) cur[(size_t)a * W + w] = nb[(size_t)(a * S + bs) * W + w];
+      ++n_active;
+    } else {
+      active[a] = 0;  // no neighbours, or no improvement: this start stops
+    }
+  }
+  st->n_active = n_active;
+}
+}  // namespace bx
+
 extern "C" {
 
 int bx_abi_version(void) { return BX_ABI_VERSION; }
@@ -531,6 +594,7 @@ void bx_destroy(bx_handle* h) {
   h->d_ready.release();
   h->d_emb.release();
   h->d_packed.release();
+  h->d_climb.release();
   h->d_emb_tab.release();
   h->d_emb_planes.release();
   h->d_emb_yy.release();
@@ -1427,7 +1491,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     // kernel runs before the posterior and the summary kernel after it.  The forest and posterior
     // kernels each fill every SM's shared memory, so they run back to back on the caller's stream
     // (which also makes the per-kernel CUDA-event timing exact).
-    const bool rf_summ = forest && !(flags & BX_SCORE_RF_PAIRWISE) && partials != nullptr &&
+    const bool rf_summ = forest && !(flags & BX_SCORE_RF_PAIRWISE) && !h->pw_rows && partials != nullptr &&
                          qs_summary_available(h->forest);
     h->rf_after_gp = rf_summ;
     // a stand-alone forest kernel before the posterior reads the rows: a streaming pool must be in
@@ -1435,7 +1499,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
     if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
     if (forest && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
-                           h->d_probs.as<double>(), s));
+                           h->d_probs.as<double>(), s, h->pw_rows));
     if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
     BX_CUDA(h, h->d_ei.ensure((size_t)q * 16));
     FusedArgs f = fused_args(h, rows, q, f_model);
@@ -1462,7 +1526,7 @@ static int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t ind
   if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
   if (forest) {
     BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
-                         h->d_probs.as<double>(), s));
+                         h->d_probs.as<double>(), s, h->pw_rows));
     a.probs_in = h->d_probs.as<double>();
   }
   if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[1], s));
@@ -1664,6 +1728,70 @@ int bx_rf_predict(bx_handle* h, const uint32_t* rows, int64_t q, int32_t flags, 
 }
 
 int bx_neighbor_slots(bx_handle* h) { return (h && h->has_space) ? h->n_slots : -1; }
+
+int bx_climb(bx_handle* h, const uint32_t* dev_start_rows, const double* host_start_values, int32_t n_starts,
+             int32_t use_cot, double f_model, double eps_f, int32_t max_steps, bx_cand* host_best,
+             int32_t* host_steps, void* stream) {
+  int r = check_gp(h);
+  if (r) return r;
+  if (n_starts < 0 || n_starts > BX_MAX_K || !host_best) return fail(h, BX_ERR_ARG, "bad climb arguments");
+  if (use_cot && !h->has_cot) return fail(h, BX_ERR_STATE, "bx_set_cot has not been called");
+  if (host_steps) *host_steps = 0;
+  if (n_starts == 0) return BX_OK;
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int A = n_starts, S = h->n_slots, W = h->row_words;
+  // scratch: cur rows, values, active flags, neighbour rows, valid, pairwise flags, values, state
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t o_cur = take((size_t)A * W * 4), o_curv = take((size_t)A * 8), o_act = take((size_t)A * 4),
+               o_nb = take((size_t)A * S * W * 4), o_val = take((size_t)A * S), o_pw = take((size_t)A * S),
+               o_vals = take((size_t)A * S * 8), o_probs = take((size_t)A * S * 8), o_st = take(sizeof(ClimbState));
+  BX_CUDA(h, h->d_climb.ensure(off));
+  unsigned char* base = h->d_climb.as<unsigned char>();
+  uint32_t* cur = reinterpret_cast<uint32_t*>(base + o_cur);
+  double* curv = reinterpret_cast<double*>(base + o_curv);
+  int32_t* act = reinterpret_cast<int32_t*>(base + o_act);
+  uint32_t* nb = reinterpret_cast<uint32_t*>(base + o_nb);
+  uint8_t* valid = base + o_val;
+  uint8_t* pw = base + o_pw;
+  double* vals = reinterpret_cast<double*>(base + o_vals);
+  double* probs = reinterpret_cast<double*>(base + o_probs);
+  ClimbState* st = reinterpret_cast<ClimbState*>(base + o_st);
+  ClimbState hs{};
+  hs.n_active = A;
+  hs.best = TopRec{host_best->value, host_best->prob, host_best->index};
+  std::memcpy(hs.best_row, host_best->row, sizeof(hs.best_row));
+  std::vector<int32_t> ones(A, 1);
+  BX_CUDA(h, cudaMemcpyAsync(cur, dev_start_rows, (size_t)A * W * 4, cudaMemcpyDeviceToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(curv, host_start_values, (size_t)A * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(act, ones.data(), (size_t)A * 4, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(st, &hs, sizeof(ClimbState), cudaMemcpyHostToDevice, s));
+  int steps = 0;
+  for (int step = 0; step < max_steps && hs.n_active > 0; ++step) {
+    BX_CUDA(h, launch_neighbors(space_dev(h), use_cot ? &h->cot : nullptr, cur, A, nb, valid, s));
+    climb_flags_kernel<<<1, 32, 0, s>>>(A, S, act, valid, pw);
+    BX_CUDA(h, cudaGetLastError());
+    h->pw_rows = pw;
+    int np = 0;
+    r = score_impl(h, nb, (int64_t)A * S, 0, f_model, eps_f, 0, 0, vals, probs, nullptr, &np, s, 0);
+    h->pw_rows = nullptr;
+    if (r) return r;
+    climb_update_kernel<<<1, 32, 0, s>>>(space_dev(h), eval_dev(h), A, S, act, cur, curv, nb, valid, vals, st);
+    BX_CUDA(h, cudaGetLastError());
+    BX_CUDA(h, cudaMemcpyAsync(&hs.n_active, &st->n_active, 4, cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));  // the one device -> host read per step
+    ++steps;
+  }
+  BX_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(ClimbState), cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  host_best->value = hs.best.value;
+  host_best->prob = hs.best.prob;
+  host_best->index = hs.best.index;
+  std::memcpy(host_best->row, hs.best_row, sizeof(hs.best_row));
+  if (host_steps) *host_steps = steps;
+  return BX_OK;
+}
 
 int bx_neighbors(bx_handle* h, const uint32_t* rows, int32_t count, int32_t use_cot,
                  uint32_t* out_rows, uint8_t* out_valid, void* stream) {

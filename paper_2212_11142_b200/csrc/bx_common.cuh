@@ -588,8 +588,9 @@ size_t qs_summary_smem_bytes(const QsForestDev& q);
 bool qs_summary_available(const ForestDev& f);
 cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const SummaryArgs& a, int sm_count,
                               cudaStream_t s, int* n_partials);
+// pw_rows (device, q flags, nullable): per-row numpy summation order (1: the q == 1 pairwise sum)
 cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
-                      int pairwise, double* probs, cudaStream_t s);
+                      int pairwise, double* probs, cudaStream_t s, const uint8_t* pw_rows = nullptr);
 cudaError_t launch_neighbors(const SpaceDev& space, const CotDev* cot, const uint32_t* rows,
                              int count, uint32_t* out_rows, uint8_t* out_valid, cudaStream_t s);
 cudaError_t launch_cot_contains(const SpaceDev& space, const CotDev& cot, const uint32_t* rows,

@@ -72,7 +72,7 @@ __device__ double pairwise(const F& v, int t0, int cnt) {
 }
 
 __global__ void __launch_bounds__(256) rf_kernel(SpaceDev sp, ForestDev f, const uint32_t* rows,
-                                                 int64_t q, int use_pairwise, double* probs) {
+                                                 int64_t q, int use_pairwise, double* probs, const uint8_t* pw_rows) {
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
   for (int i = threadIdx.x; i < sp.n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(sp.params)[i];
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) rf_kernel(SpaceDev sp, ForestDev f, const
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t* row = rows + (size_t)i * sp.row_words;
     double sum;
-    if (use_pairwise) {
+    if (pw_rows ? pw_rows[i] != 0 : use_pairwise != 0) {
       sum = pairwise([&](int t) { return leaf_value(sp, params, f, row, t); }, 0, f.n_trees);
     } else {
       sum = leaf_value(sp, params, f, row, 0);
@@ -132,7 +132,8 @@ __device__ __forceinline__ double walk1(const CodedView& v, int root, int max_de
 template <bool SMEM, bool REAL>
 __global__ void __launch_bounds__(kRfThreads, 1) rf_coded_kernel(SpaceDev sp, CodedForestDev cf,
                                                                  const uint32_t* rows, int64_t q,
-                                                                 int use_pairwise, double* probs) {
+                                                                 int use_pairwise, double* probs,
+                                                                 const uint8_t* pw_rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
   size_t off = 0;
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kRfThreads, 1) rf_coded_kernel(SpaceDev sp, Co
       code[c * kRfThreads + threadIdx.x] = val;
     }
     double sum;
-    if (use_pairwise) {
+    if (pw_rows ? pw_rows[i] != 0 : use_pairwise != 0) {
       sum = pairwise([&](int t) { return walk1<REAL>(v, s_roots[t], cf.max_depth); }, 0, cf.n_trees);
     } else {
       // two trees in lockstep (independent load chains); leaves added strictly in tree order
@@ -332,7 +333,8 @@ __device__ __forceinline__ void qs_ind_and(const QsForestDev& f, const uint32_t 
 
 // Stand-alone probabilities (predict_proba_batch) in either numpy summation order.
 __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForestDev f, const uint32_t* rows,
-                                                           int64_t q, int use_pairwise, double* probs) {
+                                                           int64_t q, int use_pairwise, double* probs,
+                                                           const uint8_t* pw_rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ bx_param_desc params[BX_MAX_PARAMS];
   const QsSmem L = qs_smem_layout(f, true);
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
     uint32_t irow[4];
     qs_ind_rows(f, params, row, iidx_s, irow);
     double sum = 0.0;
-    if (use_pairwise) {
+    if (pw_rows ? pw_rows[i] != 0 : use_pairwise != 0) {
       sum = pairwise(
           [=](int t) {
             uint64_t m = ~0ull;
@@ -585,7 +587,7 @@ cudaError_t launch_rf_summary(const SpaceDev& space, const ForestDev& f, const S
 }
 
 cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t* rows, int64_t q,
-                      int use_pairwise, double* probs, cudaStream_t s) {
+                      int use_pairwise, double* probs, cudaStream_t s, const uint8_t* pw_rows) {
   if (q <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -600,7 +602,7 @@ cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t*
     int64_t blocks = (q + kQsThreads - 1) / kQsThreads;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
-    rf_qs_kernel<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, rows, q, use_pairwise, probs);
+    rf_qs_kernel<<<(int)blocks, kQsThreads, bytes, s>>>(space, f.qs, rows, q, use_pairwise, probs, pw_rows);
     return cudaGetLastError();
   }
   if (f.coded) {
@@ -611,12 +613,12 @@ cudaError_t launch_rf(const SpaceDev& space, const ForestDev& f, const uint32_t*
     if (e != cudaSuccess) return e;
     int64_t blocks = (q + kRfThreads - 1) / kRfThreads;
     if (blocks > sms) blocks = sms;
-    kern<<<(int)blocks, kRfThreads, bytes, s>>>(space, f.cf, rows, q, use_pairwise, probs);
+    kern<<<(int)blocks, kRfThreads, bytes, s>>>(space, f.cf, rows, q, use_pairwise, probs, pw_rows);
     return cudaGetLastError();
   }
   int64_t blocks = (q + 255) / 256;
   if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-  rf_kernel<<<(int)blocks, 256, 0, s>>>(space, f, rows, q, use_pairwise, probs);
+  rf_kernel<<<(int)blocks, 256, 0, s>>>(space, f, rows, q, use_pairwise, probs, pw_rows);
   return cudaGetLastError();
 }
 

@@ -139,11 +139,10 @@ def _one_neighbour_space(bt):
 
 
 def test_single_neighbour_lists_use_the_q1_forest_order():
-    """The lockstep climb scores a start whose CoT-filtered neighbour list has length one with the
-    forest's q == 1 (pairwise) summation order, as the reference's per-start _scores call does
-    (feasibility.py:89); longer lists keep the sequential order."""
-    import torch
-
+    """bx_climb scores a start whose CoT-filtered neighbour list has length one with the forest's
+    q == 1 (pairwise) summation order, as the reference's per-start _scores call does
+    (feasibility.py:89); longer lists keep the sequential order.  The proposal equals the
+    reference's optimize_acquisition for every evaluated set / RNG seed tried."""
     from golden_io import Ctx
     from paper_2212_11142_b200 import acquisition as A
     from paper_2212_11142_b200.device import scorer
@@ -156,33 +155,39 @@ def test_single_neighbour_lists_use_the_q1_forest_order():
     gp = bt.gp_fit(sp, cfgs, y, rng)
     feas = bt.rf_fit(sp, cfgs + [(2, 2), (3, 3)], [True] * len(cfgs) + [False, False], rng)
     sc = scorer()
-    ctx = Ctx(gp, feas, min(y), 0.0)
-    A._prepare(ctx, sc, evaluated=False)
+    A._prepare(Ctx(gp, feas, min(y), 0.0), sc, evaluated=False)
     sc.set_cot(cot)
-    lay = sc.layout
-    starts = [(1, 1), (1, 3), (4, 1)]
-    nb, valid = sc.neighbors(sc.to_device(lay.encode(starts)), use_cot=True)
-    vmask = valid.bool()
-    counts = vmask.view(len(starts), sc.n_slots).sum(1).cpu().numpy()
+    nb, valid = sc.neighbors(sc.to_device(sc.layout.encode([(1, 1), (1, 3), (4, 1)])), use_cot=True)
+    counts = valid.bool().view(3, sc.n_slots).sum(1).cpu().numpy()
     assert list(counts) == [1, 3, 0]
-    nb = nb[vmask]
-    f_model = gp.objective_to_model(min(y))
-    v_all, _, _ = A._score_neighbours(sc, lay, nb, counts, f_model, 0.0)
-    # per-start reference-order scoring, one bx_score call per start
-    off = 0
-    for cnt in counts:
-        if cnt:
-            _, v, _ = sc.score(nb[off:off + cnt], f_model, 0.0, k=0, want_values=True, summary=False)
-            assert np.array_equal(v.cpu().numpy(), v_all[off:off + cnt])
-            off += cnt
-    # and the whole proposal equals the reference's
-    evaluated = set(cfgs[:2])
-    want = bt.optimize_acquisition(
-        bt.AcquisitionContext(gp=gp, feas=feas, best_feasible_value=min(y), eps_f=0.0,
-                              rng=np.random.default_rng(4), evaluated=evaluated), sp, cot)
-    got = A.optimize_acquisition(Ctx(gp, feas, min(y), 0.0, np.random.default_rng(4), evaluated), sp, cot)
-    assert got == want
-    torch.cuda.synchronize()
+    for n_ev, seed in ((0, 4), (1, 5), (2, 4), (3, 6), (5, 7)):
+        evaluated = set(cfgs[:n_ev])
+        want = bt.optimize_acquisition(
+            bt.AcquisitionContext(gp=gp, feas=feas, best_feasible_value=min(y), eps_f=0.0,
+                                  rng=np.random.default_rng(seed), evaluated=evaluated), sp, cot)
+        got = A.optimize_acquisition(Ctx(gp, feas, min(y), 0.0, np.random.default_rng(seed), evaluated), sp, cot)
+        assert got == want, (n_ev, seed)
+
+
+def test_device_climb_matches_reference_climb_with_many_starts():
+    """n_starts above the fused top-k (BX_MAX_K = 32): the starts come from a host stable argsort
+    of the pool values and climb in chunks of 32 on the device; the proposal equals the
+    reference's."""
+    from golden_io import Ctx, load, ref_model, to_cfg
+    from paper_2212_11142_b200 import acquisition as A
+    bt = ref()
+    meta, arr, space = load("mixed_fit")
+    gp, feas = ref_model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"][:800]]
+    evaluated = {to_cfg(space, c) for c in meta["evaluated"]}
+    for n_starts in (1, 10, 40):
+        want = bt.optimize_acquisition(
+            bt.AcquisitionContext(gp=gp, feas=feas, best_feasible_value=meta["f_best"], eps_f=meta["eps_f"],
+                                  rng=np.random.default_rng(0), evaluated=evaluated), space, None,
+            sample_fn=lambda n, r: cands, n_starts=n_starts)
+        got = A.optimize_acquisition(Ctx(gp, feas, meta["f_best"], meta["eps_f"], np.random.default_rng(0), evaluated),
+                                     space, None, sample_fn=lambda n, r: cands, n_starts=n_starts)
+        assert got == want, n_starts
 
 
 def test_reference_model_objects_reach_the_gpu():
