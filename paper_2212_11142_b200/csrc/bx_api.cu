@@ -623,6 +623,15 @@ int bx_gp_kernel(bx_handle* h) {
 
 int bx_gp_distance_ksteps(bx_handle* h) { return h && h->use_tc ? h->tc_ks : 0; }
 
+int bx_set_option(bx_handle* h, int32_t option, int32_t value) {
+  if (!h) return BX_ERR_ARG;
+  if (option == BX_OPT_LML_NARROW) {
+    h->lml_narrow = value != 0;
+    return BX_OK;
+  }
+  return fail(h, BX_ERR_ARG, "unknown option %d", option);
+}
+
 int bx_packed_row_words(bx_handle* h) { return h && h->has_space ? h->pack.pw : 0; }
 
 int bx_pack_rows(bx_handle* h, const uint32_t* rows, int64_t q, uint32_t* packed) {

@@ -11,6 +11,7 @@ Patch targets are where the reference binds the names it calls.
 from __future__ import annotations
 
 from . import acquisition as gpu
+from . import hyperfit
 
 TARGETS = (
     ("engine", "optimize_acquisition", gpu.optimize_acquisition),
@@ -24,19 +25,25 @@ LML_TARGETS = (
     ("surrogate", "_batched_coarse_lml", gpu.batched_coarse_lml),
     ("surrogate", "_lml_core", gpu.lml_core),
 )
+# the whole hyperparameter fit with its L-BFGS-B restarts batched on the GPU (hyperfit.py); the
+# engine binds gp_fit at import (engine.py:21)
+FIT_TARGETS = (
+    ("engine", "gp_fit", hyperfit.gp_fit),
+)
 METHODS = (
     ("surrogate", "GPModel", "predict_batch", gpu.predict_batch),
     ("feasibility", "FeasibilityModel", "predict_proba_batch", gpu.predict_proba_batch),
 )
 
 
-def install(boxtune, whole_path: bool = True, lml: bool = False):
+def install(boxtune, whole_path: bool = True, lml: bool = False, fit: bool = False):
     """Replace the reference's hot-path functions; returns a callable that undoes it.
     With whole_path=False the engine keeps the reference optimize_acquisition (which then calls
     the GPU _scores / neighbors): the per-call parity mode.  lml=True also moves the
-    hyperparameter-fit objectives (_batched_coarse_lml, _lml_core) to the GPU."""
+    hyperparameter-fit objectives (_batched_coarse_lml, _lml_core) to the GPU; fit=True replaces
+    the engine's gp_fit with the batched-restart one (hyperfit.gp_fit)."""
     saved = []
-    for mod_name, attr, fn in TARGETS + (LML_TARGETS if lml else ()):
+    for mod_name, attr, fn in TARGETS + (LML_TARGETS if lml else ()) + (FIT_TARGETS if fit else ()):
         if not whole_path and attr == "optimize_acquisition":
             continue
         mod = getattr(boxtune, mod_name)
