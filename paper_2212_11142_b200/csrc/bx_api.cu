@@ -495,42 +495,91 @@ __global__ void climb_flags_kernel(int A, int S, const int32_t* active, const ui
 
 // one step's bookkeeping (acquisition.py:193-201): per active start the argbest neighbour under
 // (value desc, configuration asc) (_argbest, :87-94), moved to iff strictly better; every scored
-// neighbour folded into the tracker (_Tracker.update, :105-111)
+// neighbour folded into the tracker (_Tracker.update, :105-111).  Warp a = start a: its lanes scan
+// the slots, then a shuffle reduction under the same total orders; thread 0 folds the starts'
+// tracker candidates.
+__device__ __forceinline__ bool climb_better(const SpaceDev& sp, const uint32_t* nb, int W, double v1, int r1, double v2,
+                                             int r2) {
+  if (r1 < 0) return false;
+  if (r2 < 0) return true;
+  if (v1 != v2) return v1 > v2;
+  return key_cmp(sp.params, sp.n_params, sp.rank_lut, nb + (size_t)r1 * W, nb + (size_t)r2 * W) < 0;
+}
+
 __global__ void climb_update_kernel(SpaceDev sp, EvalSetDev ev, int A, int S, int32_t* active, uint32_t* cur,
                                     double* curv, const uint32_t* nb, const uint8_t* valid, const double* vals,
                                     ClimbState* st) {
-  if (threadIdx.x != 0) return;
+  __shared__ int s_trk[BX_MAX_K];
+  __shared__ int s_moved[BX_MAX_K];
   const int W = sp.row_words;
-  int n_active = 0;
-  for (int a = 0; a < A; ++a) {
-    if (!active[a]) continue;
-    int bs = -1;
-    for (int s = 0; s < S; ++s) {
-      const int r = a * S + s;
-      if (!valid[r]) continue;
-      const double v = vals[r];
-      const uint32_t* row = nb + (size_t)r * W;
-      if (bs < 0 || v > vals[a * S + bs] ||
-          (v == vals[a * S + bs] && key_cmp(sp.params, sp.n_params, sp.rank_lut, row, nb + (size_t)(a * S + bs) * W) < 0))
-        bs = s;
-      if (v != -INFINITY && !(ev.count > 0 && is_evaluated(ev, row, W))) {
-        bool take = st->best.index < 0 || v > st->best.value;
-        if (!take && v == st->best.value) take = key_cmp(sp.params, sp.n_params, sp.rank_lut, row, st->best_row) < 0;
-        if (take) {
-          st->best = TopRec{v, 0.0, 0};
-          for (int w = 0; w < W; ++w) st->best_row[w] = row[w];
+  const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a < A) {
+    int br = -1, tr = -1;  // argbest row and tracker-candidate row of this lane
+    double bv = -INFINITY, tv = -INFINITY;
+    if (active[a])
+      for (int s2 = lane; s2 < S; s2 += 32) {
+        const int r = a * S + s2;
+        if (!valid[r]) continue;
+        const double v = vals[r];
+        if (climb_better(sp, nb, W, v, r, bv, br)) {
+          bv = v;
+          br = r;
+        }
+        if (v != -INFINITY && !(ev.count > 0 && is_evaluated(ev, nb + (size_t)r * W, W)) &&
+            climb_better(sp, nb, W, v, r, tv, tr)) {
+          tv = v;
+          tr = r;
         }
       }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o), otv = __shfl_xor_sync(0xffffffffu, tv, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, br, o), otr = __shfl_xor_sync(0xffffffffu, tr, o);
+      if (climb_better(sp, nb, W, ov, orow, bv, br)) {
+        bv = ov;
+        br = orow;
+      }
+      if (climb_better(sp, nb, W, otv, otr, tv, tr)) {
+        tv = otv;
+        tr = otr;
+      }
     }
-    if (bs >= 0 && vals[a * S + bs] > curv[a]) {  // acquisition.py:200
-      curv[a] = vals[a * S + bs];
-      for (int w = 0; w < W; ++w) cur[(size_t)a * W + w] = nb[(size_t)(a * S + bs) * W + w];
-      ++n_active;
-    } else {
-      active[a] = 0;  // no neighbours, or no improvement: this start stops
+    if (lane == 0) {
+      s_trk[a] = tr;
+      int moved = 0;
+      if (active[a]) {
+        if (br >= 0 && bv > curv[a]) {  // acquisition.py:200
+          curv[a] = bv;
+          moved = 1;
+        } else {
+          active[a] = 0;  // no neighbours, or no improvement: this start stops
+        }
+      }
+      s_moved[a] = moved ? br : -1;
     }
+    __syncwarp();
+    const int mr = __shfl_sync(0xffffffffu, lane == 0 ? s_moved[a] : 0, 0);
+    if (mr >= 0)
+      for (int w = lane; w < W; w += 32) cur[(size_t)a * W + w] = nb[(size_t)mr * W + w];
   }
-  st->n_active = n_active;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n_active = 0;
+    for (int i = 0; i < A; ++i) {
+      n_active += s_moved[i] >= 0 ? 1 : 0;
+      const int r = s_trk[i];
+      if (r < 0) continue;
+      const double v = vals[r];
+      const uint32_t* row = nb + (size_t)r * W;
+      bool take = st->best.index < 0 || v > st->best.value;
+      if (!take && v == st->best.value) take = key_cmp(sp.params, sp.n_params, sp.rank_lut, row, st->best_row) < 0;
+      if (take) {
+        st->best = TopRec{v, 0.0, 0};
+        for (int w = 0; w < W; ++w) st->best_row[w] = row[w];
+      }
+    }
+    st->n_active = n_active;
+  }
 }
 }  // namespace bx
 
@@ -1786,7 +1835,7 @@ int bx_climb(bx_handle* h, const uint32_t* dev_start_rows, const double* host_st
     r = score_impl(h, nb, (int64_t)A * S, 0, f_model, eps_f, 0, 0, vals, probs, nullptr, &np, s, 0);
     h->pw_rows = nullptr;
     if (r) return r;
-    climb_update_kernel<<<1, 32, 0, s>>>(space_dev(h), eval_dev(h), A, S, act, cur, curv, nb, valid, vals, st);
+    climb_update_kernel<<<1, 32 * A, 0, s>>>(space_dev(h), eval_dev(h), A, S, act, cur, curv, nb, valid, vals, st);
     BX_CUDA(h, cudaGetLastError());
     BX_CUDA(h, cudaMemcpyAsync(&hs.n_active, &st->n_active, 4, cudaMemcpyDeviceToHost, s));
     BX_CUDA(h, cudaStreamSynchronize(s));  // the one device -> host read per step

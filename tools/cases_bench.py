@@ -36,7 +36,7 @@ def main(q=1 << 20):
         for p in space.parameters:
             kinds[p.kind] = kinds.get(p.kind, 0) + 1
         print(f"{case:14s} n={len(gp.configs):4d} d={len(space.parameters):2d} {kinds} forest={feas is not None} "
-              f"kernel={sc.gp_kernel():7s} {ms:7.3f} ms  {q / ms * 1e3:,.0f} cand/s")
+              f"kernel={sc.gp_kernel():7s} ks={sc.distance_ksteps()} {ms:7.3f} ms  {q / ms * 1e3:,.0f} cand/s")
         sc.close()
 
 
