@@ -234,7 +234,8 @@ int bx_unpack_rows(bx_handle* h, const uint32_t* host_packed, int64_t q, uint32_
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the
    dense space (sample_uniform's distribution, space.py:312-332), mode 1 = leaf-uniform over the
-   chain of trees (sample_leaf_uniform's, constraints.py:471-523; needs bx_set_cot leaf counts). */
+   chain of trees (sample_leaf_uniform's, constraints.py:471-523; needs bx_set_cot leaf counts). mode 2 = path-biased over the chain of trees
+   (sample_path_biased's, constraints.py:478-501, 522-523: a uniform child at every level). */
 int bx_generate(bx_handle* h, uint64_t seed, int64_t index_base, int64_t q, int32_t mode,
                 uint32_t* dev_rows, void* stream);
 
@@ -252,16 +253,16 @@ int bx_gp_predict(bx_handle* h, const uint32_t* dev_rows, int64_t q, double* dev
 int bx_rf_predict(bx_handle* h, const uint32_t* dev_rows, int64_t q, int32_t flags,
                   double* dev_probs, void* stream);
 
-/* The hill climb of optimize_acquisition (acquisition.py:186-202) on the device.  n_starts start
-   rows (device, <= BX_MAX_K) with their values (host); per step the neighbours of every start still
+/* The hill climb of optimize_acquisition (acquisition.py:186-202) on the device.  n_starts starts
+   (<= BX_MAX_K): rows host_start_index[i] of the device pool, with their values (host); per step the neighbours of every start still
    climbing (CoT-filtered when use_cot, space.py:289-309), scored like _scores (a start with exactly
    one neighbour gets the forest's q == 1 summation order, feasibility.py:89), each start moved to
    its argbest under (value desc, configuration asc) iff strictly better (:87-94, :200), every
    scored neighbour folded into the best-unevaluated tracker (:105-111).  host_best is the tracker
    in / out (index < 0: empty; value, row).  One 4-byte device -> host read per step. */
-int bx_climb(bx_handle* h, const uint32_t* dev_start_rows, const double* host_start_values, int32_t n_starts,
-             int32_t use_cot, double f_model, double eps_f, int32_t max_steps, bx_cand* host_best,
-             int32_t* host_steps, void* stream);
+int bx_climb(bx_handle* h, const uint32_t* dev_pool_rows, const int64_t* host_start_index,
+             const double* host_start_values, int32_t n_starts, int32_t use_cot, double f_model, double eps_f,
+             int32_t max_steps, bx_cand* host_best, int32_t* host_steps, void* stream);
 
 /* All single-parameter moves of `count` rows.  Slot s of row r goes to
    dev_out_rows[(r * n_slots + s) * row_words]; dev_out_valid[r * n_slots + s] is 1 when the

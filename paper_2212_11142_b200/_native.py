@@ -93,7 +93,7 @@ _SIGS = {
     "bx_rf_predict": (C.c_int, [_p, _p, _i64, _i32, _p, _p]),
     "bx_neighbor_slots": (C.c_int, [_p]),
     "bx_neighbors": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p]),
-    "bx_climb": (C.c_int, [_p, _p, _p, _i32, _i32, _f64, _f64, _i32, _p, _p, _p]),
+    "bx_climb": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _f64, _f64, _i32, _p, _p, _p]),
     "bx_cot_contains": (C.c_int, [_p, _p, _i64, _p, _p]),
     "bx_constraints_eval": (C.c_int, [_p, _p, _i64, _p, _p]),
     "bx_lml_batched": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _p, _p]),

@@ -235,8 +235,7 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
             starts = [(st.index, st.value) for st in summ.top[:n_starts]]
         for c0 in range(0, len(starts), N.BX_MAX_K):
             chunk = starts[c0:c0 + N.BX_MAX_K]
-            idx = torch.as_tensor([i for i, _ in chunk], device=rows.device, dtype=torch.long)
-            best, _ = sc.climb(rows.index_select(0, idx), [v for _, v in chunk], cot is not None, f_model,
+            best, _ = sc.climb(rows, [i for i, _ in chunk], [v for _, v in chunk], cot is not None, f_model,
                                ctx.eps_f, best, MAX_CLIMB_STEPS)
     best_cfg = lay.decode(best.row)[0] if best is not None else None
     if best_cfg is None:

@@ -1787,9 +1787,9 @@ int bx_rf_predict(bx_handle* h, const uint32_t* rows, int64_t q, int32_t flags, 
 
 int bx_neighbor_slots(bx_handle* h) { return (h && h->has_space) ? h->n_slots : -1; }
 
-int bx_climb(bx_handle* h, const uint32_t* dev_start_rows, const double* host_start_values, int32_t n_starts,
-             int32_t use_cot, double f_model, double eps_f, int32_t max_steps, bx_cand* host_best,
-             int32_t* host_steps, void* stream) {
+int bx_climb(bx_handle* h, const uint32_t* dev_pool_rows, const int64_t* host_start_index,
+             const double* host_start_values, int32_t n_starts, int32_t use_cot, double f_model, double eps_f,
+             int32_t max_steps, bx_cand* host_best, int32_t* host_steps, void* stream) {
   int r = check_gp(h);
   if (r) return r;
   if (n_starts < 0 || n_starts > BX_MAX_K || !host_best) return fail(h, BX_ERR_ARG, "bad climb arguments");
@@ -1821,7 +1821,9 @@ int bx_climb(bx_handle* h, const uint32_t* dev_start_rows, const double* host_st
   hs.best = TopRec{host_best->value, host_best->prob, host_best->index};
   std::memcpy(hs.best_row, host_best->row, sizeof(hs.best_row));
   std::vector<int32_t> ones(A, 1);
-  BX_CUDA(h, cudaMemcpyAsync(cur, dev_start_rows, (size_t)A * W * 4, cudaMemcpyDeviceToDevice, s));
+  for (int a = 0; a < A; ++a)  // the start rows, gathered from the pool
+    BX_CUDA(h, cudaMemcpyAsync(cur + (size_t)a * W, dev_pool_rows + (size_t)host_start_index[a] * W, (size_t)W * 4,
+                               cudaMemcpyDeviceToDevice, s));
   BX_CUDA(h, cudaMemcpyAsync(curv, host_start_values, (size_t)A * 8, cudaMemcpyHostToDevice, s));
   BX_CUDA(h, cudaMemcpyAsync(act, ones.data(), (size_t)A * 4, cudaMemcpyHostToDevice, s));
   BX_CUDA(h, cudaMemcpyAsync(st, &hs, sizeof(ClimbState), cudaMemcpyHostToDevice, s));
@@ -1917,9 +1919,10 @@ int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const d
 static int check_generate(bx_handle* h, int32_t mode) {
   int r = check_space(h);
   if (r) return r;
-  if (mode != 0 && mode != 1) return fail(h, BX_ERR_ARG, "generation mode %d not in {0, 1}", mode);
+  if (mode < 0 || mode > 2) return fail(h, BX_ERR_ARG, "generation mode %d not in {0, 1, 2}", mode);
   if (mode == 1 && !(h->has_cot && h->has_leaf_count))
     return fail(h, BX_ERR_STATE, "mode 1 needs bx_set_cot with node leaf counts");
+  if (mode == 2 && !h->has_cot) return fail(h, BX_ERR_STATE, "mode 2 needs bx_set_cot");
   return BX_OK;
 }
 

@@ -417,6 +417,13 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
   qs_load_tables(f, smem, L);
   Partial* summ = &parts[warp];
   if (lane == 0) partial_init(summ);
+  // per-slot constants in shared memory (broadcast loads instead of a global load per candidate)
+  __shared__ int32_t s_soff[64], s_cpar[64], s_csub[64];
+  for (int c = tid; c < f.n_codes && c < 64; c += blockDim.x) {
+    s_soff[c] = f.soff[c];
+    s_cpar[c] = f.code_param[c];
+    s_csub[c] = f.code_sub[c];
+  }
   __syncthreads();
   const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(smem + L.mask);
   const uint32_t uval_s = (uint32_t)__cvta_generic_to_shared(smem + L.uval);
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
       if constexpr (NC > 0) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-          colr[c] = mask_s + 8u * (uint32_t)((f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
+          colr[c] = mask_s + 8u * (uint32_t)((s_soff[c] + qs_code(params[s_cpar[c]], row, s_csub[c], f.rthr)) * f.tpad);
       } else {
         for (int c = 0; c < f.n_codes; ++c)
           sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);

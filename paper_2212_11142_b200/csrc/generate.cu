@@ -8,6 +8,9 @@
 //           ChainOfTrees.sample_leaf_uniform (constraints.py:471-523), realised by a weighted
 //           descent on per-node leaf counts (uniform over leaves without materialising them);
 //           real and permutation singleton groups are drawn as in mode 0.
+//   mode 2  path-biased over the chain of trees: the distribution of sample_path_biased
+//           (constraints.py:478-501, 522-523; engine.py:216-217 with cot_sampling == "path"): every
+//           level picks one of the node's children uniformly.
 // Parity with the reference here is statistical (the reference draws from numpy's PCG64 stream);
 // membership is exact.
 #include "bx_common.cuh"
@@ -114,14 +117,17 @@ __global__ void generate_kernel(SpaceDev sp, CotDev cot, const int64_t* leaf_cou
       }
       int node = cot.group_root[g];
       for (int li = pb; li < pe; ++li) {
-        // child chosen with probability leaf_count(child) / leaf_count(node)
         const int first = cot.child_begin[node], cnt = cot.child_count[node];
-        const double r = u.next() * (double)leaf_count[node];
-        double acc = 0.0;
         int pick = first + cnt - 1;
-        for (int c = first; c < first + cnt; ++c) {
-          acc += (double)leaf_count[c];
-          if (r < acc) { pick = c; break; }
+        if (mode == 2) {  // path-biased: a uniform child at every level
+          pick = first + min(cnt - 1, (int)(u.next() * (double)cnt));
+        } else {  // leaf-uniform: child with probability leaf_count(child) / leaf_count(node)
+          const double r = u.next() * (double)leaf_count[node];
+          double acc = 0.0;
+          for (int c = first; c < first + cnt; ++c) {
+            acc += (double)leaf_count[c];
+            if (r < acc) { pick = c; break; }
+          }
         }
         row[params[cot.group_params[li]].word] = (uint32_t)cot.node_value[pick];
         node = pick;

@@ -310,11 +310,12 @@ class Scorer:
                                            _ptr(valid), self.stream))
         return out, valid
 
-    def climb(self, start_rows: torch.Tensor, start_values, use_cot: bool, f_model: float, eps_f: float,
-              best: Candidate | None, max_steps: int = 50):
-        """bx_climb: the hill climb from the start rows on the device.  Returns (best, steps): the
-        best-unevaluated tracker folded over every scored neighbour (None if still empty)."""
-        n = start_rows.shape[0]
+    def climb(self, pool_rows: torch.Tensor, start_index, start_values, use_cot: bool, f_model: float,
+              eps_f: float, best: Candidate | None, max_steps: int = 50):
+        """bx_climb: the hill climb from pool rows start_index on the device.  Returns (best, steps):
+        the best-unevaluated tracker folded over every scored neighbour (None if still empty)."""
+        idx = np.ascontiguousarray(start_index, dtype=np.int64)
+        n = len(idx)
         vals = np.ascontiguousarray(start_values, dtype=np.float64)
         c = N.Cand()
         if best is None:
@@ -323,7 +324,7 @@ class Scorer:
             c.value, c.prob, c.index = best.value, best.prob, max(best.index, 0)
             np.ctypeslib.as_array(c.row)[:len(best.row)] = best.row
         steps = C.c_int32(0)
-        self._check(self._lib.bx_climb(self.h, _ptr(start_rows.contiguous()), _ptr(vals), n, int(bool(use_cot)),
+        self._check(self._lib.bx_climb(self.h, _ptr(pool_rows), _ptr(idx), _ptr(vals), n, int(bool(use_cot)),
                                        float(f_model), float(eps_f), int(max_steps), C.byref(c), C.byref(steps),
                                        self.stream))
         return _cand(c, self.layout.row_words), int(steps.value)

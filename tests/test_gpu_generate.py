@@ -64,6 +64,45 @@ def test_leaf_uniform_over_chain_of_trees():
     sc.close()
 
 
+def test_path_biased_over_chain_of_trees():
+    """mode 2 = sample_path_biased (constraints.py:478-501): a uniform child at every level, so a
+    leaf's probability is the product of 1 / (children) along its path; the reference's own
+    sampler (same tree) gives the same distribution."""
+    sp = SearchSpace([Parameter.ordinal("a", [1, 2, 4, 8]), Parameter.ordinal("b", [1, 2, 4, 8]),
+                      Parameter.categorical("c", ["u", "v"])], ["a >= b", "c == 'u' || a > 2"])
+    cot = build_cot(sp)
+    (g,) = [g for g in cot.groups if g.kind == "tree"]
+    probs = {}
+
+    def walk(node, acc, pr):
+        if not node.children:
+            probs[tuple(acc)] = pr
+            return
+        for ch in node.children:
+            walk(ch, acc + [ch.value], pr / len(node.children))
+    walk(g.root, [], 1.0)
+    leaves = sorted(probs)
+    sc = Scorer()
+    lay = sc.set_space(sp)
+    sc.set_cot(cot)
+    q = 400_000
+    rows = sc.generate(q, seed=9, mode=2)
+    assert bool(sc.cot_contains(rows).all())
+    cfgs = lay.decode(rows_np(rows))
+    pos = {leaf: i for i, leaf in enumerate(leaves)}
+    counts = np.zeros(len(leaves))
+    for c in cfgs:
+        counts[pos[tuple(c[i] for i in g.indices)]] += 1
+    expected = np.array([probs[leaf] for leaf in leaves]) * q
+    assert chi2_ok(counts, expected)
+    ref_draw = cot.sample_path_biased(20_000, np.random.default_rng(3))
+    rc = np.zeros(len(leaves))
+    for c in ref_draw:
+        rc[pos[tuple(c[i] for i in g.indices)]] += 1
+    assert chi2_ok(rc, np.array([probs[leaf] for leaf in leaves]) * 20_000)
+    sc.close()
+
+
 def test_generation_is_counter_based():
     meta, arr, space = load("C3")
     sc = Scorer()
