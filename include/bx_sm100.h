@@ -124,8 +124,8 @@ int bx_device_sm_count(bx_handle* h);
    BX_GP_GENERIC (shared-memory FP64 kernel for n + 1 > 256). */
 enum { BX_GP_GENERIC = 0, BX_GP_DMMA = 1, BX_GP_TENSOR = 2 };
 /* Handle options.  BX_OPT_LML_NARROW = 1: bx_lml_core / bx_lml_batched run one CTA per setting
-   for any batch size, so each setting's value and gradient do not depend on the batch it came in
-   (the batched L-BFGS-B restarts of paper_2212_11142_b200.hyperfit rely on it). */
+   instead of the whole-GPU kernels (A/B measurements).  Either way a setting's value and gradient
+   do not depend on the batch it came in. */
 enum bx_option { BX_OPT_LML_NARROW = 1 };
 int bx_set_option(bx_handle* h, int32_t option, int32_t value);
 int bx_gp_kernel(bx_handle* h);

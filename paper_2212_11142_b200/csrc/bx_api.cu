@@ -2015,14 +2015,19 @@ int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const doub
     return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
   if (want_grad && !grad) return fail(h, BX_ERR_ARG, "want_grad needs a gradient buffer");
   cudaSetDevice(h->device);
-  // a few settings (the L-BFGS-B objective passes one): each spread over the whole GPU; many
-  // settings: one CTA per setting
-  if (c <= 4 && lml_wide_supported(n) && !h->lml_narrow) {
-    BX_CUDA(h, h->d_grad_scratch.ensure(lml_wide_scratch_doubles(n, D) * sizeof(double)));
-    for (int i = 0; i < c; ++i)
-      BX_CUDA(h, launch_lml_wide(sq, n, D, z, params + (size_t)i * (2 + D), prior_shape, prior_rate, use_prior,
-                                 want_grad, value + i, want_grad ? grad + (size_t)i * (2 + D) : nullptr, ok + i,
+  // the whole-GPU pipeline, settings side by side on grid.y (a setting's arithmetic does not depend
+  // on the batch: the batched L-BFGS-B restarts get the values a single call gives), in groups that
+  // keep the scratch under 1 GiB; BX_OPT_LML_NARROW: one CTA per setting
+  if (lml_wide_supported(n) && !h->lml_narrow) {
+    const size_t per = lml_wide_scratch_doubles(n, D, 1) * sizeof(double);
+    const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(c, 1), (1ull << 30) / per));
+    BX_CUDA(h, h->d_grad_scratch.ensure(lml_wide_scratch_doubles(n, D, group) * sizeof(double)));
+    for (int c0 = 0; c0 < c; c0 += group) {
+      const int g = std::min(group, c - c0);
+      BX_CUDA(h, launch_lml_wide(sq, n, D, z, params + (size_t)c0 * (2 + D), g, prior_shape, prior_rate, use_prior,
+                                 want_grad, value + c0, want_grad ? grad + (size_t)c0 * (2 + D) : nullptr, ok + c0,
                                  h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
+    }
     return BX_OK;
   }
   BX_CUDA(h, h->d_grad_scratch.ensure(lml_grad_scratch_doubles(n, c) * sizeof(double)));

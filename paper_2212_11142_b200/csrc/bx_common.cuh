@@ -611,13 +611,13 @@ cudaError_t launch_lml_grad(const double* sq, int n, int D, const double* z, con
                             double* out_value, double* out_grad, int* out_ok, double* scratch,
                             cudaStream_t s);
 size_t lml_grad_scratch_doubles(int n, int c);
-// _lml_core for one setting over the whole GPU (lml_wide.cu), n <= 512
-size_t lml_wide_scratch_doubles(int n, int D);
+// _lml_core for c settings, each over the whole GPU, side by side on grid.y (lml_wide.cu), n <= 512
+size_t lml_wide_scratch_doubles(int n, int D, int c);
 bool lml_wide_supported(int n);
 size_t lml_coarse_wide_scratch_doubles(int n, int c);
 cudaError_t launch_lml_coarse_wide(const double* sq, int n, int D, const double* z, const double* thetas, int c,
                                    double* out, double* scratch, cudaStream_t s);
-cudaError_t launch_lml_wide(const double* sq, int n, int D, const double* z, const double* prm, double prior_k,
+cudaError_t launch_lml_wide(const double* sq, int n, int D, const double* z, const double* prm, int c, double prior_k,
                             double prior_rate, int use_prior, int want_grad, double* out_value, double* out_grad,
                             int* out_ok, double* scratch, cudaStream_t s);
 cudaError_t launch_pairwise_sq(const SpaceDev& space, const uint32_t* a, int qa, const uint32_t* b,

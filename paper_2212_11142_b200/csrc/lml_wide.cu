@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(256) lw_chol_kernel(double* A0, int np, int J,
 
 // X = L^-1 (lower; X is zeroed beforehand): one warp per column, the column kept in shared memory
 constexpr int kInvW = 8;
-__global__ void __launch_bounds__(kInvW * 32) lw_inverse_kernel(const double* L, int np, double* X) {
+__global__ void __launch_bounds__(kInvW * 32) lw_inverse_kernel(const double* L0, int np, double* X0) {
   __shared__ double xs[kInvW][512 + 32];
+  const double* L = L0 + (size_t)blockIdx.y * np * np;  // setting blockIdx.y
+  double* X = X0 + (size_t)blockIdx.y * np * np;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * kInvW + warp;
   if (j >= np) return;
@@ -165,11 +167,20 @@ __device__ __forceinline__ double block_sum_lw(double v, double* red) {
   return s;
 }
 
-__global__ void __launch_bounds__(512) lw_value_kernel(const double* L, const double* X, int n, int np, int D,
-                                                       const double* z, const double* prm, double prior_k,
-                                                       double prior_rate, int use_prior, const int* fail,
-                                                       double* u, double* al, double* out_value, int* out_ok) {
+__global__ void __launch_bounds__(512) lw_value_kernel(const double* L0, const double* X0, int n, int np, int D,
+                                                       const double* z, const double* prm0, double prior_k,
+                                                       double prior_rate, int use_prior, const int* fail0,
+                                                       double* u0, double* al0, double* out_value0, int* out_ok0) {
   __shared__ double red[16];
+  const int y = blockIdx.y;  // setting
+  const double* L = L0 + (size_t)y * np * np;
+  const double* X = X0 + (size_t)y * np * np;
+  const double* prm = prm0 + (size_t)y * (2 + D);
+  const int* fail = fail0 + y;
+  double* u = u0 + (size_t)y * np;
+  double* al = al0 + (size_t)y * np;
+  double* out_value = out_value0 + y;
+  int* out_ok = out_ok0 + y;
   const int tid = threadIdx.x;
   for (int i = tid; i < n; i += blockDim.x) {  // u = L^-1 z
     double s = 0.0;
@@ -207,10 +218,16 @@ __global__ void __launch_bounds__(512) lw_value_kernel(const double* L, const do
 }
 
 // tile (a, b), a >= b, of K^-1 = X^T X fused with the gradient sums over its elements
-__global__ void __launch_bounds__(256) lw_grad_kernel(const double* X, const double* K, const double* sq,
-                                                      const double* al, const double* prm, int n, int np, int D,
-                                                      double* partial) {
+__global__ void __launch_bounds__(256) lw_grad_kernel(const double* X0, const double* K0, const double* sq,
+                                                      const double* al0, const double* prm0, int n, int np, int D,
+                                                      double* partial0) {
   __shared__ double Xa[kT][kT + 1], Xb[kT][kT + 1];
+  const int y = blockIdx.y;  // setting
+  const double* X = X0 + (size_t)y * np * np;
+  const double* K = K0 + (size_t)y * np * np;
+  const double* al = al0 + (size_t)y * np;
+  const double* prm = prm0 + (size_t)y * (2 + D);
+  double* partial = partial0 + (size_t)y * gridDim.x * (2 + D);
   __shared__ double il2[BX_MAX_PARAMS];
   __shared__ double red[8];
   int t = blockIdx.x, a = 0;
@@ -263,9 +280,13 @@ __global__ void __launch_bounds__(256) lw_grad_kernel(const double* X, const dou
   }
 }
 
-__global__ void lw_final_kernel(const double* partial, int tiles, const double* prm, int D, double prior_k,
-                                double prior_rate, int use_prior, const int* fail, double* grad) {
-  const int k = threadIdx.x;
+__global__ void lw_final_kernel(const double* partial0, int tiles, const double* prm0, int D, double prior_k,
+                                double prior_rate, int use_prior, const int* fail0, double* grad0) {
+  const int k = threadIdx.x, y = blockIdx.x;  // setting
+  const double* partial = partial0 + (size_t)y * tiles * (2 + D);
+  const double* prm = prm0 + (size_t)y * (2 + D);
+  const int* fail = fail0 + y;
+  double* grad = grad0 + (size_t)y * (2 + D);
   if (k >= 2 + D) return;
   if (*fail) {
     grad[k] = 0.0;
@@ -354,39 +375,40 @@ cudaError_t launch_lml_coarse_wide(const double* sq, int n, int D, const double*
   return cudaGetLastError();
 }
 
-size_t lml_wide_scratch_doubles(int n, int D) {
+size_t lml_wide_scratch_doubles(int n, int D, int c) {
   const int np = (n + kT - 1) / kT * kT, nb = np / kT;
-  return 3 * (size_t)np * np + 2 * (size_t)np + (size_t)nb * (nb + 1) / 2 * (2 + D) + 1;
+  return (size_t)c * (3 * (size_t)np * np + 2 * (size_t)np + (size_t)nb * (nb + 1) / 2 * (2 + D)) + (size_t)c + 1;
 }
 
 bool lml_wide_supported(int n) { return n <= 512; }
 
-// one hyperparameter setting (prm = sigma, noise, l_1..l_D in natural units)
-cudaError_t launch_lml_wide(const double* sq, int n, int D, const double* z, const double* prm, double prior_k,
+// c hyperparameter settings (prm = c rows of sigma, noise, l_1..l_D in natural units), each spread
+// over the GPU and all of them side by side on grid.y: a setting's arithmetic does not depend on c
+cudaError_t launch_lml_wide(const double* sq, int n, int D, const double* z, const double* prm, int c, double prior_k,
                             double prior_rate, int use_prior, int want_grad, double* out_value, double* out_grad,
                             int* out_ok, double* scratch, cudaStream_t s) {
-  if (n > 512) return cudaErrorInvalidValue;
+  if (n > 512 || c < 1) return cudaErrorInvalidValue;
   const int np = (n + kT - 1) / kT * kT, nb = np / kT, tiles = nb * (nb + 1) / 2;
   double* K = scratch;
-  double* L = K + (size_t)np * np;
-  double* X = L + (size_t)np * np;
-  double* u = X + (size_t)np * np;
-  double* al = u + np;
-  double* partial = al + np;
-  int* fail = reinterpret_cast<int*>(partial + (size_t)tiles * (2 + D));
-  cudaError_t e = cudaMemsetAsync(fail, 0, sizeof(int), s);
+  double* L = K + (size_t)c * np * np;
+  double* X = L + (size_t)c * np * np;
+  double* u = X + (size_t)c * np * np;
+  double* al = u + (size_t)c * np;
+  double* partial = al + (size_t)c * np;
+  int* fail = reinterpret_cast<int*>(partial + (size_t)c * tiles * (2 + D));
+  cudaError_t e = cudaMemsetAsync(fail, 0, sizeof(int) * c, s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(X, 0, (size_t)np * np * sizeof(double), s);
+  e = cudaMemsetAsync(X, 0, (size_t)c * np * np * sizeof(double), s);
   if (e != cudaSuccess) return e;
   const int g = (int)std::min<size_t>(((size_t)np * np + 255) / 256, 148 * 8);
-  lw_gram_kernel<<<g, 256, 0, s>>>(sq, n, np, D, prm, 0, K, L);
-  for (int J = 0; J < nb; ++J) lw_chol_kernel<<<nb - J, 256, 0, s>>>(L, np, J, fail);
-  lw_inverse_kernel<<<(np + kInvW - 1) / kInvW, kInvW * 32, 0, s>>>(L, np, X);
-  lw_value_kernel<<<1, 512, 0, s>>>(L, X, n, np, D, z, prm, prior_k, prior_rate, use_prior, fail, u, al,
-                                     out_value, out_ok);
+  lw_gram_kernel<<<dim3(g, c), 256, 0, s>>>(sq, n, np, D, prm, 0, K, L);
+  for (int J = 0; J < nb; ++J) lw_chol_kernel<<<dim3(nb - J, c), 256, 0, s>>>(L, np, J, fail);
+  lw_inverse_kernel<<<dim3((np + kInvW - 1) / kInvW, c), kInvW * 32, 0, s>>>(L, np, X);
+  lw_value_kernel<<<dim3(1, c), 512, 0, s>>>(L, X, n, np, D, z, prm, prior_k, prior_rate, use_prior, fail, u, al,
+                                             out_value, out_ok);
   if (want_grad) {
-    lw_grad_kernel<<<tiles, 256, 0, s>>>(X, K, sq, al, prm, n, np, D, partial);
-    lw_final_kernel<<<1, 64, 0, s>>>(partial, tiles, prm, D, prior_k, prior_rate, use_prior, fail, out_grad);
+    lw_grad_kernel<<<dim3(tiles, c), 256, 0, s>>>(X, K, sq, al, prm, n, np, D, partial);
+    lw_final_kernel<<<c, 64, 0, s>>>(partial, tiles, prm, D, prior_k, prior_rate, use_prior, fail, out_grad);
   }
   return cudaGetLastError();
 }

@@ -5,10 +5,10 @@ The reference refines the N_TOP = 8 best coarse hyperparameter settings one afte
 scipy L-BFGS-B iteration calling `_lml_core` for ONE setting (~200 calls per fit).  Here the
 restarts run concurrently - one scipy optimizer per thread - and their objective requests are
 gathered: whenever every still-running optimizer is waiting for a value, one `bx_lml_core` call
-evaluates all of their settings at once (one CTA per setting, BX_OPT_LML_NARROW, so a setting's
-value and gradient never depend on the batch it came in).  An optimizer's iterates depend only on
-its own objective values, so the result is the same as running the restarts one after another with
-the same objective, whatever the thread timing.
+evaluates all of their settings at once (the whole-GPU pipeline with the settings side by side on
+grid.y, so a setting's value and gradient are the ones a single call gives).  An optimizer's
+iterates depend only on its own objective values, so the result equals running the restarts one
+after another with the GPU `_lml_core` (`install(lml=True)`), whatever the thread timing.
 
 Everything else is the reference's own code, looked up in the caller's package: the coarse stage
 (`_search_boxes`, the RNG draw, `_batched_coarse_lml` - the GPU one when installed - and
@@ -26,7 +26,6 @@ import threading
 import numpy as np
 import torch
 
-from . import _native as N
 from .device import scorer
 
 _DEFAULT = object()
@@ -129,7 +128,6 @@ def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_tra
                 value, grad, ok = value.cpu().numpy(), grad.cpu().numpy(), ok.cpu().numpy()
             return [(np.inf, np.zeros(batch.shape[1])) if not k else (-v, -g) for v, g, k in zip(value, grad, ok)]
 
-        sc._check(sc._lib.bx_set_option(sc.h, N.BX_OPT_LML_NARROW, 1))
         batcher = _Batcher(len(starts), evaluate)
         bounds = list(zip(lo, hi))
 
@@ -144,13 +142,10 @@ def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_tra
                 batcher.done()
 
         threads = [threading.Thread(target=run, args=(t, idx), daemon=True) for t, idx in enumerate(starts)]
-        try:
-            for t in threads:
-                t.start()
-            for t in threads:
-                t.join()
-        finally:
-            sc._check(sc._lib.bx_set_option(sc.h, N.BX_OPT_LML_NARROW, 0))
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
         for r in refined.values():
             if isinstance(r, BaseException):
                 raise r

@@ -242,6 +242,13 @@ def test_batched_gp_fit_matches_reference_fit(case):
     np.testing.assert_allclose([hg.outputscale, hg.noise_variance, *hg.lengthscales],
                                [hw.outputscale, hw.noise_variance, *hw.lengthscales], rtol=1e-6)
     assert abs(got.map_value - want.map_value) <= 1e-9 * max(1.0, abs(want.map_value))
+    # batching changes nothing: the reference's sequential fit with the GPU objective installed
+    # (lml=True) reaches bit-identical hyperparameters
+    seq = _patched(bt, lambda: bt.gp_fit(space, train, y, np.random.default_rng(9)), lml=True)
+    got2 = _patched(bt, lambda: hyperfit.gp_fit(space, train, y, np.random.default_rng(9)), lml=True)
+    hs, h2 = seq.hyperparameters, got2.hyperparameters
+    assert (hs.outputscale, hs.noise_variance, hs.lengthscales) == (h2.outputscale, h2.noise_variance, h2.lengthscales)
+    assert seq.map_value == got2.map_value
 
 
 def test_patched_run_with_batched_gp_fit():

@@ -329,3 +329,26 @@ def test_lml_wide_paths_large_n(n, monkeypatch):
     assert v1 == pytest.approx(v, rel=1e-10, abs=1e-8)
     np.testing.assert_allclose(g1, g, rtol=1e-8, atol=1e-8 * np.abs(g).max())
     np.testing.assert_allclose(out1[fin], out[fin], rtol=1e-10, atol=1e-8)
+
+
+def test_lml_core_batched_equals_single_calls():
+    """bx_lml_core over c settings (side by side on grid.y) gives, bit for bit, the value, gradient
+    and ok flag of c single-setting calls: what the batched L-BFGS-B restarts rely on."""
+    import torch
+
+    from paper_2212_11142_b200.device import scorer
+    meta, arr, space = load("M200")
+    og, _ = oracle_model(meta, arr, space)
+    sq = oracle.pairwise_sq(space, og.configs, og.configs, og.use_transforms)
+    sc = scorer()
+    dev = f"cuda:{sc.device}"
+    sq_d = torch.as_tensor(sq, device=dev)
+    z = torch.as_tensor(arr["lml_z"], device=dev)
+    th = arr["lml_thetas"][:9]
+    prm = torch.as_tensor(np.exp(th), device=dev)
+    v, g, ok = sc.lml_core(sq_d, z, prm, True, None)
+    for i in range(len(th)):
+        v1, g1, ok1 = sc.lml_core(sq_d, z, prm[i:i + 1], True, None)
+        assert int(ok1.item()) == int(ok[i].item())
+        if int(ok1.item()):
+            assert v1.item() == v[i].item() and torch.equal(g1[0], g[i])
