@@ -1,0 +1,72 @@
+// bx_lml.cu — the hyperparameter-fit objectives behind the C ABI: the batched coarse LML
+// (_batched_coarse_lml), _lml_core with its gradient for c settings, and the bit-exact pairwise
+// squared distances (pairwise_sq_distances) they take.
+#include "bx_handle.cuh"
+
+extern "C" {
+int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const double* z,
+                   const double* thetas, int32_t c, double* out, void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
+    return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
+  cudaSetDevice(h->device);
+  if (lml_wide_supported(n) && !h->lml_narrow) {
+    // blocked Cholesky batched over the settings, in groups that keep the factors under 1 GiB
+    const int np = (n + 31) / 32 * 32;
+    const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)c, (1ull << 30) / ((size_t)np * np * 8)));
+    BX_CUDA(h, h->d_lml_scratch.ensure(lml_coarse_wide_scratch_doubles(n, group) * sizeof(double)));
+    for (int c0 = 0; c0 < c; c0 += group)
+      BX_CUDA(h, launch_lml_coarse_wide(sq, n, D, z, thetas + (size_t)c0 * (2 + D), std::min(group, c - c0),
+                                        out + c0, h->d_lml_scratch.as<double>(), (cudaStream_t)stream));
+    return BX_OK;
+  }
+  const size_t bytes = ((size_t)n * (n + 1) / 2 + n) * sizeof(double);
+  double* scratch = nullptr;
+  if (bytes > 200 * 1024) {
+    BX_CUDA(h, h->d_lml_scratch.ensure(lml_scratch_doubles(n, c) * sizeof(double)));
+    scratch = h->d_lml_scratch.as<double>();
+  }
+  BX_CUDA(h, launch_lml(sq, n, D, z, thetas, c, out, scratch, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const double* z,
+                const double* params, int32_t c, double prior_shape, double prior_rate,
+                int32_t use_prior, int32_t want_grad, double* value, double* grad, int32_t* ok,
+                void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
+    return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
+  if (want_grad && !grad) return fail(h, BX_ERR_ARG, "want_grad needs a gradient buffer");
+  cudaSetDevice(h->device);
+  // the whole-GPU pipeline, settings side by side on grid.y (a setting's arithmetic does not depend
+  // on the batch: the batched L-BFGS-B restarts get the values a single call gives), in groups that
+  // keep the scratch under 1 GiB; BX_OPT_LML_NARROW: one CTA per setting
+  if (lml_wide_supported(n) && !h->lml_narrow) {
+    const size_t per = lml_wide_scratch_doubles(n, D, 1) * sizeof(double);
+    const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(c, 1), (1ull << 30) / per));
+    BX_CUDA(h, h->d_grad_scratch.ensure(lml_wide_scratch_doubles(n, D, group) * sizeof(double)));
+    for (int c0 = 0; c0 < c; c0 += group) {
+      const int g = std::min(group, c - c0);
+      BX_CUDA(h, launch_lml_wide(sq, n, D, z, params + (size_t)c0 * (2 + D), g, prior_shape, prior_rate, use_prior,
+                                 want_grad, value + c0, want_grad ? grad + (size_t)c0 * (2 + D) : nullptr, ok + c0,
+                                 h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
+    }
+    return BX_OK;
+  }
+  BX_CUDA(h, h->d_grad_scratch.ensure(lml_grad_scratch_doubles(n, c) * sizeof(double)));
+  BX_CUDA(h, launch_lml_grad(sq, n, D, z, params, c, prior_shape, prior_rate, use_prior, want_grad,
+                             value, grad, ok, h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
+  return BX_OK;
+}
+
+int bx_pairwise_sq(bx_handle* h, const uint32_t* a, int32_t qa, const uint32_t* b, int32_t qb,
+                   double* out, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  cudaSetDevice(h->device);
+  BX_CUDA(h, launch_pairwise_sq(space_dev(h), a, qa, b, qb, out, (cudaStream_t)stream));
+  return BX_OK;
+}
+
+}  // extern "C"
