@@ -150,6 +150,18 @@ int bx_set_gp(bx_handle* h, const uint32_t* host_train_rows, int32_t n, const do
               const double* host_alpha, double outputscale, const double* host_lengthscales,
               double y_mean, double y_std, void* stream);
 
+/* rf_fit's tree building (feasibility.py:95-197) on the device, bit-exact: host_X / host_y = the
+   canonically sorted encode_configs matrix [n][F] and labels; per tree its bootstrap rows [n] and
+   the feature subsets its generator drew in order [max_draws][k] (host_n_drawn of them); outputs
+   [n_trees][max_nodes] in the tree's own preorder ids (-1 = none), the node counts and a status per
+   tree (0 ok, 1 needs more feature subsets: draw more from the same generator and call again,
+   2 max_nodes exceeded). */
+int bx_rf_fit(bx_handle* h, const double* host_X, const double* host_y, int32_t n, int32_t F, int32_t n_trees,
+              const int32_t* host_boot, const int32_t* host_feats, const int32_t* host_n_drawn, int32_t max_draws,
+              int32_t k, int32_t max_depth, int32_t max_nodes, int32_t* host_feature, double* host_threshold,
+              int32_t* host_left, int32_t* host_right, double* host_value, int32_t* host_n_nodes,
+              int32_t* host_status, void* stream);
+
 /* Random forest in the reference's flat layout (feasibility.py:54-71).  `constant` is the
    single-class shortcut value, or NaN when the forest has trees. */
 int bx_set_forest(bx_handle* h, const int32_t* host_feature, const double* host_threshold,

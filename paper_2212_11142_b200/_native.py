@@ -28,7 +28,7 @@ EXPORTED = (
     "bx_create", "bx_destroy", "bx_last_error", "bx_abi_version", "bx_device_sm_count",
     "bx_set_space", "bx_set_gp", "bx_set_forest", "bx_clear_forest", "bx_set_evaluated",
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
-    "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_climb", "bx_cot_contains",
+    "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_climb", "bx_rf_fit", "bx_cot_contains",
     "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64", "bx_probe_int8",
     "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps", "bx_set_option", "bx_packed_row_words", "bx_pack_rows", "bx_unpack_rows",
 )
@@ -94,6 +94,8 @@ _SIGS = {
     "bx_neighbor_slots": (C.c_int, [_p]),
     "bx_neighbors": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p]),
     "bx_climb": (C.c_int, [_p, _p, _p, _p, _i32, _i32, _f64, _f64, _i32, _p, _p, _p]),
+    "bx_rf_fit": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p, _i32, _i32, _i32, _i32,
+                            _p, _p, _p, _p, _p, _p, _p, _p]),
     "bx_cot_contains": (C.c_int, [_p, _p, _i64, _p, _p]),
     "bx_constraints_eval": (C.c_int, [_p, _p, _i64, _p, _p]),
     "bx_lml_batched": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _p, _p]),

@@ -77,6 +77,7 @@ void bx_destroy(bx_handle* h) {
   h->d_emb.release();
   h->d_packed.release();
   h->d_climb.release();
+  h->d_fit.release();
   h->d_emb_tab.release();
   h->d_emb_planes.release();
   h->d_emb_yy.release();

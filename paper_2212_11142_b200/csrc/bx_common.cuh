@@ -626,5 +626,12 @@ cudaError_t launch_gp_planes(const SpaceDev& space, const uint32_t* train_rows, 
                              const double* inv_l, uint64_t* planes, uint64_t* kmask,
                              cudaStream_t s);
 cudaError_t launch_tri_inverse(const double* L, int n, double* A, int lda, cudaStream_t s);
+// rf_fit tree building (forest_fit.cu): one CTA per tree, outputs [T][max_nodes] in local preorder ids
+size_t rf_fit_smem_bytes(int n);
+size_t rf_fit_stack_bytes(int T, int max_nodes);
+cudaError_t launch_rf_fit(const double* X, const double* y, int n, int F, int T, const int32_t* boot,
+                          const int32_t* feats, const int32_t* n_drawn, int max_draws, int k, int max_depth,
+                          int max_nodes, int32_t* feature, double* threshold, int32_t* left, int32_t* right,
+                          double* value, int32_t* n_nodes, int32_t* status, void* stack, cudaStream_t s);
 
 }  // namespace bx

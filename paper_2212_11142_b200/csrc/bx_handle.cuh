@@ -124,6 +124,7 @@ struct bx_handle {
   PackSpec pack{};                  // packed wire format of the space (bx_set_space)
   const uint8_t* pw_rows = nullptr;  // per-row forest summation order for the next score_impl (bx_climb)
   DevBuf d_climb;                    // bx_climb scratch
+  DevBuf d_fit;                      // bx_rf_fit buffers
   DevBuf d_packed;                  // streamed packed pool
   DevBuf d_panels, d_ei, d_grad_scratch, d_leaf_count, d_gen_rows;
   bool has_leaf_count = false;

@@ -336,6 +336,49 @@ int bx_clear_forest(bx_handle* h) {
   return BX_OK;
 }
 
+int bx_rf_fit(bx_handle* h, const double* X, const double* y, int32_t n, int32_t F, int32_t n_trees,
+              const int32_t* boot, const int32_t* feats, const int32_t* n_drawn, int32_t max_draws, int32_t k,
+              int32_t max_depth, int32_t max_nodes, int32_t* feature, double* threshold, int32_t* left,
+              int32_t* right, double* value, int32_t* n_nodes, int32_t* status, void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (n < 1 || F < 1 || n_trees < 1 || k < 1 || k > F || max_draws < 1 || max_nodes < 1)
+    return fail(h, BX_ERR_ARG, "bad rf_fit shape n=%d F=%d T=%d k=%d", n, F, n_trees, k);
+  if (rf_fit_smem_bytes(n) > 200 * 1024) return fail(h, BX_ERR_UNSUPPORTED, "rf_fit: %d rows exceed the tile", n);
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nt = (size_t)n_trees * max_nodes;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t oX = take((size_t)n * F * 8), oy = take((size_t)n * 8), ob = take((size_t)n_trees * n * 4),
+               of = take((size_t)n_trees * max_draws * k * 4), od = take((size_t)n_trees * 4),
+               oF = take(nt * 4), oT = take(nt * 8), oL = take(nt * 4), oR = take(nt * 4), oV = take(nt * 8),
+               oN = take((size_t)n_trees * 4), oS = take((size_t)n_trees * 4),
+               oK = take(rf_fit_stack_bytes(n_trees, max_nodes));
+  BX_CUDA(h, h->d_fit.ensure(off));
+  unsigned char* b = h->d_fit.as<unsigned char>();
+  BX_CUDA(h, cudaMemcpyAsync(b + oX, X, (size_t)n * F * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(b + oy, y, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(b + ob, boot, (size_t)n_trees * n * 4, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(b + of, feats, (size_t)n_trees * max_draws * k * 4, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(b + od, n_drawn, (size_t)n_trees * 4, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, launch_rf_fit(reinterpret_cast<double*>(b + oX), reinterpret_cast<double*>(b + oy), n, F, n_trees,
+                           reinterpret_cast<int32_t*>(b + ob), reinterpret_cast<int32_t*>(b + of),
+                           reinterpret_cast<int32_t*>(b + od), max_draws, k, max_depth, max_nodes,
+                           reinterpret_cast<int32_t*>(b + oF), reinterpret_cast<double*>(b + oT),
+                           reinterpret_cast<int32_t*>(b + oL), reinterpret_cast<int32_t*>(b + oR),
+                           reinterpret_cast<double*>(b + oV), reinterpret_cast<int32_t*>(b + oN),
+                           reinterpret_cast<int32_t*>(b + oS), b + oK, s));
+  BX_CUDA(h, cudaMemcpyAsync(feature, b + oF, nt * 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(threshold, b + oT, nt * 8, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(left, b + oL, nt * 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(right, b + oR, nt * 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(value, b + oV, nt * 8, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(n_nodes, b + oN, (size_t)n_trees * 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(status, b + oS, (size_t)n_trees * 4, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  return BX_OK;
+}
+
 }  // extern "C"
 
 static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,

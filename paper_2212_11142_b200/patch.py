@@ -11,7 +11,7 @@ Patch targets are where the reference binds the names it calls.
 from __future__ import annotations
 
 from . import acquisition as gpu
-from . import hyperfit
+from . import forest_fit, hyperfit
 
 TARGETS = (
     ("engine", "optimize_acquisition", gpu.optimize_acquisition),
@@ -25,6 +25,11 @@ LML_TARGETS = (
     ("surrogate", "_batched_coarse_lml", gpu.batched_coarse_lml),
     ("surrogate", "_lml_core", gpu.lml_core),
 )
+# the feasibility forest's tree building on the GPU (forest_fit.py; bit-exact, so on by default);
+# the engine binds rf_fit at import (engine.py:19)
+RF_TARGETS = (
+    ("engine", "rf_fit", forest_fit.rf_fit),
+)
 # the whole hyperparameter fit with its L-BFGS-B restarts batched on the GPU (hyperfit.py); the
 # engine binds gp_fit at import (engine.py:21)
 FIT_TARGETS = (
@@ -36,14 +41,16 @@ METHODS = (
 )
 
 
-def install(boxtune, whole_path: bool = True, lml: bool = False, fit: bool = False):
+def install(boxtune, whole_path: bool = True, lml: bool = False, fit: bool = False, rf: bool = True):
     """Replace the reference's hot-path functions; returns a callable that undoes it.
     With whole_path=False the engine keeps the reference optimize_acquisition (which then calls
     the GPU _scores / neighbors): the per-call parity mode.  lml=True also moves the
     hyperparameter-fit objectives (_batched_coarse_lml, _lml_core) to the GPU; fit=True replaces
-    the engine's gp_fit with the batched-restart one (hyperfit.gp_fit)."""
+    the engine's gp_fit with the batched-restart one (hyperfit.gp_fit); rf=True (default) builds
+    the feasibility forest on the GPU (forest_fit.rf_fit, bit-exact)."""
     saved = []
-    for mod_name, attr, fn in TARGETS + (LML_TARGETS if lml else ()) + (FIT_TARGETS if fit else ()):
+    targets = TARGETS + (LML_TARGETS if lml else ()) + (FIT_TARGETS if fit else ()) + (RF_TARGETS if rf else ())
+    for mod_name, attr, fn in targets:
         if not whole_path and attr == "optimize_acquisition":
             continue
         mod = getattr(boxtune, mod_name)

@@ -261,3 +261,31 @@ def test_patched_run_with_batched_gp_fit():
         got = _patched(bt, lambda: _run(bt, bench, budget, seed), whole_path=True, lml=True, fit=True)
         assert _first_divergence(got.history, want.history) is None, (name, _first_divergence(got.history,
                                                                                               want.history))
+
+
+@pytest.mark.parametrize("case", ["C3", "C4", "M200", "mixed_fit", "mixed_metrics"])
+@pytest.mark.parametrize("draws", [48, 3])
+def test_device_rf_fit_equals_reference(case, draws, monkeypatch):
+    """forest_fit.rf_fit (trees built on the GPU, feature subsets drawn from numpy in the
+    reference's order) returns the reference's FeasibilityModel arrays bit for bit; draws=3 forces
+    the "draw more and build again" path for every tree."""
+    import time
+
+    from golden_io import load, to_cfg
+    from paper_2212_11142_b200 import forest_fit
+    monkeypatch.setattr(forest_fit, "DRAWS", draws)
+    bt = ref()
+    meta, arr, space = load(case)
+    ev = [to_cfg(space, c) for c in meta["evaluated"]]
+    labels = meta["labels"]
+    t0 = time.perf_counter()
+    want = bt.rf_fit(space, ev, labels, np.random.default_rng(31), use_transforms=meta["use_transforms"])
+    t1 = time.perf_counter()
+    got = forest_fit.rf_fit(space, ev, labels, np.random.default_rng(31), use_transforms=meta["use_transforms"])
+    t2 = time.perf_counter()
+    print(f"{case}: {len(ev)} records, {len(want.feature)} nodes; reference rf_fit {t1 - t0:.3f} s, device {t2 - t1:.3f} s")
+    assert np.array_equal(got.bootstrap_seeds, want.bootstrap_seeds)
+    assert got.constant == want.constant
+    for name in ("feature", "threshold", "left", "right", "value", "roots"):
+        a, b = getattr(got, name), getattr(want, name)
+        assert a.dtype == b.dtype and np.array_equal(a, b), name
