@@ -64,7 +64,8 @@ void bx_destroy(bx_handle* h) {
                     &h->d_cnodes, &h->d_leaf_val,
                     &h->d_real_thr, &h->d_code_param, &h->d_code_sub, &h->d_leaf_idx,
                     &h->d_qmask, &h->d_qvid, &h->d_quval, &h->d_qsoff, &h->d_qcode_param,
-                    &h->d_qcode_sub, &h->d_qrthr, &h->d_qiidx, &h->d_qimask};
+                    &h->d_qcode_sub, &h->d_qrthr, &h->d_qiidx, &h->d_qimask,
+                    &h->d_qcode_param2, &h->d_qcode_sub2, &h->d_qcode_mul};
   for (DevBuf* b : bufs) b->release();
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->ev_copy) cudaEventDestroy(h->ev_copy);

@@ -121,6 +121,11 @@ struct QsForestDev {
   const int32_t* soff;       // [n_codes] offset of slot s inside a tree's stride
   const int32_t* code_param; // [n_codes] (the coded forest's slots)
   const int32_t* code_sub;
+  // a paired slot: code = code(code_param, code_sub) * code_mul + code(code_param2, code_sub2);
+  // code_param2 < 0 for a single slot (code_mul 1)
+  const int32_t* code_param2;
+  const int32_t* code_sub2;
+  const int32_t* code_mul;
   int32_t n_trees, n_codes, stride, n_uvals;
   int32_t tpad;              // row length: n_trees rounded up to 8, plus 1 (odd: bank spread)
   int32_t enabled;

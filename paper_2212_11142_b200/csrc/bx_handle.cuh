@@ -67,7 +67,8 @@ struct bx_handle {
   bool has_forest = false;
   ForestDev forest{};
   DevBuf d_nodes, d_roots, d_cnodes, d_leaf_val, d_leaf_idx, d_real_thr, d_code_param, d_code_sub;
-  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub, d_qrthr, d_qiidx, d_qimask;
+  DevBuf d_qmask, d_qvid, d_quval, d_qsoff, d_qcode_param, d_qcode_sub, d_qrthr, d_qiidx, d_qimask,
+      d_qcode_param2, d_qcode_sub2, d_qcode_mul;
   bool no_coded_forest = false;  // BX_FOREST_GENERIC debug switch (env)
   std::vector<int32_t> feat_param_host, feat_sub_host;
   std::vector<double> coord_host;

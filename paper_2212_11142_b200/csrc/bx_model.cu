@@ -628,7 +628,8 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
     };
     std::vector<Ind> ind;
     std::vector<char> taken(qparam.size(), 0);
-    std::vector<int32_t> dparam, dsub, dsoff;
+    std::vector<int32_t> dparam, dsub, dsoff, dparam2, dsub2, dmul;
+    std::vector<std::pair<int, int>> dslots;
     int dstride = 0;
     if (ok) {
       for (size_t c = 0; c < qparam.size() && ind.size() < 4; ++c)
@@ -647,28 +648,8 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
         for (int c : d.slots) taken[c] = 1;
         ind.push_back(d);
       }
-      for (size_t c = 0; c < qparam.size(); ++c) {
-        if (taken[c]) continue;
-        dparam.push_back(qparam[c]);
-        dsub.push_back(qsub[c]);
-        dsoff.push_back(dstride);
-        dstride += qrange[c];
-      }
-      ok = (size_t)T * dstride * 8 <= 160 * 1024;
     }
     if (ok) {
-      if (uval.empty()) uval.push_back(0.0);
-      // direct slots transposed to [slot value][tree] so a group of 8 trees is one 64-byte run per
-      // slot; odd row length (in 8-byte words): the <= 16 distinct code-value rows a half-warp reads
-      // with 8-byte loads fall in 16 distinct bank pairs (groups of 8 trees read t .. t+7)
-      int tpad = (T + 7) / 8 * 8 + 1;
-      std::vector<uint64_t> mt((size_t)std::max(dstride, 1) * tpad, ~0ull);
-      for (size_t c = 0, d = 0; c < qparam.size(); ++c) {
-        if (taken[c]) continue;
-        for (int v = 0; v < qrange[c]; ++v)
-          for (int t = 0; t < T; ++t) mt[(size_t)(dsoff[d] + v) * tpad + t] = mask[(size_t)t * stride + qsoff[c] + v];
-        ++d;
-      }
       // indirect tables: rows (slot, code) x itpad u16 indices (itpad = 8 * odd: 16-byte rows)
       int itpad = (T + 7) / 8 * 8;
       if ((itpad / 8) % 2 == 0) itpad += 8;
@@ -724,15 +705,75 @@ static int build_coded_forest(bx_handle* h, const std::vector<RfNode>& nodes,
         ioff += d.range;
       }
       if (imask.empty()) imask.push_back(~0ull);
+      int tpad = (T + 7) / 8 * 8 + 1;
+      // shared memory left for the direct table next to everything else rf_qs_summary_kernel holds
+      const size_t other = ((size_t)std::max<size_t>(uval.size(), 1) * 8) + (((size_t)T * 64 * 2 + 15) & ~(size_t)15) +
+                           (((size_t)std::max(irows, 1) * itpad * 2 + 15) & ~(size_t)15) + imask.size() * 8 +
+                           32 * sizeof(Partial) + 2048;
+      const size_t budget = std::min<size_t>(160 * 1024, other < 227 * 1024 ? 227 * 1024 - other : 0);
+      // direct slots, small ones paired: a pair (a, b) is one slot with code = code_a * range_b +
+      // code_b whose rows are the ANDs of the two slots' rows (one table walk instead of two);
+      // greedily the two smallest while the product stays <= 64 rows and the summary kernel's
+      // shared memory (tables + indirect tables + partials) stays within 227 KB
+      std::vector<int> single;  // dslots: (q-slot a, q-slot b or -1)
+      for (size_t c = 0; c < qparam.size(); ++c)
+        if (!taken[c]) single.push_back((int)c);
+      std::sort(single.begin(), single.end(), [&](int x, int y) { return qrange[x] < qrange[y]; });
+      int rows_total = 0;
+      for (int c : single) rows_total += qrange[c];
+      size_t i0 = 0;
+      while (i0 + 1 < single.size()) {
+        const int a = single[i0], b = single[i0 + 1];
+        const int grown = rows_total - qrange[a] - qrange[b] + qrange[a] * qrange[b];
+        if (qrange[a] * qrange[b] > 64 || (size_t)tpad * grown * 8 > budget) break;
+        dslots.push_back({a, b});
+        rows_total = grown;
+        i0 += 2;
+      }
+      for (; i0 < single.size(); ++i0) dslots.push_back({single[i0], -1});
+      std::sort(dslots.begin(), dslots.end());
+      for (const auto& ds : dslots) {
+        dparam.push_back(qparam[ds.first]);
+        dsub.push_back(qsub[ds.first]);
+        dparam2.push_back(ds.second >= 0 ? qparam[ds.second] : -1);
+        dsub2.push_back(ds.second >= 0 ? qsub[ds.second] : 0);
+        dmul.push_back(ds.second >= 0 ? qrange[ds.second] : 1);
+        dsoff.push_back(dstride);
+        dstride += qrange[ds.first] * (ds.second >= 0 ? qrange[ds.second] : 1);
+      }
+      ok = ok && (size_t)tpad * dstride * 8 <= 160 * 1024;
+      if (uval.empty()) uval.push_back(0.0);
+      // direct slots transposed to [slot value][tree] so a group of 8 trees is one 64-byte run per
+      // slot; odd row length (in 8-byte words): the <= 16 distinct code-value rows a half-warp reads
+      // with 8-byte loads fall in 16 distinct bank pairs (groups of 8 trees read t .. t+7)
+      std::vector<uint64_t> mt((size_t)std::max(dstride, 1) * tpad, ~0ull);
+      for (size_t d = 0; d < dslots.size(); ++d) {
+        const int a = dslots[d].first, b = dslots[d].second;
+        const int rb = b >= 0 ? qrange[b] : 1;
+        for (int va = 0; va < qrange[a]; ++va)
+          for (int vb = 0; vb < rb; ++vb)
+            for (int t = 0; t < T; ++t)
+              mt[(size_t)(dsoff[d] + va * rb + vb) * tpad + t] =
+                  mask[(size_t)t * stride + qsoff[a] + va] & (b >= 0 ? mask[(size_t)t * stride + qsoff[b] + vb] : ~0ull);
+      }
       if (ok) {
         qs.tpad = tpad;
         BX_CUDA(h, upload(h->d_qmask, mt.data(), mt.size()));
         BX_CUDA(h, upload(h->d_qvid, vid.data(), vid.size()));
         BX_CUDA(h, upload(h->d_quval, uval.data(), uval.size()));
-        if (dsoff.empty()) { dsoff.push_back(0); dparam.push_back(0); dsub.push_back(0); }
+        if (dsoff.empty()) {
+          dsoff.push_back(0); dparam.push_back(0); dsub.push_back(0);
+          dparam2.push_back(-1); dsub2.push_back(0); dmul.push_back(1);
+        }
         BX_CUDA(h, upload(h->d_qsoff, dsoff.data(), dsoff.size()));
         BX_CUDA(h, upload(h->d_qcode_param, dparam.data(), dparam.size()));
         BX_CUDA(h, upload(h->d_qcode_sub, dsub.data(), dsub.size()));
+        BX_CUDA(h, upload(h->d_qcode_param2, dparam2.data(), dparam2.size()));
+        BX_CUDA(h, upload(h->d_qcode_sub2, dsub2.data(), dsub2.size()));
+        BX_CUDA(h, upload(h->d_qcode_mul, dmul.data(), dmul.size()));
+        qs.code_param2 = h->d_qcode_param2.as<int32_t>();
+        qs.code_sub2 = h->d_qcode_sub2.as<int32_t>();
+        qs.code_mul = h->d_qcode_mul.as<int32_t>();
         BX_CUDA(h, upload(h->d_qrthr, rflat.data(), rflat.size()));
         BX_CUDA(h, upload(h->d_qiidx, iidx.data(), iidx.size()));
         BX_CUDA(h, upload(h->d_qimask, imask.data(), imask.size()));

@@ -249,6 +249,14 @@ __device__ __forceinline__ int qs_code(const bx_param_desc& p, const uint32_t* r
   return (int)row[p.word];
 }
 
+// a direct slot's code: single, or a pair code_a * mul + code_b (QsForestDev.code_param2)
+__device__ __forceinline__ int qs_slot_code(const bx_param_desc* params, const uint32_t* row, int p1, int s1, int p2,
+                                            int s2, int mul, const double* rthr) {
+  int c = qs_code(params[p1], row, s1, rthr);
+  if (p2 >= 0) c = c * mul + qs_code(params[p2], row, s2, rthr);
+  return c;
+}
+
 __device__ __forceinline__ int32_t lds_s32(uint32_t a) {
   int32_t v;
   asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -357,7 +365,8 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_kernel(SpaceDev sp, QsForest
     const uint32_t* row = rows + (size_t)i * sp.row_words;
     for (int c = 0; c < f.n_codes; ++c)
       sts_s32(off_s + 4u * kQsThreads * c,
-              (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
+              (f.soff[c] + qs_slot_code(params, row, f.code_param[c], f.code_sub[c], f.code_param2[c], f.code_sub2[c],
+                                        f.code_mul[c], f.rthr)) * f.tpad);
     uint32_t irow[4];
     qs_ind_rows(f, params, row, iidx_s, irow);
     double sum = 0.0;
@@ -418,11 +427,14 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
   Partial* summ = &parts[warp];
   if (lane == 0) partial_init(summ);
   // per-slot constants in shared memory (broadcast loads instead of a global load per candidate)
-  __shared__ int32_t s_soff[64], s_cpar[64], s_csub[64];
+  __shared__ int32_t s_soff[64], s_cpar[64], s_csub[64], s_cpar2[64], s_csub2[64], s_cmul[64];
   for (int c = tid; c < f.n_codes && c < 64; c += blockDim.x) {
     s_soff[c] = f.soff[c];
     s_cpar[c] = f.code_param[c];
     s_csub[c] = f.code_sub[c];
+    s_cpar2[c] = f.code_param2[c];
+    s_csub2[c] = f.code_sub2[c];
+    s_cmul[c] = f.code_mul[c];
   }
   __syncthreads();
   const uint32_t mask_s = (uint32_t)__cvta_generic_to_shared(smem + L.mask);
@@ -443,10 +455,13 @@ __global__ void __launch_bounds__(kQsThreads) rf_qs_summary_kernel(SpaceDev sp, 
       if constexpr (NC > 0) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-          colr[c] = mask_s + 8u * (uint32_t)((s_soff[c] + qs_code(params[s_cpar[c]], row, s_csub[c], f.rthr)) * f.tpad);
+          colr[c] = mask_s + 8u * (uint32_t)((s_soff[c] + qs_slot_code(params, row, s_cpar[c], s_csub[c], s_cpar2[c],
+                                                                        s_csub2[c], s_cmul[c], f.rthr)) * f.tpad);
       } else {
         for (int c = 0; c < f.n_codes; ++c)
-          sts_s32(off_s + 4u * kQsThreads * c, (f.soff[c] + qs_code(params[f.code_param[c]], row, f.code_sub[c], f.rthr)) * f.tpad);
+          sts_s32(off_s + 4u * kQsThreads * c,
+                  (f.soff[c] + qs_slot_code(params, row, f.code_param[c], f.code_sub[c], f.code_param2[c], f.code_sub2[c],
+                                            f.code_mul[c], f.rthr)) * f.tpad);
       }
       uint32_t irow[4];
       qs_ind_rows(f, params, row, iidx_s, irow);
