@@ -154,12 +154,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
     }                                                                                      \
   } while (0)
 
-// sigma * matern52(sqrt(W)) * kscale truncated to a 40-bit integer (the producers' hot path), in 16
+// sigma * matern52(sqrt(W)) * kscale rounded to a 40-bit integer (the producers' hot path), in 14
 // FP64 operations: d = sqrt(W) from rsqrt.approx + one Newton step on d (the 1/2 folded into the
 // exponent of the approximation, an integer op); e^(-sqrt5 d) as 2^(k/256) (256-entry table, k
-// clamped so the exponent stays normal; such K* truncate to 0) times a degree-4 Taylor polynomial.
-// The range reduction runs in units of d (r = d + k ln2 / (256 sqrt5), |sqrt5 r| <= ln2/512,
-// truncation < 4e-17), so -sqrt5 is folded into the polynomial coefficients instead of a multiply.
+// clamped so the exponent stays normal; such K* round to 0) times a degree-3 Taylor polynomial.
+// The range reduction runs in units of d (r = d + k ln2 / (256 sqrt5), |sqrt5 r| <= ln2/512), so
+// -sqrt5 is folded into the polynomial coefficients instead of a multiply.  Accuracy is sized to the
+// 2^-40 fixed point, not to FP64: the one-constant reduction leaves <= 5e-15 and the dropped r^4
+// term <= 1.4e-13 of K* (0.15 of the fixed-point quantum; the round-to-nearest is 0.5 of it).
 __device__ __forceinline__ unsigned long long kstar_fixed(double W, const MaternConst& m, const double* tab256) {
   const double w = W + 1e-300;                      // W = 0 -> d = 1e-150, K* = sigma
   const double y0 = rsqrt_approx(w);
@@ -170,10 +172,8 @@ __device__ __forceinline__ unsigned long long kstar_fixed(double W, const Matern
   const double t = fma(d, -825.8468306507675, 6755399441055744.0);  // -d sqrt5 256 / ln2 + 1.5 * 2^52
   const int k = max(__double2loint(t), -256 * 900);
   const double kf = t - 6755399441055744.0;
-  double r = fma(kf, 0.0012108782921131933, d);      // ln2/(256 sqrt5) split: hi (32 bits, exact product) ...
-  r = fma(kf, 1.8708673154509723e-13, r);            // ... and lo
-  double p = fma(r, 25.0 / 24.0, -1.8633899812498247);  // e^(-sqrt5 r): 25/24, -5 sqrt5/6, 5/2, -sqrt5, 1
-  p = fma(r, p, 2.5);
+  const double r = fma(kf, 0.00121087829230028, d);  // ln2 / (256 sqrt5)
+  double p = fma(r, -1.8633899812498247, 2.5);       // e^(-sqrt5 r): -5 sqrt5/6, 5/2, -sqrt5, 1
   p = fma(r, p, -2.23606797749979);
   p = fma(r, p, 1.0);
   const double tj = tab256[k & 255];
