@@ -543,9 +543,11 @@ struct TcArgs {
   // mat_resident != 0: every (chunk, slice) digit block is loaded into shared memory once per CTA
   // and stays there for all tiles (set by launch_gp_tc when it fits; else the 8-stage ring)
   int32_t mat_resident;
-  // n > 255 (two passes per tile): [grid][256 rows][128 candidates] pass-0 partial sums of the
-  // rows >= 256, written and read back by the same epilogue thread; null otherwise
+  // n > 255 (several passes per tile): [grid][16 n_chunks - 256 rows][128 candidates] partial sums
+  // of the rows >= 256, written and read back by the same epilogue thread; null otherwise
   double* part;
+  int32_t planes_pp;          // set by launch_gp_tc: planes per pass (tc_layout)
+  int32_t mat_stages;         // set by launch_gp_tc: matrix ring stages (not resident)
   // ks > 0: distances on the FP64 tensor cores, W = |x'|^2 + |y'|^2 - 2 x'.y' over the embedding
   // (EmbDim) as one product of ks k-steps of DMMA m8n8k4; the matrix digits carry the C-fragment
   // column permutation (launch_build_mdig perm).  ks == 0: FMA distances per parameter kind.
@@ -571,8 +573,12 @@ size_t panels_doubles(int ncols_pad, int rows8);
 cudaError_t launch_build_panels(const double* A, int lda, int rows_src, int ncols_pad, int rows8,
                                 double* panels, cudaStream_t s);
 cudaError_t launch_gp_fused(const FusedArgs& a, int sm_count, cudaStream_t s);
+// tensor-core posterior: n <= kTcMaxRows - 1 training points ([L^-1; alpha^T] has n + 1 rows)
+constexpr int kTcMaxRows = 4096;
 size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, int ks, int n_emb, int emb_tab_len,
                      bool aug, bool resident);
+// partial-sum scratch of the multi-pass posterior (n > 255), in doubles, for `grid` CTAs
+size_t tc_part_doubles(int n, int grid);
 size_t tc_mdig_bytes(int n);
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, int perm, cudaStream_t s);
@@ -582,6 +588,7 @@ int summary_max_partials(int sm_count);
 
 // launch_score returns the number of partials it wrote in *n_partials.
 cudaError_t launch_score(const ScoreArgs& a, int sm_count, cudaStream_t s, int* n_partials);
+int score_smem_bytes(int cpw, int ncols, int n_params);  // the generic kernel's shared memory
 // Merge partials into *out.  When pool_rows is non-NULL the rows of the top-k entries are
 // gathered from it (index - index_base); otherwise the caller fills them.
 cudaError_t launch_partial_merge(const Partial* partials, int n_partials, const SpaceDev& space, int k,

@@ -148,6 +148,7 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
   if (n < 1) return fail(h, BX_ERR_ARG, "need at least one training point");
   if (!(outputscale > 0)) return fail(h, BX_ERR_ARG, "outputscale must be positive");
   cudaSetDevice(h->device);
+  h->has_gp = false;  // until this call succeeds
   cudaStream_t s = (cudaStream_t)stream;
   const int D = h->n_params;
   std::vector<double> inv_l(D), inv_l2(D);
@@ -215,12 +216,12 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
       h->use_fused = true;
     }
   }
-  // tensor-core path: n <= 511 (32 row chunks; n > 255 runs two column passes per tile) and the
-  // shared-memory budget.  Distances on the FP64 tensor cores over the Euclidean embedding of W
+  // tensor-core path: n < kTcMaxRows (n > 255 runs one column pass per 256 columns per tile) and
+  // the shared-memory budget.  Distances on the FP64 tensor cores over the Euclidean embedding of W
   // (EmbDim) when every metric embeds and the centred coordinates stay small, else FMA distances.
   h->use_tc = false;
   h->tc_ks = 0;
-  if (!h->no_tc && n <= 511) {
+  if (!h->no_tc && n < kTcMaxRows) {
     h->tc_emb.clear();
     h->tc_tab.clear();
     std::vector<double> planes, yy;
@@ -240,9 +241,9 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
       h->tc_nch = n / 16 + 1;
       h->tc_kscale = ldexp(1.0, 40 - Ex);
       BX_CUDA(h, h->d_mdig.ensure(tc_mdig_bytes(n)));
-      BX_CUDA(h, h->d_rowscale.ensure(2 * 512 * 8));
-      if (h->tc_nsl > 8)  // pass-0 partial sums of rows >= 256: [CTA][256 rows][128 candidates]
-        BX_CUDA(h, h->d_tc_part.ensure((size_t)h->sm_count * 256 * 128 * 8));
+      BX_CUDA(h, h->d_rowscale.ensure(2 * kTcMaxRows * 8));
+      if (h->tc_nsl > 8)  // partial sums of rows >= 256: [CTA][16 nch - 256 rows][128 candidates]
+        BX_CUDA(h, h->d_tc_part.ensure(tc_part_doubles(n, h->sm_count) * 8));
       if (dmma) {
         h->tc_ks = ks;
         BX_CUDA(h, upload(h->d_emb, h->tc_emb.data(), h->tc_emb.size()));
@@ -257,6 +258,9 @@ int bx_set_gp(bx_handle* h, const uint32_t* train_rows, int32_t n, const double*
     }
   }
   BX_CUDA(h, cudaStreamSynchronize(s));  // host vectors above go out of scope
+  if (!h->use_tc && !h->use_fused && score_smem_bytes(8, h->gp_ncols, D) > 227 * 1024)
+    return fail(h, BX_ERR_UNSUPPORTED, "n = %d training points is beyond the posterior kernels (tensor-core path: n < %d)",
+                n, kTcMaxRows);
   h->outputscale = outputscale;
   h->y_mean = y_mean;
   h->y_std = y_std;

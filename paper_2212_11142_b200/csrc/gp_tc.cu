@@ -33,6 +33,8 @@
 //                    digits and stored into the candidate's TMEM lane (tcgen05.st)
 // TMEM (512 columns): two 96-column accumulators (6 groups x 16 rows) so the epilogue of one chunk
 // overlaps the MMAs of the next, then 40 columns (5 digits x 32 bytes) per column slice.
+#include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -49,14 +51,17 @@ constexpr int kN = 16;           // matrix rows per chunk
 constexpr int kDA = 6;           // matrix digits (signed)
 constexpr int kDB = 5;           // K* digits (unsigned)
 constexpr int kGroups = 6;       // a + b in 0..5
-constexpr int kStages = 8;       // matrix block ring
-constexpr int kMaxChunks = 32;   // n <= 511
+constexpr int kStages = 8;       // matrix block ring: minimum stages
+constexpr int kMaxStages = 32;   // ... and maximum (launch_gp_tc fills the spare shared memory)
+constexpr int kMaxChunks = kTcMaxRows / 16;  // n <= 4095
 constexpr int kSlots = 8;        // K* column slices held in tensor memory at a time
-// n > 255 (more than kSlots column slices): each tile runs two passes.  Pass 0 holds slices 0-7
-// (columns 0-255) in the slots and runs every row chunk — rows < 256 complete, rows >= 256 leave
-// their partial sums (exact int64, converted to double) in global scratch; pass 1 refills the slots
-// with slices 8.. and runs the chunks of rows >= 256 again over those columns, adding the partials.
-__host__ __device__ __forceinline__ int tc_passes(int nsl) { return nsl > kSlots ? 2 : 1; }
+// n > 255 (more than kSlots column slices): each tile runs one pass per 8 slices.  Pass p holds
+// slices 8p..8p+7 (columns 256p..256p+255) in the slots and runs the row chunks of rows >= 256p
+// (the lower triangle has no other blocks in those columns).  A row finishes in its last pass,
+// min(npass - 1, row / 256); before that its partial sum (exact int64, converted to double - an
+// exact integer below 2^53) is parked in global scratch by the epilogue thread that owns the
+// candidate and added back in the next pass.
+__host__ __device__ __forceinline__ int tc_passes(int nsl) { return (nsl + kSlots - 1) / kSlots; }
 // K* producer warps (a multiple of 4: kProdWarps / 4 per TMEM lane quarter).  The DMMA producers
 // (KS > 0) are written for two per quarter at 128 registers; the FMA producers (integer-heavy
 // distance code, latency bound) run four per quarter at 80 registers.
@@ -222,9 +227,13 @@ __host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
 // the tile's E embedding coordinates plus |x'|^2 (one buffer: the producers copy their A fragments
 // into registers at the start of a tile and release it).  ks == 0: per-parameter planes and
 // candidate values, double-buffered (the FMA producers read them for every slice).
+// pp (per-pass planes, n > 255 when the whole-width planes do not fit): the planes / Kendall masks /
+// |y'|^2 hold only the current pass's 256 columns and the producers reload them every pass.
 __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words, int ks, int n_emb,
-                                              int emb_tab_len, bool aug, bool resident) {
-  const int nsl = (n + 31) / 32, npad = 32 * nsl, nch = n / kN + 1;
+                                              int emb_tab_len, bool aug, bool resident, bool pp,
+                                              int stages = kStages) {
+  const int nsl = (n + 31) / 32, nch = n / kN + 1;
+  const int npad = pp ? 32 * kSlots : 32 * nsl;  // columns held in shared memory
   TcLayout L;
   int off = 0;
   L.par = off;
@@ -258,15 +267,17 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += ks > 0 ? emb_tab_len * 8 : 0;
   off = (off + 1023) & ~1023;
   L.mat = off;     // [stage][digit][16 x 32 B], or every block of the triangle when resident
-  off += (resident ? tc_block0(nch, nsl) : kStages) * kMatBlock;
+  off += (resident ? tc_block0(nch, nsl) : stages) * kMatBlock;
   L.bars = off;    // cand_full, slice_empty[8], mat_full/empty[8], acc_full/empty[2], rows_full/empty, cval_full/free[2], tmem
-  off += (1 + kSlots + 2 * kStages + 4 + 2 + 4 + 1) * 8;
+  off += (1 + kSlots + 2 * kMaxStages + 4 + 2 + 4 + 1) * 8;
   L.total = off;
   return L;
 }
 
 // KS > 0: tensor-core (DMMA) distances over the embedding with KS k-steps; KS == 0: FMA distances.
-template <bool kPrecise, int KS>
+// kMulti: n > 255, several column passes per tile (a separate instance: the one-pass kernel carries
+// none of the parking / per-pass planes code).
+template <bool kPrecise, int KS, bool kMulti>
 __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta) {
   constexpr bool kDmma = KS > 0;
   constexpr int kProdWarps = tc_prod_warps<KS>();
@@ -276,12 +287,15 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.gp.n, n_params = a.space.n_params, words = a.space.row_words;
   const int nsl = ta.n_slices, nch = ta.n_chunks, npad = 32 * nsl;
-  const int npass = tc_passes(nsl);
+  const int npass = kMulti ? tc_passes(nsl) : 1;
+  const bool pp = kMulti && ta.planes_pp != 0;  // per-pass planes (tc_layout)
+  const int nst = ta.mat_stages;                 // matrix ring stages (not resident)
+  const int ppad = pp ? 32 * kSlots : npad;  // columns of the planes in shared memory
   const int E = ta.n_emb;
   constexpr int kCvs = kM + 1;        // DMMA mode: candidate-buffer row stride (doubles)
-  const int pls = npad + 4;           // DMMA mode: planes row stride (doubles)
+  const int pls = ppad + 4;           // DMMA mode: planes row stride (doubles)
   const bool resident = ta.mat_resident != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident, pp, nst);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -299,8 +313,8 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   uint64_t* cand_full = bars;
   uint64_t* slice_empty = bars + 1;
   uint64_t* mat_full = slice_empty + kSlots;
-  uint64_t* mat_empty = mat_full + kStages;
-  uint64_t* acc_full = mat_empty + kStages;
+  uint64_t* mat_empty = mat_full + kMaxStages;
+  uint64_t* acc_full = mat_empty + kMaxStages;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* rows_full = acc_empty + 2;   // the staging buffer holds the next tile's rows
   uint64_t* rows_empty = rows_full + 1;  // the decoders are done with them
@@ -313,25 +327,35 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
 
   for (int i = tid; i < n_params * (int)sizeof(bx_param_desc) / 4; i += blockDim.x)
     reinterpret_cast<int32_t*>(params)[i] = reinterpret_cast<const int32_t*>(a.space.params)[i];
+  // the planes (DMMA: B operand and |y'|^2; FMA: per-parameter training values and Kendall masks)
+  // of columns c0 .. c0 + ppad - 1
+  auto load_planes = [&](int c0, int i0, int step) {
+    if constexpr (kDmma) {
+      for (int i = i0; i < 4 * KS * ppad; i += step) {
+        const int k = i / ppad, j = c0 + i % ppad;
+        planes[k * pls + i % ppad] = j < npad ? (uint64_t)__double_as_longlong(ta.emb_planes[(size_t)k * npad + j]) : 0;
+      }
+      if (!ta.aug)
+        for (int i = i0; i < ppad; i += step) s_yy[i] = c0 + i < npad ? ta.emb_yy[c0 + i] : 0.0;
+    } else {
+      for (int i = i0; i < n_params * ppad; i += step) {
+        const int k = i / ppad, j = c0 + i % ppad;
+        planes[i] = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
+      }
+      for (int i = i0; i < a.n_kendall * ppad; i += step) {
+        const int kk = i / ppad, j = c0 + i % ppad;
+        const size_t src = ((size_t)a.kendall_param[kk] * n + j) * 2;
+        kmask[2 * i] = j < n ? a.gp.kmask[src] : 0;
+        kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
+      }
+    }
+  };
+  if (!pp) load_planes(0, tid, blockDim.x);  // pp: the producers load each pass's columns
   if constexpr (kDmma) {
-    for (int i = tid; i < 4 * KS * npad; i += blockDim.x)
-      planes[(i / npad) * pls + i % npad] = (uint64_t)__double_as_longlong(ta.emb_planes[i]);
-    if (!ta.aug)
-      for (int j = tid; j < npad; j += blockDim.x) s_yy[j] = ta.emb_yy[j];
     for (int i = tid; i < E * (int)sizeof(EmbDim) / 4; i += blockDim.x)
       reinterpret_cast<int32_t*>(s_emb)[i] = reinterpret_cast<const int32_t*>(ta.emb)[i];
     for (int i = tid; i < ta.emb_tab_len; i += blockDim.x) s_etab[i] = ta.emb_tab[i];
   } else {
-    for (int i = tid; i < n_params * npad; i += blockDim.x) {
-      const int k = i / npad, j = i % npad;
-      planes[i] = j < n ? a.gp.planes[(size_t)k * n + j] : 0;
-    }
-    for (int i = tid; i < a.n_kendall * npad; i += blockDim.x) {
-      const int kk = i / npad, j = i % npad;
-      const size_t src = ((size_t)a.kendall_param[kk] * n + j) * 2;
-      kmask[2 * i] = j < n ? a.gp.kmask[src] : 0;
-      kmask[2 * i + 1] = j < n ? a.gp.kmask[src + 1] : 0;
-    }
     for (int k = tid; k < n_params; k += blockDim.x)
       s_cw[k] = a.space.params[k].kind == BX_PERMUTATION ? a.gp.inv_l2[k] / a.space.params[k].raw_mx : 0.0;
   }
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   if (tid == 0) {
     mb_init(cand_full, kProdWarps);
     for (int i = 0; i < kSlots; ++i) mb_init(&slice_empty[i], 1);
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < nst; ++i) {
       mb_init(&mat_full[i], 1);
       mb_init(&mat_empty[i], 1);
     }
@@ -539,9 +563,9 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       int s = 0, issued = 0;
       for (int t = 0; t < my_tiles; ++t)
         for (int p = 0; p < npass; ++p)
-        for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c)
+        for (int c = nch - 1; c >= 2 * kSlots * p; --c)
           for (int ks = kSlots * p; ks <= min(c >> 1, min(nsl, kSlots * (p + 1)) - 1); ++ks) {
-            if (issued >= kStages) {
+            if (issued >= nst) {
               mb_wait_sleep(&mat_empty[s], (ph >> s) & 1u);
               ph ^= 1u << s;
             }
@@ -550,7 +574,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
             bulk_g2s(mat + (size_t)s * kMatBlock, ta.mdig + ((size_t)c * nsl + ks) * kMatBlock, kMatBlock,
                      &mat_full[s]);
             ++issued;
-            s = (s + 1 == kStages) ? 0 : s + 1;
+            s = (s + 1 == nst) ? 0 : s + 1;
           }
     }
   } else if (warp == 0) {
@@ -570,7 +594,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       ph_c ^= 1u;
       tc_fence_after();
       if (lane == 0) TC_TRACE(1, 2, t);
-      for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
+      for (int c = nch - 1; c >= 2 * kSlots * p; --c, ++chunk_no) {
         const int buf = chunk_no & 1;
         if (chunk_no >= 2) {
           mb_wait(&acc_empty[buf], (ph_e >> buf) & 1u);
@@ -597,7 +621,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
           }
           if (!resident) {
             tc_commit_warp(&mat_empty[s]);  // the stage is free once these MMAs retire
-            s = (s + 1 == kStages) ? 0 : s + 1;
+            s = (s + 1 == nst) ? 0 : s + 1;
           }
         }
         tc_commit_warp(&acc_full[buf]);
@@ -616,44 +640,71 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
     int chunk_no = 0;
     for (int t = 0; t < my_tiles; ++t) {
       const int64_t tile = blockIdx.x + (int64_t)t * gridDim.x;
-      double ss = 0.0, mean_s = 0.0;
+      double ss = 0.0, ss1 = 0.0, mean_s = 0.0;
       for (int p = 0; p < npass; ++p)
-      for (int c = nch - 1; c >= (p == 0 ? 0 : 2 * kSlots); --c, ++chunk_no) {
-        // two passes (n > 255): rows >= 256 park their pass-0 partial sums in this CTA's scratch
-        // ([256 rows][128 candidates], coalesced per row) and add them back in pass 1
-        const int mode = (npass == 1 || c < 2 * kSlots) ? 0 : (p == 0 ? 1 : 2);
-        double* park = mode ? ta.part + (size_t)blockIdx.x * (kSlots * 32) * kM + r : nullptr;  // + (row - 256) * kM
+      for (int c = nch - 1; c >= 2 * kSlots * p; --c, ++chunk_no) {
+        // several passes (n > 255): a row >= 256 parks its partial sum in this CTA's scratch
+        // ([16 nch - 256 rows][128 candidates], coalesced per row) until its last pass.  mode 0:
+        // complete in this pass, 1: park, 3: add to the parked sum, 2: last pass, add it back.
+        const int last = min(npass - 1, c / (2 * kSlots));
+        const int mode = last == 0 ? 0 : (p == 0 ? 1 : (p < last ? 3 : 2));
+        double* park = mode ? ta.part + (size_t)blockIdx.x * (kN * nch - kSlots * 32) * kM + r : nullptr;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
         mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);  // the MMA / epilogue chain paces the kernel: spin
         ph_f ^= 1u << buf;
         tc_fence_after();
         if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
         const uint32_t base = tmem + lane_base + (uint32_t)(buf * kAccCols);
-        for (int r0 = 0; r0 < kN && kN * c + r0 <= n && !(ta.debug & 1); r0 += 8) {
-          uint32_t g[kGroups][8];
+        // exact int64 recombination of the six digit groups of row kN c + r0 + j
+        auto recombine = [&](const uint32_t (&g)[kGroups][8], int j) -> double {
+          long long Z = (long long)(int32_t)g[0][j] << 40;
+          Z += (long long)(int32_t)g[1][j] << 32;
+          Z += (long long)(int32_t)g[2][j] << 24;
+          Z += (long long)(int32_t)g[3][j] << 16;
+          Z += (long long)(int32_t)g[4][j] << 8;
+          Z += (long long)(int32_t)g[5][j];
+          return (double)Z;
+        };
+        // one loop per parking mode (uniform per chunk): the parked sums of a group of 8 rows are
+        // loaded together with its TMEM reads
+        auto drain = [&](auto mode_c) {
+          constexpr int kMode = decltype(mode_c)::value;
+          for (int r0 = 0; r0 < kN && kN * c + r0 <= n && !(ta.debug & 1); r0 += 8) {
+            uint32_t g[kGroups][8];
 #pragma unroll
-          for (int q = 0; q < kGroups; ++q) tmem_ld8(base + (uint32_t)(q * kN + r0), g[q]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int q = 0; q < kGroups; ++q) tmem_ld8(base + (uint32_t)(q * kN + r0), g[q]);
+            double prev[8];
+            if constexpr (kMode >= 2) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (ta.debug & 4) break;  // timing experiment: TMEM reads only
-            const int row = kN * c + r0 + j;
-            long long Z = (long long)(int32_t)g[0][j] << 40;
-            Z += (long long)(int32_t)g[1][j] << 32;
-            Z += (long long)(int32_t)g[2][j] << 24;
-            Z += (long long)(int32_t)g[3][j] << 16;
-            Z += (long long)(int32_t)g[4][j] << 8;
-            Z += (long long)(int32_t)g[5][j];
-            double zd = (double)Z;
-            if (mode == 1) {
-              park[(size_t)(row - kSlots * 32) * kM] = zd;
-              continue;
+              for (int j = 0; j < 8; ++j) prev[j] = park[(size_t)(kN * c + r0 + j - kSlots * 32) * kM];
             }
-            if (mode == 2) zd += park[(size_t)(row - kSlots * 32) * kM];
-            const double v = zd * rowscale_ss[row];  // 0 for the alpha row and the padding rows
-            ss = fma(v, v, ss);
-            if (row == n) mean_s = zd * rowscale[row];  // only in the alpha row's chunk
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (ta.debug & 4) break;  // timing experiment: TMEM reads only
+              const int row = kN * c + r0 + j;
+              double zd = recombine(g, j);
+              if constexpr (kMode == 1 || kMode == 3) {  // park: first pass / running sum of the passes
+                park[(size_t)(row - kSlots * 32) * kM] = kMode == 3 ? prev[j] + zd : zd;
+              } else {
+                if constexpr (kMode == 2) zd += prev[j];  // last pass: add the parked sum back
+                const double v = zd * rowscale_ss[row];  // 0 for the alpha row and the padding rows
+                // (several passes: two independent FMA chains measure faster, one pass: one chain)
+                if (kMulti && (j & 1)) ss1 = fma(v, v, ss1); else ss = fma(v, v, ss);
+                if (row == n) mean_s = zd * rowscale[row];  // only in the alpha row's chunk
+              }
+            }
           }
+        };
+        if constexpr (kMulti) {
+          switch (mode) {
+            case 1: drain(std::integral_constant<int, 1>{}); break;
+            case 2: drain(std::integral_constant<int, 2>{}); break;
+            case 3: drain(std::integral_constant<int, 3>{}); break;
+            default: drain(std::integral_constant<int, 0>{}); break;
+          }
+        } else {
+          drain(std::integral_constant<int, 0>{});  // every row completes in its one pass
         }
         tc_fence_before();
         __syncwarp();
@@ -661,6 +712,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
         if (lane == 0 && warp == 4) TC_TRACE(2, 2, c);
       }
       const int64_t gi = tile * kM + r;
+      if constexpr (kMulti) ss += ss1;
       if (gi < a.q) {
         const double var_s = fmax(sigma - ss, 0.0);                 // surrogate.py:324-325
         const double mean = a.gp.y_mean + a.gp.y_std * mean_s;      // :328
@@ -720,9 +772,14 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       for (int p = 0; p < npass; ++p) {
       const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));
       const int soff = p == 0 ? 0 : kSlots - (hi - lo);
+      if (pp) {  // every producer is done with the previous pass's columns; load this pass's
+        asm volatile("bar.sync 4, %0;" ::"r"(kProdWarps * 32) : "memory");
+        load_planes(32 * lo, pt, kProdWarps * 32);
+        asm volatile("bar.sync 4, %0;" ::"r"(kProdWarps * 32) : "memory");
+      }
       for (int ks = hi - 1; ks >= lo; --ks) {
         const int slot = ks - lo + soff;
-        const int j0 = 32 * ks;
+        const int j0 = 32 * (pp ? ks - lo : ks);  // column of the slice in the planes
         double acc[2][4][2];
 #pragma unroll
         for (int rb = 0; rb < 2; ++rb)
@@ -813,10 +870,15 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       if (pt == 0) TC_TRACE(0, 2, t);
       for (int p = 0; p < npass; ++p) {
       const int lo = kSlots * p, hi = min(nsl, kSlots * (p + 1));  // this pass's column slices
-      const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // pass 1 takes the slots pass 0 frees first
+      const int soff = p == 0 ? 0 : kSlots - (hi - lo);  // a partial last pass takes the slots freed first
+      if (pp) {  // every producer is done with the previous pass's columns; load this pass's
+        asm volatile("bar.sync 4, %0;" ::"r"(kProdWarps * 32) : "memory");
+        load_planes(32 * lo, pt, kProdWarps * 32);
+        asm volatile("bar.sync 4, %0;" ::"r"(kProdWarps * 32) : "memory");
+      }
       for (int ks = hi - 1; ks >= lo; --ks) {
         const int slot = ks - lo + soff;
-        const int j0 = 32 * ks + kColsPerItem * part;  // warp-uniform
+        const int j0 = 32 * (pp ? ks - lo : ks) + kColsPerItem * part;  // planes column; warp-uniform
         double W[kColsPerItem];
 #pragma unroll
         for (int u = 0; u < kColsPerItem; ++u) W[u] = 0.0;
@@ -824,7 +886,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
           const int k = a.num_param[i];
           const double x = __longlong_as_double((long long)cv[k * kM + c]);
           // 16-byte broadcast loads: half the shared-memory wavefronts of scalar loads
-          const double2* pl = reinterpret_cast<const double2*>(planes + (size_t)k * npad + j0);
+          const double2* pl = reinterpret_cast<const double2*>(planes + (size_t)k * ppad + j0);
 #pragma unroll
           for (int u = 0; u < kColsPerItem / 2; ++u) {
             const double2 y = pl[u];
@@ -837,7 +899,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
           const int k = a.cat_param[i];
           const uint64_t x = cv[k * kM + c];
           const double wl = a.gp.inv_l2[k];
-          const uint64_t* pl = planes + (size_t)k * npad + j0;
+          const uint64_t* pl = planes + (size_t)k * ppad + j0;
 #pragma unroll
           for (int u = 0; u < kColsPerItem; ++u) W[u] += (x != pl[u]) ? wl : 0.0;
         }
@@ -845,13 +907,13 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
           const int k = a.perm_param[i];
           const bx_param_desc& p = params[k];
           const uint64_t x = cv[k * kM + c];
-          const uint64_t* pl = planes + (size_t)k * npad + j0;
+          const uint64_t* pl = planes + (size_t)k * ppad + j0;
           // the reference's (raw / raw_mx) / l^2 (surrogate.py:222-223) as raw * (1 / l^2 / raw_mx):
           // one FMA per pair instead of a table load
           const double cw = s_cw[k];
           if (p.metric == BX_KENDALL) {  // discordant pairs: popcount of the pair-order masks
             const uint64_t xl = cmk[2 * (kend * kM + c)], xh = cmk[2 * (kend * kM + c) + 1];
-            const uint64_t* km = kmask + ((size_t)kend * npad + j0) * 2;
+            const uint64_t* km = kmask + ((size_t)kend * ppad + j0) * 2;
 #pragma unroll
             for (int u = 0; u < kColsPerItem; ++u) {
               const int raw = __popcll(xl ^ km[2 * u]) + __popcll(xh ^ km[2 * u + 1]);
@@ -954,7 +1016,7 @@ __global__ void row_scale_kernel(const double* A, int lda, int n, double sc, dou
     if (m > 0.0) frexp(m, &E);
     const bool live = row <= n && m > 0.0;
     rowscale[row] = live ? ldexp(sc, E + 2 - 56) : 0.0;                      // epilogue factor
-    rowscale[kMaxChunks * kN + row] = live ? ldexp(1.0, 48 - (E + 2)) : 0.0;  // digit scale
+    rowscale[kTcMaxRows + row] = live ? ldexp(1.0, 48 - (E + 2)) : 0.0;  // digit scale
   }
 }
 
@@ -972,7 +1034,7 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
     const int kc = perm ? 8 * (2 * ((kb >> 2) & 1) + ((kb >> 1) & 1)) + 2 * (kb >> 3) + (kb & 1) : kb;
     const int row = c * kN + r, col = ks * 32 + kc;
     const double x = (row <= n && col < n) ? A[(size_t)row * lda + col] : 0.0;
-    long long X = __double2ll_rn(x * rowscale[kMaxChunks * kN + row]);
+    long long X = __double2ll_rn(x * rowscale[kTcMaxRows + row]);
     unsigned char* out = mdig + (size_t)blk * kMatBlock + kmaj(r, kb);
 #pragma unroll
     for (int d = kDA - 1; d >= 0; --d) {
@@ -988,7 +1050,14 @@ __global__ void mdig_kernel(const double* A, int lda, int n, int nsl, int nch, c
 
 size_t tc_smem_bytes(int n, int n_params, int n_kendall, int row_words, int ks, int n_emb, int emb_tab_len,
                      bool aug, bool resident) {
-  return tc_layout(n, n_params, n_kendall, row_words, ks, n_emb, emb_tab_len, aug, resident).total;
+  // the smallest layout the kernel can run with (per-pass planes when there are several passes)
+  return tc_layout(n, n_params, n_kendall, row_words, ks, n_emb, emb_tab_len, aug, resident,
+                   tc_passes((n + 31) / 32) > 1).total;
+}
+
+size_t tc_part_doubles(int n, int grid) {
+  const int nch = n / kN + 1;
+  return tc_passes((n + 31) / 32) > 1 ? (size_t)grid * (kN * nch - kSlots * 32) * kM : 0;
 }
 
 size_t tc_mdig_bytes(int n) {
@@ -996,12 +1065,12 @@ size_t tc_mdig_bytes(int n) {
   return (size_t)nsl * nch * kMatBlock;
 }
 
-// rowscale must hold 2 * 512 doubles (epilogue factors, then digit scales)
+// rowscale must hold 2 * kTcMaxRows doubles (epilogue factors, then digit scales)
 cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsigned char* mdig,
                               double* rowscale, int perm, cudaStream_t s) {
   const int nsl = (n + 31) / 32, nch = n / kN + 1;
   if (nch > kMaxChunks) return cudaErrorInvalidValue;
-  row_scale_kernel<<<kMaxChunks * kN, 32, 0, s>>>(A, lda, n, sc, rowscale);
+  row_scale_kernel<<<kTcMaxRows, 32, 0, s>>>(A, lda, n, sc, rowscale);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   mdig_kernel<<<148, 256, 0, s>>>(A, lda, n, nsl, nch, rowscale, mdig, perm);
@@ -1011,22 +1080,37 @@ cudaError_t launch_build_mdig(const double* A, int lda, int n, double sc, unsign
 cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
   TcArgs a = a0;
   const int n = a.f.gp.n, P = a.f.space.n_params, K = a.f.n_kendall, W = a.f.space.row_words;
+  const bool multi = tc_passes(a.n_slices) > 1;
+  // the whole-width planes when they fit, else per pass (BX_TC_DEBUG bit 16: per pass whenever
+  // there are several passes)
+  a.planes_pp = multi && ((a.debug & 16) || tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, false,
+                                                      false).total > 227 * 1024);
   // matrix digits resident in shared memory when they fit (BX_TC_DEBUG bit 8: always the ring)
-  a.mat_resident = !(a.debug & 8) &&
-                   tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, true).total <= 227 * 1024;
-  const TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0);
-  if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks || a.ks > 8 || (a.ks > 0 && a.f.precise))
+  a.mat_resident = !(a.debug & 8) && tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, true,
+                                               a.planes_pp != 0).total <= 227 * 1024;
+  // the ring takes the shared memory left over, up to kMaxStages (L2 latency x MMA block rate)
+  a.mat_stages = kStages;
+  if (!a.mat_resident) {
+    const int base = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, false, a.planes_pp != 0, 0).total;
+    a.mat_stages = std::max(kStages, std::min(kMaxStages, (227 * 1024 - base) / kMatBlock));
+    if (const char* st = getenv("BX_TC_STAGES")) a.mat_stages = std::max(2, std::min(a.mat_stages, atoi(st)));
+  }
+  const TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0,
+                               a.planes_pp != 0, a.mat_stages);
+  if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks || a.ks > 8 || (a.ks > 0 && a.f.precise) ||
+      (multi && !a.part))
     return cudaErrorInvalidValue;
   if (getenv("BX_TC_INFO"))  // development aid: kernel geometry
-    fprintf(stderr, "gp_tc: n %d ks %d E %d aug %d smem %d resident %d words %d\n", n, a.ks, a.n_emb, a.aug, L.total,
-            a.mat_resident, W);
-  auto kernel = a.f.precise ? gp_tc_kernel<true, 0> : gp_tc_kernel<false, 0>;
+    fprintf(stderr, "gp_tc: n %d ks %d E %d aug %d smem %d resident %d planes_pp %d stages %d words %d\n", n, a.ks,
+            a.n_emb, a.aug, L.total, a.mat_resident, a.planes_pp, a.mat_stages, W);
+  auto kernel = a.f.precise ? (multi ? gp_tc_kernel<true, 0, true> : gp_tc_kernel<true, 0, false>)
+                            : (multi ? gp_tc_kernel<false, 0, true> : gp_tc_kernel<false, 0, false>);
   int threads = tc_threads<0>();
   switch (a.ks) {
-#define BX_KS(k)                             \
-    case k:                                  \
-      kernel = gp_tc_kernel<false, k>;       \
-      threads = tc_threads<k>();             \
+#define BX_KS(k)                                                                   \
+    case k:                                                                        \
+      kernel = multi ? gp_tc_kernel<false, k, true> : gp_tc_kernel<false, k, false>; \
+      threads = tc_threads<k>();                                                   \
       break;
     BX_KS(1) BX_KS(2) BX_KS(3) BX_KS(4) BX_KS(5) BX_KS(6) BX_KS(7) BX_KS(8)
 #undef BX_KS

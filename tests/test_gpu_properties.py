@@ -127,10 +127,10 @@ def test_space_exhausted_raises():
     assert A.optimize_acquisition(ctx, sp, cot) == allc[5]
 
 
-@pytest.mark.parametrize("n", [64, 200, 250, 300, 500])
+@pytest.mark.parametrize("n", [64, 200, 250, 300, 500, 1000, 1800])
 def test_mixed_space_large_n_against_oracle(n):
     """C5 (d=10 mixed: log-ordinal, integer, real, categorical, Spearman and Kendall permutations)
-    at n up to 500 — the tensor-core kernel (one column pass for n <= 255, two beyond) — against the
+    at n up to 1800 — the tensor-core kernel (one column pass per 256 columns) — against the
     oracle's FP64 posterior on a sample of a 2^18 pool (BASELINE config 5 uses n = 500)."""
     import oracle
     from paper_2212_11142_b200 import scenarios
@@ -147,7 +147,7 @@ def test_mixed_space_large_n_against_oracle(n):
                 lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
     gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
     sc.set_gp(gp)
-    assert sc.gp_kernel() == "tensor"  # n > 255: two column passes per tile
+    assert sc.gp_kernel() == "tensor"  # n > 255: several column passes per tile
     rows = sc.to_device(scenarios.sample_rows_uniform(lay, 1 << 18, rng))
     mean, var = (x.cpu().numpy() for x in sc.predict(rows))
     idx = rng.choice(len(mean), 1500, replace=False)
@@ -233,11 +233,57 @@ def test_matrix_ring_matches_resident_matrix(c3, monkeypatch):
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
 
 
-@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 255, 256, 257, 511, 512])
+@pytest.mark.parametrize("n,no_dmma", [(300, False), (500, False), (500, True), (1100, True)])
+def test_per_pass_planes_match_whole_width(n, no_dmma, monkeypatch):
+    """With several column passes the producers' planes (DMMA B operand / |y'|^2, or the FMA
+    producers' training values and Kendall masks) are held either whole-width or one pass's 256
+    columns at a time, reloaded each pass; both give bit-identical posteriors (BX_TC_DEBUG=16
+    forces per-pass planes; at n = 1100 the FMA producers need them anyway, and the oracle checks)."""
+    import oracle
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    if no_dmma:
+        monkeypatch.setenv("BX_TC_NO_DMMA", "1")
+    space = scenarios.build_space("C5", _bt.space)
+    rng = np.random.default_rng(n + 5)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    cfgs = lay.decode(scenarios.sample_rows_uniform(lay, n, rng))
+    y = np.array([scenarios.objective("C5", c) for c in cfgs])
+    hyp = Hyper(outputscale=1.1, noise_variance=1e-3,
+                lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
+    gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+    rows_h = scenarios.sample_rows_uniform(lay, 3 * 148 * 128 + 77, rng)
+    sc.close()
+    out = []
+    for pp in (False, True):
+        monkeypatch.setenv("BX_TC_DEBUG", "16" if pp else "0")
+        sc = Scorer()
+        sc.set_space(space)
+        sc.set_gp(gp)
+        assert sc.gp_kernel() == "tensor"
+        assert sc.distance_ksteps() == (0 if no_dmma else 5)
+        mean, var = sc.predict(sc.to_device(rows_h))
+        out.append((mean.cpu().numpy(), var.cpu().numpy()))
+        sc.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    idx = rng.choice(len(rows_h), 600, replace=False)
+    sample = lay.decode(rows_h[idx])
+    og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
+                         L=gp._cho[0], alpha=gp.alpha, y_mean=gp.y_mean, y_std=gp.y_std)
+    m0, v0 = oracle.gp.predict(og, sample)
+    np.testing.assert_allclose(out[1][0][idx], m0, rtol=1e-5, atol=1e-9 * np.abs(m0).max())
+    np.testing.assert_allclose(out[1][1][idx], v0, rtol=1e-5, atol=1e-9 * np.abs(v0).max())
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 255, 256, 257, 511, 512, 767, 768, 1023, 1024, 1500, 2047, 2048, 4095, 4096])
 def test_posterior_size_boundaries(n):
     """Training-set sizes at the tile / pass boundaries of the tensor-core posterior (32-column
-    slices, 16-row chunks, one vs two column passes at 256, the 511 limit) and the generic kernel
-    beyond, against the oracle on a numeric space (C3) and a mixed one (C5)."""
+    slices, 16-row chunks, one column pass per 256 columns, per-pass planes once the whole-width
+    ones outgrow shared memory, the 4095 limit) against the oracle on a numeric space (C3) and a
+    mixed one (C5); n = 4096 is refused by bx_set_gp (the generic kernel's shared memory is long
+    exceeded there) instead of failing at score time."""
     import oracle
     from paper_2212_11142_b200.device import Scorer
     from paper_2212_11142_b200.models import GPState, Hyper
@@ -255,8 +301,14 @@ def test_posterior_size_boundaries(n):
         hyp = Hyper(outputscale=1.3, noise_variance=1e-3,
                     lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
         gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+        if n >= 4096:
+            from paper_2212_11142_b200._native import NativeError
+            with pytest.raises(NativeError, match="beyond the posterior kernels"):
+                sc.set_gp(gp)
+            sc.close()
+            continue
         sc.set_gp(gp)
-        assert sc.gp_kernel() == ("tensor" if n <= 511 else "generic")
+        assert sc.gp_kernel() == "tensor"
         q = 3 * 128 + 17
         rows = sc.to_device(scenarios.sample_rows_uniform(lay, q, rng))
         mean, var = (x.cpu().numpy() for x in sc.predict(rows))

@@ -16,6 +16,10 @@ from paper_2212_11142_b200.models import GPState, Hyper  # noqa: E402
 
 
 def main(n=500, q=1 << 20):
+    import os
+    trace = os.environ.pop("LARGE_N_TRACE", None)  # file: CTA 0's role timeline of one predict
+    if trace:
+        os.environ["BX_TC_TRACE"] = ""
     space = scenarios.build_space("C5")
     rng = np.random.default_rng(5)
     sc = Scorer()
@@ -39,6 +43,11 @@ def main(n=500, q=1 << 20):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ms = float(np.median(ts))
+    if trace:
+        os.environ["BX_TC_TRACE"] = trace
+        sc.predict(rows)
+        torch.cuda.synchronize()
+        del os.environ["BX_TC_TRACE"]
     print(f"predict 2^20: {ms:.3f} ms  {q / ms * 1e3:,.0f} cand/s  (runs: {' '.join(f'{t:.2f}' for t in ts)})")
     sample = lay.decode(rows[:2000].cpu().numpy().view(np.uint32))
     og = oracle.OracleGP(space, gp.configs, hyp.outputscale, hyp.noise_variance, hyp.lengthscales,
