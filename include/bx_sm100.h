@@ -132,6 +132,9 @@ int bx_gp_kernel(bx_handle* h);
 /* Tensor-core posterior only: the DMMA k-steps of its distance product over the Euclidean
    embedding of W (0: FMA distances per parameter kind, or not the tensor-core kernel). */
 int bx_gp_distance_ksteps(bx_handle* h);
+/* ... and the embedding's coordinate count E (|x'|^2 + |y'|^2 rides in two extra k-rows when
+   E + 2 <= 4 k-steps, else it is added to the products). */
+int bx_gp_embedding_dims(bx_handle* h);
 
 /* ---- model state (once per BO iteration) ------------------------------------------------ */
 /* Space tables.  coord_lut / rank_lut are host arrays indexed by bx_param_desc offsets;
@@ -242,6 +245,13 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
 int bx_packed_row_words(bx_handle* h);
 int bx_pack_rows(bx_handle* h, const uint32_t* host_rows, int64_t q, uint32_t* host_packed);
 int bx_unpack_rows(bx_handle* h, const uint32_t* host_packed, int64_t q, uint32_t* host_rows);
+
+/* Host-side: n draws of numpy's Generator.permutation(m) (m <= 16) replayed from a PCG64 state -
+   state = {state_hi, state_lo, inc_hi, inc_lo}, has_uint32 / uinteger = the generator's 32-bit
+   buffer - written as packed rows (element at position i in nibble m-1-i, 0-based values); the
+   state is advanced exactly as the n Python calls advance it (space.py:330-331).  No device work. */
+int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n, int32_t m,
+                          uint64_t* packed);
 
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the

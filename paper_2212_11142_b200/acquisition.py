@@ -14,11 +14,13 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import sampling
 from .device import Candidate, Scorer, scorer
 
 N_CANDIDATES = 5000   # acquisition.py:23
 N_STARTS = 10         # acquisition.py:24
 MAX_CLIMB_STEPS = 50  # acquisition.py:25
+FAST_SAMPLER = True   # default samplers drawn straight into rows (sampling.py); False: the caller's
 
 
 class SpaceExhausted(Exception):
@@ -200,25 +202,39 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     """`optimize_acquisition` (acquisition.py:152-206) with every score, top-k, tracker reduction and
     neighbour set computed on the GPU."""
     Exhausted = _exhausted_type(space)
-    if sample_fn is None:
-        sample_fn = _default_sampler(space, cot)
-    raw = sample_fn(n_candidates, ctx.rng)
-    candidates = list(dict.fromkeys(raw))
-    if not candidates:
-        raise Exhausted("candidate sampler produced nothing")
     sc = scorer()
     lay = _prepare(ctx, sc, evaluated=True)
+    rows_h = None
+    if sample_fn is None and cot is None and FAST_SAMPLER and n_candidates >= 1 \
+            and sampling.is_reference_sampler(_sample_uniform_for(space)):
+        # the default samplers (acquisition.py:114-134) straight into rows, same RNG stream
+        if not space.constraints:
+            rows_h = sampling.uniform_rows(lay, n_candidates, ctx.rng)
+        else:
+            sc.set_constraints(space)
+            rows_h = sampling.rejection_rows(
+                lay, n_candidates, ctx.rng,
+                lambda b: sc.constraints_eval(sc.to_device(b)).cpu().numpy().astype(bool))
+        rows_h = sampling.unique_rows(rows_h)  # dict.fromkeys: first draws, in order
+    else:
+        if sample_fn is None:
+            sample_fn = _default_sampler(space, cot)
+        candidates = list(dict.fromkeys(sample_fn(n_candidates, ctx.rng)))
+        if candidates:
+            rows_h = lay.encode(candidates)
+    if rows_h is None or len(rows_h) == 0:
+        raise Exhausted("candidate sampler produced nothing")
     if cot is not None:
         sc.set_cot(cot)
     f_model = ctx.gp.objective_to_model(ctx.best_feasible_value)
-    rows = sc.to_device(lay.encode(candidates))
+    rows = sc.to_device(rows_h)
     many = local_search and n_starts > N.BX_MAX_K  # the fused top-k holds BX_MAX_K records
     summ, pool_vals, _ = sc.score(rows, f_model, ctx.eps_f, k=min(n_starts, N.BX_MAX_K),
-                                  want_values=many, rf_pairwise=len(candidates) == 1)
+                                  want_values=many, rf_pairwise=len(rows_h) == 1)
     if summ.n_finite == 0:  # acquisition.py:179-184
         if summ.best_prob is None:
             return _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted)
-        return candidates[summ.best_prob.index]
+        return lay.decode(rows_h[summ.best_prob.index])[0]
 
     best = summ.best
     if local_search:

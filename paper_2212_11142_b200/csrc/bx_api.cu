@@ -106,6 +106,7 @@ int bx_gp_kernel(bx_handle* h) {
 }
 
 int bx_gp_distance_ksteps(bx_handle* h) { return h && h->use_tc ? h->tc_ks : 0; }
+int bx_gp_embedding_dims(bx_handle* h) { return h && h->use_tc && h->tc_ks ? (int)h->tc_emb.size() : 0; }
 
 int bx_set_option(bx_handle* h, int32_t option, int32_t value) {
   if (!h) return BX_ERR_ARG;

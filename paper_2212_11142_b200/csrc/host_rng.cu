@@ -1,0 +1,83 @@
+// host_rng.cu — the candidate pool's permutation draws without a Python loop (host code).
+//
+// The reference's uniform sampler (space.py:312-332) draws each permutation parameter as n calls of
+// numpy's Generator.permutation(m): arange(m) shuffled in place by Fisher-Yates from the top,
+// j = random_interval(i) for i = m-1 .. 1 (numpy/random/_generator.pyx shuffle -> _shuffle_raw,
+// distributions.c random_interval: the smallest all-ones mask >= i, 32-bit draws rejected above i).
+// The 32-bit draws come from PCG64 (XSL-RR 128/64: step the 128-bit LCG, output rotr64(hi ^ lo,
+// hi >> 58)), each 64-bit output serving two draws, low half first, the high half buffered in the
+// generator's has_uint32 / uinteger state.  Replaying that stream here from the generator's state
+// gives the same permutations and the same final state as the Python loop, so the pool - and the
+// RNG stream the BO loop continues with - is the reference's.
+#include <cstdint>
+
+#include "bx_sm100.h"
+
+namespace {
+
+using u128 = unsigned __int128;
+
+struct Pcg64 {
+  u128 state, inc;
+  int has32;
+  uint32_t buf;
+
+  uint64_t next64() {
+    const u128 mult = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    state = state * mult + inc;
+    const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    const unsigned rot = (unsigned)(hi >> 58);
+    const uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64 - rot) & 63));
+  }
+  uint32_t next32() {
+    if (has32) {
+      has32 = 0;
+      return buf;
+    }
+    const uint64_t v = next64();
+    has32 = 1;
+    buf = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+  }
+  // random_interval(max) for max < 2^32
+  uint32_t interval(uint32_t max) {
+    if (max == 0) return 0;
+    uint32_t mask = max;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    uint32_t v;
+    while ((v = next32() & mask) > max) {
+    }
+    return v;
+  }
+};
+
+}  // namespace
+
+extern "C" int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n,
+                                     int32_t m, uint64_t* packed) {
+  if (!state || !has_uint32 || !uinteger || n < 0 || m < 1 || m > 16 || (n > 0 && !packed)) return BX_ERR_ARG;
+  Pcg64 g{((u128)state[0] << 64) | state[1], ((u128)state[2] << 64) | state[3], *has_uint32 != 0, *uinteger};
+  for (int64_t r = 0; r < n; ++r) {
+    uint8_t a[16];
+    for (int i = 0; i < m; ++i) a[i] = (uint8_t)i;
+    for (int i = m - 1; i >= 1; --i) {
+      const uint32_t j = g.interval((uint32_t)i);
+      const uint8_t t = a[i];
+      a[i] = a[j];
+      a[j] = t;
+    }
+    uint64_t x = 0;  // layout.pack_perm: element at position i (0-based value) in nibble m-1-i
+    for (int i = 0; i < m; ++i) x = (x << 4) | a[i];
+    packed[r] = x;
+  }
+  state[0] = (uint64_t)(g.state >> 64);
+  state[1] = (uint64_t)g.state;
+  *has_uint32 = g.has32;
+  *uinteger = g.buf;
+  return BX_OK;
+}

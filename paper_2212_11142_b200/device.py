@@ -233,6 +233,10 @@ class Scorer:
         """DMMA k-steps of the tensor-core posterior's embedding distance product (0: FMA)."""
         return int(self._lib.bx_gp_distance_ksteps(self.h))
 
+    def embedding_dims(self) -> int:
+        """Coordinates E of the Euclidean embedding the DMMA distances run over (0: FMA)."""
+        return int(self._lib.bx_gp_embedding_dims(self.h))
+
     def last_timing(self) -> dict:
         """CUDA-event durations (ms) of the forest / fused-score / merge kernels of the last
         score(..., timing=True) call."""

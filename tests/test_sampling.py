@@ -1,0 +1,93 @@
+"""The encoded-row candidate samplers (sampling.py) against the reference's own samplers: same rows
+in the same order and the same generator state afterwards (host code; the reference is shipped in
+oracle/_ref or read from /root/reference)."""
+import numpy as np
+import pytest
+
+from paper_2212_11142_b200 import sampling, scenarios
+from paper_2212_11142_b200.layout import SpaceLayout, pack_perm
+
+pytestmark = pytest.mark.reference
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from golden_io import ref as load_ref
+    return load_ref()
+
+
+def _same_state(a, b):
+    assert repr(a.bit_generator.state) == repr(b.bit_generator.state)
+    assert np.array_equal(a.integers(1 << 62, size=7), b.integers(1 << 62, size=7))  # and the stream on
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 7, 9, 16])
+@pytest.mark.parametrize("n,odd", [(0, False), (1, True), (5, False), (300, True), (300, False)])
+def test_permutations_replay_numpy(m, n, odd):
+    """bx_pcg64_permutations = n calls of Generator.permutation(m), with the 32-bit buffer either
+    empty or holding a half-used draw (odd)."""
+    for seed in (0, 7, 12345):
+        a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+        if odd:  # one bounded 32-bit draw leaves the high half buffered
+            a.integers(10), b.integers(10)
+        got = sampling.permutation_rows(a, n, m)
+        want = np.array([pack_perm(b.permutation(m) + 1, m) for _ in range(n)], dtype=np.uint64)
+        assert np.array_equal(got, want)
+        _same_state(a, b)
+
+
+def test_permutations_other_bit_generators():
+    """Non-PCG64 generators take the permutations from rng.permutation itself."""
+    a, b = np.random.Generator(np.random.Philox(3)), np.random.Generator(np.random.Philox(3))
+    got = sampling.permutation_rows(a, 50, 6)
+    want = np.array([pack_perm(b.permutation(6) + 1, 6) for _ in range(50)], dtype=np.uint64)
+    assert np.array_equal(got, want)
+    _same_state(a, b)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_uniform_rows_are_the_reference_pool(ref, name):
+    """uniform_rows = encode(sample_uniform(space, n, rng)) (space.py:312-332), state included."""
+    space = scenarios.build_space(name, ref.space)
+    lay = SpaceLayout(space)
+    for seed, n in ((1, 1), (2, 5000), (3, 777)):
+        a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+        got = sampling.uniform_rows(lay, n, a)
+        want = lay.encode(ref.space.sample_uniform(space, n, b))
+        assert np.array_equal(got, want)
+        _same_state(a, b)
+        assert lay.decode(got) == lay.decode(want)
+
+
+def test_unique_rows_is_dict_fromkeys(ref):
+    """First-occurrence de-duplication in draw order on a small discrete space full of repeats."""
+    space = ref.space.SearchSpace([ref.space.Parameter("a", "ordinal", values=(1, 2, 4)),
+                                   ref.space.Parameter("b", "categorical", values=("x", "y")),
+                                   ref.space.Parameter("p", "permutation", size=3)])
+    lay = SpaceLayout(space)
+    a, b = np.random.default_rng(9), np.random.default_rng(9)
+    got = sampling.unique_rows(sampling.uniform_rows(lay, 400, a))
+    want = list(dict.fromkeys(ref.space.sample_uniform(space, 400, b)))
+    assert lay.decode(got) == want
+    assert np.array_equal(got, lay.encode(want))
+
+
+def test_rejection_rows_follow_the_reference_front_end(ref):
+    """rejection_rows = the reference's rejection sampler (acquisition.py:122-134) on a space with
+    known constraints (feasibility evaluated on the host here)."""
+    from boxtune.constraints import eval_constraint
+    from boxtune.acquisition import _default_sampler
+    space = scenarios.build_space("C2", ref.space)
+    assert space.constraints
+    lay = SpaceLayout(space)
+
+    def feasible(rows):
+        return [all(eval_constraint(c, space.as_dict(cfg)) is True for c in space.constraints)
+                for cfg in lay.decode(rows)]
+
+    for seed, n in ((4, 300), (5, 1)):
+        a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+        got = sampling.rejection_rows(lay, n, a, feasible)
+        want = _default_sampler(space, None)(n, b)
+        assert lay.decode(got) == want
+        _same_state(a, b)
