@@ -252,6 +252,11 @@ int bx_unpack_rows(bx_handle* h, const uint32_t* host_packed, int64_t q, uint32_
    state is advanced exactly as the n Python calls advance it (space.py:330-331).  No device work. */
 int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n, int32_t m,
                           uint64_t* packed);
+/* ... and n draws of Generator.choice(pop, size=k, replace=False) (pop <= 10000: Floyd's algorithm
+   and a shuffle), k indices per draw into out[n][k] - the rf_fit feature subsets
+   (feasibility.py:119). */
+int bx_pcg64_choice(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n, int32_t pop, int32_t k,
+                    int32_t* out);
 
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the

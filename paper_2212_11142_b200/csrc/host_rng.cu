@@ -40,6 +40,22 @@ struct Pcg64 {
     buf = (uint32_t)(v >> 32);
     return (uint32_t)v;
   }
+  // bounded_lemire_uint32: uniform on [0, rng] (numpy's random_bounded_uint64 for rng < 2^32)
+  uint32_t lemire(uint32_t rng) {
+    if (rng == 0) return 0;  // no draw
+    if (rng == 0xFFFFFFFFu) return next32();
+    const uint32_t excl = rng + 1;
+    uint64_t m = (uint64_t)next32() * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+      const uint32_t threshold = (0xFFFFFFFFu - rng) % excl;
+      while (left < threshold) {
+        m = (uint64_t)next32() * excl;
+        left = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
   // random_interval(max) for max < 2^32
   uint32_t interval(uint32_t max) {
     if (max == 0) return 0;
@@ -56,12 +72,51 @@ struct Pcg64 {
   }
 };
 
+Pcg64 load(const uint64_t* state, const int32_t* has_uint32, const uint32_t* uinteger) {
+  return Pcg64{((u128)state[0] << 64) | state[1], ((u128)state[2] << 64) | state[3], *has_uint32 != 0, *uinteger};
+}
+void store(const Pcg64& g, uint64_t* state, int32_t* has_uint32, uint32_t* uinteger) {
+  state[0] = (uint64_t)(g.state >> 64);
+  state[1] = (uint64_t)g.state;
+  *has_uint32 = g.has32;
+  *uinteger = g.buf;
+}
+
 }  // namespace
+
+// n draws of Generator.choice(pop, size=k, replace=False) for pop <= 10000 (the rf_fit feature
+// subsets, feasibility.py:119): Floyd's algorithm (j = pop-k .. pop-1: v uniform on [0, j], taken
+// unless already chosen, else j) followed by _shuffle_int of the k chosen (Fisher-Yates from the top
+// with v uniform on [0, i] by Lemire's method) (numpy/random/_generator.pyx choice, non-tail branch).
+extern "C" int bx_pcg64_choice(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n, int32_t pop,
+                               int32_t k, int32_t* out) {
+  if (!state || !has_uint32 || !uinteger || n < 0 || pop < 1 || pop > 10000 || k < 0 || k > pop ||
+      (n > 0 && k > 0 && !out))
+    return BX_ERR_ARG;
+  Pcg64 g = load(state, has_uint32, uinteger);
+  for (int64_t r = 0; r < n; ++r) {
+    int32_t* idx = out + r * k;
+    for (int32_t j = pop - k; j < pop; ++j) {
+      const int32_t v = (int32_t)g.lemire((uint32_t)j);
+      bool seen = false;
+      for (int32_t t = 0; t < j - (pop - k); ++t) seen |= idx[t] == v;
+      idx[j - (pop - k)] = seen ? j : v;
+    }
+    for (int32_t i = k - 1; i >= 1; --i) {  // _shuffle_int: bounded Lemire draws, not random_interval
+      const uint32_t s = g.lemire((uint32_t)i);
+      const int32_t t = idx[i];
+      idx[i] = idx[s];
+      idx[s] = t;
+    }
+  }
+  store(g, state, has_uint32, uinteger);
+  return BX_OK;
+}
 
 extern "C" int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n,
                                      int32_t m, uint64_t* packed) {
   if (!state || !has_uint32 || !uinteger || n < 0 || m < 1 || m > 16 || (n > 0 && !packed)) return BX_ERR_ARG;
-  Pcg64 g{((u128)state[0] << 64) | state[1], ((u128)state[2] << 64) | state[3], *has_uint32 != 0, *uinteger};
+  Pcg64 g = load(state, has_uint32, uinteger);
   for (int64_t r = 0; r < n; ++r) {
     uint8_t a[16];
     for (int i = 0; i < m; ++i) a[i] = (uint8_t)i;
@@ -75,9 +130,6 @@ extern "C" int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint3
     for (int i = 0; i < m; ++i) x = (x << 4) | a[i];
     packed[r] = x;
   }
-  state[0] = (uint64_t)(g.state >> 64);
-  state[1] = (uint64_t)g.state;
-  *has_uint32 = g.has32;
-  *uinteger = g.buf;
+  store(g, state, has_uint32, uinteger);
   return BX_OK;
 }

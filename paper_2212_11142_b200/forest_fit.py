@@ -20,6 +20,7 @@ import numpy as np
 
 from . import _native as N
 from .device import scorer
+from .sampling import choice_rows
 
 _DEFAULT = object()
 DRAWS = 48  # feature subsets drawn per tree up front (M200-sized forests use ~30)
@@ -53,7 +54,9 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
     k = max(1, round(math.sqrt(F)))
     gens = [np.random.default_rng(int(s)) for s in seeds]
     boot = np.stack([g.integers(0, n, size=n) for g in gens]).astype(np.int32)
-    draws = [[g.choice(F, size=k, replace=False) for _ in range(DRAWS)] for g in gens]
+    # the feature subsets in the order the tree's generator draws them (replayed from its PCG64
+    # state by bx_pcg64_choice: no per-draw Python call)
+    draws = [choice_rows(g, DRAWS, F, k) for g in gens]
     max_nodes = 2 * n + 2
     sc = scorer()
     lib = sc._lib
@@ -67,7 +70,7 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
         feats = np.zeros((T, max_draws, k), dtype=np.int32)
         nd = np.zeros(T, dtype=np.int32)
         for i, t in enumerate(todo):
-            feats[i, :len(draws[t])] = np.asarray(draws[t], dtype=np.int32)
+            feats[i, :len(draws[t])] = draws[t]
             nd[i] = len(draws[t])
         out_f = np.empty((T, max_nodes), np.int32)
         out_t = np.empty((T, max_nodes), np.float64)
@@ -83,7 +86,7 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
         again = []
         for i, t in enumerate(todo):
             if out_s[i] == 1:  # more feature subsets: continue the tree's own generator
-                draws[t].extend(gens[t].choice(F, size=k, replace=False) for _ in range(DRAWS))
+                draws[t] = np.concatenate([draws[t], choice_rows(gens[t], DRAWS, F, k)])
                 again.append(t)
             elif out_s[i] != 0:
                 raise N.NativeError(N.BX_ERR_UNSUPPORTED, f"rf_fit: tree {t} exceeded {max_nodes} nodes")

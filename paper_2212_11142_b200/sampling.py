@@ -39,20 +39,8 @@ def is_reference_sampler(fn) -> bool:
 def permutation_rows(rng, n: int, m: int) -> np.ndarray:
     """[rng.permutation(m) for _ in range(n)] packed as layout rows (uint64, 0-based elements)."""
     out = np.empty(n, dtype=np.uint64)
-    st = rng.bit_generator.state
-    if st.get("bit_generator") == "PCG64" and n > 0:
-        s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
-        state = np.array([s >> 64, s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
-        has32 = C.c_int32(int(st["has_uint32"]))
-        uint = C.c_uint32(int(st["uinteger"]))
-        code = N.lib().bx_pcg64_permutations(state.ctypes.data_as(C.c_void_p), C.byref(has32), C.byref(uint), n, m,
-                                             out.ctypes.data_as(C.c_void_p))
-        if code != N.BX_OK:
-            raise N.NativeError(code, "bx_pcg64_permutations")
-        st["state"]["state"] = (int(state[0]) << 64) | int(state[1])
-        st["has_uint32"] = int(has32.value)
-        st["uinteger"] = int(uint.value)
-        rng.bit_generator.state = st
+    if rng.bit_generator.state.get("bit_generator") == "PCG64" and n > 0:
+        _pcg64_call(rng, N.lib().bx_pcg64_permutations, n, m, out.ctypes.data_as(C.c_void_p))
         return out
     for r in range(n):
         x = 0
@@ -115,3 +103,30 @@ def unique_rows(rows: np.ndarray) -> np.ndarray:
         return rows
     first.sort()
     return rows[first]
+
+
+def _pcg64_call(rng, fn, *args):
+    """Run a bx_pcg64_* replay on rng's PCG64 state and store the advanced state back."""
+    st = rng.bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    state = np.array([s >> 64, s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
+    has32 = C.c_int32(int(st["has_uint32"]))
+    uint = C.c_uint32(int(st["uinteger"]))
+    code = fn(state.ctypes.data_as(C.c_void_p), C.byref(has32), C.byref(uint), *args)
+    if code != N.BX_OK:
+        raise N.NativeError(code, fn.__name__)
+    st["state"]["state"] = (int(state[0]) << 64) | int(state[1])
+    st["has_uint32"] = int(has32.value)
+    st["uinteger"] = int(uint.value)
+    rng.bit_generator.state = st
+
+
+def choice_rows(rng, n: int, pop: int, k: int) -> np.ndarray:
+    """[rng.choice(pop, size=k, replace=False) for _ in range(n)] as an (n, k) int32 array."""
+    out = np.empty((n, k), dtype=np.int32)
+    if rng.bit_generator.state.get("bit_generator") == "PCG64" and pop <= 10000 and n > 0 and k > 0:
+        _pcg64_call(rng, N.lib().bx_pcg64_choice, n, pop, k, out.ctypes.data_as(C.c_void_p))
+        return out
+    for r in range(n):
+        out[r] = rng.choice(pop, size=k, replace=False)
+    return out

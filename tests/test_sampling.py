@@ -91,3 +91,17 @@ def test_rejection_rows_follow_the_reference_front_end(ref):
         want = _default_sampler(space, None)(n, b)
         assert lay.decode(got) == want
         _same_state(a, b)
+
+
+@pytest.mark.parametrize("pop,k", [(1, 1), (2, 1), (5, 2), (21, 5), (100, 10), (100, 100), (10000, 3), (30, 0)])
+def test_choice_replays_numpy(pop, k):
+    """bx_pcg64_choice = n calls of Generator.choice(pop, size=k, replace=False) (the rf_fit feature
+    subsets), generator state included."""
+    for seed, odd in ((0, False), (3, True), (99, False)):
+        a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+        if odd:
+            a.integers(10), b.integers(10)
+        got = sampling.choice_rows(a, 200, pop, k)
+        want = np.array([b.choice(pop, size=k, replace=False) for _ in range(200)], dtype=np.int32).reshape(200, k)
+        assert np.array_equal(got, want)
+        _same_state(a, b)
