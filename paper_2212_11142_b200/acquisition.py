@@ -205,7 +205,11 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     sc = scorer()
     lay = _prepare(ctx, sc, evaluated=True)
     rows_h = None
-    if sample_fn is None and cot is None and FAST_SAMPLER and n_candidates >= 1 \
+    if sample_fn is None and cot is not None and FAST_SAMPLER and n_candidates >= 1 \
+            and sampling.is_reference_cot(cot):
+        # leaf-uniform chain-of-trees pool (acquisition.py:115-116) straight into rows
+        rows_h = sampling.unique_rows(sampling.cot_rows(lay, cot, n_candidates, ctx.rng))
+    elif sample_fn is None and cot is None and FAST_SAMPLER and n_candidates >= 1 \
             and sampling.is_reference_sampler(_sample_uniform_for(space)):
         # the default samplers (acquisition.py:114-134) straight into rows, same RNG stream
         if not space.constraints:
@@ -219,9 +223,16 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     else:
         if sample_fn is None:
             sample_fn = _default_sampler(space, cot)
-        candidates = list(dict.fromkeys(sample_fn(n_candidates, ctx.rng)))
-        if candidates:
-            rows_h = lay.encode(candidates)
+        raw = sample_fn(n_candidates, ctx.rng)
+        hit = _POOL_CACHE.get("k")
+        if hit is not None and hit[0] is raw and hit[1] is lay and hit[2] == len(raw):
+            rows_h = hit[3]  # the engine's enumerated small feasible set: the same list every iteration
+        else:
+            candidates = list(dict.fromkeys(raw))
+            if candidates:
+                rows_h = lay.encode(candidates)
+                if isinstance(raw, list):
+                    _POOL_CACHE["k"] = (raw, lay, len(raw), rows_h)
     if rows_h is None or len(rows_h) == 0:
         raise Exhausted("candidate sampler produced nothing")
     if cot is not None:
@@ -288,6 +299,9 @@ def _chunks(it, n):
             buf = []
     if buf:
         yield buf
+
+
+_POOL_CACHE: dict = {}
 
 
 def _exhaustion_fallback(ctx, space, cot, sc, f_model, Exhausted):

@@ -172,29 +172,39 @@ class SpaceLayout:
         rows = np.zeros((q, self.row_words), dtype=np.uint32)
         if q == 0:
             return rows
-        as64 = rows.view(np.uint64) if self.row_words % 2 == 0 else None
-        for k, (p, slot) in enumerate(zip(self._params, self.slots)):
-            col = [cfg[k] for cfg in configs]
-            if p.kind == "real":
-                v = np.asarray(col, dtype=np.float64)
-                v = np.where(v == 0.0, 0.0, v)  # -0.0 == 0.0 in tuple equality
-                c = numeric_coords(p, v, self.use_transforms)
-                as64[:, slot.word // 2] = v.view(np.uint64)
-                as64[:, slot.word // 2 + 1] = np.asarray(c, np.float64).view(np.uint64)
-            elif p.kind == "permutation":
-                m = p.size
-                arr = np.asarray(col, dtype=np.int64).reshape(q, m)
-                packed = np.zeros(q, dtype=np.uint64)
-                for i in range(m):
-                    packed = (packed << np.uint64(4)) | (arr[:, i] - 1).astype(np.uint64)
-                as64[:, slot.word // 2] = packed
-            else:
-                idx = slot.index
-                try:
-                    rows[:, slot.word] = [idx[v] for v in col]
-                except KeyError as exc:
-                    raise ValueError(f"{p.name}: value {exc.args[0]!r} outside domain") from None
+        for k in range(self.n_params):
+            self.encode_param(rows, k, [cfg[k] for cfg in configs])
         return rows
+
+    def encode_param(self, rows: np.ndarray, k: int, col) -> None:
+        """Write parameter k's values `col` (one per row) into its words of `rows`."""
+        p, slot = self._params[k], self.slots[k]
+        q = rows.shape[0]
+        as64 = rows.view(np.uint64)
+        if p.kind == "real":
+            v = np.asarray(col, dtype=np.float64)
+            v = np.where(v == 0.0, 0.0, v)  # -0.0 == 0.0 in tuple equality
+            c = numeric_coords(p, v, self.use_transforms)
+            as64[:, slot.word // 2] = v.view(np.uint64)
+            as64[:, slot.word // 2 + 1] = np.asarray(c, np.float64).view(np.uint64)
+        elif p.kind == "permutation":
+            m = p.size
+            arr = np.asarray(col, dtype=np.int64).reshape(q, m)
+            packed = np.zeros(q, dtype=np.uint64)
+            for i in range(m):
+                packed = (packed << np.uint64(4)) | (arr[:, i] - 1).astype(np.uint64)
+            as64[:, slot.word // 2] = packed
+        else:
+            idx = slot.index
+            try:
+                rows[:, slot.word] = [idx[v] for v in col]
+            except KeyError as exc:
+                raise ValueError(f"{p.name}: value {exc.args[0]!r} outside domain") from None
+
+    def param_words(self, k: int) -> slice:
+        """The row words parameter k occupies."""
+        p, w = self._params[k], self.slots[k].word
+        return slice(w, w + (4 if p.kind == "real" else 2 if p.kind == "permutation" else 1))
 
     def decode(self, rows) -> list:
         """(q, row_words) rows -> configuration tuples with the reference's value types."""

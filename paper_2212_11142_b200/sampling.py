@@ -12,6 +12,9 @@ in the row format directly:
 * permutations: bx_pcg64_permutations replays numpy's Generator.permutation from the PCG64 state
   (Fisher-Yates from the top with random_interval draws on the buffered 32-bit stream) and leaves
   the generator in the state the n Python calls would;
+* the chain-of-trees leaf-uniform sampler (constraints.py:471-518, the default pool when known
+  constraints exist): per dependency group the same `rng.integers(leaf_count, size=n)` draw, then a
+  gather from the group's encoded leaf rows; real / permutation singletons as above;
 * `dict.fromkeys` de-duplication becomes first-occurrence unique rows (a row determines its
   configuration and vice versa).
 
@@ -34,6 +37,14 @@ _M64 = (1 << 64) - 1
 def is_reference_sampler(fn) -> bool:
     """True when `fn` is the stock `sample_uniform` of a boxtune-style space module."""
     return getattr(fn, "__name__", "") == "sample_uniform" and getattr(fn, "__module__", "").endswith(".space")
+
+
+def is_reference_cot(cot) -> bool:
+    """True for the stock ChainOfTrees (its leaf-uniform sampler is the one cot_rows replays)."""
+    t = type(cot)
+    return (t.__name__ == "ChainOfTrees" and t.__module__.endswith(".constraints")
+            and getattr(t.sample_leaf_uniform, "__module__", "") == t.__module__
+            and hasattr(cot, "groups") and hasattr(cot, "_ensure_leaf_arrays"))
 
 
 def permutation_rows(rng, n: int, m: int) -> np.ndarray:
@@ -130,3 +141,55 @@ def choice_rows(rng, n: int, pop: int, k: int) -> np.ndarray:
     for r in range(n):
         out[r] = rng.choice(pop, size=k, replace=False)
     return out
+
+
+def _leaf_table(lay, cot, g):
+    """The encoded rows (only the group's words set) of a tree group's leaf paths, cached."""
+    cache = lay.__dict__.setdefault("_cot_tables", {})
+    key = (id(cot), id(g))
+    hit = cache.get(key)
+    if hit is not None and hit[0] is g.leaf_values:
+        return hit[1]
+    paths = g.leaf_values
+    table = np.zeros((len(paths), lay.row_words), dtype=np.uint32)
+    for j, k in enumerate(g.indices):
+        lay.encode_param(table, k, [path[j] for path in paths])
+    cache[key] = (paths, table)
+    return table
+
+
+def cot_rows(lay, cot, n: int, rng) -> np.ndarray:
+    """lay.encode(cot.sample_leaf_uniform(n, rng)) with the same RNG consumption
+    (constraints.py:471-518, the leaf-uniform mode): per group in order - a tree with leaf arrays
+    draws `rng.integers(leaf_count, size=n)` and gathers its encoded leaf rows; a real singleton
+    draws n scalar uniforms (one vector call consumes the stream identically); a permutation
+    singleton n permutations (replayed); a tree too large for leaf arrays runs the reference's own
+    per-draw descent and its output is encoded."""
+    space = lay.space
+    if n < 1 or cot.count() == 0:
+        return lay.encode(cot.sample_leaf_uniform(n, rng))  # the reference raises its own error
+    rows = np.zeros((n, lay.row_words), dtype=np.uint32)
+    as64 = rows.view(np.uint64)
+    for g in cot.groups:
+        if g.kind != "tree":
+            k = g.indices[0]
+            p = space.parameters[k]
+            if p.kind == "permutation":
+                as64[:, lay.slots[k].word // 2] = permutation_rows(rng, n, p.size)
+            elif p.kind == "real":
+                lay.encode_param(rows, k, rng.uniform(p.lo, p.hi, size=n))
+            else:
+                lay.encode_param(rows, k, [p.sample(rng) for _ in range(n)])
+            continue
+        cot._ensure_leaf_arrays(g)
+        if g.leaf_values is not None:
+            idx = rng.integers(g.root.leaf_count, size=n)
+            table = _leaf_table(lay, cot, g)
+            for k in g.indices:
+                ws = lay.param_words(k)
+                rows[:, ws] = table[idx, ws]
+        else:
+            out = cot._sample_group(g, n, rng, False)
+            for j, k in enumerate(g.indices):
+                lay.encode_param(rows, k, [v[j] for v in out])
+    return rows

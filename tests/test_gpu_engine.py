@@ -289,3 +289,20 @@ def test_device_rf_fit_equals_reference(case, draws, monkeypatch):
     for name in ("feature", "threshold", "left", "right", "value", "roots"):
         a, b = getattr(got, name), getattr(want, name)
         assert a.dtype == b.dtype and np.array_equal(a, b), name
+
+
+def test_patched_loop_on_chain_of_trees_pool_is_the_reference_history():
+    """C3 (known constraints, 10 parameters, chain of trees larger than the 5000-candidate pool,
+    hidden resource rule): the leaf-uniform pool is drawn straight into rows (sampling.cot_rows)
+    and the whole run still equals the reference's."""
+    bt = ref()
+    from paper_2212_11142_b200 import scenarios
+    space = scenarios.build_space("C3", bt.space)
+    assert bt.build_cot(space).count() > 5000
+    bench = bt.Benchmark("c3-cot", space, lambda c: scenarios.objective("C3", c),
+                         hidden_rule=lambda c: scenarios.hidden_ok("C3", c), default_budget=24)
+    want = _run(bt, bench, 24, 4)
+    got = _patched(bt, lambda: _run(bt, bench, 24, 4), whole_path=True)
+    assert _first_divergence(got.history, want.history) is None, _first_divergence(got.history,
+                                                                                   want.history)
+    assert sum(r.phase == "bo" for r in got.history) > 0

@@ -105,3 +105,37 @@ def test_choice_replays_numpy(pop, k):
         want = np.array([b.choice(pop, size=k, replace=False) for _ in range(200)], dtype=np.int32).reshape(200, k)
         assert np.array_equal(got, want)
         _same_state(a, b)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_cot_rows_are_the_reference_leaf_uniform_pool(ref, name):
+    """cot_rows = encode(cot.sample_leaf_uniform(n, rng)) (constraints.py:471-518): tree groups,
+    permutation singletons, generator state included."""
+    space = scenarios.build_space(name, ref.space)
+    cot = ref.build_cot(space)
+    lay = SpaceLayout(space)
+    for seed, n in ((1, 1), (2, 5000), (3, 333)):
+        a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+        got = sampling.cot_rows(lay, cot, n, a)
+        want = cot.sample_leaf_uniform(n, b)
+        assert lay.decode(got) == want
+        assert np.array_equal(got, lay.encode(want))
+        _same_state(a, b)
+
+
+def test_cot_rows_real_and_permutation_singletons(ref):
+    """A chain of trees with a real and a permutation singleton next to a constrained pair."""
+    S = ref.space
+    space = S.SearchSpace([S.Parameter("a", "ordinal", values=(1, 2, 4, 8)),
+                           S.Parameter("x", "real", lo=0.5, hi=3.0),
+                           S.Parameter("b", "integer", lo=1, hi=6),
+                           S.Parameter("p", "permutation", size=4)],
+                          constraints=["a * b <= 12"])
+    cot = ref.build_cot(space)
+    assert sorted(g.kind for g in cot.groups) == ["permutation", "real", "tree"]
+    lay = SpaceLayout(space)
+    a, b = np.random.default_rng(8), np.random.default_rng(8)
+    got = sampling.cot_rows(lay, cot, 2000, a)
+    want = cot.sample_leaf_uniform(2000, b)
+    assert lay.decode(got) == want
+    _same_state(a, b)
