@@ -650,7 +650,9 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
         const int mode = last == 0 ? 0 : (p == 0 ? 1 : (p < last ? 3 : 2));
         double* park = mode ? ta.part + (size_t)blockIdx.x * (kN * nch - kSlots * 32) * kM + r : nullptr;  // + (row - 256) * kM
         const int buf = chunk_no & 1;
-        mb_wait(&acc_full[buf], (ph_f >> buf) & 1u);  // the MMA / epilogue chain paces the kernel: spin
+        // parked, not spinning: measured the same at M200 / C3 and leaves the issue slots to the
+        // producers sharing the sub-partition
+        mb_wait_sleep(&acc_full[buf], (ph_f >> buf) & 1u);
         ph_f ^= 1u << buf;
         tc_fence_after();
         if (lane == 0 && warp == 4) TC_TRACE(2, 1, c);
@@ -998,8 +1000,11 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       if (pt == 0) TC_TRACE(0, 6, t);
     }
   }
+  // the copy / decoder warps (1-3) never touch tensor memory: they leave as soon as their work is
+  // done; the TMEM users meet on a named barrier before warp 0 frees it
+  if (warp >= 1 && warp <= 3) return;
   tc_fence_before();
-  __syncthreads();
+  asm volatile("bar.sync 5, %0;" ::"r"((int)blockDim.x - 96) : "memory");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
