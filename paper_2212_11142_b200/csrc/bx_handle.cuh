@@ -9,7 +9,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <functional>
 #include <string>
 #include <vector>
 #include <unordered_map>
@@ -325,5 +324,4 @@ int check_gp(bx_handle* h) {
 // shared across the translation units (defined in bx_score.cu / bx_model.cu)
 int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base, double f_model, double eps_f,
                int32_t k, int32_t flags, double* values, double* probs_out, Partial* partials, int* n_partials,
-               cudaStream_t s, int timing, bool track_prob = false, cudaEvent_t rows_ready = nullptr,
-               const std::function<int()>& after_posterior_launch = nullptr);
+               cudaStream_t s, int timing, bool track_prob = false, cudaEvent_t rows_ready = nullptr);

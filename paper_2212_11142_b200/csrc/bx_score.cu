@@ -155,16 +155,7 @@ static SummaryArgs last_summary_args(bx_handle* h, const uint32_t* rows, int64_t
 int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base,
                       double f_model, double eps_f, int32_t k, int32_t flags, double* values,
                       double* probs_out, Partial* partials, int* n_partials, cudaStream_t s,
-                      int timing, bool track_prob, cudaEvent_t rows_ready,
-                      const std::function<int()>& after_posterior_launch) {
-  // streaming pools: the host-to-device copies are enqueued right after the posterior launch (the
-  // kernel waits on their ready flags), so the GPU starts while the host is still issuing them
-  bool issued = !after_posterior_launch;
-  auto issue = [&]() -> int {
-    if (issued) return BX_OK;
-    issued = true;
-    return after_posterior_launch();
-  };
+                      int timing, bool track_prob, cudaEvent_t rows_ready) {
   ScoreArgs a{};
   a.space = space_dev(h);
   a.gp = gp_dev(h);
@@ -194,10 +185,7 @@ int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base
                          qs_summary_available(h->forest);
     h->rf_after_gp = rf_summ;
     // a stand-alone forest kernel before the posterior reads the rows: a streaming pool must be in
-    if (forest && !rf_summ) {
-      if (int e = issue()) return e;
-      if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
-    }
+    if (rows_ready && forest && !rf_summ) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
     if (timing == 1 && !rf_summ) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
     if (forest && !rf_summ)
       BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
@@ -209,7 +197,6 @@ int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base
     f.var_out = h->d_ei.as<double>() + q;
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[2], s));
     BX_CUDA(h, launch_posterior(h, f, s));
-    if (int e = issue()) return e;
     if (timing) BX_CUDA(h, cudaEventRecord(h->ev_t[3], s));
     SummaryArgs m = last_summary_args(h, rows, q, index_base, eps_f, k, values, probs_out, partials);
     m.track_prob = track_prob ? 1 : 0;
@@ -226,8 +213,6 @@ int score_impl(bx_handle* h, const uint32_t* rows, int64_t q, int64_t index_base
     BX_CUDA(h, launch_summary(m, h->sm_count, s, n_partials));
     return BX_OK;
   }
-  if (int e = issue()) return e;
-  if (rows_ready) BX_CUDA(h, cudaStreamWaitEvent(s, rows_ready, 0));
   if (timing == 1) BX_CUDA(h, cudaEventRecord(h->ev_t[0], s));
   if (forest) {
     BX_CUDA(h, launch_rf(a.space, h->forest, rows, q, (flags & BX_SCORE_RF_PAIRWISE) ? 1 : 0,
@@ -327,8 +312,34 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
   uint32_t* dst = packed ? h->d_packed.as<uint32_t>() : pool;  // where the host rows land
   Partial* parts = h->d_partials.as<Partial>();
   const bool forest = h->has_forest && h->forest.has_trees;
-  if (h->use_tc && (!forest || qs_summary_available(h->forest)) && !(flags & BX_SCORE_RF_PAIRWISE) &&
-      (!packed || h->pack.pw <= 16)) {
+  // Packed rows in pinned (hence mapped) host memory: the posterior's row prefetcher bulk-copies
+  // each tile's packed rows straight from host memory over the bus - no copy engine, no ready
+  // flags, nothing that depends on the copy running concurrently with the kernel (profilers and
+  // CUDA_LAUNCH_BLOCKING serialise the two).  BX_TC_DEBUG bit 64: always the copy path.
+  const uint32_t* mapped = nullptr;
+  if (packed && h->use_tc && !(h->tc_debug & 64)) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host_rows) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+      mapped = static_cast<const uint32_t*>(at.devicePointer);
+    cudaGetLastError();  // pageable memory: clear the attribute query's error, take the copy path
+  }
+  if (mapped && (!forest || qs_summary_available(h->forest)) && !(flags & BX_SCORE_RF_PAIRWISE) &&
+      h->pack.pw <= 16) {
+    for (int pass = 0; pass < 2; ++pass) {  // pass 2 (probability tracker) only if every value is -inf
+      int np = 0;
+      h->stream_packed = pass == 0 ? mapped : nullptr;  // pass 2 reads the pool the decoders unpacked
+      r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags, nullptr, nullptr, parts, &np, s, false,
+                     pass == 1);
+      h->stream_packed = nullptr;
+      if (r) return r;
+      BX_CUDA(h, launch_summary_merge(parts, np, space_dev(h), k, nullptr, 0,
+                                      h->d_summary.as<bx_score_summary>(), s));
+      BX_CUDA(h, cudaMemcpyAsync(summary, h->d_summary.p, sizeof(bx_score_summary), cudaMemcpyDeviceToHost, s));
+      BX_CUDA(h, cudaStreamSynchronize(s));
+      if (summary->n_finite != 0) break;
+    }
+  } else if (h->use_tc && (!forest || qs_summary_available(h->forest)) && !(flags & BX_SCORE_RF_PAIRWISE) &&
+             (!packed || h->pack.pw <= 16)) {
     // Streaming: the whole pool is copied in 2^16-row chunks on the copy stream, each followed by a
     // 4-byte ready flag written by the copy engine; one posterior launch consumes tiles as their
     // chunk lands (the row prefetcher waits on the flag; packed rows are unpacked by its decoders,
@@ -349,24 +360,20 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     BX_CUDA(h, cudaMemsetAsync(ready, 0, (size_t)n_chunks * 4, s));
     BX_CUDA(h, cudaEventRecord(h->ev_done, s));
     BX_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_done, 0));
-    auto copies = [&]() -> int {  // issued by score_impl right after the posterior launch
-      for (int64_t c = 0; c < n_chunks; ++c) {
-        const int64_t off = c << shift, len = std::min<int64_t>((int64_t)1 << shift, q - off);
-        BX_CUDA(h, cudaMemcpyAsync(dst + (size_t)off * HW, host_rows + (size_t)off * HW, (size_t)len * HW * 4,
-                                   cudaMemcpyHostToDevice, h->copy_stream));
-        BX_CUDA(h, cudaMemcpyAsync(ready + c, h->h_ones + c, 4, cudaMemcpyHostToDevice, h->copy_stream));
-      }
-      BX_CUDA(h, cudaEventRecord(h->ev_copy, h->copy_stream));
-      return BX_OK;
-    };
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      const int64_t off = c << shift, len = std::min<int64_t>((int64_t)1 << shift, q - off);
+      BX_CUDA(h, cudaMemcpyAsync(dst + (size_t)off * HW, host_rows + (size_t)off * HW, (size_t)len * HW * 4,
+                                 cudaMemcpyHostToDevice, h->copy_stream));
+      BX_CUDA(h, cudaMemcpyAsync(ready + c, h->h_ones + c, 4, cudaMemcpyHostToDevice, h->copy_stream));
+    }
+    BX_CUDA(h, cudaEventRecord(h->ev_copy, h->copy_stream));
     for (int pass = 0; pass < 2; ++pass) {  // pass 2 (probability tracker) only if every value is -inf
       int np = 0;
       h->stream_ready = pass == 0 ? ready : nullptr;
       h->stream_shift = shift;
       h->stream_packed = (pass == 0 && packed) ? dst : nullptr;  // pass 2 reads the unpacked pool
       r = score_impl(h, pool, q, index_base, f_model, eps_f, k, flags, nullptr, nullptr, parts, &np, s, false,
-                     pass == 1, pass == 0 ? h->ev_copy : nullptr,
-                     pass == 0 ? std::function<int()>(copies) : std::function<int()>());
+                     pass == 1, pass == 0 ? h->ev_copy : nullptr);
       h->stream_ready = nullptr;
       h->stream_packed = nullptr;
       if (r) return r;
