@@ -229,10 +229,12 @@ int bx_score(bx_handle* h, const uint32_t* dev_rows, int64_t q, int64_t index_ba
              double eps_f, int32_t k, int32_t flags, double* dev_values, double* dev_probs,
              bx_score_summary* host_summary, void* stream);
 
-/* Same as bx_score but the pool is a HOST buffer (pinned or pageable): the call copies it to
-   the device in chunks overlapped with scoring.  This is the end-to-end entry point.  With
-   BX_SCORE_PACKED the host rows are in the packed wire format (bx_pack_rows), which the
-   tensor-core posterior unpacks on the fly: 2-4x fewer bytes over PCIe for typical spaces. */
+/* Same as bx_score but the pool is a HOST buffer (pinned or pageable).  This is the end-to-end
+   entry point.  With BX_SCORE_PACKED the host rows are in the packed wire format (bx_pack_rows),
+   which the tensor-core posterior unpacks on the fly (2-4x fewer bytes over PCIe for typical
+   spaces); a packed pool in pinned memory is read by the posterior straight from host memory
+   (zero-copy), otherwise the call copies the pool in chunks that the posterior consumes as they
+   land. */
 int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t index_base,
                   double f_model, double eps_f, int32_t k, int32_t flags,
                   bx_score_summary* host_summary, void* stream);
