@@ -3,12 +3,12 @@ rank 2).
 
 The reference refines the N_TOP = 8 best coarse hyperparameter settings one after another, each
 scipy L-BFGS-B iteration calling `_lml_core` for ONE setting (~200 calls per fit).  Here the
-restarts run concurrently - one scipy optimizer per thread - and their objective requests are
-gathered: whenever every still-running optimizer is waiting for a value, one `bx_lml_core` call
-evaluates all of their settings at once (the whole-GPU pipeline with the settings side by side on
-grid.y, so a setting's value and gradient are the ones a single call gives).  An optimizer's
-iterates depend only on its own objective values, so the result equals running the restarts one
-after another with the GPU `_lml_core` (`install(lml=True)`), whatever the thread timing.
+restarts step in lockstep (`lbfgsb.minimize_lockstep`: scipy's own L-BFGS-B routine, one state
+machine per restart, no threads): whenever every still-running restart waits for a value, one
+`bx_lml_core` call evaluates all of their settings at once (the whole-GPU pipeline with the
+settings side by side on grid.y, so a setting's value and gradient are the ones a single call
+gives).  A restart's iterates depend only on its own objective values, so the result equals running
+the restarts one after another with the GPU `_lml_core` (`install(lml=True)`).
 
 Everything else is the reference's own code, looked up in the caller's package: the coarse stage
 (`_search_boxes`, the RNG draw, `_batched_coarse_lml` - the GPU one when installed - and
@@ -21,12 +21,12 @@ from __future__ import annotations
 
 import importlib
 import math
-import threading
 
 import numpy as np
 import torch
 
 from .device import scorer
+from .lbfgsb import minimize_lockstep
 
 _DEFAULT = object()
 
@@ -36,57 +36,10 @@ def _surrogate(space):
     return importlib.import_module(pkg + ".surrogate")
 
 
-class _Batcher:
-    """Gathers objective requests of concurrent optimizers; evaluates a batch when every active
-    optimizer is waiting."""
-
-    def __init__(self, n_active: int, evaluate):
-        self.cv = threading.Condition()
-        self.pending: dict = {}
-        self.results: dict = {}
-        self.active = n_active
-        self.evaluate = evaluate
-        self.calls = 0
-        self.error = None
-
-    def _maybe_run(self):
-        if self.pending and len(self.pending) == self.active:
-            ids = sorted(self.pending)
-            try:
-                out = self.evaluate(np.stack([self.pending[i] for i in ids]))
-                for i, r in zip(ids, out):
-                    self.results[i] = r
-            except BaseException as exc:  # surface it in every waiting thread
-                self.error = exc
-                for i in ids:
-                    self.results[i] = None
-            self.calls += 1
-            self.pending.clear()
-            self.cv.notify_all()
-
-    def request(self, tid: int, theta: np.ndarray):
-        with self.cv:
-            self.pending[tid] = np.array(theta, dtype=np.float64)
-            self._maybe_run()
-            while tid not in self.results:
-                self.cv.wait()
-            r = self.results.pop(tid)
-        if r is None:
-            raise RuntimeError("batched objective failed") from self.error
-        return r
-
-    def done(self):
-        with self.cv:
-            self.active -= 1
-            self._maybe_run()
-
-
 def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_transforms: bool = True,
            advanced: bool = True):
     """Drop-in for `gp_fit` (surrogate.py:478-541): same arguments, RNG consumption, errors and
     returned `GPModel` (with `map_value` and `start_values`)."""
-    from scipy.optimize import minimize
-
     S = _surrogate(space)
     if prior is _DEFAULT:
         prior = S.LengthscalePrior()
@@ -128,28 +81,10 @@ def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_tra
                 value, grad, ok = value.cpu().numpy(), grad.cpu().numpy(), ok.cpu().numpy()
             return [(np.inf, np.zeros(batch.shape[1])) if not k else (-v, -g) for v, g, k in zip(value, grad, ok)]
 
-        batcher = _Batcher(len(starts), evaluate)
-        bounds = list(zip(lo, hi))
-
-        def run(tid, idx):
-            try:
-                refined[idx] = minimize(lambda th: batcher.request(tid, th), thetas[idx], jac=True,
-                                        method="L-BFGS-B", bounds=bounds,
-                                        options={"maxiter": S.MAX_OPT_ITERS, "ftol": S.OPT_TOL})
-            except BaseException as exc:
-                refined[idx] = exc
-            finally:
-                batcher.done()
-
-        threads = [threading.Thread(target=run, args=(t, idx), daemon=True) for t, idx in enumerate(starts)]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        for r in refined.values():
-            if isinstance(r, BaseException):
-                raise r
-        gp_fit.last_batched_calls = batcher.calls
+        results, calls = minimize_lockstep(evaluate, [thetas[i] for i in starts], list(zip(lo, hi)),
+                                           S.MAX_OPT_ITERS, S.OPT_TOL)  # surrogate.py:524-526
+        refined = dict(zip(starts, results))
+        gp_fit.last_batched_calls = calls
 
     best_theta, best_value = None, -np.inf
     for idx in order:  # surrogate.py:518-531, candidate order
@@ -157,9 +92,9 @@ def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_tra
             continue
         theta, value = thetas[idx], scores[idx]
         if advanced:
-            res = refined[int(idx)]
-            if np.isfinite(res.fun) and -res.fun > value:
-                theta, value = res.x, -res.fun
+            x, fun = refined[int(idx)]
+            if np.isfinite(fun) and -fun > value:
+                theta, value = x, -fun
         if value > best_value:
             best_theta, best_value = theta, value
     if best_theta is None:
