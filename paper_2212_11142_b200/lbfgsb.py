@@ -14,8 +14,13 @@ one batched GPU call per step and no Python threads are involved.
 from __future__ import annotations
 
 import numpy as np
-from scipy.optimize import _lbfgsb
-from scipy.optimize._lbfgsb_py import HAS_ILP64
+
+try:  # scipy's compiled routine and the integer width it was built with (scipy >= 1.15 layout)
+    from scipy.optimize import _lbfgsb
+    from scipy.optimize._lbfgsb_py import HAS_ILP64
+except ImportError:  # another scipy layout: the restarts run through minimize() one by one
+    _lbfgsb = None
+    HAS_ILP64 = False
 
 
 class _Machine:
@@ -90,6 +95,12 @@ def minimize_lockstep(evaluate, x0s, bounds, maxiter: int, ftol: float, gtol: fl
     """Minimise from every start in x0s; evaluate(X (k, n)) -> [(f, g)] for k points at a time.
     Returns [(x, fun)] per start (what `minimize(...).x / .fun` would give) and the number of
     evaluate calls."""
+    if _lbfgsb is None:
+        from scipy.optimize import minimize
+        res = [minimize(lambda th: evaluate(th[None, :])[0], x0, jac=True, method="L-BFGS-B", bounds=bounds,
+                        options={"maxiter": maxiter, "ftol": ftol, "gtol": gtol, "maxcor": maxcor, "maxfun": maxfun,
+                                 "maxls": maxls}) for x0 in x0s]
+        return [(r.x, r.fun) for r in res], sum(r.nfev for r in res)
     lo = np.asarray([b[0] for b in bounds], dtype=np.float64)
     hi = np.asarray([b[1] for b in bounds], dtype=np.float64)
     ms = [_Machine(np.asarray(x, dtype=np.float64).ravel(), lo, hi, maxcor, ftol, gtol, maxiter, maxfun, maxls)

@@ -47,12 +47,48 @@ def is_reference_cot(cot) -> bool:
             and hasattr(cot, "groups") and hasattr(cot, "_ensure_leaf_arrays"))
 
 
+_REPLAY_OK = None
+
+
+def replay_ok() -> bool:
+    """Whether bx_pcg64_* reproduce this NumPy's Generator.permutation / choice (checked once on
+    scratch generators; a NumPy whose algorithms differ gets the Python calls instead)."""
+    global _REPLAY_OK
+    if _REPLAY_OK is None:
+        try:
+            ok = True
+            for seed, m, pop, k in ((11, 5, 21, 5), (12, 9, 64, 8)):
+                a, b = np.random.default_rng(seed), np.random.default_rng(seed)
+                a.integers(7), b.integers(7)  # a half-used 32-bit buffer
+                got = _replay_permutations(a, 64, m)
+                want = [sum(int(v) << (4 * (m - 1 - i)) for i, v in enumerate(b.permutation(m))) for _ in range(64)]
+                ok &= [int(x) for x in got] == want
+                got = _replay_choice(a, 64, pop, k)
+                ok &= all(np.array_equal(got[r], b.choice(pop, size=k, replace=False)) for r in range(64))
+                ok &= repr(a.bit_generator.state) == repr(b.bit_generator.state)
+            _REPLAY_OK = bool(ok)
+        except Exception:
+            _REPLAY_OK = False
+    return _REPLAY_OK
+
+
+def _replay_permutations(rng, n, m):
+    out = np.empty(n, dtype=np.uint64)
+    _pcg64_call(rng, N.lib().bx_pcg64_permutations, n, m, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def _replay_choice(rng, n, pop, k):
+    out = np.empty((n, k), dtype=np.int32)
+    _pcg64_call(rng, N.lib().bx_pcg64_choice, n, pop, k, out.ctypes.data_as(C.c_void_p))
+    return out
+
+
 def permutation_rows(rng, n: int, m: int) -> np.ndarray:
     """[rng.permutation(m) for _ in range(n)] packed as layout rows (uint64, 0-based elements)."""
     out = np.empty(n, dtype=np.uint64)
-    if rng.bit_generator.state.get("bit_generator") == "PCG64" and n > 0:
-        _pcg64_call(rng, N.lib().bx_pcg64_permutations, n, m, out.ctypes.data_as(C.c_void_p))
-        return out
+    if rng.bit_generator.state.get("bit_generator") == "PCG64" and n > 0 and replay_ok():
+        return _replay_permutations(rng, n, m)
     for r in range(n):
         x = 0
         for v in rng.permutation(m):
@@ -135,9 +171,8 @@ def _pcg64_call(rng, fn, *args):
 def choice_rows(rng, n: int, pop: int, k: int) -> np.ndarray:
     """[rng.choice(pop, size=k, replace=False) for _ in range(n)] as an (n, k) int32 array."""
     out = np.empty((n, k), dtype=np.int32)
-    if rng.bit_generator.state.get("bit_generator") == "PCG64" and pop <= 10000 and n > 0 and k > 0:
-        _pcg64_call(rng, N.lib().bx_pcg64_choice, n, pop, k, out.ctypes.data_as(C.c_void_p))
-        return out
+    if rng.bit_generator.state.get("bit_generator") == "PCG64" and pop <= 10000 and n > 0 and k > 0 and replay_ok():
+        return _replay_choice(rng, n, pop, k)
     for r in range(n):
         out[r] = rng.choice(pop, size=k, replace=False)
     return out

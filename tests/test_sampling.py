@@ -139,3 +139,8 @@ def test_cot_rows_real_and_permutation_singletons(ref):
     want = cot.sample_leaf_uniform(2000, b)
     assert lay.decode(got) == want
     _same_state(a, b)
+
+
+def test_replay_self_check_passes_on_this_numpy():
+    """The one-time check that guards the PCG64 replays holds for the NumPy in this image."""
+    assert sampling.replay_ok()
