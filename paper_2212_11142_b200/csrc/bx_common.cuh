@@ -534,7 +534,9 @@ struct TcArgs {
   int32_t n_coord;            // coord_lut entries
   double exp2tab256[256];     // 2^(j/256), correctly rounded (host long double)
   int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
-                              // 4 epilogue TMEM reads without the arithmetic, 8 matrix ring (not resident)
+                              // 4 epilogue TMEM reads without the arithmetic, 8 matrix ring (not resident),
+                              // 16 per-pass planes (n > 255); bx_score_host: 64 the copy path for
+                              // packed pinned pools instead of zero-copy
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
   // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
   // is in device memory (written by the copy stream after the chunk), null = all rows present
