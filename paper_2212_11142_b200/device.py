@@ -246,8 +246,9 @@ class Scorer:
 
     def score_host(self, rows: np.ndarray | torch.Tensor, f_model: float, eps_f: float = 0.0,
                    k: int = 10, index_base: int = 0, packed: bool = False) -> Summary:
-        """bx_score_host: the pool stays in (pinned) host memory; copies overlap the scoring.
-        packed=True: the rows are in the packed wire format (pack())."""
+        """bx_score_host: the pool stays in host memory.  packed=True: the rows are in the packed
+        wire format (pack()); from pinned memory the posterior reads them zero-copy, otherwise
+        chunked copies overlap the scoring."""
         q = rows.shape[0]
         s = N.ScoreSummary()
         self._check(self._lib.bx_score_host(self.h, _ptr(rows), q, index_base, float(f_model),

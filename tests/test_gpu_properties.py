@@ -165,11 +165,13 @@ def test_mixed_space_large_n_against_oracle(n):
                                              ("M200", 131075, None, False), ("mixed_metrics", 70003, None, False),
                                              ("M200", 70001, None, True)])
 def test_streaming_host_pool_matches_device_pool(case, q, eps, walk, monkeypatch):
-    """bx_score_host streams the pool (chunked copies + ready flags consumed by one posterior
-    launch), encoded or in the packed wire format (unpacked by the posterior's decoders); its
-    summary equals bx_score's on the same rows — ragged sizes, a forest-less case, the FMA
-    producers (mixed_metrics), the all -inf fallback (eps_f > 1: probability tracker) and the
-    non-streaming path (node-walk forest before the posterior: one copy + a device unpack kernel)."""
+    """bx_score_host on a host pool: encoded (chunked copies + ready flags consumed by one
+    posterior launch), packed in pinned memory (read zero-copy by the posterior's row prefetcher)
+    and packed in pageable memory (the chunked copies); the packed forms are unpacked by the
+    posterior's decoders.  Every summary equals bx_score's on the same rows — ragged sizes, a
+    forest-less case, the FMA producers (mixed_metrics), the all -inf fallback (eps_f > 1:
+    probability tracker) and the non-streaming path (node-walk forest before the posterior: one
+    copy + a device unpack kernel)."""
     from paper_2212_11142_b200.device import Scorer
     if walk:
         monkeypatch.setenv("BX_FOREST_WALK", "1")
@@ -184,9 +186,11 @@ def test_streaming_host_pool_matches_device_pool(case, q, eps, walk, monkeypatch
     rows_h = scenarios.sample_rows_uniform(sc.layout, q, np.random.default_rng(q))
     pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory()
     x, _, _ = sc.score(sc.to_device(rows_h), f, eps_f, k=10)
-    packed = torch.from_numpy(sc.pack(rows_h).view(np.int32)).pin_memory()
+    packed_h = sc.pack(rows_h)
+    packed = torch.from_numpy(packed_h.view(np.int32)).pin_memory()
     for y in (sc.score_host(pinned.numpy().view(np.uint32), f, eps_f, k=10),
-              sc.score_host(packed.numpy().view(np.uint32), f, eps_f, k=10, packed=True)):
+              sc.score_host(packed.numpy().view(np.uint32), f, eps_f, k=10, packed=True),
+              sc.score_host(packed_h, f, eps_f, k=10, packed=True)):
         assert (x.n_scored, x.n_finite) == (y.n_scored, y.n_finite)
         assert [c.index for c in x.top] == [c.index for c in y.top]
         assert [c.value for c in x.top] == [c.value for c in y.top]
