@@ -37,6 +37,7 @@ bx_handle* bx_create(int device) {
   if (const char* dbg = getenv("BX_TC_DEBUG")) h->tc_debug = atoi(dbg);
   h->tc_trace = getenv("BX_TC_TRACE") != nullptr;
   if (const char* ln = getenv("BX_LML_NARROW")) h->lml_narrow = ln[0] == '1';
+  if (const char* sm = getenv("BX_LML_SMALL_MAX")) h->lml_small_max = atoi(sm);
   if (const char* nd = getenv("BX_TC_NO_DMMA")) h->tc_no_dmma = nd[0] == '1';
   const char* fw = getenv("BX_FOREST_WALK");
   h->no_qs_forest = fw && fw[0] == '1';

@@ -625,6 +625,11 @@ cudaError_t launch_lml_grad(const double* sq, int n, int D, const double* z, con
                             double* out_value, double* out_grad, int* out_ok, double* scratch,
                             cudaStream_t s);
 size_t lml_grad_scratch_doubles(int n, int c);
+// _lml_core (+ gradient) with everything in one CTA's shared memory, one CTA per setting (small n)
+bool lml_small_supported(int n);
+cudaError_t launch_lml_small(const double* sq, int n, int D, const double* z, const double* prm, int c,
+                             double prior_k, double prior_rate, int use_prior, int want_grad, double* out_value,
+                             double* out_grad, int* out_ok, cudaStream_t s);
 // _lml_core for c settings, each over the whole GPU, side by side on grid.y (lml_wide.cu), n <= 512
 size_t lml_wide_scratch_doubles(int n, int D, int c);
 bool lml_wide_supported(int n);

@@ -116,6 +116,7 @@ struct bx_handle {
   bool tc_no_dmma = false;                 // BX_TC_NO_DMMA=1: FMA distances
   bool tc_trace = false;                   // BX_TC_TRACE set (role timeline dump)
   bool lml_narrow = false;                 // BX_LML_NARROW=1: _lml_core always one CTA per setting
+  int lml_small_max = 40;                  // _lml_core in one CTA's shared memory up to this n (BX_LML_SMALL_MAX)
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale, d_tc_part;

@@ -10,7 +10,9 @@ int bx_lml_batched(bx_handle* h, const double* sq, int32_t n, int32_t D, const d
   if (n < 1 || D < 1 || D > BX_MAX_PARAMS || c < 0)
     return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
   cudaSetDevice(h->device);
-  if (lml_wide_supported(n) && !h->lml_narrow) {
+  // small n: one CTA per setting with the packed triangle in shared memory beats the blocked
+  // whole-GPU pipeline (measured crossover ~ n = 100)
+  if (lml_wide_supported(n) && !h->lml_narrow && n > 96) {
     // blocked Cholesky batched over the settings, in groups that keep the factors under 1 GiB
     const int np = (n + 31) / 32 * 32;
     const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)c, (1ull << 30) / ((size_t)np * np * 8)));
@@ -39,9 +41,16 @@ int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const doub
     return fail(h, BX_ERR_ARG, "bad lml shape n=%d D=%d c=%d", n, D, c);
   if (want_grad && !grad) return fail(h, BX_ERR_ARG, "want_grad needs a gradient buffer");
   cudaSetDevice(h->device);
-  // the whole-GPU pipeline, settings side by side on grid.y (a setting's arithmetic does not depend
-  // on the batch: the batched L-BFGS-B restarts get the values a single call gives), in groups that
-  // keep the scratch under 1 GiB; BX_OPT_LML_NARROW: one CTA per setting
+  // small n (<= 40, the measured crossover; the kernel takes up to 232): one CTA per setting with
+  // everything in its shared memory (lml_small_kernel); larger n: the whole-GPU pipeline, settings side by side on grid.y, in groups that keep the scratch
+  // under 1 GiB.  Either way a setting's arithmetic does not depend on the batch (the batched
+  // L-BFGS-B restarts get the values a single call gives).  BX_OPT_LML_NARROW: the one-CTA-per-
+  // setting kernel with global scratch (any n; the cross-check of the other two).
+  if (lml_small_supported(n) && n <= h->lml_small_max && !h->lml_narrow) {
+    BX_CUDA(h, launch_lml_small(sq, n, D, z, params, c, prior_shape, prior_rate, use_prior, want_grad, value,
+                                want_grad ? grad : nullptr, ok, (cudaStream_t)stream));
+    return BX_OK;
+  }
   if (lml_wide_supported(n) && !h->lml_narrow) {
     const size_t per = lml_wide_scratch_doubles(n, D, 1) * sizeof(double);
     const int group = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(c, 1), (1ull << 30) / per));

@@ -356,6 +356,182 @@ __global__ void __launch_bounds__(kGradThreads) lml_grad_kernel(const double* sq
   }
 }
 
+// ---- _lml_core for small n: one CTA per setting, everything in shared memory ---------------------
+// The lower triangle of Ky (packed, row-major: (i, k) at i (i + 1) / 2 + k) is factored in place
+// (right-looking, a warp per row of the trailing update), u = L^-1 z and alpha = L^-T u are one
+// warp's forward / backward sweeps, L is inverted in place (X = L^-1, columns from the last: X_ij =
+// -(sum_{k=j+1..i} X_ik L_kj) / L_jj with column j of L saved first), and the gradient sums take
+// K^-1_ab = sum_{k >= a} X_ka X_kb per lower entry (a thread per entry).  Same formulas and
+// operation order within each entry as lml_grad_kernel (surrogate.py:356-400); a setting's
+// arithmetic does not depend on the batch.  n <= kSmallLmlMaxN (the triangle plus three vectors fit
+// in 227 KB); launch latency and block-wide steps instead of global-memory round trips.
+constexpr int kSmallThreads = 512;
+constexpr int kSmallLmlMaxN = 232;
+
+__global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* sq, int n, int D, const double* z,
+                                                                  const double* prm, double prior_k, double prior_rate,
+                                                                  int use_prior, int want_grad, double* out_value,
+                                                                  double* out_grad, int* out_ok) {
+  extern __shared__ __align__(16) double sm[];
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kSmallThreads / 32;
+  const size_t tri = (size_t)n * (n + 1) / 2, nn = (size_t)n * n;
+  double* Lp = sm;            // [tri]
+  double* u = Lp + tri;       // [n]
+  double* al = u + n;         // [n]
+  double* col = al + n;       // [n] column j of L while it is inverted
+  __shared__ double inv_l2[BX_MAX_PARAMS];
+  __shared__ double red[kWarps];
+  __shared__ int failed;
+  const double* p = prm + (size_t)c * (2 + D);
+  const double sigma = p[0];
+  const double noise = fmax(p[1], 1e-6);  // NOISE_FLOOR
+  for (int k = tid; k < D; k += blockDim.x) inv_l2[k] = 1.0 / (p[2 + k] * p[2 + k]);
+  if (tid == 0) failed = 0;
+  __syncthreads();
+  // Ky lower triangle (surrogate.py:365-371); a warp per row: contiguous packed entries
+  for (int i = warp; i < n; i += kWarps) {
+    const size_t r0 = tri_idx(i, 0);
+    for (int k2 = lane; k2 <= i; k2 += 32) {
+      const size_t t = (size_t)i * n + k2;
+      double W = 0.0;
+      for (int k = 0; k < D; ++k) W = fma(sq[(size_t)k * nn + t], inv_l2[k], W);
+      const double d = sqrt(fmax(W, 0.0));
+      const double E = exp(-kSqrt5 * d);
+      const double kv = sigma * ((1.0 + kSqrt5 * d + (5.0 / 3.0) * W) * E);
+      Lp[r0 + k2] = (i == k2) ? kv + noise + 1e-9 : kv;
+    }
+  }
+  __syncthreads();
+  // right-looking Cholesky
+  for (int j = 0; j < n; ++j) {
+    const double piv = Lp[tri_idx(j, j)];
+    if (!(piv > 0.0)) {  // potrf: a_jj <= 0 or NaN (uniform: every thread reads the same value)
+      if (tid == 0) failed = 1;
+      break;
+    }
+    const double ljj = sqrt(piv);
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) col[i] = Lp[tri_idx(i, j)] / ljj;
+    __syncthreads();
+    if (tid == 0) Lp[tri_idx(j, j)] = ljj;
+    for (int i = j + 1 + warp; i < n; i += kWarps) {
+      const size_t r0 = tri_idx(i, 0);
+      const double ci = col[i];
+      if (lane == 0) Lp[r0 + j] = ci;
+      for (int k = j + 1 + lane; k <= i; k += 32) Lp[r0 + k] -= ci * col[k];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (failed) {
+    if (tid == 0) {
+      out_ok[c] = 0;
+      out_value[c] = -INFINITY;
+    }
+    if (want_grad)
+      for (int k = tid; k < 2 + D; k += blockDim.x) out_grad[(size_t)c * (2 + D) + k] = 0.0;
+    return;
+  }
+  // u = L^-1 z and alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374): warp 0
+  if (warp == 0) {
+    for (int i = 0; i < n; ++i) {
+      const size_t r0 = tri_idx(i, 0);
+      double s = 0.0;
+      for (int k = lane; k < i; k += 32) s = fma(Lp[r0 + k], u[k], s);
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) u[i] = (z[i] - s) / Lp[r0 + i];
+      __syncwarp();
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1 + lane; k < n; k += 32) s = fma(Lp[tri_idx(k, i)], al[k], s);
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) al[i] = (u[i] - s) / Lp[tri_idx(i, i)];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double za = 0.0, ld = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    za = fma(z[i], al[i], za);
+    ld += log(Lp[tri_idx(i, i)]);
+  }
+  za = block_sum(za, red);
+  ld = block_sum(ld, red);
+  double value = -0.5 * za - ld - 0.5 * n * log(2.0 * 3.14159265358979323846);
+  if (use_prior) {  // Gamma(k, rate) log density per lengthscale (surrogate.py:380-383)
+    double sl = 0.0, sll = 0.0;
+    for (int k = 0; k < D; ++k) {
+      sl += p[2 + k];
+      sll += log(p[2 + k]);
+    }
+    value += D * (prior_k * log(prior_rate) - lgamma(prior_k)) + (prior_k - 1.0) * sll - prior_rate * sl;
+  }
+  if (tid == 0) {
+    out_ok[c] = 1;
+    out_value[c] = value;
+  }
+  if (!want_grad) return;
+  // X = L^-1 in place, last column first
+  for (int j = n - 1; j >= 0; --j) {
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) col[i] = Lp[tri_idx(i, j)];
+    __syncthreads();
+    const double xjj = 1.0 / Lp[tri_idx(j, j)];
+    for (int i = j + 1 + warp; i < n; i += kWarps) {
+      const size_t r0 = tri_idx(i, 0);
+      double s = 0.0;
+      for (int k = j + 1 + lane; k <= i; k += 32) s = fma(Lp[r0 + k], col[k], s);
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) Lp[r0 + j] = -s * xjj;
+    }
+    __syncthreads();
+    if (tid == 0) Lp[tri_idx(j, j)] = xjj;
+  }
+  __syncthreads();
+  // M = alpha alpha^T - X^T X; gradient sums over the full matrix (symmetric: off-diagonal lower
+  // entries counted twice) (surrogate.py:386-399)
+  double g0 = 0.0, g1 = 0.0;
+  double gl[BX_MAX_PARAMS];
+  for (int k = 0; k < D; ++k) gl[k] = 0.0;
+  for (size_t t = tid; t < tri; t += blockDim.x) {
+    int a = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while (tri_idx(a + 1, 0) <= t) ++a;
+    while (tri_idx(a, 0) > t) --a;
+    const int b = (int)(t - tri_idx(a, 0));  // a >= b
+    double kinv = 0.0;
+    for (int k = a; k < n; ++k) kinv = fma(Lp[tri_idx(k, a)], Lp[tri_idx(k, b)], kinv);
+    const double M = al[a] * al[b] - kinv;
+    const double w = a == b ? 1.0 : 2.0;
+    const size_t e = (size_t)a * n + b;
+    double W = 0.0;
+    for (int k = 0; k < D; ++k) W = fma(sq[(size_t)k * nn + e], inv_l2[k], W);
+    const double d = sqrt(fmax(W, 0.0));
+    const double E = exp(-kSqrt5 * d);
+    const double kv = sigma * ((1.0 + kSqrt5 * d + (5.0 / 3.0) * W) * E);
+    g0 = fma(w * M, kv, g0);
+    if (a == b) g1 += M;
+    const double MG = w * M * ((1.0 + kSqrt5 * d) * E);
+    for (int k = 0; k < D; ++k) gl[k] = fma(MG, sq[(size_t)k * nn + e], gl[k]);
+  }
+  g0 = block_sum(g0, red);
+  g1 = block_sum(g1, red);
+  double* g = out_grad + (size_t)c * (2 + D);
+  if (tid == 0) {
+    g[0] = 0.5 * g0;
+    g[1] = 0.5 * noise * g1;
+  }
+  const double scale = (5.0 / 6.0) * sigma;
+  for (int k = 0; k < D; ++k) {
+    const double s = block_sum(gl[k], red);
+    if (tid == 0) {
+      const double l = p[2 + k];
+      double gk = (scale / (l * l)) * s;
+      if (use_prior) gk += (prior_k - 1.0) - prior_rate * l;
+      g[2 + k] = gk;
+    }
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
   if (b > 148 * 16) b = 148 * 16;
@@ -376,6 +552,21 @@ cudaError_t launch_lml_grad(const double* sq, int n, int D, const double* z, con
   if (c <= 0) return cudaSuccess;
   lml_grad_kernel<<<c, kGradThreads, 0, s>>>(sq, n, D, z, prm, prior_k, prior_rate, use_prior,
                                               want_grad, out_value, out_grad, out_ok, scratch);
+  return cudaGetLastError();
+}
+
+bool lml_small_supported(int n) { return n >= 1 && n <= kSmallLmlMaxN; }
+
+cudaError_t launch_lml_small(const double* sq, int n, int D, const double* z, const double* prm, int c,
+                             double prior_k, double prior_rate, int use_prior, int want_grad, double* out_value,
+                             double* out_grad, int* out_ok, cudaStream_t s) {
+  if (c <= 0) return cudaSuccess;
+  if (!lml_small_supported(n)) return cudaErrorInvalidValue;
+  const size_t bytes = ((size_t)n * (n + 1) / 2 + 3 * (size_t)n) * sizeof(double);
+  cudaError_t e = set_smem(lml_small_kernel, (int)bytes);
+  if (e != cudaSuccess) return e;
+  lml_small_kernel<<<c, kSmallThreads, bytes, s>>>(sq, n, D, z, prm, prior_k, prior_rate, use_prior, want_grad,
+                                                   out_value, out_grad, out_ok);
   return cudaGetLastError();
 }
 

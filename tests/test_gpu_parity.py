@@ -294,11 +294,12 @@ def test_embedding_distances_match_fma_distances(case, monkeypatch):
     close(v1, v0, rtol=1e-7)
 
 
-@pytest.mark.parametrize("n", [64, 300, 500])
+@pytest.mark.parametrize("n", [7, 40, 64, 200, 300, 500])
 def test_lml_wide_paths_large_n(n, monkeypatch):
-    """The whole-GPU _lml_core (one setting over every SM) and the batched blocked coarse LML at
-    n up to 500 (BASELINE config 5) against the oracle, and against the one-CTA-per-setting kernels
-    (BX_LML_NARROW=1)."""
+    """_lml_core with its gradient - the shared-memory kernel (n <= 40) or the whole-GPU pipeline
+    (one setting over every SM) - and the coarse LML (one CTA per setting up to n = 96, else the
+    batched blocked pipeline) at n up to 500 (BASELINE config 5) against the oracle, and against
+    the one-CTA-per-setting global-memory kernels (BX_LML_NARROW=1)."""
     from paper_2212_11142_b200 import acquisition as A
     from paper_2212_11142_b200.device import Scorer
 
@@ -352,3 +353,30 @@ def test_lml_core_batched_equals_single_calls():
         assert int(ok1.item()) == int(ok[i].item())
         if int(ok1.item()):
             assert v1.item() == v[i].item() and torch.equal(g1[0], g[i])
+
+
+@pytest.mark.parametrize("n", [100, 232])
+def test_lml_small_kernel_up_to_its_shared_memory_limit(n, monkeypatch):
+    """The one-CTA shared-memory _lml_core (packed triangle factored and inverted in place) at sizes
+    beyond its default range (BX_LML_SMALL_MAX), up to the largest triangle that fits: value and
+    gradient against the oracle and equal to the whole-GPU pipeline's to FP64 rounding."""
+    from paper_2212_11142_b200 import acquisition as A
+    from paper_2212_11142_b200.device import Scorer
+
+    rng = np.random.default_rng(n + 1)
+    D = 10
+    X = rng.uniform(0, 1, (n, D))
+    sq = np.stack([(X[:, k, None] - X[None, :, k]) ** 2 for k in range(D)])
+    z = rng.standard_normal(n)
+    args = (sq, z, 0.9, 1e-4, rng.uniform(0.3, 2.0, D))
+    v, g = A.lml_core(*args, want_grad=True)  # default: the whole-GPU pipeline at this n
+    monkeypatch.setenv("BX_LML_SMALL_MAX", "232")
+    sc = Scorer()
+    monkeypatch.setattr(A, "scorer", lambda: sc)
+    v1, g1 = A.lml_core(*args, want_grad=True)
+    sc.close()
+    v0, g0 = oracle.lml_core(*args, want_grad=True, prior=None)
+    assert v1 == pytest.approx(v0, rel=1e-9, abs=1e-7)
+    np.testing.assert_allclose(g1, g0, rtol=1e-7, atol=1e-7 * np.abs(g0).max())
+    assert v1 == pytest.approx(v, rel=1e-10, abs=1e-8)
+    np.testing.assert_allclose(g1, g, rtol=1e-8, atol=1e-8 * np.abs(g).max())

@@ -1,5 +1,6 @@
-"""gp_fit at small n (the engine's early iterations): the reference's vs hyperfit.gp_fit wall time,
-batched objective calls and the time spent inside them.  python tools/fit_small_n.py"""
+"""gp_fit: the reference's vs hyperfit.gp_fit wall time, batched objective calls and the time spent
+inside them.  python tools/fit_small_n.py [case] [--lml]  (--lml: the GPU coarse LML stage too,
+as install(lml=True) routes it; BASELINE configs[3] is case C4)"""
 import sys
 import time
 from pathlib import Path
@@ -14,13 +15,16 @@ from golden_io import ref  # noqa: E402
 from paper_2212_11142_b200 import hyperfit, scenarios  # noqa: E402
 
 
-def main():
+def main(case="C5", lml=False):
     bt = ref()
-    space = scenarios.build_space("C5", bt.space)
+    space = scenarios.build_space(case, bt.space)
+    if lml:
+        from paper_2212_11142_b200.patch import install
+        install(bt, whole_path=False, lml=True, fit=False, rf=False)
     for n in (10, 20, 40, 100, 200):
         rng = np.random.default_rng(n)
         cfgs = list(dict.fromkeys(bt.space.sample_uniform(space, n + 20, rng)))[:n]
-        y = np.array([scenarios.objective("C5", c) for c in cfgs])
+        y = np.array([scenarios.objective(case, c) for c in cfgs])
         t = time.perf_counter()
         bt.surrogate.gp_fit(space, cfgs, y, np.random.default_rng(1))
         t_ref = time.perf_counter() - t
@@ -51,9 +55,10 @@ def main():
             t_gpu = time.perf_counter() - t
         finally:
             hyperfit.scorer = orig
-        print(f"n {n:4d}: reference {t_ref * 1e3:7.1f} ms, hyperfit {t_gpu * 1e3:7.1f} ms "
+        print(f"{case} n {n:4d}: reference {t_ref * 1e3:7.1f} ms, hyperfit {t_gpu * 1e3:7.1f} ms "
               f"({hyperfit.gp_fit.last_batched_calls} batched calls, {spent[0] * 1e3:.1f} ms in lml_core)")
 
 
 if __name__ == "__main__":
-    main()
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(args[0] if args else "C5", "--lml" in sys.argv)
