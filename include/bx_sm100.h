@@ -129,6 +129,15 @@ enum { BX_GP_GENERIC = 0, BX_GP_DMMA = 1, BX_GP_TENSOR = 2 };
 enum bx_option { BX_OPT_LML_NARROW = 1 };
 int bx_set_option(bx_handle* h, int32_t option, int32_t value);
 int bx_gp_kernel(bx_handle* h);
+/* GPModel.__init__ (surrogate.py:286-303) on the device: the Gram of the n training rows
+   (dev_train_rows, encoded) under (outputscale, noise_variance, lengthscales[n_params]) with the
+   noise floor and jitter on its diagonal, its Cholesky factor and alpha = K^-1 z for the
+   standardised targets host_z[n].  Writes host_L (n x n, row-major, lower, zeros above) and
+   host_alpha (n); BX_ERR_NOT_PD when the factorisation fails (numpy's LinAlgError).  n <= 512.
+   Values are FP64, not bit-identical to LAPACK's. */
+int bx_gp_factor(bx_handle* h, const uint32_t* dev_train_rows, int32_t n, const double* host_z, double outputscale,
+                 double noise_variance, const double* lengthscales, double* host_L, double* host_alpha, void* stream);
+
 /* Tensor-core posterior only: the DMMA k-steps of its distance product over the Euclidean
    embedding of W (0: FMA distances per parameter kind, or not the tensor-core kernel). */
 int bx_gp_distance_ksteps(bx_handle* h);

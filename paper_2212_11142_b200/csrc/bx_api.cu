@@ -87,6 +87,7 @@ void bx_destroy(bx_handle* h) {
   h->d_mdig.release();
   h->d_rowscale.release();
   h->d_tc_part.release();
+  h->d_factor.release();
   h->d_ei.release();
   h->d_grad_scratch.release();
   h->d_leaf_count.release();

@@ -633,6 +633,9 @@ cudaError_t launch_lml_small(const double* sq, int n, int D, const double* z, co
 // _lml_core for c settings, each over the whole GPU, side by side on grid.y (lml_wide.cu), n <= 512
 size_t lml_wide_scratch_doubles(int n, int D, int c);
 bool lml_wide_supported(int n);
+cudaError_t launch_gp_factor(const double* sq, int n, int D, const double* z, const double* prm, double* scratch,
+                             const double** L_out, const double** al_out, const int** fail_out,
+                             const double** X_out, cudaStream_t s);
 size_t lml_coarse_wide_scratch_doubles(int n, int c);
 cudaError_t launch_lml_coarse_wide(const double* sq, int n, int D, const double* z, const double* thetas, int c,
                                    double* out, double* scratch, cudaStream_t s);

@@ -120,6 +120,7 @@ struct bx_handle {
   int tc_nsl = 0, tc_nch = 0;
   double tc_kscale = 0;
   DevBuf d_mdig, d_rowscale, d_tc_part;
+  DevBuf d_factor;  // bx_gp_factor: distances, z, hyperparameters, one setting's factorisation scratch
   bool matern_precise = false;  // BX_MATERN_PRECISE debug switch (env)
   int mt = 0, rows8 = 0, n_kendall = 0;
   int32_t kendall_param[BX_MAX_PARAMS] = {0};

@@ -69,6 +69,44 @@ int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const doub
   return BX_OK;
 }
 
+int bx_gp_factor(bx_handle* h, const uint32_t* dev_train_rows, int32_t n, const double* host_z, double outputscale,
+                 double noise_variance, const double* lengthscales, double* host_L, double* host_alpha, void* stream) {
+  int r = check_space(h);
+  if (r) return r;
+  if (n < 1 || n > 512) return fail(h, BX_ERR_UNSUPPORTED, "bx_gp_factor: n = %d outside 1..512", n);
+  if (!dev_train_rows || !host_z || !lengthscales || !host_L || !host_alpha) return fail(h, BX_ERR_ARG, "null argument");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int D = h->n_params;
+  std::vector<double> prm(2 + D);
+  prm[0] = outputscale;
+  prm[1] = noise_variance;
+  for (int k = 0; k < D; ++k) prm[2 + k] = lengthscales[k];
+  // [D][n][n] squared distances | z | prm | the lml_wide scratch of one setting
+  const size_t sq_d = (size_t)D * n * n;
+  BX_CUDA(h, h->d_factor.ensure((sq_d + n + 2 + D + lml_wide_scratch_doubles(n, D, 1)) * sizeof(double)));
+  double* sq = h->d_factor.as<double>();
+  double* z = sq + sq_d;
+  double* p = z + n;
+  double* scratch = p + 2 + D;
+  BX_CUDA(h, launch_pairwise_sq(space_dev(h), dev_train_rows, n, dev_train_rows, n, sq, s));
+  BX_CUDA(h, cudaMemcpyAsync(z, host_z, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  BX_CUDA(h, cudaMemcpyAsync(p, prm.data(), prm.size() * 8, cudaMemcpyHostToDevice, s));
+  const double *L, *al, *X;
+  const int* failed;
+  BX_CUDA(h, launch_gp_factor(sq, n, D, z, p, scratch, &L, &al, &failed, &X, s));
+  const int np = (n + 31) / 32 * 32;
+  int fl = 0;
+  BX_CUDA(h, cudaMemcpy2DAsync(host_L, (size_t)n * 8, L, (size_t)np * 8, (size_t)n * 8, n, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(host_alpha, al, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaMemcpyAsync(&fl, failed, sizeof(int), cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  if (fl) return fail(h, BX_ERR_NOT_PD, "Gram matrix is not positive definite (potrf info > 0)");
+  for (int i = 0; i < n; ++i)  // the strict upper triangle of the factor is zero (np.tril)
+    for (int j = i + 1; j < n; ++j) host_L[(size_t)i * n + j] = 0.0;
+  return BX_OK;
+}
+
 int bx_pairwise_sq(bx_handle* h, const uint32_t* a, int32_t qa, const uint32_t* b, int32_t qb,
                    double* out, void* stream) {
   int r = check_space(h);

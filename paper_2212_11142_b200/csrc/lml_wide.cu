@@ -413,4 +413,39 @@ cudaError_t launch_lml_wide(const double* sq, int n, int D, const double* z, con
   return cudaGetLastError();
 }
 
+// GPModel.__init__ (surrogate.py:286-303) on the device for one hyperparameter setting: Gram with
+// noise floor + jitter, the blocked Cholesky, L^-1 and alpha = L^-T L^-1 z, in the scratch layout
+// of launch_lml_wide (c = 1); the factor is left at L (row stride np), alpha at al, the failure
+// flag (potrf info > 0) at fail.
+cudaError_t launch_gp_factor(const double* sq, int n, int D, const double* z, const double* prm, double* scratch,
+                             const double** L_out, const double** al_out, const int** fail_out,
+                             const double** X_out, cudaStream_t s) {
+  if (n > 512 || n < 1) return cudaErrorInvalidValue;
+  const int np = (n + kT - 1) / kT * kT, nb = np / kT, tiles = nb * (nb + 1) / 2;
+  double* K = scratch;
+  double* L = K + (size_t)np * np;
+  double* X = L + (size_t)np * np;
+  double* u = X + (size_t)np * np;
+  double* al = u + np;
+  double* partial = al + np;
+  int* fail = reinterpret_cast<int*>(partial + (size_t)tiles * (2 + D));
+  double* val = partial;  // the value kernel's outputs (unused here) in the partial-sum area
+  int* ok = fail + 1;
+  cudaError_t e = cudaMemsetAsync(fail, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(X, 0, (size_t)np * np * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  const int g = (int)std::min<size_t>(((size_t)np * np + 255) / 256, 148 * 8);
+  lw_gram_kernel<<<dim3(g, 1), 256, 0, s>>>(sq, n, np, D, prm, 0, nullptr, L);
+  for (int J = 0; J < nb; ++J) lw_chol_kernel<<<dim3(nb - J, 1), 256, 0, s>>>(L, np, J, fail);
+  lw_inverse_kernel<<<dim3((np + kInvW - 1) / kInvW, 1), kInvW * 32, 0, s>>>(L, np, X);
+  lw_value_kernel<<<dim3(1, 1), 512, 0, s>>>(L, X, n, np, D, z, prm, 0.0, 0.0, 0, fail, u, al, val, ok);
+  *L_out = L;
+  *al_out = al;
+  *fail_out = fail;
+  *X_out = X;
+  return cudaGetLastError();
+}
+
 }  // namespace bx
+

@@ -352,6 +352,18 @@ class Scorer:
                                              _ptr(out), self.stream))
         return out
 
+    def gp_factor(self, rows: torch.Tensor, z: np.ndarray, outputscale: float, noise_variance: float,
+                  lengthscales) -> tuple:
+        """bx_gp_factor: (L (n, n) lower, alpha (n,)) of GPModel.__init__ computed on the device."""
+        n = rows.shape[0]
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        ls = np.ascontiguousarray(lengthscales, dtype=np.float64)
+        L = np.empty((n, n), dtype=np.float64)
+        alpha = np.empty(n, dtype=np.float64)
+        self._check(self._lib.bx_gp_factor(self.h, _ptr(rows), n, _ptr(z), float(outputscale), float(noise_variance),
+                                           _ptr(ls), _ptr(L), _ptr(alpha), self.stream))
+        return L, alpha
+
     def lml_core(self, sq: torch.Tensor, z: torch.Tensor, params: torch.Tensor, want_grad: bool,
                  prior=None):
         """bx_lml_core: (values[c], grads[c, 2+D] | None, ok[c]) for rows (sigma, noise, l...)."""

@@ -49,8 +49,9 @@ class GPState:
 
     @classmethod
     def fit(cls, space, configs, y, hyperparameters, *, log_objective=False, use_transforms=True,
-            scorer=None):
-        """GPModel.__init__ numerics with the Gram's squared distances from the device."""
+            scorer=None, device=False):
+        """GPModel.__init__ numerics with the Gram's squared distances from the device; device=True:
+        the Gram, its Cholesky factor and alpha on the device too (bx_gp_factor)."""
         from .device import scorer as _scorer
 
         sc = scorer or _scorer()
@@ -64,6 +65,11 @@ class GPState:
             sd = 1.0
         z = (y - mu) / sd
         rows = sc.to_device(lay.encode(configs))
+        if device:
+            L, alpha = sc.gp_factor(rows, z, hyperparameters.outputscale, hyperparameters.noise_variance,
+                                    hyperparameters.lengthscales)
+            return cls(space, configs, hyperparameters, L, alpha, mu, sd,
+                       log_objective=log_objective, use_transforms=use_transforms)
         sq = sc.pairwise_sq(rows, rows).cpu().numpy()
         inv = 1.0 / np.asarray(hyperparameters.lengthscales, float) ** 2
         W = np.einsum("kab,k->ab", sq, inv)

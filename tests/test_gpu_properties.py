@@ -474,3 +474,49 @@ def test_full_pool_selection_against_oracle(case, mode):
     best = min((i for i in order[:1000] if ov[i] == ov[first] and cfgs[i] not in ev), key=lambda i: cfgs[i])
     assert summ.best.index == best and summ.n_finite == int(np.isfinite(ov).sum())
     sc.close()
+
+
+@pytest.mark.parametrize("case,n", [("C3", 200), ("C5", 37), ("C5", 300), ("M200", 200)])
+def test_gp_factor_on_device_matches_host_factorisation(case, n):
+    """bx_gp_factor (GPModel.__init__ on the device: Gram, Cholesky, alpha) against the host
+    factorisation of the same Gram (scipy cho_factor) - L and alpha to FP64 rounding - and the
+    posterior of a model built either way."""
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    space = scenarios.build_space("C5" if case == "M200" else case, _bt.space)
+    rng = np.random.default_rng(n)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, n + 40, rng))))[:n]
+    y = np.array([scenarios.objective("C5" if case == "M200" else case, c) for c in cfgs])
+    hyp = Hyper(outputscale=1.4, noise_variance=1e-4, lengthscales=tuple(rng.uniform(0.5, 2.5, len(space.parameters))))
+    host = GPState.fit(space, cfgs, y, hyp, scorer=sc, log_objective=True)
+    dev = GPState.fit(space, cfgs, y, hyp, scorer=sc, log_objective=True, device=True)
+    Lh, Ld = host._cho[0], dev._cho[0]
+    np.testing.assert_allclose(Ld, Lh, rtol=1e-10, atol=1e-12 * np.abs(Lh).max())
+    assert np.all(np.triu(Ld, 1) == 0.0)
+    np.testing.assert_allclose(dev.alpha, host.alpha, rtol=1e-7, atol=1e-9 * np.abs(host.alpha).max())
+    rows = sc.to_device(scenarios.sample_rows_uniform(lay, 4096, rng))
+    sc.set_gp(host)
+    m0, v0 = (x.cpu().numpy() for x in sc.predict(rows))
+    sc.set_gp(dev)
+    m1, v1 = (x.cpu().numpy() for x in sc.predict(rows))
+    np.testing.assert_allclose(m1, m0, rtol=1e-7, atol=1e-9 * np.abs(m0).max())
+    np.testing.assert_allclose(v1, v0, rtol=1e-6, atol=1e-9 * np.abs(v0).max())
+    sc.close()
+
+
+def test_gp_factor_reports_a_failed_factorisation():
+    """A Gram that is not positive definite -> BX_ERR_NOT_PD (numpy's LinAlgError)."""
+    from paper_2212_11142_b200._native import NativeError, BX_ERR_NOT_PD
+    from paper_2212_11142_b200.device import Scorer
+    space = scenarios.build_space("C3", _bt.space)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    cfgs = list(dict.fromkeys(lay.decode(scenarios.sample_rows_uniform(lay, 40, np.random.default_rng(3)))))[:20]
+    rows = sc.to_device(lay.encode(cfgs))
+    with pytest.raises(NativeError) as e:
+        sc.gp_factor(rows, np.zeros(20), -1.0, 0.0, np.ones(len(space.parameters)))  # negative outputscale
+    assert e.value.code == BX_ERR_NOT_PD
+    sc.close()
