@@ -268,6 +268,14 @@ int bx_pcg64_permutations(uint64_t* state, int32_t* has_uint32, uint32_t* uinteg
    (feasibility.py:119). */
 int bx_pcg64_choice(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, int64_t n, int32_t pop, int32_t k,
                     int32_t* out);
+/* ... and the random-forest fit's per-tree draws (feasibility.py:119-190, replacing the n_trees
+   np.random.default_rng(seed) generators): tree t's generator is seeded from seeds[t] (< 2^64) as
+   SeedSequence + PCG64 seed it, draws its bootstrap rows integers(0, n, size=n) into boot[t][n]
+   and then ndraws feature subsets choice(pop, size=k, replace=False) into subsets[t][ndraws][k];
+   its state afterwards goes to state[t][4] / has_uint32[t] / uinteger[t] (bx_pcg64_choice
+   continues it). */
+int bx_pcg64_forest_draws(const uint64_t* seeds, int32_t n_trees, int64_t n, int32_t pop, int32_t k, int32_t ndraws,
+                          int32_t* boot, int32_t* subsets, uint64_t* state, int32_t* has_uint32, uint32_t* uinteger);
 
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the

@@ -82,6 +82,61 @@ void store(const Pcg64& g, uint64_t* state, int32_t* has_uint32, uint32_t* uinte
   *uinteger = g.buf;
 }
 
+// np.random.default_rng(seed) for 0 <= seed < 2^64: SeedSequence(seed) (numpy/random/bit_generator.pyx:
+// the entropy as little-endian 32-bit words mixed into a 4-word pool by hashmix / mix, then
+// generate_state(4, uint64) hashed out of the pool) seeds PCG64 (pcg64_set_seed: state = 0,
+// inc = 2 initseq + 1, step, state += initstate, step) with an empty 32-bit buffer.
+Pcg64 seeded(uint64_t seed) {
+  uint32_t ent[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const int nent = (seed >> 32) ? 2 : 1;
+  uint32_t hc = 0x43b0d7e5u;
+  auto hashmix = [&hc](uint32_t v) {
+    v ^= hc;
+    hc *= 0x931e8875u;
+    v *= hc;
+    return v ^ (v >> 16);
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    const uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t pool[4];
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < nent ? ent[i] : 0u);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b)
+      if (a != b) pool[b] = mix(pool[b], hashmix(pool[a]));
+  uint32_t hb = 0x8b51f9ddu, w[8];
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i & 3] ^ hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    w[i] = v ^ (v >> 16);
+  }
+  uint64_t u[4];
+  for (int i = 0; i < 4; ++i) u[i] = (uint64_t)w[2 * i] | ((uint64_t)w[2 * i + 1] << 32);
+  Pcg64 g{0, ((((u128)u[2] << 64) | u[3]) << 1) | 1u, 0, 0u};
+  g.next64();
+  g.state += ((u128)u[0] << 64) | u[1];
+  g.next64();
+  return g;
+}
+
+// Generator.choice(pop, size=k, replace=False) for pop <= 10000 into idx[k]
+void choice(Pcg64& g, int32_t pop, int32_t k, int32_t* idx) {
+  for (int32_t j = pop - k; j < pop; ++j) {
+    const int32_t v = (int32_t)g.lemire((uint32_t)j);
+    bool seen = false;
+    for (int32_t t = 0; t < j - (pop - k); ++t) seen |= idx[t] == v;
+    idx[j - (pop - k)] = seen ? j : v;
+  }
+  for (int32_t i = k - 1; i >= 1; --i) {  // _shuffle_int: bounded Lemire draws, not random_interval
+    const uint32_t s = g.lemire((uint32_t)i);
+    const int32_t t = idx[i];
+    idx[i] = idx[s];
+    idx[s] = t;
+  }
+}
+
 }  // namespace
 
 // n draws of Generator.choice(pop, size=k, replace=False) for pop <= 10000 (the rf_fit feature
@@ -94,22 +149,31 @@ extern "C" int bx_pcg64_choice(uint64_t* state, int32_t* has_uint32, uint32_t* u
       (n > 0 && k > 0 && !out))
     return BX_ERR_ARG;
   Pcg64 g = load(state, has_uint32, uinteger);
-  for (int64_t r = 0; r < n; ++r) {
-    int32_t* idx = out + r * k;
-    for (int32_t j = pop - k; j < pop; ++j) {
-      const int32_t v = (int32_t)g.lemire((uint32_t)j);
-      bool seen = false;
-      for (int32_t t = 0; t < j - (pop - k); ++t) seen |= idx[t] == v;
-      idx[j - (pop - k)] = seen ? j : v;
-    }
-    for (int32_t i = k - 1; i >= 1; --i) {  // _shuffle_int: bounded Lemire draws, not random_interval
-      const uint32_t s = g.lemire((uint32_t)i);
-      const int32_t t = idx[i];
-      idx[i] = idx[s];
-      idx[s] = t;
-    }
-  }
+  for (int64_t r = 0; r < n; ++r) choice(g, pop, k, out + r * k);
   store(g, state, has_uint32, uinteger);
+  return BX_OK;
+}
+
+// The random-forest fit's per-tree draws (feasibility.py:119-190): for each seed t, the tree's
+// generator np.random.default_rng(seeds[t]), its bootstrap rows g.integers(0, n, size=n) (Lemire
+// draws on [0, n-1], numpy's random_bounded_uint64_fill) and then ndraws feature subsets
+// g.choice(pop, size=k, replace=False); the generator's state afterwards goes to state[4t..4t+3] /
+// has_uint32[t] / uinteger[t] so that bx_pcg64_choice can continue it.
+extern "C" int bx_pcg64_forest_draws(const uint64_t* seeds, int32_t n_trees, int64_t n, int32_t pop, int32_t k,
+                                     int32_t ndraws, int32_t* boot, int32_t* subsets, uint64_t* state,
+                                     int32_t* has_uint32, uint32_t* uinteger) {
+  if (n_trees < 0 || n < 1 || n > 0x7FFFFFFF || pop < 1 || pop > 10000 || k < 0 || k > pop || ndraws < 0 ||
+      (n_trees > 0 && (!seeds || !boot || !state || !has_uint32 || !uinteger || (ndraws > 0 && k > 0 && !subsets))))
+    return BX_ERR_ARG;
+  for (int32_t t = 0; t < n_trees; ++t) {
+    Pcg64 g = seeded(seeds[t]);
+    int32_t* b = boot + (int64_t)t * n;
+    for (int64_t i = 0; i < n; ++i) b[i] = (int32_t)g.lemire((uint32_t)(n - 1));
+    for (int32_t r = 0; r < ndraws; ++r) choice(g, pop, k, subsets + ((int64_t)t * ndraws + r) * k);
+    store(g, state + 4 * (int64_t)t, has_uint32 + t, uinteger + t);
+    state[4 * (int64_t)t + 2] = (uint64_t)(g.inc >> 64);
+    state[4 * (int64_t)t + 3] = (uint64_t)g.inc;
+  }
   return BX_OK;
 }
 

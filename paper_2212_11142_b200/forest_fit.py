@@ -2,9 +2,10 @@
 
 The reference's own pieces do everything but the tree building: `encode_configs`, the canonical
 lexsort of the rows, the per-tree bootstrap seeds drawn from the caller's RNG, the single-class
-shortcut and the `FeasibilityModel` returned.  Each tree's generator is numpy's: the bootstrap rows
-and, in order, the feature subsets its eligible nodes draw (`tree_rng.choice(F, k, replace=False)`,
-feasibility.py:119) are drawn on the host exactly as the reference draws them; the device walks
+shortcut and the `FeasibilityModel` returned.  Each tree's generator (`default_rng(seed)`): the
+bootstrap rows and, in order, the feature subsets its eligible nodes draw (`tree_rng.choice(F, k,
+replace=False)`, feasibility.py:119) are drawn on the host exactly as the reference draws them -
+replayed natively for the whole forest (sampling.TreeStreams, bx_pcg64_forest_draws); the device walks
 the tree depth first (bx_rf_fit, forest_fit.cu) so its i-th eligible node takes the i-th subset.
 A tree that needs more subsets than were drawn is built again after drawing more from the same
 generator.  The arrays - node ids, features, thresholds, children, leaf values - equal the
@@ -20,7 +21,7 @@ import numpy as np
 
 from . import _native as N
 from .device import scorer
-from .sampling import choice_rows
+from .sampling import TreeStreams
 
 _DEFAULT = object()
 DRAWS = 48  # feature subsets drawn per tree up front (M200-sized forests use ~30)
@@ -52,11 +53,11 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
         return model
     n, F = X.shape
     k = max(1, round(math.sqrt(F)))
-    gens = [np.random.default_rng(int(s)) for s in seeds]
-    boot = np.stack([g.integers(0, n, size=n) for g in gens]).astype(np.int32)
-    # the feature subsets in the order the tree's generator draws them (replayed from its PCG64
-    # state by bx_pcg64_choice: no per-draw Python call)
-    draws = [choice_rows(g, DRAWS, F, k) for g in gens]
+    # each tree's generator default_rng(seed): bootstrap rows, then the feature subsets in the order
+    # it draws them - replayed natively for the whole forest (bx_pcg64_forest_draws), no per-tree
+    # or per-draw Python call
+    streams = TreeStreams(seeds, n, F, k, DRAWS)
+    boot, draws = streams.boot, streams.draws
     max_nodes = 2 * n + 2
     sc = scorer()
     lib = sc._lib
@@ -86,7 +87,7 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
         again = []
         for i, t in enumerate(todo):
             if out_s[i] == 1:  # more feature subsets: continue the tree's own generator
-                draws[t] = np.concatenate([draws[t], choice_rows(gens[t], DRAWS, F, k)])
+                streams.more(t, DRAWS)
                 again.append(t)
             elif out_s[i] != 0:
                 raise N.NativeError(N.BX_ERR_UNSUPPORTED, f"rf_fit: tree {t} exceeded {max_nodes} nodes")

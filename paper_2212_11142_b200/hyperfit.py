@@ -77,8 +77,7 @@ def gp_fit(space, configs, y, rng, prior=_DEFAULT, log_objective="auto", use_tra
             # objective passes them (surrogate.py:510-516)
             prm = np.array([[math.exp(t[0]), math.exp(t[1]), *np.exp(t[2:])] for t in batch])
             with torch.cuda.device(sc.device):
-                value, grad, ok = sc.lml_core(sq_d, z_d, torch.as_tensor(prm, device=dev), True, prior)
-                value, grad, ok = value.cpu().numpy(), grad.cpu().numpy(), ok.cpu().numpy()
+                value, grad, ok = sc.lml_core_host(sq_d, z_d, prm, prior)
             return [(np.inf, np.zeros(batch.shape[1])) if not k else (-v, -g) for v, g, k in zip(value, grad, ok)]
 
         results, calls = minimize_lockstep(evaluate, [thetas[i] for i in starts], list(zip(lo, hi)),

@@ -66,6 +66,14 @@ def replay_ok() -> bool:
                 got = _replay_choice(a, 64, pop, k)
                 ok &= all(np.array_equal(got[r], b.choice(pop, size=k, replace=False)) for r in range(64))
                 ok &= repr(a.bit_generator.state) == repr(b.bit_generator.state)
+            seeds = [0, 5, (1 << 32) - 1, 123456789]
+            f = TreeStreams(seeds, 9, 13, 3, 4, native=True)
+            for t, s in enumerate(seeds):
+                g = np.random.default_rng(s)
+                ok &= np.array_equal(f.boot[t], g.integers(0, 9, size=9))
+                ok &= all(np.array_equal(f.draws[t][r], g.choice(13, size=3, replace=False)) for r in range(4))
+                f.more(t, 2)
+                ok &= all(np.array_equal(f.draws[t][r], g.choice(13, size=3, replace=False)) for r in (4, 5))
             _REPLAY_OK = bool(ok)
         except Exception:
             _REPLAY_OK = False
@@ -228,3 +236,51 @@ def cot_rows(lay, cot, n: int, rng) -> np.ndarray:
             for j, k in enumerate(g.indices):
                 lay.encode_param(rows, k, [v[j] for v in out])
     return rows
+
+
+class TreeStreams:
+    """The random-forest fit's per-tree generators (feasibility.py:119-190): tree t's generator is
+    np.random.default_rng(seeds[t]); it draws the bootstrap rows `integers(0, n, size=n)` (`boot[t]`)
+    and then the feature subsets `choice(pop, size=k, replace=False)` in order (`draws[t]`, ndraws up
+    front, `more(t, count)` continues the same generator).  With PCG64 replay available the whole
+    forest's draws are one bx_pcg64_forest_draws call (SeedSequence seeding included) and the
+    continuations bx_pcg64_choice calls on the kept states; otherwise numpy's generators draw them."""
+
+    def __init__(self, seeds, n: int, pop: int, k: int, ndraws: int, native: bool | None = None):
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        T = len(seeds)
+        self.pop, self.k = pop, k
+        if native is None:
+            native = pop <= 10000 and replay_ok()
+        self.native = native
+        if native:
+            self.boot = np.empty((T, n), np.int32)
+            sub = np.empty((T, ndraws, k), np.int32)
+            self._state = np.empty((T, 4), np.uint64)
+            self._has32 = np.empty(T, np.int32)
+            self._uint = np.empty(T, np.uint32)
+            p = lambda a: a.ctypes.data_as(C.c_void_p)
+            code = N.lib().bx_pcg64_forest_draws(p(seeds), T, n, pop, k, ndraws, p(self.boot), p(sub), p(self._state),
+                                                 p(self._has32), p(self._uint))
+            if code != N.BX_OK:
+                raise N.NativeError(code, "bx_pcg64_forest_draws")
+            self.draws = list(sub)
+        else:
+            self._gens = [np.random.default_rng(int(s)) for s in seeds]
+            self.boot = np.stack([g.integers(0, n, size=n) for g in self._gens]).astype(np.int32).reshape(T, n)
+            self.draws = [choice_rows(g, ndraws, pop, k) for g in self._gens]
+
+    def more(self, t: int, count: int) -> None:
+        """Append the next `count` feature subsets of tree t's generator to draws[t]."""
+        if self.native:
+            out = np.empty((count, self.k), np.int32)
+            st = self._state[t]  # a view: the advanced state is written back in place
+            code = N.lib().bx_pcg64_choice(st.ctypes.data_as(C.c_void_p),
+                                           self._has32[t:].ctypes.data_as(C.c_void_p),
+                                           self._uint[t:].ctypes.data_as(C.c_void_p), count, self.pop, self.k,
+                                           out.ctypes.data_as(C.c_void_p))
+            if code != N.BX_OK:
+                raise N.NativeError(code, "bx_pcg64_choice")
+        else:
+            out = choice_rows(self._gens[t], count, self.pop, self.k)
+        self.draws[t] = np.concatenate([self.draws[t], out])

@@ -144,3 +144,20 @@ def test_cot_rows_real_and_permutation_singletons(ref):
 def test_replay_self_check_passes_on_this_numpy():
     """The one-time check that guards the PCG64 replays holds for the NumPy in this image."""
     assert sampling.replay_ok()
+
+
+@pytest.mark.parametrize("n,pop,k", [(1, 1, 1), (2, 13, 4), (40, 13, 4), (200, 30, 5), (7, 100, 10)])
+def test_tree_streams_replay_the_per_tree_generators(n, pop, k):
+    """TreeStreams (bx_pcg64_forest_draws: SeedSequence + PCG64 seeding, the bootstrap integers and
+    the feature subsets) = np.random.default_rng(seed) per tree, continuations included."""
+    seeds = np.random.default_rng(n).integers(0, 2 ** 32, size=60, dtype=np.uint64)
+    seeds[:3] = [0, 1, 2 ** 32 - 1]
+    f = sampling.TreeStreams(seeds, n, pop, k, 6)
+    assert f.native
+    for t in (0, 1, 2, 31, 59):
+        g = np.random.default_rng(int(seeds[t]))
+        assert np.array_equal(f.boot[t], g.integers(0, n, size=n))
+        f.more(t, 5)
+        assert np.array_equal(f.draws[t], np.array([g.choice(pop, size=k, replace=False) for _ in range(11)]))
+        f.more(t, 1)
+        assert np.array_equal(f.draws[t][-1], g.choice(pop, size=k, replace=False))
