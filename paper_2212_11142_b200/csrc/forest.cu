@@ -285,35 +285,56 @@ struct QsSmem {
 __host__ __device__ inline QsSmem qs_smem_layout(const QsForestDev& f, bool offs) {
   QsSmem L;
   size_t o = 0;
+  // every region starts on 16 bytes and is copied in whole 16-byte units (qs_load_tables)
   L.mask = o;
-  o += (size_t)f.stride * f.tpad * 8;
+  o += ((size_t)f.stride * f.tpad * 8 + 15) & ~(size_t)15;
   L.uval = o;
-  o += (size_t)f.n_uvals * 8;
+  o += ((size_t)f.n_uvals * 8 + 15) & ~(size_t)15;
   L.vid = o;
   o += ((size_t)f.n_trees * 64 * 2 + 15) & ~(size_t)15;
   L.iidx = o;
   o += f.n_ind ? (((size_t)f.n_iidx_rows * f.itpad * 2 + 15) & ~(size_t)15) : 0;
   L.imask = o;
-  o += f.n_ind ? (size_t)f.n_imask * 8 : 0;
+  o += f.n_ind ? (((size_t)f.n_imask * 8 + 15) & ~(size_t)15) : 0;
   L.offs = o;
   o += offs ? (size_t)f.n_codes * kQsThreads * 4 : 0;
   L.end = (o + 15) & ~(size_t)15;
   return L;
 }
 
+// The tables go to shared memory as bulk asynchronous copies (cp.async.bulk, one elected thread,
+// completion counted on an mbarrier): ~165 KB arrive in ~2 us where the element-wise loop took ~30
+// us per CTA (a round of L2 latency per 8 KB).  Every region is a whole number of 16-byte units;
+// the device arrays are allocated 16 bytes past their ends (upload()), so the rounded copies stay
+// inside them.  Ends with a __syncthreads (the barrier also orders the callers' own shared stores).
 __device__ void qs_load_tables(const QsForestDev& f, unsigned char* smem, const QsSmem& L) {
-  uint64_t* s_mask = reinterpret_cast<uint64_t*>(smem + L.mask);
-  double* s_uval = reinterpret_cast<double*>(smem + L.uval);
-  uint16_t* s_vid = reinterpret_cast<uint16_t*>(smem + L.vid);
-  for (int i = threadIdx.x; i < f.stride * f.tpad; i += blockDim.x) s_mask[i] = f.mask[i];
-  for (int i = threadIdx.x; i < f.n_uvals; i += blockDim.x) s_uval[i] = f.uval[i];
-  for (int i = threadIdx.x; i < f.n_trees * 64; i += blockDim.x) s_vid[i] = f.vid[i];
-  if (f.n_ind) {
-    uint16_t* s_iidx = reinterpret_cast<uint16_t*>(smem + L.iidx);
-    uint64_t* s_imask = reinterpret_cast<uint64_t*>(smem + L.imask);
-    for (int i = threadIdx.x; i < f.n_iidx_rows * f.itpad; i += blockDim.x) s_iidx[i] = f.iidx[i];
-    for (int i = threadIdx.x; i < f.n_imask; i += blockDim.x) s_imask[i] = f.imask[i];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+  const uint32_t sizes[5] = {(uint32_t)(L.uval - L.mask), (uint32_t)(L.vid - L.uval), (uint32_t)(L.iidx - L.vid),
+                             (uint32_t)(L.imask - L.iidx), (uint32_t)(L.offs - L.imask)};
+  if (threadIdx.x == 0) {
+    const void* src[5] = {f.mask, f.uval, f.vid, f.iidx, f.imask};
+    const size_t dst[5] = {L.mask, L.uval, L.vid, L.iidx, L.imask};
+    uint32_t total = 0;
+    for (int r = 0; r < 5; ++r) total += sizes[r];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(total) : "memory");
+    for (int r = 0; r < 5; ++r)
+      if (sizes[r])
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(smem + dst[r])), "l"(src[r]), "r"(sizes[r]), "r"(b)
+                     : "memory");
+  }
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(done) : "r"(b) : "memory");
+  __syncthreads();
 }
 
 // indirect slots of one candidate: the shared address of its index row (tree 0)
