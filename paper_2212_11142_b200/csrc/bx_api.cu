@@ -84,6 +84,7 @@ void bx_destroy(bx_handle* h) {
   h->d_emb_planes.release();
   h->d_emb_yy.release();
   if (h->h_ones) cudaFreeHost(h->h_ones);
+  if (h->h_climb_flag) cudaFreeHost(h->h_climb_flag);
   h->d_mdig.release();
   h->d_rowscale.release();
   h->d_tc_part.release();

@@ -2,6 +2,7 @@
 // device pools (bx_score), streamed host pools encoded or packed (bx_score_host), device-generated
 // pools (bx_generate, bx_score_generated), the predict entry points and the device hill climb
 // (bx_climb).
+#include <algorithm>
 #include "bx_handle.cuh"
 
 namespace bx {
@@ -23,7 +24,7 @@ namespace bx {
 // bx_climb state on the device: per start the current row, value and an active flag; the tracker
 struct ClimbState {
   int32_t n_active;
-  int32_t pad;
+  int32_t steps;                     // steps that had an active start (the host's loop count)
   TopRec best;                       // index >= 0 once set
   uint32_t best_row[BX_MAX_ROW_WORDS];
 };
@@ -56,8 +57,12 @@ __global__ void climb_update_kernel(SpaceDev sp, EvalSetDev ev, int A, int S, in
                                     ClimbState* st) {
   __shared__ int s_trk[BX_MAX_K];
   __shared__ int s_moved[BX_MAX_K];
+  __shared__ int s_any;
   const int W = sp.row_words;
   const int a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  if (a < A && lane == 0 && active[a]) s_any = 1;
   if (a < A) {
     int br = -1, tr = -1;  // argbest row and tracker-candidate row of this lane
     double bv = -INFINITY, tv = -INFINITY;
@@ -124,6 +129,7 @@ __global__ void climb_update_kernel(SpaceDev sp, EvalSetDev ev, int A, int S, in
       }
     }
     st->n_active = n_active;
+    st->steps += s_any;  // a step after every start stopped (a batched launch) changes nothing
   }
 }
 }  // namespace bx
@@ -485,21 +491,31 @@ int bx_climb(bx_handle* h, const uint32_t* dev_pool_rows, const int64_t* host_st
   BX_CUDA(h, cudaMemcpyAsync(curv, host_start_values, (size_t)A * 8, cudaMemcpyHostToDevice, s));
   BX_CUDA(h, cudaMemcpyAsync(act, ones.data(), (size_t)A * 4, cudaMemcpyHostToDevice, s));
   BX_CUDA(h, cudaMemcpyAsync(st, &hs, sizeof(ClimbState), cudaMemcpyHostToDevice, s));
-  int steps = 0;
-  for (int step = 0; step < max_steps && hs.n_active > 0; ++step) {
-    BX_CUDA(h, launch_neighbors(space_dev(h), use_cot ? &h->cot : nullptr, cur, A, nb, valid, s));
-    climb_flags_kernel<<<1, 32, 0, s>>>(A, S, act, valid, pw);
-    BX_CUDA(h, cudaGetLastError());
-    h->pw_rows = pw;
-    int np = 0;
-    r = score_impl(h, nb, (int64_t)A * S, 0, f_model, eps_f, 0, 0, vals, probs, nullptr, &np, s, 0);
-    h->pw_rows = nullptr;
-    if (r) return r;
-    climb_update_kernel<<<1, 32 * A, 0, s>>>(space_dev(h), eval_dev(h), A, S, act, cur, curv, nb, valid, vals, st);
-    BX_CUDA(h, cudaGetLastError());
-    BX_CUDA(h, cudaMemcpyAsync(&hs.n_active, &st->n_active, 4, cudaMemcpyDeviceToHost, s));
-    BX_CUDA(h, cudaStreamSynchronize(s));  // the one device -> host read per step
-    ++steps;
+  if (!h->h_climb_flag) BX_CUDA(h, cudaMallocHost(&h->h_climb_flag, 64));
+  // Steps go out in batches of kClimbBatch with one 4-byte read of the active count per batch: a
+  // step whose starts have all stopped is a no-op (no start moves, nothing is folded, the step
+  // count does not advance), so the batch's tail changes nothing, and the host stays ahead of the
+  // device instead of waiting on every step.
+  constexpr int kClimbBatch = 4;
+  for (int step = 0; step < max_steps && hs.n_active > 0;) {
+    const int batch = std::min(kClimbBatch, max_steps - step);
+    for (int b = 0; b < batch; ++b) {
+      BX_CUDA(h, launch_neighbors(space_dev(h), use_cot ? &h->cot : nullptr, cur, A, nb, valid, s));
+      climb_flags_kernel<<<1, 32, 0, s>>>(A, S, act, valid, pw);
+      BX_CUDA(h, cudaGetLastError());
+      h->pw_rows = pw;
+      int np = 0;
+      r = score_impl(h, nb, (int64_t)A * S, 0, f_model, eps_f, 0, 0, vals, probs, nullptr, &np, s, 0);
+      h->pw_rows = nullptr;
+      if (r) return r;
+      climb_update_kernel<<<1, 32 * A, 0, s>>>(space_dev(h), eval_dev(h), A, S, act, cur, curv, nb, valid, vals,
+                                               st);
+      BX_CUDA(h, cudaGetLastError());
+    }
+    step += batch;
+    BX_CUDA(h, cudaMemcpyAsync(h->h_climb_flag, &st->n_active, 4, cudaMemcpyDeviceToHost, s));
+    BX_CUDA(h, cudaStreamSynchronize(s));  // the one device -> host read per batch
+    hs.n_active = *h->h_climb_flag;
   }
   BX_CUDA(h, cudaMemcpyAsync(&hs, st, sizeof(ClimbState), cudaMemcpyDeviceToHost, s));
   BX_CUDA(h, cudaStreamSynchronize(s));
@@ -507,7 +523,7 @@ int bx_climb(bx_handle* h, const uint32_t* dev_pool_rows, const int64_t* host_st
   host_best->prob = hs.best.prob;
   host_best->index = hs.best.index;
   std::memcpy(host_best->row, hs.best_row, sizeof(hs.best_row));
-  if (host_steps) *host_steps = steps;
+  if (host_steps) *host_steps = hs.steps;
   return BX_OK;
 }
 
