@@ -432,22 +432,44 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
       for (int k = tid; k < 2 + D; k += blockDim.x) out_grad[(size_t)c * (2 + D) + k] = 0.0;
     return;
   }
-  // u = L^-1 z and alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374): warp 0
+  // u = L^-1 z and alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374): warp 0, column
+  // sweeps - lane l keeps the running sums of rows l, l + 32, ... in registers; each step the owner
+  // of row i finishes it and broadcasts the solved entry, every lane folds it into its rows (one
+  // division, one shuffle and one FMA per step instead of a five-level reduction per row)
   if (warp == 0) {
+    constexpr int kRowsPerLane = (kSmallLmlMaxN + 31) / 32;
+    double acc[kRowsPerLane];
+#pragma unroll
+    for (int m = 0; m < kRowsPerLane; ++m) acc[m] = 0.0;
     for (int i = 0; i < n; ++i) {
-      const size_t r0 = tri_idx(i, 0);
-      double s = 0.0;
-      for (int k = lane; k < i; k += 32) s = fma(Lp[r0 + k], u[k], s);
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) u[i] = (z[i] - s) / Lp[r0 + i];
-      __syncwarp();
+      double ui = 0.0;
+#pragma unroll
+      for (int m = 0; m < kRowsPerLane; ++m)
+        if (lane + 32 * m == i) ui = (z[i] - acc[m]) / Lp[tri_idx(i, i)];
+      ui = __shfl_sync(0xffffffffu, ui, i & 31);
+      if (lane == (i & 31)) u[i] = ui;
+#pragma unroll
+      for (int m = 0; m < kRowsPerLane; ++m) {
+        const int k = lane + 32 * m;
+        if (k > i && k < n) acc[m] = fma(Lp[tri_idx(k, i)], ui, acc[m]);
+      }
     }
+#pragma unroll
+    for (int m = 0; m < kRowsPerLane; ++m) acc[m] = 0.0;
+    __syncwarp();
     for (int i = n - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1 + lane; k < n; k += 32) s = fma(Lp[tri_idx(k, i)], al[k], s);
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) al[i] = (u[i] - s) / Lp[tri_idx(i, i)];
-      __syncwarp();
+      double ai = 0.0;
+#pragma unroll
+      for (int m = 0; m < kRowsPerLane; ++m)
+        if (lane + 32 * m == i) ai = (u[i] - acc[m]) / Lp[tri_idx(i, i)];
+      ai = __shfl_sync(0xffffffffu, ai, i & 31);
+      if (lane == (i & 31)) al[i] = ai;
+      const size_t r0 = tri_idx(i, 0);
+#pragma unroll
+      for (int m = 0; m < kRowsPerLane; ++m) {
+        const int j = lane + 32 * m;
+        if (j < i) acc[m] = fma(Lp[r0 + j], ai, acc[m]);
+      }
     }
   }
   __syncthreads();
