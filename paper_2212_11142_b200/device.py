@@ -54,8 +54,7 @@ class Summary:
 def _cand(c: N.Cand, words: int) -> Candidate | None:
     if c.index < 0:
         return None
-    return Candidate(float(c.value), float(c.prob), int(c.index),
-                     np.ctypeslib.as_array(c.row)[:words].copy())
+    return Candidate(c.value, c.prob, c.index, np.frombuffer(c.row, dtype=np.uint32, count=words).copy())
 
 
 class Scorer:
