@@ -536,7 +536,9 @@ struct TcArgs {
   int32_t debug;              // BX_TC_DEBUG bits (timing experiments only): 1 no epilogue, 2 no MMAs,
                               // 4 epilogue TMEM reads without the arithmetic, 8 matrix ring (not resident),
                               // 16 per-pass planes (n > 255); bx_score_host: 64 the copy path for
-                              // packed pinned pools instead of zero-copy
+                              // packed pinned pools instead of zero-copy, 128 the zero-copy path
+                              // over a device copy of the pool (isolates the bus reads); 32 packed
+                              // rows staged in the row buffer (no separate buffer)
   long long* trace;           // optional role timeline of CTA 0 (BX_TC_TRACE=file), else null
   // streaming host pools: rows arrive by chunks of 2^ready_shift rows; ready[c] != 0 once chunk c
   // is in device memory (written by the copy stream after the chunk), null = all rows present
@@ -566,6 +568,7 @@ struct TcArgs {
   // full rows to f.rows (read by the forest / summary kernels after this one)
   const uint32_t* packed;
   PackSpec pack;
+  int32_t pk_sep;             // set by launch_gp_tc: packed rows in their own staging buffer
 };
 
 

@@ -328,6 +328,10 @@ int bx_score_host(bx_handle* h, const uint32_t* host_rows, int64_t q, int64_t in
     if (cudaPointerGetAttributes(&at, host_rows) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
       mapped = static_cast<const uint32_t*>(at.devicePointer);
     cudaGetLastError();  // pageable memory: clear the attribute query's error, take the copy path
+    if (mapped && (h->tc_debug & 128)) {  // timing experiment: the same path over a device copy
+      BX_CUDA(h, cudaMemcpyAsync(dst, host_rows, (size_t)q * HW * 4, cudaMemcpyHostToDevice, s));
+      mapped = dst;
+    }
   }
   if (mapped && (!forest || qs_summary_available(h->forest)) && !(flags & BX_SCORE_RF_PAIRWISE) &&
       h->pack.pw <= 16) {

@@ -212,7 +212,7 @@ __device__ __forceinline__ void tmem_st2(uint32_t addr, uint32_t v0, uint32_t v1
 }
 
 struct TcLayout {
-  int par, planes, kmask, cval, cmask, exp2, cw, rowscale, yy, rows, stab, emb, emb_tab, mat, bars, total;
+  int par, planes, kmask, cval, cmask, exp2, cw, rowscale, yy, rows, pk, stab, emb, emb_tab, mat, bars, total;
 };
 
 // (chunk c, slice ks <= min(c / 2, nsl - 1)) blocks of the lower triangle, chunk-major: index of
@@ -231,7 +231,7 @@ __host__ __device__ __forceinline__ int tc_block0(int c, int nsl) {
 // |y'|^2 hold only the current pass's 256 columns and the producers reload them every pass.
 __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall, int words, int ks, int n_emb,
                                               int emb_tab_len, bool aug, bool resident, bool pp,
-                                              int stages = kStages) {
+                                              int stages = kStages, int pk_bytes = 0) {
   const int nsl = (n + 31) / 32, nch = n / kN + 1;
   const int npad = pp ? 32 * kSlots : 32 * nsl;  // columns held in shared memory
   TcLayout L;
@@ -259,6 +259,8 @@ __host__ __device__ inline TcLayout tc_layout(int n, int n_params, int n_kendall
   off += (ks > 0 && !aug) ? npad * 8 : 0;
   L.rows = off;      // [128 x row_words] encoded rows of the next tile (bulk-copy staging)
   off += ((kM * words * 4) + 15) & ~15;
+  L.pk = off;        // pk_bytes > 0: [128 x packed words] a tile's packed rows (TcArgs.pk_sep)
+  off += (pk_bytes + 15) & ~15;
   L.stab = off;      // coord_lut / lengthscale of the finite numeric domains (FMA producers)
   off += ks > 0 ? 0 : kMaxCoord * 8;
   L.emb = off;
@@ -295,7 +297,8 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   constexpr int kCvs = kM + 1;        // DMMA mode: candidate-buffer row stride (doubles)
   const int pls = ppad + 4;           // DMMA mode: planes row stride (doubles)
   const bool resident = ta.mat_resident != 0;
-  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident, pp, nst);
+  const TcLayout L = tc_layout(n, n_params, a.n_kendall, words, KS, E, ta.emb_tab_len, ta.aug != 0, resident, pp, nst,
+                               ta.pk_sep ? kM * ta.pack.pw * 4 : 0);
   bx_param_desc* params = reinterpret_cast<bx_param_desc*>(smem + L.par);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem + L.planes);
   uint64_t* kmask = reinterpret_cast<uint64_t*>(smem + L.kmask);
@@ -322,6 +325,11 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
   uint64_t* cval_free = cval_full + 2;   // [2] every producer is done with them
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cval_free + 2);
   uint32_t* rowsbuf = reinterpret_cast<uint32_t*>(smem + L.rows);
+  // pk_sep: packed rows land in their own buffer, released as soon as the decoders hold them in
+  // registers, so the prefetcher fetches the next tile (over the bus, for a zero-copy host pool)
+  // while this one is being decoded; else they land at the end of the staging buffer
+  uint32_t* pkbuf = reinterpret_cast<uint32_t*>(smem + L.pk);
+  const bool pk_sep = ta.pk_sep != 0;
   // rows are staged by 16-byte bulk copies when the pool pointer allows it
   const bool stage_rows = (reinterpret_cast<uintptr_t>(a.rows) & 15) == 0;
 
@@ -442,10 +450,13 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
             const int o = cc * pw + w;
-            pk[h2][w] = (w < pw && gi < a.q) ? (o < spw ? rowsbuf[pk_off + o] : ta.packed[(size_t)gi * pw + w]) : 0u;
+            pk[h2][w] = (w < pw && gi < a.q)
+                            ? (o < spw ? (pk_sep ? pkbuf[o] : rowsbuf[pk_off + o]) : ta.packed[(size_t)gi * pw + w])
+                            : 0u;
           }
         }
         asm volatile("bar.sync 3, 64;" ::: "memory");
+        if (pk_sep && dt == 0) mb_arrive(rows_empty);  // the prefetcher may fetch the next tile now
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
           const int cc = dt + 64 * h2;
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
         }
         asm volatile("bar.sync 3, 64;" ::: "memory");
         if (dt == 0) {
-          mb_arrive(rows_empty);
+          if (!(ta.packed && pk_sep)) mb_arrive(rows_empty);
           mb_arrive(&cval_full[0]);
         }
         continue;
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
         cv[idx] = v;
       }
       asm volatile("bar.sync 3, 64;" ::: "memory");
-      if (dt == 0) mb_arrive(rows_empty);
+      if (dt == 0 && !(ta.packed && pk_sep)) mb_arrive(rows_empty);
       uint64_t* cm = cmask + (size_t)buf * a.n_kendall * kM * 2;
       for (int idx = dt; idx < a.n_kendall * kM; idx += 64) {
         const int kk = idx / kM, cc = idx % kM;
@@ -540,7 +551,7 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       if (sw > 0) {
         mb_expect(rows_full, (uint32_t)sw * 4);
         if (ta.packed)
-          bulk_g2s(rowsbuf + pk_off, ta.packed + (size_t)tile * kM * pw, (uint32_t)sw * 4, rows_full);
+          bulk_g2s(pk_sep ? pkbuf : rowsbuf + pk_off, ta.packed + (size_t)tile * kM * pw, (uint32_t)sw * 4, rows_full);
         else
           bulk_g2s(rowsbuf, a.rows + (size_t)tile * kM * words, (uint32_t)sw * 4, rows_full);
       } else {
@@ -1100,14 +1111,25 @@ cudaError_t launch_gp_tc(const TcArgs& a0, int sm_count, cudaStream_t s) {
     a.mat_stages = std::max(kStages, std::min(kMaxStages, (227 * 1024 - base) / kMatBlock));
     if (const char* st = getenv("BX_TC_STAGES")) a.mat_stages = std::max(2, std::min(a.mat_stages, atoi(st)));
   }
-  const TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0,
-                               a.planes_pp != 0, a.mat_stages);
+  TcLayout L = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0,
+                         a.planes_pp != 0, a.mat_stages);
+  // packed pools: their own staging buffer when it fits next to everything else (BX_TC_DEBUG bit
+  // 32: never), the static shared memory counted
+  a.pk_sep = 0;
+  if (a.packed && !(a.debug & 32)) {
+    const TcLayout L2 = tc_layout(n, P, K, W, a.ks, a.n_emb, a.emb_tab_len, a.aug != 0, a.mat_resident != 0,
+                                  a.planes_pp != 0, a.mat_stages, kM * a.pack.pw * 4);
+    if (L2.total + 1024 <= 227 * 1024) {
+      a.pk_sep = 1;
+      L = L2;
+    }
+  }
   if (L.total > 227 * 1024 || a.n_chunks > kMaxChunks || a.ks > 8 || (a.ks > 0 && a.f.precise) ||
       (multi && !a.part))
     return cudaErrorInvalidValue;
   if (getenv("BX_TC_INFO"))  // development aid: kernel geometry
-    fprintf(stderr, "gp_tc: n %d ks %d E %d aug %d smem %d resident %d planes_pp %d stages %d words %d\n", n, a.ks,
-            a.n_emb, a.aug, L.total, a.mat_resident, a.planes_pp, a.mat_stages, W);
+    fprintf(stderr, "gp_tc: n %d ks %d E %d aug %d smem %d resident %d planes_pp %d stages %d words %d pk_sep %d\n", n,
+            a.ks, a.n_emb, a.aug, L.total, a.mat_resident, a.planes_pp, a.mat_stages, W, a.pk_sep);
   auto kernel = a.f.precise ? (multi ? gp_tc_kernel<true, 0, true> : gp_tc_kernel<true, 0, false>)
                             : (multi ? gp_tc_kernel<false, 0, true> : gp_tc_kernel<false, 0, false>);
   int threads = tc_threads<0>();
