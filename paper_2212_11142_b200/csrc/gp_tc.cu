@@ -465,7 +465,12 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
             uint32_t* dstr = rowsbuf + cc * words;
             unpack_row(ta.pack, pk[h2], dstr, words);
             uint32_t* g = const_cast<uint32_t*>(a.rows) + (size_t)gi * words;
-            for (int w = 0; w < words; ++w) g[w] = dstr[w];
+            if ((words & 3) == 0 && stage_rows) {  // 16-byte stores (16-byte aligned pool and rows)
+              for (int w = 0; w < words; w += 4)
+                *reinterpret_cast<uint4*>(g + w) = *reinterpret_cast<const uint4*>(dstr + w);
+            } else {
+              for (int w = 0; w < words; ++w) g[w] = dstr[w];
+            }
           }
         }
         asm volatile("bar.sync 3, 64;" ::: "memory");
