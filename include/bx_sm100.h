@@ -305,7 +305,9 @@ int bx_rf_predict(bx_handle* h, const uint32_t* dev_rows, int64_t q, int32_t fla
    one neighbour gets the forest's q == 1 summation order, feasibility.py:89), each start moved to
    its argbest under (value desc, configuration asc) iff strictly better (:87-94, :200), every
    scored neighbour folded into the best-unevaluated tracker (:105-111).  host_best is the tracker
-   in / out (index < 0: empty; value, row).  One 4-byte device -> host read per step. */
+   in / out (index < 0: empty; value, row).  Steps are issued four at a time with one 4-byte
+   device -> host read per four (a step after every start stopped changes nothing); *host_steps =
+   the steps that had a climbing start, the reference's loop count. */
 int bx_climb(bx_handle* h, const uint32_t* dev_pool_rows, const int64_t* host_start_index,
              const double* host_start_values, int32_t n_starts, int32_t use_cot, double f_model, double eps_f,
              int32_t max_steps, bx_cand* host_best, int32_t* host_steps, void* stream);
