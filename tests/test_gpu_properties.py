@@ -202,6 +202,39 @@ def test_streaming_host_pool_matches_device_pool(case, q, eps, walk, monkeypatch
     sc.close()
 
 
+@pytest.mark.parametrize("n,q", [(300, 70001), (1000, 40003)])
+def test_packed_host_pool_with_several_column_passes(n, q):
+    """The packed host paths (zero-copy from pinned memory, chunked copies from pageable memory)
+    through the multi-pass posterior (n > 255: its own packed staging buffer when it fits next to
+    the per-pass state) give bx_score's summary on the same rows; ragged pool sizes."""
+    from paper_2212_11142_b200 import scenarios
+    from paper_2212_11142_b200.device import Scorer
+    from paper_2212_11142_b200.models import GPState, Hyper
+
+    space = scenarios.build_space("C5", _bt.space)
+    rng = np.random.default_rng(n + 7)
+    sc = Scorer()
+    lay = sc.set_space(space)
+    cfgs = lay.decode(scenarios.sample_rows_uniform(lay, n, rng))
+    y = np.array([scenarios.objective("C5", c) for c in cfgs])
+    hyp = Hyper(outputscale=1.3, noise_variance=1e-4,
+                lengthscales=tuple(rng.uniform(0.8, 3.0, len(space.parameters))))
+    gp = GPState.fit(space, cfgs, y, hyp, scorer=sc)
+    sc.set_gp(gp)
+    assert sc.gp_kernel() == "tensor"
+    rows_h = scenarios.sample_rows_uniform(lay, q, rng)
+    f = gp.objective_to_model(float(np.min(y)))
+    x, _, _ = sc.score(sc.to_device(rows_h), f, 0.0, k=10)
+    packed_h = sc.pack(rows_h)
+    packed = torch.from_numpy(packed_h.view(np.int32)).pin_memory()
+    for yv in (sc.score_host(packed.numpy().view(np.uint32), f, 0.0, k=10, packed=True),
+               sc.score_host(packed_h, f, 0.0, k=10, packed=True)):
+        assert (x.n_scored, x.n_finite) == (yv.n_scored, yv.n_finite)
+        assert [(c.index, c.value, tuple(c.row)) for c in x.top] == [(c.index, c.value, tuple(c.row)) for c in yv.top]
+        assert (x.best.index, tuple(x.best.row)) == (yv.best.index, tuple(yv.best.row))
+    sc.close()
+
+
 @pytest.mark.parametrize("case", ["mixed_fit", "mixed_metrics", "C1", "C2", "C3", "C4", "M200"])
 def test_packed_wire_format_round_trip(case):
     """bx_pack_rows / bx_unpack_rows: every parameter at its bit width, real coordinates recomputed
