@@ -8,14 +8,13 @@ logic of the hill climb.
 """
 from __future__ import annotations
 
-import math
 
 import numpy as np
 import torch
 
 from . import _native as N
 from . import sampling
-from .device import Candidate, Scorer, scorer
+from .device import Scorer, scorer
 
 N_CANDIDATES = 5000   # acquisition.py:23
 N_STARTS = 10         # acquisition.py:24
