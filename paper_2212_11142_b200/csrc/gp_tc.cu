@@ -439,41 +439,61 @@ __global__ void __launch_bounds__((tc_threads<KS>()), 1) gp_tc_kernel(TcArgs ta)
       mb_wait_sleep(rows_full, (uint32_t)(t & 1));
       int sw = staged_words(tile);
       if (ta.packed) {
-        // unpack: packed rows (staged or, for a ragged tail, global) into registers, then the full
-        // rows into the staging buffer and to HBM (the forest / summary kernels read them)
+        // unpack: packed rows (staged or, for a ragged tail, global) into full rows in the staging
+        // buffer and to HBM (the forest / summary kernels read them)
         const int spw = staged_packed(tile);
-        uint32_t pk[2][16];
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int cc = dt + 64 * h2;
-          const int64_t gi = tile * kM + cc;
-#pragma unroll
-          for (int w = 0; w < 16; ++w) {
-            const int o = cc * pw + w;
-            pk[h2][w] = (w < pw && gi < a.q)
-                            ? (o < spw ? (pk_sep ? pkbuf[o] : rowsbuf[pk_off + o]) : ta.packed[(size_t)gi * pw + w])
-                            : 0u;
+        auto write_back = [&](const uint32_t* dstr, int64_t gi) {
+          uint32_t* g = const_cast<uint32_t*>(a.rows) + (size_t)gi * words;
+          if ((words & 3) == 0 && stage_rows) {  // 16-byte stores (16-byte aligned pool and rows)
+            for (int w = 0; w < words; w += 4)
+              *reinterpret_cast<uint4*>(g + w) = *reinterpret_cast<const uint4*>(dstr + w);
+          } else {
+            for (int w = 0; w < words; ++w) g[w] = dstr[w];
           }
-        }
-        asm volatile("bar.sync 3, 64;" ::: "memory");
-        if (pk_sep && dt == 0) mb_arrive(rows_empty);  // the prefetcher may fetch the next tile now
+        };
+        if (pk_sep) {
+          // packed rows in their own buffer: unpacked straight from it (or, for a ragged tail,
+          // from global), then the buffer goes back to the prefetcher for the next tile
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int cc = dt + 64 * h2;
-          const int64_t gi = tile * kM + cc;
-          if (gi < a.q) {
-            uint32_t* dstr = rowsbuf + cc * words;
-            unpack_row(ta.pack, pk[h2], dstr, words);
-            uint32_t* g = const_cast<uint32_t*>(a.rows) + (size_t)gi * words;
-            if ((words & 3) == 0 && stage_rows) {  // 16-byte stores (16-byte aligned pool and rows)
-              for (int w = 0; w < words; w += 4)
-                *reinterpret_cast<uint4*>(g + w) = *reinterpret_cast<const uint4*>(dstr + w);
-            } else {
-              for (int w = 0; w < words; ++w) g[w] = dstr[w];
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int cc = dt + 64 * h2;
+            const int64_t gi = tile * kM + cc;
+            if (gi < a.q) {
+              const uint32_t* src = (cc + 1) * pw <= spw ? pkbuf + cc * pw : ta.packed + (size_t)gi * pw;
+              uint32_t* dstr = rowsbuf + cc * words;
+              unpack_row(ta.pack, src, dstr, words);
+              write_back(dstr, gi);
             }
           }
+          asm volatile("bar.sync 3, 64;" ::: "memory");
+          if (dt == 0) mb_arrive(rows_empty);  // the prefetcher may fetch the next tile now
+        } else {
+          // packed rows at the end of the staging buffer: every thread takes its packed rows into
+          // registers before any full row overwrites them
+          uint32_t pk[2][16];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int cc = dt + 64 * h2;
+            const int64_t gi = tile * kM + cc;
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+              const int o = cc * pw + w;
+              pk[h2][w] = (w < pw && gi < a.q) ? (o < spw ? rowsbuf[pk_off + o] : ta.packed[(size_t)gi * pw + w]) : 0u;
+            }
+          }
+          asm volatile("bar.sync 3, 64;" ::: "memory");
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int cc = dt + 64 * h2;
+            const int64_t gi = tile * kM + cc;
+            if (gi < a.q) {
+              uint32_t* dstr = rowsbuf + cc * words;
+              unpack_row(ta.pack, pk[h2], dstr, words);
+              write_back(dstr, gi);
+            }
+          }
+          asm volatile("bar.sync 3, 64;" ::: "memory");
         }
-        asm volatile("bar.sync 3, 64;" ::: "memory");
         sw = (int)(min((int64_t)kM, a.q - tile * kM) * words);  // every row is now staged
       }
       if constexpr (kDmma) {
