@@ -249,7 +249,8 @@ def optimize_acquisition(ctx, space, cot=None, sample_fn=None, local_search: boo
     best = summ.best
     if local_search:
         # the climb of every start runs on the device (bx_climb): per step one neighbour launch, the
-        # scoring launches and one bookkeeping launch, and a single 4-byte read of the active count.
+        # scoring launches and one bookkeeping launch; one 4-byte read of the active count per four
+        # steps.
         # Each start's trajectory depends only on its own state and the tracker is a maximum under a
         # total order (value desc, configuration asc), so the lockstep result equals the reference's
         # start-after-start loop (acquisition.py:186-205).

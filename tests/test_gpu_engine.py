@@ -190,6 +190,39 @@ def test_device_climb_matches_reference_climb_with_many_starts():
         assert got == want, n_starts
 
 
+@pytest.mark.parametrize("cap", [1, 2, 3, 5, 7, 50])
+def test_device_climb_step_cap_matches_reference(cap, monkeypatch):
+    """The climb's steps go out four per device -> host read; a cap that is not a multiple of four
+    still stops every start after exactly `cap` steps (MAX_CLIMB_STEPS patched on both sides), and
+    the reported step count is the reference loop's (the longest start's iterations, <= cap)."""
+    from golden_io import Ctx, load, ref_model, to_cfg
+    from paper_2212_11142_b200 import acquisition as A
+    from paper_2212_11142_b200 import device as D
+    bt = ref()
+    meta, arr, space = load("mixed_fit")
+    gp, feas = ref_model(meta, arr, space)
+    cands = [to_cfg(space, c) for c in meta["cands"][:800]]
+    evaluated = {to_cfg(space, c) for c in meta["evaluated"]}
+    monkeypatch.setattr(bt.acquisition, "MAX_CLIMB_STEPS", cap)
+    monkeypatch.setattr(A, "MAX_CLIMB_STEPS", cap)
+    steps = []
+    orig = D.Scorer.climb
+
+    def climb(self, *a, **k):
+        out = orig(self, *a, **k)
+        steps.append(out[1])
+        return out
+    monkeypatch.setattr(D.Scorer, "climb", climb)
+    want = bt.optimize_acquisition(
+        bt.AcquisitionContext(gp=gp, feas=feas, best_feasible_value=meta["f_best"], eps_f=meta["eps_f"],
+                              rng=np.random.default_rng(0), evaluated=evaluated), space, None,
+        sample_fn=lambda n, r: cands)
+    got = A.optimize_acquisition(Ctx(gp, feas, meta["f_best"], meta["eps_f"], np.random.default_rng(0), evaluated),
+                                 space, None, sample_fn=lambda n, r: cands)
+    assert got == want
+    assert steps and all(1 <= s <= cap for s in steps)
+
+
 def test_reference_model_objects_reach_the_gpu():
     """The reference's own GPModel / FeasibilityModel / ChainOfTrees / SearchSpace objects are
     consumed as they are (the fixtures' models rebuilt through the reference constructors)."""
