@@ -462,14 +462,18 @@ struct PackSpec {
   int32_t n, pw;  // parameters, packed words per row
   PackParam p[BX_MAX_PARAMS];
 };
+// bits 1..64 starting at bit `bit`: a 64-bit window over the field's first two words (a third
+// only when a wide field straddles it); never reads a word the field does not touch
 __host__ __device__ __forceinline__ uint64_t pk_get(const uint32_t* pk, int bit, int bits) {
-  uint64_t v = 0;
-  for (int got = 0; got < bits;) {  // at most 32 bits per word step
-    const int w = (bit + got) >> 5, o = (bit + got) & 31, take = (32 - o < bits - got) ? 32 - o : bits - got;
-    v |= (uint64_t)((pk[w] >> o) & (take == 32 ? 0xFFFFFFFFu : ((1u << take) - 1u))) << got;
-    got += take;
+  const int w = bit >> 5, o = bit & 31;
+  if (bits <= 32) {
+    uint64_t win = pk[w];
+    if (o + bits > 32) win |= (uint64_t)pk[w + 1] << 32;
+    return (win >> o) & (bits == 32 ? 0xFFFFFFFFull : ((1ull << bits) - 1));
   }
-  return v;
+  uint64_t v = ((uint64_t)pk[w] | ((uint64_t)pk[w + 1] << 32)) >> o;
+  if (o > 0 && o + bits > 64) v |= (uint64_t)pk[w + 2] << (64 - o);
+  return bits == 64 ? v : (v & ((1ull << bits) - 1));
 }
 __host__ __device__ __forceinline__ void pk_put(uint32_t* pk, int bit, int bits, uint64_t v) {
   for (int put = 0; put < bits;) {
