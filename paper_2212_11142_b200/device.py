@@ -34,7 +34,7 @@ def _host(a, dtype) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=dtype))
 
 
-@dataclass
+@dataclass(slots=True)
 class Candidate:
     value: float
     prob: float
@@ -49,6 +49,9 @@ class Summary:
     top: list          # [Candidate], stable argsort(-values)[:k] with -inf excluded
     best: Candidate | None       # tracker over values (unevaluated, finite)
     best_prob: Candidate | None  # tracker over probabilities (unevaluated)
+
+
+_CAND_SIZE, _TOP_OFF, _ROW_OFF = C.sizeof(N.Cand), N.ScoreSummary.top.offset, N.Cand.row.offset
 
 
 def _cand(c: N.Cand, words: int) -> Candidate | None:
@@ -199,9 +202,13 @@ class Scorer:
 
     # -- hot path -------------------------------------------------------------------------------
     def _summary(self, s: N.ScoreSummary) -> Summary:
-        w = self.layout.row_words
-        top = [_cand(s.top[i], w) for i in range(s.n_top)]
-        return Summary(int(s.n_scored), int(s.n_finite), top, _cand(s.best, w), _cand(s.best_prob, w))
+        w, n = self.layout.row_words, s.n_top
+        # the top-k rows in one copy out of the struct (rows[i] are views of it)
+        raw = np.frombuffer(s, dtype=np.uint8)
+        rows = raw[_TOP_OFF:_TOP_OFF + n * _CAND_SIZE].reshape(n, _CAND_SIZE)[:, _ROW_OFF:_ROW_OFF + 4 * w]
+        rows = rows.copy().view(np.uint32)
+        top = [Candidate(c.value, c.prob, c.index, rows[i]) for i, c in enumerate(s.top[:n])]
+        return Summary(s.n_scored, s.n_finite, top, _cand(s.best, w), _cand(s.best_prob, w))
 
     def score(self, rows: torch.Tensor, f_model: float, eps_f: float = 0.0, k: int = 10,
               want_values: bool = False, summary: bool = True, rf_pairwise: bool | None = None,
