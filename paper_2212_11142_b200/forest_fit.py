@@ -63,16 +63,24 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
     lib = sc._lib
     Xc = np.ascontiguousarray(X, dtype=np.float64)
     yc = np.ascontiguousarray(y, dtype=np.float64)
-    trees = [None] * n_trees
-    todo = list(range(n_trees))
-    while todo:
-        max_draws = max(len(draws[t]) for t in todo)
+    # every tree's node arrays, [tree][node] (a tree finishes in the round whose draws sufficed)
+    all_f = np.empty((n_trees, max_nodes), np.int32)
+    all_t = np.empty((n_trees, max_nodes), np.float64)
+    all_l = np.empty((n_trees, max_nodes), np.int32)
+    all_r = np.empty((n_trees, max_nodes), np.int32)
+    all_v = np.empty((n_trees, max_nodes), np.float64)
+    all_n = np.zeros(n_trees, np.int64)
+    todo = np.arange(n_trees)
+    while len(todo):
+        lens = np.array([len(draws[t]) for t in todo], dtype=np.int32)
+        max_draws = int(lens.max())
         T = len(todo)
-        feats = np.zeros((T, max_draws, k), dtype=np.int32)
-        nd = np.zeros(T, dtype=np.int32)
-        for i, t in enumerate(todo):
-            feats[i, :len(draws[t])] = draws[t]
-            nd[i] = len(draws[t])
+        if (lens == max_draws).all():
+            feats = np.ascontiguousarray(np.stack([draws[t] for t in todo]), dtype=np.int32)
+        else:
+            feats = np.zeros((T, max_draws, k), dtype=np.int32)
+            for i, t in enumerate(todo):
+                feats[i, :lens[i]] = draws[t]
         out_f = np.empty((T, max_nodes), np.int32)
         out_t = np.empty((T, max_nodes), np.float64)
         out_l = np.empty((T, max_nodes), np.int32)
@@ -81,35 +89,28 @@ def rf_fit(space, configs, labels, rng, n_trees=_DEFAULT, max_depth=_DEFAULT, us
         out_n = np.empty(T, np.int32)
         out_s = np.empty(T, np.int32)
         p = lambda a: a.ctypes.data_as(C.c_void_p)
-        sc._check(lib.bx_rf_fit(sc.h, p(Xc), p(yc), n, F, T, p(np.ascontiguousarray(boot[todo])), p(feats), p(nd),
+        sc._check(lib.bx_rf_fit(sc.h, p(Xc), p(yc), n, F, T, p(np.ascontiguousarray(boot[todo])), p(feats), p(lens),
                                 max_draws, k, max_depth, max_nodes, p(out_f), p(out_t), p(out_l), p(out_r), p(out_v),
                                 p(out_n), p(out_s), sc.stream))
-        again = []
-        for i, t in enumerate(todo):
-            if out_s[i] == 1:  # more feature subsets: continue the tree's own generator
-                streams.more(t, DRAWS)
-                again.append(t)
-            elif out_s[i] != 0:
-                raise N.NativeError(N.BX_ERR_UNSUPPORTED, f"rf_fit: tree {t} exceeded {max_nodes} nodes")
-            else:
-                m = int(out_n[i])
-                trees[t] = (out_f[i, :m].copy(), out_t[i, :m].copy(), out_l[i, :m].copy(), out_r[i, :m].copy(),
-                            out_v[i, :m].copy())
-        todo = again
-    feature, threshold, left, right, value, roots = [], [], [], [], [], []
-    base = 0
-    for f, th, lft, rgt, v in trees:  # the reference appends tree after tree to flat arrays
-        roots.append(base)
-        feature.append(f)
-        threshold.append(th)
-        left.append(np.where(lft >= 0, lft + base, -1))
-        right.append(np.where(rgt >= 0, rgt + base, -1))
-        value.append(v)
-        base += len(f)
-    model.feature = np.concatenate(feature).astype(np.int32)
-    model.threshold = np.concatenate(threshold)
-    model.left = np.concatenate(left).astype(np.int32)
-    model.right = np.concatenate(right).astype(np.int32)
-    model.value = np.concatenate(value)
-    model.roots = np.asarray(roots, np.int32)
+        bad = np.flatnonzero((out_s != 0) & (out_s != 1))
+        if len(bad):
+            raise N.NativeError(N.BX_ERR_UNSUPPORTED, f"rf_fit: tree {int(todo[bad[0]])} exceeded {max_nodes} nodes")
+        done = out_s == 0
+        for dst, src in ((all_f, out_f), (all_t, out_t), (all_l, out_l), (all_r, out_r), (all_v, out_v)):
+            dst[todo[done]] = src[done]
+        all_n[todo[done]] = out_n[done]
+        for t in todo[~done]:  # more feature subsets: continue the tree's own generator
+            streams.more(int(t), DRAWS)
+        todo = todo[~done]
+    # the reference appends tree after tree to flat arrays: node j of tree t at roots[t] + j, child
+    # indices shifted by the tree's base
+    roots = np.cumsum(all_n) - all_n
+    keep = np.arange(max_nodes)[None, :] < all_n[:, None]
+    shift = roots[:, None]
+    model.feature = all_f[keep].astype(np.int32)
+    model.threshold = all_t[keep]
+    model.left = np.where(all_l >= 0, all_l + shift, -1)[keep].astype(np.int32)
+    model.right = np.where(all_r >= 0, all_r + shift, -1)[keep].astype(np.int32)
+    model.value = all_v[keep]
+    model.roots = roots.astype(np.int32)
     return model
