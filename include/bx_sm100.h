@@ -277,6 +277,11 @@ int bx_pcg64_choice(uint64_t* state, int32_t* has_uint32, uint32_t* uinteger, in
 int bx_pcg64_forest_draws(const uint64_t* seeds, int32_t n_trees, int64_t n, int32_t pop, int32_t k, int32_t ndraws,
                           int32_t* boot, int32_t* subsets, uint64_t* state, int32_t* has_uint32, uint32_t* uinteger);
 
+/* Host-side: first-occurrence de-duplication of q encoded rows (list(dict.fromkeys(raw)),
+   acquisition.py:173): writes the indices of the first occurrences, in order, to first_idx[q] and
+   returns their count (negative: -bx_status).  No device work. */
+int64_t bx_unique_rows(const uint32_t* rows, int64_t q, int32_t words, int64_t* first_idx);
+
 /* Device-side candidate generation: q rows for global indices
    index_base .. index_base+q-1 from Philox4x32-10 keyed by (seed, index); mode 0 = uniform over the
    dense space (sample_uniform's distribution, space.py:312-332), mode 1 = leaf-uniform over the

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "libbx_sm100.so"
-SOURCES = ["host_rng.cu", "bx_api.cu", "bx_model.cu", "bx_score.cu", "bx_lml.cu", "score.cu", "score_summary.cu", "gp_fused.cu", "gp_tc.cu", "forest.cu", "feasible.cu",
+SOURCES = ["host_rng.cu", "host_rows.cu", "bx_api.cu", "bx_model.cu", "bx_score.cu", "bx_lml.cu", "score.cu", "score_summary.cu", "gp_fused.cu", "gp_tc.cu", "forest.cu", "feasible.cu",
            "gp_linalg.cu", "probe.cu", "merge.cu", "generate.cu", "lml_wide.cu", "forest_fit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -148,16 +148,17 @@ def rejection_rows(lay, n: int, rng, feasible) -> np.ndarray:
 
 
 def unique_rows(rows: np.ndarray) -> np.ndarray:
-    """First occurrences, in order (list(dict.fromkeys(configs)))."""
+    """First occurrences, in order (list(dict.fromkeys(configs))): bx_unique_rows, a hash set over
+    the rows in one pass."""
     if len(rows) < 2:
         return rows
-    rows = np.ascontiguousarray(rows)
-    key = rows.view(np.dtype((np.void, rows.shape[1] * 4))).ravel()
-    _, first = np.unique(key, return_index=True)
-    if len(first) == len(rows):
-        return rows
-    first.sort()
-    return rows[first]
+    rows = np.ascontiguousarray(rows, dtype=np.uint32)
+    first = np.empty(len(rows), dtype=np.int64)
+    n = N.lib().bx_unique_rows(rows.ctypes.data_as(C.c_void_p), len(rows), rows.shape[1],
+                               first.ctypes.data_as(C.c_void_p))
+    if n < 0:
+        raise N.NativeError(int(-n), "bx_unique_rows")
+    return rows if n == len(rows) else rows[first[:n]]
 
 
 def _pcg64_call(rng, fn, *args):

@@ -68,3 +68,19 @@ def test_package_refuses_cpu_execution():
     from paper_2212_11142_b200.device import Scorer
     with pytest.raises(RuntimeError, match="CUDA"):
         Scorer()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_unique_rows_is_dict_fromkeys_order(seed):
+    """bx_unique_rows (host code) keeps the first occurrence of every row in draw order, as
+    list(dict.fromkeys(raw)) does (acquisition.py:173) - pools full of repeats, ragged widths."""
+    import numpy as np
+
+    from paper_2212_11142_b200 import sampling
+    rng = np.random.default_rng(seed)
+    for _ in range(60):
+        q, w = int(rng.integers(2, 4000)), int(rng.integers(1, 20))
+        rows = rng.integers(0, int(rng.integers(2, 5)), size=(q, w)).astype(np.uint32)
+        want = np.array(list(dict.fromkeys(map(tuple, rows))), dtype=np.uint32).reshape(-1, w)
+        assert np.array_equal(sampling.unique_rows(rows), want)
+    assert N.lib().bx_unique_rows(None, -1, 4, None) < 0
