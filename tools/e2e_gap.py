@@ -48,6 +48,5 @@ run("bx_score device rows", lambda: sc.score(rows, f_model, eps, k=10))
 run("bx_score device rows + timing", lambda: sc.score(rows, f_model, eps, k=10, timing=True))
 print("   kernels:", sc.last_timing())
 run("bx_score_host packed pinned", lambda: sc.score_host(packed_h, f_model, eps, k=10, packed=True))
-run("bx_score_host encoded pinned", lambda: sc.score_host(
-    torch.from_numpy(rows_h.view(np.int32)).pin_memory().numpy().view(np.uint32) if False else rows_pinned,
-    f_model, eps, k=10)) if (rows_pinned := torch.from_numpy(rows_h.view(np.int32)).pin_memory().numpy().view(np.uint32)) is not None else None
+rows_pinned = torch.from_numpy(rows_h.view(np.int32)).pin_memory().numpy().view(np.uint32)
+run("bx_score_host encoded pinned", lambda: sc.score_host(rows_pinned, f_model, eps, k=10))
