@@ -113,23 +113,35 @@ __global__ void climb_update_kernel(SpaceDev sp, EvalSetDev ev, int A, int S, in
       for (int w = lane; w < W; w += 32) cur[(size_t)a * W + w] = nb[(size_t)mr * W + w];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int n_active = 0;
-    for (int i = 0; i < A; ++i) {
-      n_active += s_moved[i] >= 0 ? 1 : 0;
-      const int r = s_trk[i];
-      if (r < 0) continue;
-      const double v = vals[r];
-      const uint32_t* row = nb + (size_t)r * W;
-      bool take = st->best.index < 0 || v > st->best.value;
-      if (!take && v == st->best.value) take = key_cmp(sp.params, sp.n_params, sp.rank_lut, row, st->best_row) < 0;
-      if (take) {
-        st->best = TopRec{v, 0.0, 0};
-        for (int w = 0; w < W; ++w) st->best_row[w] = row[w];
+  if (threadIdx.x < 32) {
+    // warp 0: the starts' tracker candidates reduced under the tracker's total order (value desc,
+    // configuration asc) - the maximum the start-by-start fold reaches - then one fold into it
+    const int i = threadIdx.x;
+    int r = i < A ? s_trk[i] : -1;
+    double v = r >= 0 ? vals[r] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int orow = __shfl_xor_sync(0xffffffffu, r, o);
+      if (climb_better(sp, nb, W, ov, orow, v, r)) {
+        v = ov;
+        r = orow;
       }
     }
-    st->n_active = n_active;
-    st->steps += s_any;  // a step after every start stopped (a batched launch) changes nothing
+    const unsigned moved = __ballot_sync(0xffffffffu, i < A && s_moved[i] >= 0);
+    if (i == 0) {
+      if (r >= 0) {
+        const uint32_t* row = nb + (size_t)r * W;
+        bool take = st->best.index < 0 || v > st->best.value;
+        if (!take && v == st->best.value) take = key_cmp(sp.params, sp.n_params, sp.rank_lut, row, st->best_row) < 0;
+        if (take) {
+          st->best = TopRec{v, 0.0, 0};
+          for (int w = 0; w < W; ++w) st->best_row[w] = row[w];
+        }
+      }
+      st->n_active = __popc(moved);
+      st->steps += s_any;  // a step after every start stopped (a batched launch) changes nothing
+    }
   }
 }
 }  // namespace bx
