@@ -348,6 +348,12 @@ int bx_lml_core(bx_handle* h, const double* dev_sq, int32_t n, int32_t D, const 
                 const double* dev_params, int32_t c, double prior_shape, double prior_rate,
                 int32_t use_prior, int32_t want_grad, double* dev_value, double* dev_grad,
                 int32_t* dev_ok, void* stream);
+/* ... the same with host parameters and host results (gradient always): host_params[c][2+D] in,
+   host_value[c], host_grad[c][2+D], host_ok[c] out through one pinned staging buffer; returns
+   after the results are in host memory (hyperfit's L-BFGS-B objective, surrogate.py:510-516). */
+int bx_lml_core_host(bx_handle* h, const double* dev_sq, int32_t n, int32_t D, const double* dev_z,
+                     const double* host_params, int32_t c, double prior_shape, double prior_rate, int32_t use_prior,
+                     double* host_value, double* host_grad, int32_t* host_ok, void* stream);
 
 /* Per-parameter squared distances between rows (pairwise_sq_distances, surrogate.py:173-198),
    dev_out: D x qa x qb f64. */

@@ -30,7 +30,7 @@ EXPORTED = (
     "bx_set_cot", "bx_clear_cot", "bx_set_constraints", "bx_score", "bx_score_host",
     "bx_gp_predict", "bx_rf_predict", "bx_neighbor_slots", "bx_neighbors", "bx_climb", "bx_rf_fit", "bx_cot_contains",
     "bx_constraints_eval", "bx_lml_batched", "bx_pairwise_sq", "bx_last_timing", "bx_probe_fp64", "bx_probe_int8",
-    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps", "bx_gp_embedding_dims", "bx_pcg64_permutations", "bx_pcg64_choice", "bx_pcg64_forest_draws", "bx_unique_rows", "bx_gp_factor", "bx_set_option", "bx_packed_row_words", "bx_pack_rows", "bx_unpack_rows",
+    "bx_lml_core", "bx_generate", "bx_score_generated", "bx_gp_kernel", "bx_gp_distance_ksteps", "bx_gp_embedding_dims", "bx_pcg64_permutations", "bx_pcg64_choice", "bx_pcg64_forest_draws", "bx_unique_rows", "bx_lml_core_host", "bx_gp_factor", "bx_set_option", "bx_packed_row_words", "bx_pack_rows", "bx_unpack_rows",
 )
 BX_SCORE_TIMING = 4
 BX_SCORE_TIMING_POSTERIOR = 8
@@ -80,6 +80,7 @@ _SIGS = {
     "bx_pcg64_choice": (C.c_int, [_p, _p, _p, _i64, _i32, _i32, _p]),
     "bx_pcg64_forest_draws": (C.c_int, [_p, _i32, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _p]),
     "bx_unique_rows": (_i64, [_p, _i64, _i32, _p]),
+    "bx_lml_core_host": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _f64, _f64, _i32, _p, _p, _p, _p]),
     "bx_gp_factor": (C.c_int, [_p, _p, _i32, _p, _f64, _f64, _p, _p, _p, _p]),
     "bx_set_option": (C.c_int, [_p, _i32, _i32]),
     "bx_packed_row_words": (C.c_int, [_p]),

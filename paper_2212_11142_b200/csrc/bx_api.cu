@@ -85,6 +85,8 @@ void bx_destroy(bx_handle* h) {
   h->d_emb_yy.release();
   if (h->h_ones) cudaFreeHost(h->h_ones);
   if (h->h_climb_flag) cudaFreeHost(h->h_climb_flag);
+  if (h->h_lml_stage) cudaFreeHost(h->h_lml_stage);
+  h->d_lml_stage.release();
   h->d_mdig.release();
   h->d_rowscale.release();
   h->d_tc_part.release();

@@ -128,6 +128,9 @@ struct bx_handle {
   const uint8_t* pw_rows = nullptr;  // per-row forest summation order for the next score_impl (bx_climb)
   DevBuf d_climb;                    // bx_climb scratch
   int32_t* h_climb_flag = nullptr;   // pinned: bx_climb's per-step active count (an async 4-byte read)
+  void* h_lml_stage = nullptr;       // pinned staging of bx_lml_core_host (parameters in, results out)
+  size_t h_lml_stage_bytes = 0;
+  DevBuf d_lml_stage;
   DevBuf d_fit;                      // bx_rf_fit buffers
   DevBuf d_packed;                  // streamed packed pool
   DevBuf d_panels, d_ei, d_grad_scratch, d_leaf_count, d_gen_rows;

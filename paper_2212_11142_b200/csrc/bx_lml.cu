@@ -1,6 +1,8 @@
 // bx_lml.cu — the hyperparameter-fit objectives behind the C ABI: the batched coarse LML
 // (_batched_coarse_lml), _lml_core with its gradient for c settings, and the bit-exact pairwise
 // squared distances (pairwise_sq_distances) they take.
+#include <cstring>
+
 #include "bx_handle.cuh"
 
 extern "C" {
@@ -66,6 +68,44 @@ int bx_lml_core(bx_handle* h, const double* sq, int32_t n, int32_t D, const doub
   BX_CUDA(h, h->d_grad_scratch.ensure(lml_grad_scratch_doubles(n, c) * sizeof(double)));
   BX_CUDA(h, launch_lml_grad(sq, n, D, z, params, c, prior_shape, prior_rate, use_prior, want_grad,
                              value, grad, ok, h->d_grad_scratch.as<double>(), (cudaStream_t)stream));
+  return BX_OK;
+}
+
+// bx_lml_core with host parameters and results (the L-BFGS-B driver's call, hyperfit.py): the
+// settings go up and (values, grads, ok) come back through one pinned staging buffer and one
+// device scratch, one copy each way and one stream synchronisation.
+int bx_lml_core_host(bx_handle* h, const double* sq, int32_t n, int32_t D, const double* z, const double* host_params,
+                     int32_t c, double prior_shape, double prior_rate, int32_t use_prior, double* host_value,
+                     double* host_grad, int32_t* host_ok, void* stream) {
+  if (!h) return BX_ERR_ARG;
+  if (c < 0 || D < 1 || D > BX_MAX_PARAMS) return fail(h, BX_ERR_ARG, "bad lml shape D=%d c=%d", D, c);
+  if (c == 0) return BX_OK;
+  if (!host_params || !host_value || !host_grad || !host_ok) return fail(h, BX_ERR_ARG, "null argument");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t np = (size_t)c * (2 + D), nout = (size_t)c * (3 + D) + ((size_t)c + 1) / 2;  // value, grad, ok
+  const size_t bytes = (np + nout) * sizeof(double);
+  if (h->h_lml_stage_bytes < bytes) {
+    if (h->h_lml_stage) cudaFreeHost(h->h_lml_stage);
+    h->h_lml_stage = nullptr;
+    h->h_lml_stage_bytes = 0;
+    BX_CUDA(h, cudaMallocHost(&h->h_lml_stage, bytes));
+    h->h_lml_stage_bytes = bytes;
+  }
+  BX_CUDA(h, h->d_lml_stage.ensure(bytes));
+  double* hs = static_cast<double*>(h->h_lml_stage);
+  double* ds = h->d_lml_stage.as<double>();
+  std::memcpy(hs, host_params, np * sizeof(double));
+  BX_CUDA(h, cudaMemcpyAsync(ds, hs, np * sizeof(double), cudaMemcpyHostToDevice, s));
+  int32_t* d_ok = reinterpret_cast<int32_t*>(ds + np + (size_t)c * (3 + D));
+  const int r = bx_lml_core(h, sq, n, D, z, ds, c, prior_shape, prior_rate, use_prior, 1, ds + np, ds + np + c, d_ok,
+                            stream);
+  if (r) return r;
+  BX_CUDA(h, cudaMemcpyAsync(hs + np, ds + np, nout * sizeof(double), cudaMemcpyDeviceToHost, s));
+  BX_CUDA(h, cudaStreamSynchronize(s));
+  std::memcpy(host_value, hs + np, (size_t)c * sizeof(double));
+  std::memcpy(host_grad, hs + np + c, (size_t)c * (2 + D) * sizeof(double));
+  std::memcpy(host_ok, hs + np + (size_t)c * (3 + D), (size_t)c * sizeof(int32_t));
   return BX_OK;
 }
 

@@ -371,7 +371,7 @@ constexpr int kSmallLmlMaxN = 232;
 __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* sq, int n, int D, const double* z,
                                                                   const double* prm, double prior_k, double prior_rate,
                                                                   int use_prior, int want_grad, double* out_value,
-                                                                  double* out_grad, int* out_ok) {
+                                                                  double* out_grad, int* out_ok, int sep_x) {
   extern __shared__ __align__(16) double sm[];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int kWarps = kSmallThreads / 32;
@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
   double* Lp = sm;            // [tri]
   double* u = Lp + tri;       // [n]
   double* al = u + n;         // [n]
-  double* col = al + n;       // [n] column j of L while it is inverted
+  double* col = al + n;       // [n] column j of L while it is inverted in place
+  double* Xs = col + n;       // [tri] X = L^-1 beside L when sep_x (launch_lml_small)
   __shared__ double inv_l2[BX_MAX_PARAMS];
   __shared__ double red[kWarps];
   __shared__ int failed;
@@ -494,20 +495,42 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
     out_value[c] = value;
   }
   if (!want_grad) return;
-  // X = L^-1 in place, last column first
-  for (int j = n - 1; j >= 0; --j) {
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) col[i] = Lp[tri_idx(i, j)];
-    __syncthreads();
-    const double xjj = 1.0 / Lp[tri_idx(j, j)];
-    for (int i = j + 1 + warp; i < n; i += kWarps) {
+  // X = L^-1: X_ii = 1 / L_ii, X_ij = -(sum_{k=j+1..i} X_ik L_kj) / L_jj for j < i
+  const double* X = Lp;
+  if (sep_x) {
+    // beside L (which stays intact): a row needs only its own entries and L, so each warp runs its
+    // rows from the diagonal leftwards with no block-wide step - the same sums in the same order
+    // as the in-place sweep below, hence the same bits
+    for (int i = warp; i < n; i += kWarps) {
       const size_t r0 = tri_idx(i, 0);
-      double s = 0.0;
-      for (int k = j + 1 + lane; k <= i; k += 32) s = fma(Lp[r0 + k], col[k], s);
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      if (lane == 0) Lp[r0 + j] = -s * xjj;
+      if (lane == 0) Xs[r0 + i] = 1.0 / Lp[r0 + i];
+      __syncwarp();
+      for (int j = i - 1; j >= 0; --j) {
+        const double xjj = 1.0 / Lp[tri_idx(j, j)];
+        double s = 0.0;
+        for (int k = j + 1 + lane; k <= i; k += 32) s = fma(Xs[r0 + k], Lp[tri_idx(k, j)], s);
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) Xs[r0 + j] = -s * xjj;
+        __syncwarp();
+      }
     }
-    __syncthreads();
-    if (tid == 0) Lp[tri_idx(j, j)] = xjj;
+    X = Xs;
+  } else {
+    // in place, last column first (column j of L saved before its rows are overwritten)
+    for (int j = n - 1; j >= 0; --j) {
+      for (int i = j + 1 + tid; i < n; i += blockDim.x) col[i] = Lp[tri_idx(i, j)];
+      __syncthreads();
+      const double xjj = 1.0 / Lp[tri_idx(j, j)];
+      for (int i = j + 1 + warp; i < n; i += kWarps) {
+        const size_t r0 = tri_idx(i, 0);
+        double s = 0.0;
+        for (int k = j + 1 + lane; k <= i; k += 32) s = fma(Lp[r0 + k], col[k], s);
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) Lp[r0 + j] = -s * xjj;
+      }
+      __syncthreads();
+      if (tid == 0) Lp[tri_idx(j, j)] = xjj;
+    }
   }
   __syncthreads();
   // M = alpha alpha^T - X^T X; gradient sums over the full matrix (symmetric: off-diagonal lower
@@ -521,7 +544,7 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
     while (tri_idx(a, 0) > t) --a;
     const int b = (int)(t - tri_idx(a, 0));  // a >= b
     double kinv = 0.0;
-    for (int k = a; k < n; ++k) kinv = fma(Lp[tri_idx(k, a)], Lp[tri_idx(k, b)], kinv);
+    for (int k = a; k < n; ++k) kinv = fma(X[tri_idx(k, a)], X[tri_idx(k, b)], kinv);
     const double M = al[a] * al[b] - kinv;
     const double w = a == b ? 1.0 : 2.0;
     const size_t e = (size_t)a * n + b;
@@ -535,19 +558,29 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
     const double MG = w * M * ((1.0 + kSqrt5 * d) * E);
     for (int k = 0; k < D; ++k) gl[k] = fma(MG, sq[(size_t)k * nn + e], gl[k]);
   }
-  g0 = block_sum(g0, red);
-  g1 = block_sum(g1, red);
-  double* g = out_grad + (size_t)c * (2 + D);
-  if (tid == 0) {
-    g[0] = 0.5 * g0;
-    g[1] = 0.5 * noise * g1;
+  // the 2 + D block sums in one pass: each warp's xor-reduced partial per quantity, then thread 0
+  // adds the warps in order (block_sum's arithmetic, one barrier instead of 2 (2 + D))
+  __shared__ double red_all[BX_MAX_PARAMS + 2][kWarps];
+  for (int q = 0; q < 2 + D; ++q) {
+    double v = q == 0 ? g0 : (q == 1 ? g1 : gl[q - 2]);
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) red_all[q][warp] = v;
   }
-  const double scale = (5.0 / 6.0) * sigma;
-  for (int k = 0; k < D; ++k) {
-    const double s = block_sum(gl[k], red);
-    if (tid == 0) {
+  __syncthreads();
+  if (tid == 0) {
+    double tot[BX_MAX_PARAMS + 2];
+    for (int q = 0; q < 2 + D; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += red_all[q][w];
+      tot[q] = s;
+    }
+    double* g = out_grad + (size_t)c * (2 + D);
+    g[0] = 0.5 * tot[0];
+    g[1] = 0.5 * noise * tot[1];
+    const double scale = (5.0 / 6.0) * sigma;
+    for (int k = 0; k < D; ++k) {
       const double l = p[2 + k];
-      double gk = (scale / (l * l)) * s;
+      double gk = (scale / (l * l)) * tot[2 + k];
       if (use_prior) gk += (prior_k - 1.0) - prior_rate * l;
       g[2 + k] = gk;
     }
@@ -584,11 +617,14 @@ cudaError_t launch_lml_small(const double* sq, int n, int D, const double* z, co
                              double* out_grad, int* out_ok, cudaStream_t s) {
   if (c <= 0) return cudaSuccess;
   if (!lml_small_supported(n)) return cudaErrorInvalidValue;
-  const size_t bytes = ((size_t)n * (n + 1) / 2 + 3 * (size_t)n) * sizeof(double);
+  const size_t tri = (size_t)n * (n + 1) / 2;
+  // X = L^-1 beside L (warp-per-row inverse, no block barriers) when both triangles fit
+  const int sep_x = want_grad && (2 * tri + 3 * (size_t)n) * sizeof(double) <= 200 * 1024 ? 1 : 0;
+  const size_t bytes = ((sep_x ? 2 : 1) * tri + 3 * (size_t)n) * sizeof(double);
   cudaError_t e = set_smem(lml_small_kernel, (int)bytes);
   if (e != cudaSuccess) return e;
   lml_small_kernel<<<c, kSmallThreads, bytes, s>>>(sq, n, D, z, prm, prior_k, prior_rate, use_prior, want_grad,
-                                                   out_value, out_grad, out_ok);
+                                                   out_value, out_grad, out_ok, sep_x);
   return cudaGetLastError();
 }
 

@@ -386,32 +386,20 @@ class Scorer:
         return value, grad, ok
 
     def lml_core_host(self, sq: torch.Tensor, z: torch.Tensor, params: np.ndarray, prior=None):
-        """lml_core with host parameters and results through one pinned staging buffer: the c
-        settings go up and (values, grads, ok) come back in one copy each (the L-BFGS-B driver's
-        per-iteration call, hyperfit.py)."""
+        """bx_lml_core_host: lml_core with host parameters and host results (values, grads, ok) - one
+        staged copy each way inside the library (the L-BFGS-B driver's per-iteration call,
+        hyperfit.py)."""
         D, n, _ = sq.shape
         params = np.ascontiguousarray(params, dtype=np.float64)
-        c, w = params.shape
-        nin, nout = c * w, c * (3 + D) + (c + 1) // 2  # params | value, grad | ok (int32)
-        if getattr(self, "_lml_stage", None) is None or self._lml_stage[0].numel() < nin + nout:
-            size = max(nin + nout, 4096)
-            self._lml_stage = (torch.empty(size, dtype=torch.float64, pin_memory=True),
-                               torch.empty(size, dtype=torch.float64, device=sq.device))
-        host, dev = self._lml_stage
-        hv = host.numpy()
-        hv[:nin] = params.ravel()
-        dev[:nin].copy_(host[:nin], non_blocking=True)
-        base = dev.data_ptr()
-        value, grad, ok = base + 8 * nin, base + 8 * (nin + c), base + 8 * (nin + c * (3 + D))
+        c = params.shape[0]
+        value = np.empty(c, dtype=np.float64)
+        grad = np.empty((c, 2 + D), dtype=np.float64)
+        ok = np.empty(c, dtype=np.int32)
         k, rate = (float(prior.shape), float(prior.rate)) if prior is not None else (0.0, 0.0)
-        self._check(self._lib.bx_lml_core(self.h, _ptr(sq.contiguous()), n, D, _ptr(z.contiguous()),
-                                          C.c_void_p(base), c, k, rate, int(prior is not None), 1,
-                                          C.c_void_p(value), C.c_void_p(grad), C.c_void_p(ok), self.stream))
-        host[nin:nin + nout].copy_(dev[nin:nin + nout], non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        out = hv[nin:nin + nout]
-        return (out[:c].copy(), out[c:c * (3 + D)].reshape(c, 2 + D).copy(),
-                out[c * (3 + D):].view(np.int32)[:c].copy())
+        self._check(self._lib.bx_lml_core_host(self.h, _ptr(sq), n, D, _ptr(z), _ptr(params), c, k, rate,
+                                               int(prior is not None), _ptr(value), _ptr(grad), _ptr(ok),
+                                               self.stream))
+        return value, grad, ok
 
     def lml_batched(self, sq: torch.Tensor, z: torch.Tensor, thetas: torch.Tensor) -> torch.Tensor:
         D, n, _ = sq.shape
