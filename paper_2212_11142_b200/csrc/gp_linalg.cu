@@ -368,6 +368,52 @@ __global__ void __launch_bounds__(kGradThreads) lml_grad_kernel(const double* sq
 constexpr int kSmallThreads = 512;
 constexpr int kSmallLmlMaxN = 232;
 
+// u = L^-1 z and alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374) by one warp as column
+// sweeps: lane l keeps the running sums of rows l, l + 32, ... (R register slots) in registers;
+// each step the owner of row i finishes it and broadcasts the solved entry, every lane folds it
+// into its rows (one division, one shuffle and one FMA per step instead of a five-level reduction
+// per row).  R is the smallest power of two >= ceil(n / 32): the per-step bookkeeping is R wide.
+template <int R>
+__device__ __forceinline__ void small_sweeps(int n, const double* z, const double* Lp, double* u, double* al,
+                                             int lane) {
+  double acc[R], zr[R];
+#pragma unroll
+  for (int m = 0; m < R; ++m) {
+    acc[m] = 0.0;
+    zr[m] = lane + 32 * m < n ? z[lane + 32 * m] : 0.0;  // z out of the step chain (global memory)
+  }
+  for (int i = 0; i < n; ++i) {
+    double ui = 0.0;
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+      if (lane + 32 * m == i) ui = (zr[m] - acc[m]) / Lp[tri_idx(i, i)];
+    ui = __shfl_sync(0xffffffffu, ui, i & 31);
+    if (lane == (i & 31)) u[i] = ui;
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int k = lane + 32 * m;
+      if (k > i && k < n) acc[m] = fma(Lp[tri_idx(k, i)], ui, acc[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < R; ++m) acc[m] = 0.0;
+  __syncwarp();
+  for (int i = n - 1; i >= 0; --i) {
+    double ai = 0.0;
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+      if (lane + 32 * m == i) ai = (u[i] - acc[m]) / Lp[tri_idx(i, i)];
+    ai = __shfl_sync(0xffffffffu, ai, i & 31);
+    if (lane == (i & 31)) al[i] = ai;
+    const size_t r0 = tri_idx(i, 0);
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int j = lane + 32 * m;
+      if (j < i) acc[m] = fma(Lp[r0 + j], ai, acc[m]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* sq, int n, int D, const double* z,
                                                                   const double* prm, double prior_k, double prior_rate,
                                                                   int use_prior, int want_grad, double* out_value,
@@ -433,45 +479,13 @@ __global__ void __launch_bounds__(kSmallThreads) lml_small_kernel(const double* 
       for (int k = tid; k < 2 + D; k += blockDim.x) out_grad[(size_t)c * (2 + D) + k] = 0.0;
     return;
   }
-  // u = L^-1 z and alpha = L^-T u (the two TRTRS calls, surrogate.py:373-374): warp 0, column
-  // sweeps - lane l keeps the running sums of rows l, l + 32, ... in registers; each step the owner
-  // of row i finishes it and broadcasts the solved entry, every lane folds it into its rows (one
-  // division, one shuffle and one FMA per step instead of a five-level reduction per row)
+  // u = L^-1 z and alpha = L^-T u: warp 0 (small_sweeps)
   if (warp == 0) {
-    constexpr int kRowsPerLane = (kSmallLmlMaxN + 31) / 32;
-    double acc[kRowsPerLane];
-#pragma unroll
-    for (int m = 0; m < kRowsPerLane; ++m) acc[m] = 0.0;
-    for (int i = 0; i < n; ++i) {
-      double ui = 0.0;
-#pragma unroll
-      for (int m = 0; m < kRowsPerLane; ++m)
-        if (lane + 32 * m == i) ui = (z[i] - acc[m]) / Lp[tri_idx(i, i)];
-      ui = __shfl_sync(0xffffffffu, ui, i & 31);
-      if (lane == (i & 31)) u[i] = ui;
-#pragma unroll
-      for (int m = 0; m < kRowsPerLane; ++m) {
-        const int k = lane + 32 * m;
-        if (k > i && k < n) acc[m] = fma(Lp[tri_idx(k, i)], ui, acc[m]);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kRowsPerLane; ++m) acc[m] = 0.0;
-    __syncwarp();
-    for (int i = n - 1; i >= 0; --i) {
-      double ai = 0.0;
-#pragma unroll
-      for (int m = 0; m < kRowsPerLane; ++m)
-        if (lane + 32 * m == i) ai = (u[i] - acc[m]) / Lp[tri_idx(i, i)];
-      ai = __shfl_sync(0xffffffffu, ai, i & 31);
-      if (lane == (i & 31)) al[i] = ai;
-      const size_t r0 = tri_idx(i, 0);
-#pragma unroll
-      for (int m = 0; m < kRowsPerLane; ++m) {
-        const int j = lane + 32 * m;
-        if (j < i) acc[m] = fma(Lp[r0 + j], ai, acc[m]);
-      }
-    }
+    const int rpl = (n + 31) >> 5;  // rows per lane: the fewest register slots that cover n
+    if (rpl <= 1) small_sweeps<1>(n, z, Lp, u, al, lane);
+    else if (rpl <= 2) small_sweeps<2>(n, z, Lp, u, al, lane);
+    else if (rpl <= 4) small_sweeps<4>(n, z, Lp, u, al, lane);
+    else small_sweeps<8>(n, z, Lp, u, al, lane);
   }
   __syncthreads();
   double za = 0.0, ld = 0.0;
